@@ -1,0 +1,200 @@
+/* libpmorb200 -- C ABI of the B200 (sm_100a) SPAI / SPAI-update / block-solve
+ * path of "Preconditioned Linear Solves for Parametric Model Order Reduction"
+ * (arXiv 1809.06574).
+ *
+ * The reference (`pmorprec`, pure Python over numpy/scipy) has no FFI layer:
+ * its boundary for this path is the Python API.  Each entry point below is
+ * the native replacement of one reference function (or of the numpy/scipy
+ * call inside it) and cites it as file:line under /root/reference/pkg/src/
+ * pmorprec.  The Python package paper_1809_06574_b200 binds them with ctypes
+ * (see INTEGRATION.md for the binding a reference maintainer would add).
+ *
+ * Conventions
+ *  - every pointer argument named d_* is DEVICE memory owned by the caller;
+ *    h_* pointers are host memory read during the call;
+ *  - indices are int32, values float64 (the reference's complex128 carries
+ *    only zero imaginary parts on the real BASELINE inputs);
+ *  - dense blocks are ROW-MAJOR n x k with a leading dimension (ld >= k);
+ *  - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and never synchronises;
+ *  - the library never allocates: scratch comes in via (d_ws, ws_bytes),
+ *    sized by the matching *_workspace() query;
+ *  - return codes: PMP_OK, PMP_ERR_ARG (-> ValueError), PMP_ERR_CUDA
+ *    (-> RuntimeError with pmp_last_error()), PMP_ERR_WORKSPACE;
+ *  - all reductions are fixed-order: repeated calls are bitwise identical.
+ */
+#ifndef PMORB200_H
+#define PMORB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMP_OK 0
+#define PMP_ERR_ARG (-1)
+#define PMP_ERR_CUDA (-2)
+#define PMP_ERR_WORKSPACE (-3)
+
+#define PMP_MAX_TERMS 16
+
+const char* pmp_last_error(void);
+int pmp_version(void);
+
+/* ---- kernel 1: assembly ------------------------------------------------
+ * Replaces SecondOrderModel.assemble (rpmor.py:92-107, _eval_terms :41-49)
+ * when mode == 0, and AffineFamily.evaluate (affine.py:118-134) when
+ * mode == 1, over a precomputed union pattern (affine.py:97-116).
+ * Term t contributes h_coef[t] * value; h_first[t] == 1 marks the constant
+ * term that opens its group (coefficient ignored).  Groups (h_group):
+ * 0 = mass (scaled by s^2), 1 = damping (scaled by s), 2 = stiffness.
+ * h_kind[t] == 0: d_term_vals[t] holds one value per union entry;
+ * h_kind[t] == 1: it holds a length-nrows diagonal (needs d_rowid).
+ * Per entry the arithmetic is the reference's exactly (no FMA), so the
+ * result is bit-identical.  Exact zeros (mode 0) / |v| < 1e-300 (mode 1)
+ * are written as 0.0 and counted into *d_zero_count (int, accumulated). */
+int pmp_assemble(int nnz, int nterms, const double* const* h_term_vals, const int32_t* h_kind,
+                 const int32_t* h_group, const int32_t* h_first, const double* h_coef, int mode,
+                 double s, const int32_t* d_rowid, const int32_t* d_colidx, double* d_out,
+                 const int32_t* d_perm, double* d_out_perm, int32_t* d_zero_count, void* stream);
+
+/* Drop entries whose value is exactly 0.0 (as_csr eliminate_zeros,
+ * sparsecore.py:43).  Output arrays have capacity nnz; d_out_rowptr[n]
+ * holds the new nnz. */
+size_t pmp_compact_workspace(int n);
+int pmp_compact_zeros(int n, const int32_t* d_rowptr, const int32_t* d_colidx,
+                      const double* d_vals, int32_t* d_out_rowptr, int32_t* d_out_colidx,
+                      double* d_out_vals, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- structure: CSR <-> CSC ---------------------------------------------
+ * Transposed structure of an n x n CSR plus the permutation
+ * d_perm[e_in] = e_out (A.tocsc() at spai.py:320; _assemble_and_stats COO
+ * -> CSR at spai.py:307).  Rows of the output are sorted.  When drop_zeros
+ * is set and d_vals is given, entries equal to 0.0 are skipped (their
+ * d_perm is -1) and values are transposed into d_out_vals. */
+size_t pmp_transpose_workspace(int n, int nnz);
+int pmp_transpose(int n, int nnz, const int32_t* d_ptr, const int32_t* d_idx,
+                  const double* d_vals, int drop_zeros, int32_t* d_out_ptr, int32_t* d_out_idx,
+                  double* d_out_vals, int32_t* d_perm, void* d_ws, size_t ws_bytes,
+                  void* stream);
+/* d_dst[d_perm[e]] = d_src[e] for d_perm[e] >= 0 */
+int pmp_permute(int nnz, const int32_t* d_perm, const double* d_src, double* d_dst, void* stream);
+
+/* ---- kernel 2: SPAI pattern gather (spai_pattern level 0, spai.py:182-207)
+ * I_j = rows(A(:, j)) U {j} for an n x n matrix in CSC. */
+size_t pmp_pattern_l0_workspace(int n);
+int pmp_pattern_l0(int n, const int32_t* d_colptr, const int32_t* d_rowidx, int32_t* d_iptr,
+                   int32_t* d_iidx, void* d_ws, size_t ws_bytes, void* stream);
+/* Size pass only: d_iptr[0..n] (exclusive scan of |I_j|); d_iptr[n] = total. */
+int pmp_pattern_l0_ptr(int n, const int32_t* d_colptr, const int32_t* d_rowidx, int32_t* d_iptr,
+                       void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- kernels 3/4: batched column least squares (spai.py:229-292) --------
+ * For each listed column j: J = unique(rows(T(:,j)) U rows(A(:,k)), k in I_j)
+ * (spai.py:237-240); dense A(J, I_j) with the target scattered on J;
+ * column-pivoted Householder QR; rank by |R_kk| > eps |R_00|; minimum-norm
+ * complete-orthogonal solve when rank deficient (LAPACK gelsy semantics,
+ * spai.py:250); explicit residual ||t - A(J,I) z||_2 (spai.py:252).
+ * T == NULL (d_tcolptr NULL) means the identity target (SPAI build,
+ * spai.py:362); otherwise T is the reference matrix (update, update.py:75).
+ *
+ * team: 32 (warp per column), 128 or 256 (CTA per column).  Team scratch is
+ * sized from (lcap, mcap, ncap) = (pow2 bound on the gathered row list,
+ * max |J|, max |I|) -- see pmp_ls_team_bytes.  use_global != 0 keeps the
+ * team scratch in d_ws (for columns whose dense block exceeds shared
+ * memory); otherwise it lives in shared memory.
+ * mode 0: solve (writes d_coef at the I_j slots, d_resid[j], d_flags[j] bit 0
+ *         = rank deficient);
+ * mode 1: plan (writes |J_j| into d_msize[j] only);
+ * mode 2: export J (writes J_j into d_jidx at d_jptr[j]; tests only). */
+size_t pmp_ls_team_bytes(int team, int lcap, int mcap, int ncap);
+int pmp_ls_bound(int ncols, const int32_t* d_cols, const int32_t* d_iptr, const int32_t* d_iidx,
+                 const int32_t* d_acolptr, const int32_t* d_tcolptr, int32_t* d_lsize,
+                 void* stream);
+int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int ncap, int ncols,
+                   const int32_t* d_cols, int n, const int32_t* d_iptr, const int32_t* d_iidx,
+                   const int32_t* d_acolptr, const int32_t* d_arowidx, const double* d_avals,
+                   const int32_t* d_tcolptr, const int32_t* d_trowidx, const double* d_tvals,
+                   double* d_coef, double* d_resid, int32_t* d_flags, int32_t* d_msize,
+                   const int32_t* d_jptr, int32_t* d_jidx, void* d_ws, size_t ws_bytes,
+                   void* stream);
+
+/* ---- level-1 augmentation (_augmented_column, spai.py:210-222) ----------
+ * Weights w_r = sum over k ascending of |a_rk| |a_kj| (no FMA; scipy's
+ * csc_matmat order); candidates outside the base support
+ * ranked by (w desc, row asc), top max(max_fill - |base|, 0) kept, union
+ * with base.  For each listed column j = d_cols[c], mode 0 writes the new
+ * support size to d_newsize[j]; mode 1 writes the support at d_newptr[j]
+ * into d_newidx. */
+size_t pmp_augment_team_bytes(int lcap);
+int pmp_augment(int mode, int lcap, int use_global, int ncols, const int32_t* d_cols,
+                int max_fill, const int32_t* d_iptr, const int32_t* d_iidx,
+                const int32_t* d_acolptr, const int32_t* d_arowidx, const double* d_avals,
+                int32_t* d_newsize, const int32_t* d_newptr, int32_t* d_newidx, void* d_ws,
+                size_t ws_bytes, void* stream);
+
+/* ---- kernel 5a: CSR SpMM (Preconditioner.apply spai.py:82-89; op and true
+ * residual krylov.py:140-147, :231) -----------------------------------------
+ * Y = alpha * A X + beta * Y0 over s <= 32 columns.  Y0 may alias Y; beta
+ * == 0 ignores Y0. */
+int pmp_spmm(int n, const int32_t* d_rowptr, const int32_t* d_colidx, const double* d_vals,
+             int s, const double* d_x, int ldx, double alpha, double beta, const double* d_y0,
+             int ldy0, double* d_y, int ldy, void* stream);
+
+/* ---- kernel 5b: block orthogonalisation (krylov.py:160-161, :189-196) ---
+ * G = V^T W (kv x nw, row-major, device), fixed-order two-level reduction. */
+size_t pmp_gram_workspace(int n, int kv, int nw);
+int pmp_gram(int n, int kv, const double* d_v, int ldv, int nw, const double* d_w, int ldw,
+             double* d_g, void* d_ws, size_t ws_bytes, void* stream);
+/* Out = beta * Out + alpha * V H, H kv x nc row-major on the device
+ * (W - V H, dXt = V Y, images = V G Y: krylov.py:195, :221-223, :246). */
+int pmp_tsmm(int n, int kv, const double* d_v, int ldv, int nc, const double* d_h, double alpha,
+             double beta, double* d_out, int ldo, void* stream);
+
+/* ---- kernel 5c: TSQR, R factor only (the geqp3 inside _qr_deflate,
+ * krylov.py:79-95).  Householder QR per row chunk + in-order reduction of
+ * the chunk R factors; writes the nz x nz upper-triangular R (row-major). */
+size_t pmp_tsqr_workspace(int n, int nz);
+int pmp_tsqr_r(int n, int nz, const double* d_z, int ldz, double* d_r, void* d_ws,
+               size_t ws_bytes, void* stream);
+
+/* ---- helpers ------------------------------------------------------------ */
+/* dst[:, dst_cols[c]] = src[:, src_cols[c]] for c < nc (NULL = identity). */
+int pmp_copy_cols(int n, int nc, const double* d_src, int lds, const int32_t* d_src_cols,
+                  double* d_dst, int ldd, const int32_t* d_dst_cols, void* stream);
+/* dst[:, dst_cols[c]] = beta * dst[:, dst_cols[c]] + alpha * src[:, src_cols[c]]
+ * (beta == 0 ignores dst). */
+int pmp_axpby_cols(int n, int nc, double alpha, const double* d_src, int lds,
+                   const int32_t* d_src_cols, double beta, double* d_dst, int ldd,
+                   const int32_t* d_dst_cols, void* stream);
+/* *d_count += #{j < n : d_flags[j] & mask}; *d_count must be zeroed. */
+int pmp_count_flags(int n, const int32_t* d_flags, int mask, int32_t* d_count, void* stream);
+/* d_out[c] = #{j in list: d_resid[d_cols? d_cols[c]: c] > ep}; compaction
+ * of the columns whose residual exceeds ep (spai.py:287) into d_out_cols,
+ * count into *d_count (zeroed by caller); order preserved. */
+size_t pmp_select_workspace(int ncols);
+int pmp_select_gt(int ncols, const int32_t* d_cols, const double* d_resid, double ep,
+                  int32_t* d_out_cols, int32_t* d_count, void* d_ws, size_t ws_bytes,
+                  void* stream);
+/* exclusive scan of n int32 counts into n+1 outputs (d_out[n] = total) */
+size_t pmp_scan_workspace(int n);
+int pmp_scan(int n, const int32_t* d_in, int32_t* d_out, void* d_ws, size_t ws_bytes,
+             void* stream);
+/* Final SPAI/update column layout after the level-1 pass (spai.py:287-291):
+ * column j keeps its augmented support and coefficients when the augmented
+ * pattern has a non-empty column j, its base ones otherwise. */
+int pmp_merge_sizes(int n, const int32_t* d_base_ptr, const int32_t* d_aug_ptr, int32_t* d_size,
+                    void* stream);
+int pmp_merge_columns(int n, const int32_t* d_base_ptr, const int32_t* d_base_idx,
+                      const double* d_base_coef, const int32_t* d_aug_ptr,
+                      const int32_t* d_aug_idx, const double* d_aug_coef,
+                      const int32_t* d_out_ptr, int32_t* d_out_idx, double* d_out_coef,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMORB200_H */

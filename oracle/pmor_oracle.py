@@ -446,6 +446,9 @@ def run_sequence(workload, kind="spai-update-first", level=0, tol=1e-8, systems=
     A1 = P1 = Aprev = Pprev = None
     out = []
     for idx, (s, p) in enumerate(pts):
+        if (systems is not None and idx not in systems and idx > 0
+                and kind == "spai-update-first"):
+            continue        # independent of (A1, P1) only: nothing to carry
         A = assemble_mdk(workload.mass_terms, workload.damping_terms,
                          workload.stiffness_terms, s, p)
         if idx == 0 or kind == "spai":

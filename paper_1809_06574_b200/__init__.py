@@ -1,0 +1,23 @@
+"""B200-native (sm_100a) SPAI / SPAI-update / block-GCRO path of
+"Preconditioned Linear Solves for Parametric Model Order Reduction"
+(arXiv 1809.06574).
+
+The public names mirror the reference package ``pmorprec``
+(/root/reference/pkg/src/pmorprec/__init__.py:4-64) for the hot path:
+assembly, spai_pattern / spai_column / spai_build, update_first /
+update_second / sequence_precondition, block_gcro_solve / gcro_solve and
+the sequence driver.  Compute runs in libpmorb200.so (hand-written CUDA
+for sm_100a, bound with ctypes); PyTorch supplies device memory, streams
+and torch.distributed.  There is no CPU fallback.
+"""
+
+from .device import DeviceCSR, DevicePattern, Structure
+from .krylov import (SolveReport, SolverBreakdown, SolverConfig, apply_preconditioner,
+                     block_gcro_solve, gcro_solve)
+from .model import AffineFamily, SecondOrderModel, evaluate, pmor_l_sequence
+from .sequence import PrecondPolicy, SequencePreconditioner, run_sequence
+from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, spai_build,
+                   spai_column, spai_pattern)
+from .update import UpdateConfig, SequenceStep, sequence_precondition, update_first, update_second
+
+__version__ = "0.1.0"

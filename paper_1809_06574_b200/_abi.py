@@ -1,0 +1,117 @@
+"""ctypes binding of libpmorb200.so (include/pmorb200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (plain
+nvcc, sm_100a).  There is no CPU fallback: if the library is missing or
+fails to load, every device entry point raises.
+"""
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmorb200.so")
+
+PMP_OK = 0
+PMP_ERR_ARG = -1
+PMP_ERR_CUDA = -2
+PMP_ERR_WORKSPACE = -3
+
+_lib = None
+
+c_int = ctypes.c_int
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_sz = ctypes.c_size_t
+
+_SIGS = {
+    "pmp_last_error": ([], ctypes.c_char_p),
+    "pmp_version": ([], c_int),
+    "pmp_assemble": ([c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_dbl, c_vp, c_vp, c_vp,
+                      c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_compact_workspace": ([c_int], c_sz),
+    "pmp_compact_zeros": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_transpose_workspace": ([c_int, c_int], c_sz),
+    "pmp_transpose": ([c_int, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
+                       c_vp], c_int),
+    "pmp_permute": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_pattern_l0_workspace": ([c_int], c_sz),
+    "pmp_pattern_l0": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_pattern_l0_ptr": ([c_int, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_ls_team_bytes": ([c_int, c_int, c_int, c_int], c_sz),
+    "pmp_ls_bound": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_ls_columns": ([c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp,
+                        c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                        c_vp, c_sz, c_vp], c_int),
+    "pmp_augment_team_bytes": ([c_int], c_sz),
+    "pmp_augment": ([c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                     c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_spmm": ([c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_dbl, c_dbl, c_vp, c_int, c_vp,
+                  c_int, c_vp], c_int),
+    "pmp_gram_workspace": ([c_int, c_int, c_int], c_sz),
+    "pmp_gram": ([c_int, c_int, c_vp, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_tsmm": ([c_int, c_int, c_vp, c_int, c_int, c_vp, c_dbl, c_dbl, c_vp, c_int, c_vp], c_int),
+    "pmp_tsqr_workspace": ([c_int, c_int], c_sz),
+    "pmp_tsqr_r": ([c_int, c_int, c_vp, c_int, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_copy_cols": ([c_int, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp], c_int),
+    "pmp_axpby_cols": ([c_int, c_int, c_dbl, c_vp, c_int, c_vp, c_dbl, c_vp, c_int, c_vp, c_vp],
+                       c_int),
+    "pmp_count_flags": ([c_int, c_vp, c_int, c_vp, c_vp], c_int),
+    "pmp_select_workspace": ([c_int], c_sz),
+    "pmp_select_gt": ([c_int, c_vp, c_vp, c_dbl, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_scan_workspace": ([c_int], c_sz),
+    "pmp_scan": ([c_int, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_merge_columns": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+                          c_int),
+    "pmp_merge_sizes": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def load(path=None):
+    """Load the library (no CUDA device needed to load it)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError("libpmorb200.so not built (%s): run __graft_entry__.build()" % p)
+    lib = ctypes.CDLL(p)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def lib():
+    return load()
+
+
+def check(rc, what=""):
+    if rc == PMP_OK:
+        return
+    msg = lib().pmp_last_error().decode(errors="replace")
+    if rc == PMP_ERR_ARG:
+        raise ValueError("%s: %s" % (what, msg))
+    raise RuntimeError("%s failed (%d): %s" % (what, rc, msg))
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    check(rc, name)

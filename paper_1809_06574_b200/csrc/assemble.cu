@@ -1,0 +1,126 @@
+// Kernel 1: A(sigma, p) = (s^2 M(p) + s D(p)) + K(p) over a fixed union
+// pattern (SecondOrderModel.assemble, rpmor.py:92-107 / _eval_terms :41-49),
+// or the affine sum A0 + sum_j c_j A_j (AffineFamily.evaluate,
+// affine.py:118-134).  One thread per stored entry, streaming and
+// HBM-bound: every term value is read once, the result written once (plus
+// once more, permuted, when a transposed copy is requested).
+//
+// Bit-exactness: scipy evaluates each entry as
+//   acc = T0; acc = acc + c_i * T_i (c_i != 0, term order)        per group
+//   val = ((s*s) * m + s * d) + 1.0 * k                            groups
+// with every product and sum rounded separately (complex arithmetic with a
+// zero imaginary part degenerates to exactly these real operations).  The
+// __dmul_rn / __dadd_rn intrinsics forbid FMA contraction so the device
+// reproduces that rounding sequence bit for bit.
+#include "common.cuh"
+
+namespace pmp {
+
+struct AsmRecipe {
+  int nterms;
+  int mode;  // 0 MDK, 1 affine
+  int any_diag;
+  double s, s2;
+  const double* vals[PMP_MAX_TERMS];
+  int kind[PMP_MAX_TERMS];
+  int group[PMP_MAX_TERMS];
+  int first[PMP_MAX_TERMS];
+  double coef[PMP_MAX_TERMS];
+};
+
+__device__ __forceinline__ double term_value(const AsmRecipe& R, int t, int e, bool diag, int row) {
+  if (R.kind[t] == 0) return __ldg(R.vals[t] + e);
+  return diag ? __ldg(R.vals[t] + row) : 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_assemble(AsmRecipe R, int nnz, const int* __restrict__ rowid,
+                                                  const int* __restrict__ colidx,
+                                                  double* __restrict__ out, const int* __restrict__ perm,
+                                                  double* __restrict__ out_perm, int* zero_count) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  bool zero = false;
+  if (e < nnz) {
+    bool diag = false;
+    int row = 0;
+    if (R.any_diag) {
+      row = __ldg(rowid + e);
+      diag = (__ldg(colidx + e) == row);
+    }
+    double gacc[3] = {0.0, 0.0, 0.0};
+    bool gpres[3] = {false, false, false};
+#pragma unroll 1
+    for (int t = 0; t < R.nterms; ++t) {
+      const int g = R.group[t];
+      const double v = term_value(R, t, e, diag, row);
+      if (R.first[t]) {
+        gacc[g] = v;
+        gpres[g] = true;
+      } else {
+        gacc[g] = __dadd_rn(gacc[g], __dmul_rn(R.coef[t], v));
+      }
+    }
+    double val;
+    if (R.mode == 0) {
+      bool have = false;
+      val = 0.0;
+      const double gc[3] = {R.s2, R.s, 1.0};
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        if (!gpres[g]) continue;
+        double part = __dmul_rn(gc[g], gacc[g]);
+        val = have ? __dadd_rn(val, part) : part;
+        have = true;
+      }
+      if (val == 0.0) val = 0.0;  // canonical +0 for dropped entries
+    } else {
+      val = gacc[0];
+      if (fabs(val) < 1e-300) val = 0.0;
+    }
+    zero = (val == 0.0);
+    out[e] = val;
+    if (perm) out_perm[perm[e]] = val;
+  }
+  unsigned b = __ballot_sync(0xffffffffu, zero);
+  if ((threadIdx.x & 31) == 0 && b && zero_count) atomicAdd(zero_count, __popc(b));
+}
+
+}  // namespace pmp
+
+using namespace pmp;
+
+extern "C" int pmp_assemble(int nnz, int nterms, const double* const* h_term_vals,
+                            const int32_t* h_kind, const int32_t* h_group, const int32_t* h_first,
+                            const double* h_coef, int mode, double s, const int32_t* d_rowid,
+                            const int32_t* d_colidx, double* d_out, const int32_t* d_perm,
+                            double* d_out_perm, int32_t* d_zero_count, void* stream) {
+  if (nterms < 1 || nterms > PMP_MAX_TERMS || nnz < 0 || (mode != 0 && mode != 1)) {
+    set_error("pmp_assemble: bad arguments (nterms=%d, nnz=%d, mode=%d)", nterms, nnz, mode);
+    return PMP_ERR_ARG;
+  }
+  AsmRecipe R;
+  R.nterms = nterms;
+  R.mode = mode;
+  R.s = s;
+  R.s2 = s * s;  // host double multiply: same rounding as numpy's s*s
+  R.any_diag = 0;
+  for (int t = 0; t < nterms; ++t) {
+    R.vals[t] = h_term_vals[t];
+    R.kind[t] = h_kind[t];
+    R.group[t] = h_group[t];
+    R.first[t] = h_first[t];
+    R.coef[t] = h_coef[t];
+    if (h_group[t] < 0 || h_group[t] > 2 || (mode == 1 && h_group[t] != 0)) {
+      set_error("pmp_assemble: bad group %d for term %d", h_group[t], t);
+      return PMP_ERR_ARG;
+    }
+    if (h_kind[t] == 1) R.any_diag = 1;
+  }
+  if (R.any_diag && !d_rowid) {
+    set_error("pmp_assemble: diagonal terms need d_rowid");
+    return PMP_ERR_ARG;
+  }
+  if (nnz == 0) return PMP_OK;
+  k_assemble<<<ceil_div(nnz, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      R, nnz, d_rowid, d_colidx, d_out, d_perm, d_out_perm, d_zero_count);
+  return cuda_status("pmp_assemble");
+}

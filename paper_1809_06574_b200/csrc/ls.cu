@@ -1,0 +1,827 @@
+// Kernels 3/4: batched per-column least squares for the SPAI build
+// (spai.py:229-292, min ||e_j - A p||) and the SPAI update (update.py:66-75,
+// min ||a1_j - A_l q||), plus the level-1 pattern augmentation
+// (spai.py:210-222).
+//
+// One "team" (a warp, or a 128/256-thread CTA) owns one column at a time.
+// Per column it
+//   1. gathers J = unique(target rows U rows(A(:,k)), k in I_j)
+//      (spai.py:237-240) by a bitonic sort + compaction in team memory,
+//   2. scatters the dense |J| x |I| block A(J, I) and the target into team
+//      memory (column-major, leading dimension |J|),
+//   3. runs a column-pivoted Householder QR on it (LAPACK geqp3/dlarfg
+//      conventions), decides the rank by |R_kk| > eps |R_00| (gelsy uses
+//      rcond = eps, spai.py:250), back-substitutes -- or, when rank
+//      deficient, applies the RZ complete orthogonal factorisation to get
+//      gelsy's minimum-norm solution,
+//   4. recomputes the residual ||t - A(J,I) z||_2 explicitly (spai.py:252),
+//   5. writes z into the CSC slots of column j.
+// Team memory is shared memory (warp / CTA tiers) or a global-memory slice
+// (columns whose dense block exceeds shared memory).  All reductions are
+// fixed-order, so results are bitwise reproducible.
+#include <float.h>
+
+#include "common.cuh"
+
+namespace pmp {
+
+struct LsParams {
+  int mode;  // 0 solve, 1 plan (|J|), 2 export J
+  int ncols;
+  const int* cols;
+  int n;
+  const int* iptr;
+  const int* iidx;
+  const int* acolptr;
+  const int* arowidx;
+  const double* avals;
+  const int* tcolptr;  // NULL => identity target
+  const int* trowidx;
+  const double* tvals;
+  double* coef;
+  double* resid;
+  int* flags;
+  int* msize;
+  const int* jptr;
+  int* jidx;
+  int lcap, mcap, ncap;
+  size_t team_bytes;
+  char* gws;
+};
+
+// team memory layout --------------------------------------------------------
+struct LsMem {
+  double* M;     // mcap * (ncap + 1)
+  double* nrm;   // ncap + 1
+  double* w;     // ncap + 1
+  double* z;     // ncap + 1
+  double* tau;   // ncap + 1
+  double* red;   // 16
+  int* list;     // lcap
+  int* sup;      // ncap + 1
+  int* perm;     // ncap + 1
+  int* off;      // ncap + 2
+  int* misc;     // 16
+};
+
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+__host__ __device__ inline size_t ls_team_bytes(int lcap, int mcap, int ncap) {
+  size_t d = (size_t)mcap * (ncap + 1) + 4 * (size_t)(ncap + 1) + 16;
+  size_t i = (size_t)lcap + 3 * (size_t)(ncap + 1) + 1 + 16;
+  return align16(d * sizeof(double)) + align16(i * sizeof(int));
+}
+
+__device__ inline LsMem ls_carve(char* base, int lcap, int mcap, int ncap) {
+  LsMem m;
+  double* d = reinterpret_cast<double*>(base);
+  m.M = d;
+  d += (size_t)mcap * (ncap + 1);
+  m.nrm = d;
+  d += ncap + 1;
+  m.w = d;
+  d += ncap + 1;
+  m.z = d;
+  d += ncap + 1;
+  m.tau = d;
+  d += ncap + 1;
+  m.red = d;
+  d += 16;
+  size_t dbytes = align16(((size_t)mcap * (ncap + 1) + 4 * (size_t)(ncap + 1) + 16) * sizeof(double));
+  int* i = reinterpret_cast<int*>(base + dbytes);
+  m.list = i;
+  i += lcap;
+  m.sup = i;
+  i += ncap + 1;
+  m.perm = i;
+  i += ncap + 1;
+  m.off = i;
+  i += ncap + 2;
+  m.misc = i;
+  return m;
+}
+
+// in-place exclusive prefix of a[0..len) into a[0..len] (a[len] = total);
+// executed by warp 0 of the team, the caller syncs afterwards
+__device__ inline void warp0_exclusive_scan(int* a, int len, int tid) {
+  if (tid >= 32) return;
+  int carry = 0;
+  for (int base = 0; base < len; base += 32) {
+    int i = base + tid;
+    int v = i < len ? a[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (tid >= o) x += y;
+    }
+    if (i < len) a[i] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (tid == 0) a[len] = carry;
+}
+
+template <int T>
+__device__ inline void bitonic_sort(int* a, int lp2, const Team<T>& tm) {
+  for (int k = 2; k <= lp2; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = tm.tid; i < lp2; i += T) {
+        int ixj = i ^ jj;
+        if (ixj > i) {
+          int x = a[i], y = a[ixj];
+          bool asc = (i & k) == 0;
+          if ((x > y) == asc) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      tm.sync();
+    }
+  }
+}
+
+// stable in-place compaction of a[0..len) keeping keep(i, value) == true;
+// returns the kept count (all team threads).  cnt: >= T/32 + 2 ints of team
+// scratch.  keep() may read a[i-1] through `prev` (the original value).
+template <int T, class K>
+__device__ inline int team_compact(int* a, double* wv, int len, const Team<T>& tm, int* cnt, K keep) {
+  const int lane = tm.tid & 31, wid = tm.tid >> 5;
+  int running = 0;
+  int carry_prev = kIntMax;  // original value of a[base - 1]
+  for (int base = 0; base < len; base += T) {
+    int i = base + tm.tid;
+    int v = i < len ? a[i] : kIntMax;
+    double wval = (wv && i < len) ? wv[i] : 0.0;
+    int prev = (tm.tid == 0) ? carry_prev : ((i - 1 < len) ? a[i - 1] : kIntMax);
+    bool f = (i < len) && keep(i, v, prev, wval);
+    unsigned b = __ballot_sync(0xffffffffu, f);
+    int wpre = __popc(b & ((1u << lane) - 1u));
+    int woff = 0, total = __popc(b);
+    int last_orig = __shfl_sync(0xffffffffu, v, 31);
+    if (T > 32) {
+      if (lane == 0) cnt[wid] = __popc(b);
+      if (tm.tid == T - 1) cnt[T / 32] = v;
+      __syncthreads();
+      total = 0;
+      for (int q = 0; q < T / 32; ++q) {
+        if (q < wid) woff += cnt[q];
+        total += cnt[q];
+      }
+      last_orig = cnt[T / 32];
+      __syncthreads();
+    } else {
+      __syncwarp();
+    }
+    if (f) {
+      a[running + woff + wpre] = v;
+      if (wv) wv[running + woff + wpre] = wval;
+    }
+    running += total;
+    carry_prev = last_orig;
+    tm.sync();
+  }
+  return running;
+}
+
+// gather the row list for column j: target rows + rows of A(:, sup[c]);
+// returns its length; pads to a power of two with kIntMax and sorts.
+template <int T>
+__device__ inline int gather_sorted_rows(const LsParams& P, int j, const LsMem& m, int nI, int t0,
+                                         int tl, const Team<T>& tm, int* lp2_out) {
+  for (int c = tm.tid; c < nI; c += T) {
+    int k = m.sup[c];
+    m.off[c] = P.acolptr[k + 1] - P.acolptr[k];
+  }
+  tm.sync();
+  warp0_exclusive_scan(m.off, nI, tm.tid);
+  tm.sync();
+  const int L = tl + m.off[nI];
+  int lp2 = 1;
+  while (lp2 < L) lp2 <<= 1;
+  for (int q = tm.tid; q < lp2; q += T) {
+    int r;
+    if (q >= L) {
+      r = kIntMax;
+    } else if (q < tl) {
+      r = (t0 < 0) ? j : P.trowidx[t0 + q];
+    } else {
+      int qq = q - tl;
+      // last c with off[c] <= qq
+      int lo = 0, hi = nI;  // off[0] = 0 <= qq < off[nI]
+      while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (m.off[mid] <= qq)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      int k = m.sup[lo];
+      r = P.arowidx[P.acolptr[k] + (qq - m.off[lo])];
+    }
+    m.list[q] = r;
+  }
+  tm.sync();
+  bitonic_sort<T>(m.list, lp2, tm);
+  *lp2_out = lp2;
+  return L;
+}
+
+template <int T>
+__device__ void ls_column(const LsParams& P, int j, char* mem, int tid) {
+  LsMem m = ls_carve(mem, P.lcap, P.mcap, P.ncap);
+  Team<T> tm{tid, m.red};
+  const int i0 = P.iptr[j];
+  const int nI = P.iptr[j + 1] - i0;
+  int t0, tl;
+  if (P.tcolptr) {
+    t0 = P.tcolptr[j];
+    tl = P.tcolptr[j + 1] - t0;
+  } else {
+    t0 = -1;
+    tl = 1;
+  }
+  for (int c = tid; c < nI; c += T) m.sup[c] = P.iidx[i0 + c];
+  tm.sync();
+
+  int lp2;
+  const int L = gather_sorted_rows<T>(P, j, m, nI, t0, tl, tm, &lp2);
+  (void)L;
+  const int mJ = team_compact<T>(m.list, nullptr, lp2, tm, m.misc + 4,
+                                 [](int i, int v, int prev, double) {
+                                   return v != kIntMax && (i == 0 || v != prev);
+                                 });
+  const int* J = m.list;
+
+  if (P.mode == 1) {
+    if (tid == 0) P.msize[j] = mJ;
+    tm.sync();
+    return;
+  }
+  if (P.mode == 2) {
+    int o = P.jptr[j];
+    for (int i = tid; i < mJ; i += T) P.jidx[o + i] = J[i];
+    tm.sync();
+    return;
+  }
+
+  // ---- degenerate sizes (spai.py:241-242) -----------------------------------
+  if (nI == 0 || mJ == 0) {
+    double s = 0.0;
+    for (int q = tid; q < tl; q += T) {
+      double v = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
+      s += v * v;
+    }
+    s = tm.sum(s);
+    for (int c = tid; c < nI; c += T) P.coef[i0 + c] = 0.0;
+    if (tid == 0) {
+      P.resid[j] = sqrt(s);
+      P.flags[j] = 0;
+    }
+    tm.sync();
+    return;
+  }
+
+  const int mm = mJ, n = nI;
+  double* M = m.M;
+  const size_t msz = (size_t)mm * (n + 1);
+  for (size_t q = tid; q < msz; q += T) M[q] = 0.0;
+  for (int c = tid; c <= n; c += T) m.perm[c] = c;
+  tm.sync();
+  // scatter A(J, I) (off[] still holds the per-column prefix) and the target
+  {
+    const int tot = m.off[n];
+    for (int q = tid; q < tot + tl; q += T) {
+      if (q < tot) {
+        int lo = 0, hi = n;
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (m.off[mid] <= q)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        int e = P.acolptr[m.sup[lo]] + (q - m.off[lo]);
+        int pos = lower_bound_i(J, mm, P.arowidx[e]);
+        M[pos + (size_t)lo * mm] = P.avals[e];
+      } else {
+        int qq = q - tot;
+        int r = (t0 < 0) ? j : P.trowidx[t0 + qq];
+        double v = (t0 < 0) ? 1.0 : P.tvals[t0 + qq];
+        M[lower_bound_i(J, mm, r) + (size_t)n * mm] = v;
+      }
+    }
+  }
+  tm.sync();
+
+  // ---- column-pivoted Householder QR ----------------------------------------
+  const int K = mm < n ? mm : n;
+  for (int k = 0; k < K; ++k) {
+    // squared norms of the trailing columns over rows k..m-1
+    tm.colsum(
+        n - k, k, mm,
+        [&](int c, int i) {
+          double v = M[i + (size_t)(k + c) * mm];
+          return v * v;
+        },
+        m.nrm + k);
+    tm.sync();
+    if (tid == 0) {
+      int p = k;
+      double best = m.nrm[k];
+      for (int c = k + 1; c < n; ++c)
+        if (m.nrm[c] > best) {
+          best = m.nrm[c];
+          p = c;
+        }
+      m.misc[0] = p;
+      if (p != k) {
+        int t = m.perm[k];
+        m.perm[k] = m.perm[p];
+        m.perm[p] = t;
+      }
+    }
+    tm.sync();
+    const int p = m.misc[0];
+    if (p != k) {
+      for (int i = tid; i < mm; i += T) {
+        double a = M[i + (size_t)k * mm];
+        M[i + (size_t)k * mm] = M[i + (size_t)p * mm];
+        M[i + (size_t)p * mm] = a;
+      }
+      tm.sync();
+    }
+    // dlarfg on M[k:m, k]
+    double part = 0.0;
+    for (int i = k + 1 + tid; i < mm; i += T) {
+      double v = M[i + (size_t)k * mm];
+      part += v * v;
+    }
+    const double xn2 = tm.sum(part);
+    if (tid == 0) {
+      double alpha = M[k + (size_t)k * mm];
+      double tau = 0.0, scal = 0.0;
+      if (xn2 > 0.0) {
+        double beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+        M[k + (size_t)k * mm] = beta;
+      }
+      m.tau[k] = tau;
+      m.w[n] = scal;  // temporary slot
+    }
+    tm.sync();
+    const double tau = m.tau[k];
+    if (tau != 0.0) {
+      const double scal = m.w[n];
+      for (int i = k + 1 + tid; i < mm; i += T) M[i + (size_t)k * mm] *= scal;
+      tm.sync();
+      // w_j = M[k,j] + sum_{i>k} v_i M[i,j] for j = k+1..n (rhs included)
+      tm.colsum(
+          n - k, k + 1, mm,
+          [&](int c, int i) { return M[i + (size_t)k * mm] * M[i + (size_t)(k + 1 + c) * mm]; },
+          m.w + k + 1);
+      tm.sync();
+      for (int c = tid; c < n - k; c += T) m.w[k + 1 + c] += M[k + (size_t)(k + 1 + c) * mm];
+      tm.sync();
+      const int rows = mm - k, ncol = n - k;
+      for (int q = tid; q < rows * ncol; q += T) {
+        int i = k + q % rows;
+        int jj = k + 1 + q / rows;
+        double wj = m.w[jj];
+        if (i == k)
+          M[k + (size_t)jj * mm] -= tau * wj;
+        else
+          M[i + (size_t)jj * mm] -= tau * wj * M[i + (size_t)k * mm];
+      }
+      tm.sync();
+    }
+  }
+
+  // ---- rank (gelsy rcond = eps) and solve: warp 0 ---------------------------
+  if (tid < 32) {
+    const int lane = tid;
+    int r = 0;
+    const double r00 = K > 0 ? fabs(M[0]) : 0.0;
+    if (r00 > 0.0) {
+      r = 1;
+      while (r < K && fabs(M[r + (size_t)r * mm]) > DBL_EPSILON * r00) ++r;
+    }
+    double* y = m.z;  // y[0..n)
+    for (int i = lane; i < n; i += 32) y[i] = (i < r) ? M[i + (size_t)n * mm] : 0.0;
+    __syncwarp();
+    if (r < n) {
+      // RZ: annihilate R[i, r:n] for i = r-1 .. 0 (dtzrzf)
+      for (int i = r - 1; i >= 0; --i) {
+        double s2 = 0.0;
+        for (int c = r + lane; c < n; c += 32) {
+          double v = M[i + (size_t)c * mm];
+          s2 += v * v;
+        }
+        s2 = warp_sum(s2);
+        double alpha = M[i + (size_t)i * mm];
+        double tz = 0.0, scal = 0.0, beta = alpha;
+        if (s2 > 0.0) {
+          beta = -copysign(hypot(alpha, sqrt(s2)), alpha);
+          tz = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        __syncwarp();
+        if (tz != 0.0) {
+          for (int c = r + lane; c < n; c += 32) M[i + (size_t)c * mm] *= scal;
+          __syncwarp();
+          if (lane == 0) M[i + (size_t)i * mm] = beta;
+          // rows l < i: w = R[l,i] + sum_c R[l,c] v_c
+          for (int l = lane; l < i; l += 32) {
+            double wl = M[l + (size_t)i * mm];
+            for (int c = r; c < n; ++c) wl += M[l + (size_t)c * mm] * M[i + (size_t)c * mm];
+            M[l + (size_t)i * mm] -= tz * wl;
+            for (int c = r; c < n; ++c) M[l + (size_t)c * mm] -= tz * wl * M[i + (size_t)c * mm];
+          }
+        }
+        if (lane == 0) m.tau[i] = tz;
+        __syncwarp();
+      }
+    }
+    // back substitution on the leading r x r triangle (column oriented)
+    for (int k = r - 1; k >= 0; --k) {
+      double zk = y[k] / M[k + (size_t)k * mm];
+      __syncwarp();
+      if (lane == 0) y[k] = zk;
+      for (int i = lane; i < k; i += 32) y[i] -= M[i + (size_t)k * mm] * zk;
+      __syncwarp();
+    }
+    if (r < n) {
+      // x = H_{r-1} ... H_0 [y; 0]
+      for (int i = 0; i < r; ++i) {
+        double tz = m.tau[i];
+        if (tz == 0.0) continue;
+        double s = 0.0;
+        for (int c = r + lane; c < n; c += 32) s += M[i + (size_t)c * mm] * y[c];
+        s = warp_sum(s) + y[i];
+        __syncwarp();
+        if (lane == 0) y[i] -= tz * s;
+        for (int c = r + lane; c < n; c += 32) y[c] -= tz * s * M[i + (size_t)c * mm];
+        __syncwarp();
+      }
+    }
+    // un-permute into w[] (original support order)
+    for (int k = lane; k < n; k += 32) m.w[m.perm[k]] = y[k];
+    if (lane == 0) m.misc[1] = r;
+  }
+  tm.sync();
+  const int rank = m.misc[1];
+
+  // ---- explicit residual t - A(J, I) z (spai.py:252) -------------------------
+  double* res = M;  // reuse
+  for (int i = tid; i < mm; i += T) res[i] = 0.0;
+  tm.sync();
+  for (int q = tid; q < tl; q += T) {
+    int r = (t0 < 0) ? j : P.trowidx[t0 + q];
+    res[lower_bound_i(J, mm, r)] = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
+  }
+  tm.sync();
+  for (int c = 0; c < n; ++c) {
+    const double zc = m.w[c];
+    const int k = m.sup[c];
+    const int lo = P.acolptr[k], hi = P.acolptr[k + 1];
+    for (int e = lo + tid; e < hi; e += T) res[lower_bound_i(J, mm, P.arowidx[e])] -= P.avals[e] * zc;
+    tm.sync();
+  }
+  double part = 0.0;
+  for (int i = tid; i < mm; i += T) part += res[i] * res[i];
+  const double rn2 = tm.sum(part);
+  for (int c = tid; c < n; c += T) P.coef[i0 + c] = m.w[c];
+  if (tid == 0) {
+    P.resid[j] = sqrt(rn2);
+    P.flags[j] = (rank < n) ? 1 : 0;
+  }
+  tm.sync();
+}
+
+template <int T, bool GLOBAL>
+__global__ void k_ls(LsParams P) {
+  extern __shared__ __align__(16) char smem[];
+  const int per_block = blockDim.x / T;
+  const int team = threadIdx.x / T;
+  const int tid = threadIdx.x % T;
+  char* mem = GLOBAL ? (P.gws + (size_t)blockIdx.x * P.team_bytes) : (smem + (size_t)team * P.team_bytes);
+  for (int c = blockIdx.x * per_block + team; c < P.ncols; c += gridDim.x * per_block) {
+    const int j = P.cols ? P.cols[c] : c;
+    ls_column<T>(P, j, mem, tid);
+  }
+}
+
+__global__ void k_ls_bound(int ncols, const int* cols, const int* iptr, const int* iidx,
+                           const int* acolptr, const int* tcolptr, int* lsize) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  int j = cols ? cols[c] : c;
+  int L = tcolptr ? tcolptr[j + 1] - tcolptr[j] : 1;
+  for (int e = iptr[j]; e < iptr[j + 1]; ++e) {
+    int k = iidx[e];
+    L += acolptr[k + 1] - acolptr[k];
+  }
+  lsize[c] = L;
+}
+
+// ---------------------------------------------------------------------------
+// level-1 augmentation (spai.py:210-222)
+// ---------------------------------------------------------------------------
+
+struct AugParams {
+  int mode;
+  int ncols;
+  const int* cols;
+  int max_fill;
+  const int* iptr;
+  const int* iidx;
+  const int* acolptr;
+  const int* arowidx;
+  const double* avals;
+  int* newsize;
+  const int* newptr;
+  int* newidx;
+  int lcap;
+  size_t team_bytes;
+  char* gws;
+};
+
+__host__ __device__ inline size_t aug_team_bytes(int lcap) {
+  return align16(((size_t)lcap + 16) * sizeof(double)) + align16(((size_t)lcap + 64 + 16) * sizeof(int));
+}
+
+// |A(r, k)| by binary search in CSC column k (0 if structurally absent)
+__device__ inline double abs_entry(const AugParams& P, int r, int k) {
+  int lo = P.acolptr[k], hi = P.acolptr[k + 1];
+  int pos = lo + lower_bound_i(P.arowidx + lo, hi - lo, r);
+  return (pos < hi && P.arowidx[pos] == r) ? fabs(P.avals[pos]) : 0.0;
+}
+
+template <int T>
+__device__ void aug_column(const AugParams& P, int c, char* mem, int tid) {
+  double* w = reinterpret_cast<double*>(mem);
+  double* red = w + P.lcap;
+  int* list = reinterpret_cast<int*>(mem + align16(((size_t)P.lcap + 16) * sizeof(double)));
+  int* off = list + P.lcap;  // 64 + 16 ints: misc
+  Team<T> tm{tid, red};
+  const int j = P.cols ? P.cols[c] : c;
+  const int b0 = P.iptr[j], nb = P.iptr[j + 1] - b0;
+  const int* base = P.iidx + b0;
+  const int klo = P.acolptr[j], khi = P.acolptr[j + 1];
+  // two-hop candidate rows: rows(A(:, k)) for k in rows(A(:, j))
+  int L = 0;
+  for (int e = klo; e < khi; ++e) {
+    int k = P.arowidx[e];
+    L += P.acolptr[k + 1] - P.acolptr[k];
+  }
+  int lp2 = 1;
+  while (lp2 < L) lp2 <<= 1;
+  for (int q = tid; q < lp2; q += T) {
+    int r = kIntMax;
+    if (q < L) {
+      int acc = 0;
+      for (int e = klo; e < khi; ++e) {
+        int k = P.arowidx[e];
+        int len = P.acolptr[k + 1] - P.acolptr[k];
+        if (q < acc + len) {
+          r = P.arowidx[P.acolptr[k] + (q - acc)];
+          break;
+        }
+        acc += len;
+      }
+    }
+    list[q] = r;
+  }
+  tm.sync();
+  bitonic_sort<T>(list, lp2, tm);
+  int C0 = team_compact<T>(list, nullptr, lp2, tm, off, [](int i, int v, int prev, double) {
+    return v != kIntMax && (i == 0 || v != prev);
+  });
+  // weights in the reference's order: k ascending over rows(A(:, j)), each
+  // product and partial sum rounded (csc_matmat), exact zeros dropped
+  for (int q = tid; q < C0; q += T) {
+    int r = list[q];
+    double acc = 0.0;
+    for (int e = klo; e < khi; ++e) {
+      int k = P.arowidx[e];
+      double ark = abs_entry(P, r, k);
+      if (ark != 0.0) acc = __dadd_rn(acc, __dmul_rn(ark, fabs(P.avals[e])));
+    }
+    bool in_base = false;
+    int pb = lower_bound_i(base, nb, r);
+    if (pb < nb && base[pb] == r) in_base = true;
+    w[q] = (in_base || acc == 0.0) ? -1.0 : acc;  // -1 marks "not a candidate"
+  }
+  tm.sync();
+  int C = team_compact<T>(list, w, C0, tm, off, [](int, int, int, double wv) { return wv >= 0.0; });
+  const int room = P.max_fill - nb > 0 ? P.max_fill - nb : 0;
+  int kept = C;
+  if (C > room) {
+    // keep the first `room` by (w desc, row asc): rank by counting
+    for (int q = tid; q < C; q += T) {
+      double wq = w[q];
+      int rq = list[q];
+      int rank = 0;
+      for (int t = 0; t < C; ++t) {
+        double wt = w[t];
+        rank += (wt > wq) || (wt == wq && list[t] < rq);
+      }
+      w[q] = rank < room ? 1.0 : -1.0;
+    }
+    tm.sync();
+    kept = team_compact<T>(list, w, C, tm, off, [](int, int, int, double wv) { return wv >= 0.0; });
+  }
+  if (P.mode == 0) {
+    if (tid == 0) P.newsize[j] = nb + kept;
+    tm.sync();
+    return;
+  }
+  // union of two disjoint sorted lists: merge by rank
+  int* out = P.newidx + P.newptr[j];
+  for (int q = tid; q < nb; q += T) {
+    int v = base[q];
+    out[q + lower_bound_i(list, kept, v)] = v;
+  }
+  for (int q = tid; q < kept; q += T) {
+    int v = list[q];
+    out[q + lower_bound_i(base, nb, v)] = v;
+  }
+  tm.sync();
+}
+
+template <int T, bool GLOBAL>
+__global__ void k_aug(AugParams P) {
+  extern __shared__ __align__(16) char smem[];
+  const int per_block = blockDim.x / T;
+  const int team = threadIdx.x / T;
+  const int tid = threadIdx.x % T;
+  char* mem = GLOBAL ? (P.gws + (size_t)blockIdx.x * P.team_bytes) : (smem + (size_t)team * P.team_bytes);
+  for (int c = blockIdx.x * per_block + team; c < P.ncols; c += gridDim.x * per_block)
+    aug_column<T>(P, c, mem, tid);
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int T, bool G>
+static int launch_ls(LsParams P, cudaStream_t st, size_t ws_bytes) {
+  const size_t tb = P.team_bytes;
+  if (G) {
+    int grid = num_sms() * 2;
+    if (grid > P.ncols) grid = P.ncols;
+    if ((size_t)grid * tb > ws_bytes) grid = (int)(ws_bytes / tb);
+    if (grid < 1) {
+      set_error("pmp_ls_columns: global workspace too small (%zu < %zu)", ws_bytes, tb);
+      return PMP_ERR_WORKSPACE;
+    }
+    k_ls<T, true><<<grid, T, 0, st>>>(P);
+  } else {
+    int per_block = (T == 32) ? 8 : 1;
+    while (per_block > 1 && per_block * tb > 96 * 1024) per_block >>= 1;
+    size_t sm = per_block * tb;
+    if (sm > 227 * 1024) {
+      set_error("pmp_ls_columns: team needs %zu B of shared memory", sm);
+      return PMP_ERR_ARG;
+    }
+    cudaFuncSetAttribute(k_ls<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int grid = ceil_div(P.ncols, per_block);
+    k_ls<T, false><<<grid, T * per_block, sm, st>>>(P);
+  }
+  return cuda_status("pmp_ls_columns");
+}
+
+template <int T, bool G>
+static int launch_aug(AugParams P, cudaStream_t st, size_t ws_bytes) {
+  const size_t tb = P.team_bytes;
+  if (G) {
+    int grid = num_sms() * 2;
+    if (grid > P.ncols) grid = P.ncols;
+    if ((size_t)grid * tb > ws_bytes) grid = (int)(ws_bytes / tb);
+    if (grid < 1) {
+      set_error("pmp_augment: global workspace too small");
+      return PMP_ERR_WORKSPACE;
+    }
+    k_aug<T, true><<<grid, T, 0, st>>>(P);
+  } else {
+    int per_block = (T == 32) ? 8 : 1;
+    while (per_block > 1 && per_block * tb > 96 * 1024) per_block >>= 1;
+    size_t sm = per_block * tb;
+    if (sm > 227 * 1024) {
+      set_error("pmp_augment: team needs %zu B of shared memory", sm);
+      return PMP_ERR_ARG;
+    }
+    cudaFuncSetAttribute(k_aug<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_aug<T, false><<<ceil_div(P.ncols, per_block), T * per_block, sm, st>>>(P);
+  }
+  return cuda_status("pmp_augment");
+}
+
+}  // namespace pmp
+
+using namespace pmp;
+
+extern "C" {
+
+size_t pmp_ls_team_bytes(int team, int lcap, int mcap, int ncap) {
+  (void)team;
+  return ls_team_bytes(lcap, mcap, ncap);
+}
+
+int pmp_ls_bound(int ncols, const int32_t* cols, const int32_t* iptr, const int32_t* iidx,
+                 const int32_t* acolptr, const int32_t* tcolptr, int32_t* lsize, void* st) {
+  if (ncols <= 0) return PMP_OK;
+  k_ls_bound<<<ceil_div(ncols, 256), 256, 0, reinterpret_cast<cudaStream_t>(st)>>>(
+      ncols, cols, iptr, iidx, acolptr, tcolptr, lsize);
+  return cuda_status("pmp_ls_bound");
+}
+
+int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int ncap, int ncols,
+                   const int32_t* cols, int n, const int32_t* iptr, const int32_t* iidx,
+                   const int32_t* acolptr, const int32_t* arowidx, const double* avals,
+                   const int32_t* tcolptr, const int32_t* trowidx, const double* tvals,
+                   double* coef, double* resid, int32_t* flags, int32_t* msize,
+                   const int32_t* jptr, int32_t* jidx, void* ws, size_t ws_bytes, void* st) {
+  if (mode < 0 || mode > 2 || (team != 32 && team != 128 && team != 256) || lcap < 1 ||
+      mcap < 0 || ncap < 0 || ncols < 0 || (lcap & (lcap - 1))) {
+    set_error("pmp_ls_columns: bad arguments (mode=%d team=%d lcap=%d)", mode, team, lcap);
+    return PMP_ERR_ARG;
+  }
+  if (ncols == 0) return PMP_OK;
+  LsParams P;
+  P.mode = mode;
+  P.ncols = ncols;
+  P.cols = cols;
+  P.n = n;
+  P.iptr = iptr;
+  P.iidx = iidx;
+  P.acolptr = acolptr;
+  P.arowidx = arowidx;
+  P.avals = avals;
+  P.tcolptr = tcolptr;
+  P.trowidx = trowidx;
+  P.tvals = tvals;
+  P.coef = coef;
+  P.resid = resid;
+  P.flags = flags;
+  P.msize = msize;
+  P.jptr = jptr;
+  P.jidx = jidx;
+  P.lcap = lcap;
+  P.mcap = (mode == 0) ? mcap : 0;
+  P.ncap = ncap;
+  P.team_bytes = ls_team_bytes(lcap, P.mcap, ncap);
+  P.gws = (char*)ws;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  if (use_global) {
+    if (team == 32) return launch_ls<32, true>(P, s, ws_bytes);
+    if (team == 128) return launch_ls<128, true>(P, s, ws_bytes);
+    return launch_ls<256, true>(P, s, ws_bytes);
+  }
+  if (team == 32) return launch_ls<32, false>(P, s, ws_bytes);
+  if (team == 128) return launch_ls<128, false>(P, s, ws_bytes);
+  return launch_ls<256, false>(P, s, ws_bytes);
+}
+
+size_t pmp_augment_team_bytes(int lcap) { return aug_team_bytes(lcap); }
+
+int pmp_augment(int mode, int lcap, int use_global, int ncols, const int32_t* cols, int max_fill,
+                const int32_t* iptr, const int32_t* iidx, const int32_t* acolptr,
+                const int32_t* arowidx, const double* avals, int32_t* newsize,
+                const int32_t* newptr, int32_t* newidx, void* ws, size_t ws_bytes, void* st) {
+  if ((mode != 0 && mode != 1) || lcap < 1 || (lcap & (lcap - 1))) {
+    set_error("pmp_augment: bad arguments");
+    return PMP_ERR_ARG;
+  }
+  if (ncols <= 0) return PMP_OK;
+  AugParams P;
+  P.mode = mode;
+  P.ncols = ncols;
+  P.cols = cols;
+  P.max_fill = max_fill;
+  P.iptr = iptr;
+  P.iidx = iidx;
+  P.acolptr = acolptr;
+  P.arowidx = arowidx;
+  P.avals = avals;
+  P.newsize = newsize;
+  P.newptr = newptr;
+  P.newidx = newidx;
+  P.lcap = lcap;
+  P.team_bytes = aug_team_bytes(lcap);
+  P.gws = (char*)ws;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  if (use_global) return launch_aug<256, true>(P, s, ws_bytes);
+  if (lcap <= 2048) return launch_aug<32, false>(P, s, ws_bytes);
+  return launch_aug<256, false>(P, s, ws_bytes);
+}
+
+}  // extern "C"

@@ -1,0 +1,445 @@
+"""Right-preconditioned block GCRO on the B200 -- same API and control flow
+as ``pmorprec.krylov`` (krylov.py:32-290).
+
+Split of the work:
+  * every n-sized operation runs on the device through libpmorb200:
+    the operator A P V (CSR SpMM chain, krylov.py:140-147), the outer
+    projection and the two-pass block Gram-Schmidt (tall-skinny Gram +
+    update, krylov.py:189-196), the R factor of the rank-revealing QR
+    (TSQR, krylov.py:88) and the new basis block Q = Z Pi R^-1 (tall-skinny
+    multiply), solution / residual / outer-space updates (krylov.py:221-269);
+  * the tiny dense algebra stays on the host exactly as in the reference:
+    the pivoted QR of the s x s R factor (scipy geqp3, krylov.py:88), the
+    (k + cap) x (k + m) least-squares problem (numpy gelsd, krylov.py:211)
+    and every control-flow decision (restart, deflation rank, stopping,
+    breakdown, outer-space fold and truncation: krylov.py:152-271).
+One small device->host copy (a few KB) per block step carries all the
+small matrices the host needs; n-sized data never leaves HBM.
+"""
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import torch
+
+from . import _abi
+from .device import DeviceCSR, _dev, scratch
+from .spai import Preconditioner, _as_dev_csr, _block_to_dev
+
+
+class SolverBreakdown(RuntimeError):
+    """No new Krylov direction while the residual is above tolerance
+    (krylov.py:32-34)."""
+
+
+@dataclass
+class SolverConfig:
+    tol: float = 1e-10
+    max_iters: int = 1000
+    outer_space_dim: int = 10
+    inner_restart: int = 50
+    deflation_tol: float = 1e-12
+
+    def __post_init__(self):
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be at least 1")
+        if self.inner_restart < 1:
+            raise ValueError("inner_restart must be at least 1")
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    converged: bool = False
+    residual_history: list = field(default_factory=list)
+    matvec_count: int = 0
+    precond_apply_count: int = 0
+    wall_time: float = 0.0
+    reorth_passes: int = 0
+
+    @property
+    def final_residuals(self):
+        return self.residual_history[-1] if self.residual_history else None
+
+
+def apply_preconditioner(P, V):
+    """Apply a right preconditioner to a block (krylov.py:68-76)."""
+    if not isinstance(P, Preconditioner):
+        raise TypeError("expected a Preconditioner")
+    return P.apply(V)
+
+
+def _safe_rel(norms, refs):
+    out = np.zeros_like(norms)
+    nz = refs > 0
+    out[nz] = norms[nz] / refs[nz]
+    return out
+
+
+# reorthogonalise a new basis block when cond(R11) exceeds this (the block
+# Q = Z Pi R11^-1 then loses more than ~1e-13 of orthogonality)
+_REORTH_COND = 1e3
+
+
+class _Dev:
+    """Device buffers and kernel wrappers for one block solve."""
+
+    def __init__(self, n, s, cap, kc):
+        self.n, self.s, self.cap, self.kc = n, s, cap, kc
+        dev = _dev()
+        f = lambda *shape: torch.empty(*shape, dtype=torch.float64, device=dev)
+        self.V = f(max(n * cap, 1))
+        self.C = f(max(n * kc, 1))
+        self.U = f(max(n * kc, 1))
+        self.bufs = {name: f(max(n * s, 1)) for name in
+                     ("W", "T0", "T1", "T2", "Z", "dX", "Xa", "Rb", "Q")}
+        self.w1 = f(max(n, 1))
+        self.z1 = f(max(n, 1))
+        # small device matrices, fetched to the host in one copy
+        self.off = {}
+        o = 0
+        for name, size in (("G1", kc * s), ("G2", cap * s), ("G3", cap * s), ("RT", s * s),
+                           ("NRM", s * s), ("H", (cap + kc) * s), ("T", s * s),
+                           ("H1", kc + 1)):
+            self.off[name] = o
+            o += size
+        self.sm = f(o)
+        self.hm = torch.empty(o, dtype=torch.float64, pin_memory=True)
+        self.hin = torch.empty(o, dtype=torch.float64, pin_memory=True)
+        self.hm_np = self.hm.numpy()
+        self.hin_np = self.hin.numpy()
+        sc = scratch()
+        self.gram_ws = sc.get("gram", _abi.lib().pmp_gram_workspace(n, cap + kc, s), zero=True)
+        self.tsqr_ws = sc.get("tsqr", _abi.lib().pmp_tsqr_workspace(n, s), zero=True)
+        self.st = _abi.stream()
+        self.launches = 0
+
+    def p(self, name, col=0):
+        """Pointer to a buffer (optionally offset by `col` doubles)."""
+        t = self.bufs[name] if name in self.bufs else getattr(self, name)
+        return t.data_ptr() + 8 * col
+
+    def smp(self, name):
+        return self.sm.data_ptr() + 8 * self.off[name]
+
+    def gram(self, Vp, ldv, kv, Wp, ldw, nw, out):
+        if kv == 0 or nw == 0:
+            return
+        _abi.call("pmp_gram", self.n, kv, Vp, ldv, nw, Wp, ldw, self.smp(out),
+                  _abi.ptr(self.gram_ws), self.gram_ws.numel(), self.st)
+        self.launches += 1
+
+    def tsmm(self, Vp, ldv, kv, Hp, nc, alpha, beta, Op, ldo):
+        if nc == 0:
+            return
+        if kv == 0:
+            if beta == 0.0:
+                _abi.call("pmp_axpby_cols", self.n, nc, 0.0, Op, ldo, None, 0.0, Op, ldo, None,
+                          self.st)
+                self.launches += 1
+            return
+        _abi.call("pmp_tsmm", self.n, kv, Vp, ldv, nc, Hp, float(alpha), float(beta), Op, ldo,
+                  self.st)
+        self.launches += 1
+
+    def tsqr(self, Zp, ldz, nz):
+        _abi.call("pmp_tsqr_r", self.n, nz, Zp, ldz, self.smp("RT"), _abi.ptr(self.tsqr_ws),
+                  self.tsqr_ws.numel(), self.st)
+        self.launches += 1
+
+    def put(self, name, arr):
+        """Stage a small host matrix into the device small buffer."""
+        a = np.ascontiguousarray(arr, dtype=np.float64).ravel()
+        o = self.off[name]
+        self.hin_np[o:o + a.size] = a
+        self.sm[o:o + a.size].copy_(self.hin[o:o + a.size], non_blocking=True)
+        return self.smp(name)
+
+    def fetch(self):
+        self.hm.copy_(self.sm, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    def get(self, name, rows, cols):
+        o = self.off[name]
+        return self.hm_np[o:o + rows * cols].reshape(rows, cols).copy()
+
+    def copy_cols(self, nc, src, lds, sc, dst, ldd, dc):
+        _abi.call("pmp_copy_cols", self.n, nc, src, lds, _abi.ptr(sc), dst, ldd, _abi.ptr(dc),
+                  self.st)
+        self.launches += 1
+
+    def axpby(self, nc, alpha, src, lds, sc, beta, dst, ldd, dc):
+        _abi.call("pmp_axpby_cols", self.n, nc, float(alpha), src, lds, _abi.ptr(sc),
+                  float(beta), dst, ldd, _abi.ptr(dc), self.st)
+        self.launches += 1
+
+
+def _deflate(D, Zp, ldz, mz, outp, ldo, tol, report):
+    """Rank-revealing QR of the n x mz block at Zp (krylov.py:79-95):
+    device TSQR R factor, host pivoted QR of R (geqp3), device
+    Q = Z Pi R11^-1 written to outp.  Returns (rank, R[:rank] un-pivoted)."""
+    if mz == 0:
+        return 0, np.zeros((0, 0))
+    D.tsqr(Zp, ldz, mz)
+    D.fetch()
+    return _deflate_finish(D, Zp, ldz, mz, outp, ldo, tol, report)
+
+
+def _deflate_finish(D, Zp, ldz, mz, outp, ldo, tol, report):
+    RT = np.triu(D.get("RT", mz, mz))
+    Qs, Rs, piv = scipy.linalg.qr(RT, mode="economic", pivoting=True)
+    d = np.abs(np.diag(Rs))
+    if d.size == 0 or d[0] == 0.0:
+        return 0, np.zeros((0, mz))
+    r = int(np.sum(d > tol * d[0]))
+    inv = np.empty_like(piv)
+    inv[piv] = np.arange(piv.size)
+    Rout = Rs[:r][:, inv]
+    R11 = Rs[:r, :r]
+    Rinv = scipy.linalg.solve_triangular(R11, np.eye(r), lower=False)
+    T = np.zeros((mz, r))
+    T[piv[:r], :] = Rinv
+    if d[0] / d[r - 1] > _REORTH_COND:
+        # Q1 = Z T, then one Cholesky-QR pass restores orthogonality:
+        # Q = Q1 R2^-1, R = R2 R
+        D.tsmm(Zp, ldz, mz, D.put("T", T), r, 1.0, 0.0, D.p("Q"), D.s)
+        D.gram(D.p("Q"), D.s, r, D.p("Q"), D.s, r, "NRM")
+        D.fetch()
+        G2 = D.get("NRM", r, r)
+        R2 = np.linalg.cholesky(0.5 * (G2 + G2.T)).T
+        R2inv = scipy.linalg.solve_triangular(R2, np.eye(r), lower=False)
+        D.tsmm(D.p("Q"), D.s, r, D.put("T", R2inv), r, 1.0, 0.0, outp, ldo)
+        report.reorth_passes += 1
+        return r, R2 @ Rout
+    D.tsmm(Zp, ldz, mz, D.put("T", T), r, 1.0, 0.0, outp, ldo)
+    return r, Rout
+
+
+def _colnorms(D, Wp, ldw, nw):
+    D.gram(Wp, ldw, nw, Wp, ldw, nw, "NRM")
+    D.fetch()
+    g = np.diag(D.get("NRM", nw, nw)).copy()
+    return np.sqrt(np.maximum(g, 0.0))
+
+
+def block_gcro_solve(A, B, P=None, cfg=None):
+    """Solve A X = B for all columns of B simultaneously (krylov.py:105-275).
+
+    ``A`` may be a scipy matrix or a DeviceCSR; ``B`` a numpy array (the
+    solution comes back as numpy) or a CUDA tensor (solution stays on the
+    device)."""
+    cfg = cfg or SolverConfig()
+    A = _as_dev_csr(A)
+    n = A.n
+    host_out = not torch.is_tensor(B)
+    if host_out:
+        B = np.asarray(B)
+        if B.ndim == 2 and B.shape[0] != n:
+            raise ValueError("right-hand side has %d rows, matrix is %dx%d" % (B.shape[0], n, n))
+    Bd = _block_to_dev(B)
+    if Bd.shape[0] != n:
+        raise ValueError("right-hand side has %d rows, matrix is %dx%d" % (Bd.shape[0], n, n))
+    if P is not None and not isinstance(P, Preconditioner):
+        raise TypeError("P must be a Preconditioner or None")
+    if P is not None and P.dim != n:
+        raise ValueError("preconditioner dimension %d does not match system %d" % (P.dim, n))
+    X, report = _solve(A, Bd, P, cfg)
+    return (X.cpu().numpy() if host_out else X), report
+
+
+def _solve(A, B, P, cfg):
+    n, s = B.shape
+    t_start = time.perf_counter()
+    report = SolveReport()
+    cap = cfg.inner_restart + 2 * s + 2
+    kc = cfg.outer_space_dim + s
+    D = _Dev(n, s, cap, kc)
+    st = D.st
+    dev = _dev()
+    X = torch.zeros(n, s, dtype=torch.float64, device=dev)
+    Xt = torch.zeros(n, s, dtype=torch.float64, device=dev)
+    R = B.clone()
+    Xp, Xtp, Rp, Bp = X.data_ptr(), Xt.data_ptr(), R.data_ptr(), B.data_ptr()
+    bnorms = _colnorms(D, Bp, s, s)
+    last_rel = np.where(bnorms > 0, 1.0, 0.0)
+    report.residual_history.append(last_rel.copy())
+    active = np.flatnonzero(bnorms > 0)
+    prev_norms = bnorms.copy()     # ||R[:, j]|| as of the last true residual
+    tmp = [D.bufs["T0"], D.bufs["T1"]]
+
+    def op(Vp, ldv, sb, Wp):
+        if P is not None:
+            P.apply_dev(Vp, ldv, sb, D.p("T2"), s, tmp)
+            report.precond_apply_count += sb
+            A.spmm(D.p("T2"), s, sb, Wp, s)
+        else:
+            A.spmm(Vp, ldv, sb, Wp, s)
+        report.matvec_count += sb
+
+    k = 0          # outer-space dimension (columns of C / U in use)
+    while active.size and report.iterations < cfg.max_iters:
+        na = active.size
+        act_dev = torch.as_tensor(active.astype(np.int32), device=dev)
+        start_rel = _safe_rel(prev_norms[active], bnorms[active])
+        # Ract -> Z buffer (n x na, ld s)
+        D.copy_cols(na, Rp, s, act_dev, D.p("Z"), s, None)
+        if k:
+            D.gram(D.p("C"), kc, k, D.p("Z"), s, na, "G1")
+            D.tsmm(D.p("C"), kc, k, D.smp("G1"), na, -1.0, 1.0, D.p("Z"), s)
+        D.tsqr(D.p("Z"), s, na)
+        D.fetch()
+        rhs_c = D.get("G1", k, na) if k else np.zeros((0, na))
+        bs, S0 = _deflate_finish(D, D.p("Z"), s, na, D.p("V"), cap, cfg.deflation_tol, report)
+        if bs == 0:
+            raise SolverBreakdown(
+                "projected residual block vanished with %d unconverged column(s)" % na)
+        Hb = np.zeros((cap, cap))
+        Bmat = np.zeros((k, cap))
+        rhs_v = np.zeros((cap, na))
+        rhs_v[:bs] = S0
+        m = 0
+        total = bs
+        Y = None
+        G = None
+        exhausted = False
+        cycle_converged = False
+        while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
+               and m < cfg.inner_restart):
+            q0, q1 = m, total
+            sb = q1 - q0
+            Wp = D.p("W")
+            op(D.p("V", q0), cap, sb, Wp)
+            report.iterations += 1
+            if k:
+                D.gram(D.p("C"), kc, k, Wp, s, sb, "G1")
+                D.tsmm(D.p("C"), kc, k, D.smp("G1"), sb, -1.0, 1.0, Wp, s)
+            D.gram(D.p("V"), cap, total, Wp, s, sb, "G2")
+            D.tsmm(D.p("V"), cap, total, D.smp("G2"), sb, -1.0, 1.0, Wp, s)
+            D.gram(D.p("V"), cap, total, Wp, s, sb, "G3")
+            D.tsmm(D.p("V"), cap, total, D.smp("G3"), sb, -1.0, 1.0, Wp, s)
+            D.tsqr(Wp, s, sb)
+            D.fetch()
+            if k:
+                Bmat[:, q0:q1] = D.get("G1", k, sb)
+            Hb[:total, q0:q1] += D.get("G2", total, sb)
+            Hb[:total, q0:q1] += D.get("G3", total, sb)
+            bs_next, Rn = _deflate_finish(D, Wp, s, sb, D.p("V", total), cap, cfg.deflation_tol,
+                                          report)
+            Hb[total:total + bs_next, q0:q1] = Rn
+            m = total
+            total += bs_next
+
+            rows_v = total
+            G = np.zeros((k + rows_v, k + m))
+            if k:
+                G[:k, :k] = np.eye(k)
+                G[:k, k:] = Bmat[:, :m]
+            G[k:, k:] = Hb[:rows_v, :m]
+            rhs = np.vstack([rhs_c, rhs_v[:rows_v]])
+            Y, _, _, _ = np.linalg.lstsq(G, rhs, rcond=None)
+            est = _safe_rel(np.linalg.norm(rhs - G @ Y, axis=0), bnorms[active])
+            last_rel[active] = est
+            report.residual_history.append(last_rel.copy())
+            cycle_converged = bool(np.all(est <= cfg.tol))
+            exhausted = bs_next == 0
+
+        if Y is None:
+            break
+
+        # dXt = V Y_v + U Y_u ; Xt[:, active] += dXt     (krylov.py:221-224)
+        D.tsmm(D.p("V"), cap, m, D.put("H", Y[k:]), na, 1.0, 0.0, D.p("dX"), s)
+        if k:
+            D.tsmm(D.p("U"), kc, k, D.put("G1", Y[:k]), na, 1.0, 1.0, D.p("dX"), s)
+        D.axpby(na, 1.0, D.p("dX"), s, None, 1.0, Xtp, s, act_dev)
+        # X = P Xt ; R = B - A X                          (krylov.py:225-233)
+        D.copy_cols(na, Xtp, s, act_dev, D.p("Z"), s, None)
+        if P is not None:
+            P.apply_dev(D.p("Z"), s, na, D.p("Xa"), s, tmp)
+            report.precond_apply_count += na
+            xa = D.p("Xa")
+        else:
+            xa = D.p("Z")
+        D.copy_cols(na, xa, s, None, Xp, s, act_dev)
+        D.copy_cols(na, Bp, s, act_dev, D.p("Rb"), s, None)
+        A.spmm(xa, s, na, D.p("Rb"), s, alpha=-1.0, beta=1.0, Y0=D.p("Rb"), ldy0=s)
+        report.matvec_count += na
+        D.copy_cols(na, D.p("Rb"), s, None, Rp, s, act_dev)
+        tn = _colnorms(D, D.p("Rb"), s, na)
+        prev_norms[active] = tn
+        true_rel = _safe_rel(tn, bnorms[active])
+        last_rel[active] = true_rel
+        report.residual_history.append(last_rel.copy())
+
+        still = true_rel > cfg.tol
+        if exhausted and np.all(still) and np.all(true_rel >= start_rel * (1 - 1e-10)):
+            raise SolverBreakdown(
+                "Krylov subspace exhausted without residual reduction "
+                "(%d column(s) above tolerance)" % int(np.sum(still)))
+
+        # fold the cycle's directions into the outer space (krylov.py:244-269);
+        # skipped when no further cycle can run -- (U, C) are never read again
+        if np.any(still) and report.iterations < cfg.max_iters:
+            img = G @ Y
+            D.tsmm(D.p("V"), cap, total, D.put("H", img[k:]), na, 1.0, 0.0, D.p("Rb"), s)
+            if k:
+                D.tsmm(D.p("C"), kc, k, D.put("G1", img[:k]), na, 1.0, 1.0, D.p("Rb"), s)
+            kk = k
+            for col in range(na):
+                D.copy_cols(1, D.p("Rb", col), s, None, D.p("w1"), 1, None)
+                D.copy_cols(1, D.p("dX", col), s, None, D.p("z1"), 1, None)
+                w0 = _colnorms(D, D.p("w1"), 1, 1)[0]
+                if w0 == 0.0:
+                    continue
+                if kk:
+                    for _ in range(2):
+                        D.gram(D.p("C"), kc, kk, D.p("w1"), 1, 1, "H1")
+                        D.tsmm(D.p("C"), kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("w1"), 1)
+                        D.tsmm(D.p("U"), kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("z1"), 1)
+                nw = _colnorms(D, D.p("w1"), 1, 1)[0]
+                if nw <= 1e-10 * w0:
+                    continue
+                D.axpby(1, 1.0 / nw, D.p("w1"), 1, None, 0.0, D.p("C", kk), kc, None)
+                D.axpby(1, 1.0 / nw, D.p("z1"), 1, None, 0.0, D.p("U", kk), kc, None)
+                kk += 1
+            if kk > cfg.outer_space_dim:
+                drop = kk - cfg.outer_space_dim
+                keep = cfg.outer_space_dim
+                for name in ("C", "U"):
+                    _shift_left(D, name, kc, drop, keep)
+                kk = keep
+            k = kk
+        active = active[still]
+
+    report.converged = active.size == 0
+    report.wall_time = time.perf_counter() - t_start
+    report.device_launches = D.launches
+    return X, report
+
+
+def _shift_left(D, name, kc, drop, keep):
+    """Keep the last `keep` columns of the outer matrix (krylov.py:267-269),
+    staging through a scratch block so the copy never overlaps itself."""
+    n = D.n
+    tmp = torch.empty(max(n * keep, 1), dtype=torch.float64, device=_dev())
+    D.copy_cols(keep, D.p(name, drop), kc, None, tmp.data_ptr(), keep, None)
+    D.copy_cols(keep, tmp.data_ptr(), keep, None, D.p(name), kc, None)
+
+
+def gcro_solve(A, b, P=None, cfg=None):
+    """Single right-hand side: the 1-column block solve, iterate for
+    iterate (krylov.py:278-290)."""
+    if torch.is_tensor(b):
+        if b.dim() != 1:
+            raise ValueError("gcro_solve expects a vector; use block_gcro_solve for blocks")
+        X, report = block_gcro_solve(A, b[:, None], P=P, cfg=cfg)
+    else:
+        b = np.asarray(b)
+        if b.ndim != 1:
+            raise ValueError("gcro_solve expects a vector; use block_gcro_solve for blocks")
+        X, report = block_gcro_solve(A, b[:, None], P=P, cfg=cfg)
+    report.residual_history = [float(r[0]) for r in report.residual_history]
+    return X[:, 0], report

@@ -1,0 +1,267 @@
+"""Parametric system assembly on the B200 (kernel 1).
+
+``SecondOrderModel.assemble(s, p)`` = (s^2 M(p) + s D(p)) + K(p)
+(rpmor.py:92-107) and ``AffineFamily.evaluate(point)`` = A0 + sum c_j A_j
+(affine.py:118-134) over a union pattern built once per model
+(affine.py:97-116).  Term values are laid out once in HBM: a term whose
+pattern is the diagonal is stored as an n-vector, every other term is
+expanded onto the union pattern (one float64 per union entry), so one
+streaming kernel evaluates every entry in the reference's exact operation
+order (bit-identical values) and writes the CSR values -- plus the CSC copy
+when the system is not symmetric -- in a single pass.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _abi
+from .device import DeviceCSR, Structure, _dev, f64, i32, scratch
+
+
+def _canon(T):
+    T = sp.csr_matrix(T)
+    if np.iscomplexobj(T.data):
+        if T.nnz and np.any(T.data.imag != 0):
+            raise NotImplementedError("complex-valued terms are not supported by the B200 path")
+        T = sp.csr_matrix((T.data.real, T.indices, T.indptr), shape=T.shape)
+    T = sp.csr_matrix(T, dtype=np.float64, copy=True)
+    T.sum_duplicates()
+    T.sort_indices()
+    T.eliminate_zeros()
+    return T
+
+
+def _real_scalar(c, what):
+    c = complex(c)
+    if c.imag != 0:
+        raise NotImplementedError("complex %s is not supported by the B200 path yet" % what)
+    return c.real
+
+
+class _UnionTerms:
+    """Union pattern of a list of terms and their device layout."""
+
+    def __init__(self, terms):
+        n = terms[0].shape[0]
+        S = None
+        for T in terms:
+            ones = sp.csr_matrix((np.ones(T.nnz), T.indices, T.indptr), shape=T.shape)
+            S = ones if S is None else S + ones
+        S = sp.csr_matrix(S)
+        S.sort_indices()
+        self.n = n
+        self.symmetric = all(((T - T.T).nnz == 0) or not np.any((T - T.T).data) for T in terms)
+        sym_pattern = (S - S.T).nnz == 0
+        self.structure = Structure(n, i32(S.indptr), i32(S.indices),
+                                   symmetric_pattern=sym_pattern or None)
+        rows = np.repeat(np.arange(n), np.diff(S.indptr))
+        self.vals = []
+        self.kinds = []
+        for T in terms:
+            Tc = T.tocoo()
+            if Tc.nnz and np.all(Tc.row == Tc.col):
+                d = np.zeros(n)
+                d[Tc.row] = Tc.data
+                self.vals.append(f64(d))
+                self.kinds.append(1)
+            else:
+                # slot of every term entry inside the union row
+                pos = np.empty(T.nnz, dtype=np.int64)
+                for i in range(n):
+                    lo, hi = S.indptr[i], S.indptr[i + 1]
+                    tlo, thi = T.indptr[i], T.indptr[i + 1]
+                    if thi > tlo:
+                        pos[tlo:thi] = lo + np.searchsorted(S.indices[lo:hi], T.indices[tlo:thi])
+                full = np.zeros(S.nnz)
+                full[pos] = T.data
+                self.vals.append(f64(full))
+                self.kinds.append(0)
+        self.rowid = i32(rows) if 1 in self.kinds else None
+        if not self.symmetric:
+            self.structure.csc()
+
+    def run(self, recipe, mode, s):
+        """recipe: list of (term index, group, first, coef)."""
+        st = self.structure
+        nt = len(recipe)
+        ptrs = (ctypes_array_vp([self.vals[t].data_ptr() for t, _, _, _ in recipe]))
+        kind = np.array([self.kinds[t] for t, _, _, _ in recipe], dtype=np.int32)
+        group = np.array([g for _, g, _, _ in recipe], dtype=np.int32)
+        first = np.array([f for _, _, f, _ in recipe], dtype=np.int32)
+        coef = np.array([c for _, _, _, c in recipe], dtype=np.float64)
+        out = torch.empty(max(st.nnz, 1), dtype=torch.float64, device=_dev())[:st.nnz]
+        zc = scratch().get("zero_count", 4, zero=False)[:4].view(torch.int32)
+        zc.zero_()
+        perm = out_perm = None
+        if not self.symmetric:
+            perm = st.csc()[2]
+            out_perm = torch.empty_like(out)
+        _abi.call("pmp_assemble", st.nnz, nt, ptrs, kind.ctypes.data, group.ctypes.data,
+                  first.ctypes.data, coef.ctypes.data, mode, float(s), _abi.ptr(self.rowid),
+                  _abi.ptr(st.colidx), _abi.ptr(out), _abi.ptr(perm), _abi.ptr(out_perm),
+                  _abi.ptr(zc), _abi.stream())
+        nz = int(zc.item())
+        if nz:
+            return _compacted(st, out)
+        A = DeviceCSR(st, out, symmetric=self.symmetric)
+        if out_perm is not None:
+            A._csc_vals = out_perm
+        return A
+
+
+def ctypes_array_vp(values):
+    import ctypes
+    arr = (ctypes.c_void_p * len(values))(*values)
+    return ctypes.cast(arr, ctypes.c_void_p)
+
+
+def _compacted(st, vals):
+    """Drop exact zeros (as_csr, sparsecore.py:43): the system gets its own
+    structure (rare path)."""
+    n = st.n
+    rowptr = torch.empty(n + 1, dtype=torch.int32, device=_dev())
+    colidx = torch.empty(max(st.nnz, 1), dtype=torch.int32, device=_dev())
+    v = torch.empty(max(st.nnz, 1), dtype=torch.float64, device=_dev())
+    ws = scratch().get("compact", _abi.lib().pmp_compact_workspace(n))
+    _abi.call("pmp_compact_zeros", n, _abi.ptr(st.rowptr), _abi.ptr(st.colidx), _abi.ptr(vals),
+              _abi.ptr(rowptr), _abi.ptr(colidx), _abi.ptr(v), _abi.ptr(ws), ws.numel(),
+              _abi.stream())
+    nnz = int(rowptr[n].item())
+    A = DeviceCSR(Structure(n, rowptr, colidx[:nnz]), v[:nnz], symmetric=False)
+    M = A.to_scipy(drop_zeros=False)
+    A.symmetric = (M - M.T).nnz == 0
+    return A
+
+
+@dataclass
+class SecondOrderModel:
+    """Second-order system s^2 M(p) + s D(p) + K(p) (rpmor.py:52-107), with
+    term lists [T0, T1, ...] meaning T(p) = T0 + sum_i p_i T_i."""
+
+    family: object = None
+    mass_terms: list = None
+    damping_terms: list = None
+    stiffness_terms: list = None
+    rhs: np.ndarray = None
+    output: np.ndarray = None
+
+    @classmethod
+    def from_affine(cls, family):
+        return cls(family=family, rhs=family.rhs, output=family.output)
+
+    @classmethod
+    def from_mdk(cls, mass_terms, damping_terms, stiffness_terms, rhs=None, output=None):
+        def clean(ts):
+            return None if ts is None else [_canon(T) for T in ts]
+        m = cls(mass_terms=clean(mass_terms), damping_terms=clean(damping_terms),
+                stiffness_terms=clean(stiffness_terms),
+                rhs=None if rhs is None else np.atleast_2d(np.asarray(rhs, dtype=np.float64).T).T,
+                output=None if output is None else np.asarray(output, dtype=np.float64))
+        if m.mass_terms is None and m.damping_terms is None and m.stiffness_terms is None:
+            raise ValueError("need at least one of mass/damping/stiffness terms")
+        return m
+
+    @property
+    def dim(self):
+        if self.family is not None:
+            return self.family.dim
+        for ts in (self.stiffness_terms, self.damping_terms, self.mass_terms):
+            if ts is not None:
+                return ts[0].shape[0]
+        raise ValueError("empty model")
+
+    def _union(self):
+        u = getattr(self, "_u", None)
+        if u is None:
+            terms, groups = [], []
+            for g, ts in enumerate((self.mass_terms, self.damping_terms, self.stiffness_terms)):
+                for T in ts or []:
+                    terms.append(T)
+                    groups.append(g)
+            u = _UnionTerms(terms)
+            u.groups = groups
+            self._u = u
+        return u
+
+    @property
+    def structure(self):
+        return self._union().structure
+
+    def assemble(self, s, pvals):
+        """(s^2 M(p) + s D(p)) + K(p) as a device CSR, bit-identical to the
+        reference's canonical CSR (rpmor.py:92-107)."""
+        if self.family is not None:
+            raise ValueError("affine-form models are evaluated at expansion points; "
+                             "use family.evaluate")
+        s = _real_scalar(s, "shift")
+        pv = [_real_scalar(c, "parameter") for c in np.atleast_1d(pvals)]
+        u = self._union()
+        recipe = []
+        t = 0
+        for g, ts in enumerate((self.mass_terms, self.damping_terms, self.stiffness_terms)):
+            if ts is None:
+                continue
+            recipe.append((t, g, 1, 1.0))
+            for i, c in enumerate(pv[:len(ts) - 1]):
+                if c != 0:
+                    recipe.append((t + i + 1, g, 0, c))
+            t += len(ts)
+        return u.run(recipe, 0, s)
+
+
+class AffineFamily:
+    """Affine family A0 + sum_j p_j A_j on the device (affine.py:60-134)."""
+
+    def __init__(self, terms, rhs=None, output=None):
+        terms = [_canon(T) for T in terms]
+        if len(terms) < 2:
+            raise ValueError("an affine family needs at least two terms")
+        n = terms[0].shape[0]
+        for T in terms:
+            if T.shape != (n, n):
+                raise ValueError("all terms must be square with equal dimension; got %s vs %s"
+                                 % (T.shape, (n, n)))
+        self.terms = terms
+        self.rhs = None if rhs is None else np.asarray(rhs, dtype=np.float64).reshape(n, -1)
+        self.output = None if output is None else np.asarray(output, dtype=np.float64)
+        self._u = None
+
+    @property
+    def dim(self):
+        return self.terms[0].shape[0]
+
+    @property
+    def n_params(self):
+        return len(self.terms) - 1
+
+    def evaluate(self, point):
+        vals = getattr(point, "values", point)
+        coeffs = [_real_scalar(c, "parameter") for c in np.atleast_1d(vals)]
+        if len(coeffs) != self.n_params:
+            raise ValueError("point has %d components, family has %d parameters"
+                             % (len(coeffs), self.n_params))
+        if self._u is None:
+            self._u = _UnionTerms(self.terms)
+        recipe = [(0, 0, 1, 1.0)]
+        for j, c in enumerate(coeffs):
+            if c != 0:
+                recipe.append((j + 1, 0, 0, c))
+        return self._u.run(recipe, 1, 0.0)
+
+
+def evaluate(family, point):
+    return family.evaluate(point)
+
+
+def pmor_l_sequence(model, s_grid, p_grid):
+    """All (A(s_k, p_j), B) systems, frequency grid outermost
+    (zoo.py:268-284); matrices stay on the device."""
+    s_grid, p_grid = list(s_grid), list(p_grid)
+    if not s_grid or not p_grid:
+        raise ValueError("both grids must be nonempty")
+    if model.rhs is None:
+        raise ValueError("model has no right-hand side")
+    return [(model.assemble(s, np.atleast_1d(p)), model.rhs) for s in s_grid for p in p_grid]

@@ -1,0 +1,229 @@
+"""Sequence driver: assemble -> SPAI / SPAI-update -> block GCRO over the
+(sigma, p) grid, on one or several GPUs.
+
+Mirrors the reference's ``PrecondPolicy`` / ``SequencePreconditioner``
+(rpmor.py:177-218) and the composition of SURVEY.md 3.4 (``pmor_l_sequence``
+order, zoo.py:268-284: sigma outermost, p inner; first system gets a fresh
+SPAI, the others the configured update).
+
+Multi-GPU (one process per GPU, torch.distributed over NCCL): with the
+"first" approach every system depends only on (A1, P1) (rpmor.py:208-210),
+so systems are dealt round-robin over ranks by their global sequence index.
+Every rank assembles A1 and its own systems locally from the replicated
+terms; the level-0 pattern -- hence the CSR structure of P1 -- is
+deterministic, so rank 0 builds P1 and one broadcast of its values
+(nnz(P1) float64) replicates it.  Per-system scalars are all-gathered at
+the end; solutions stay on their owner GPU.  "spai" runs independently per
+rank; "spai-update-second" has a true chain dependency and therefore runs
+as replicas (every rank walks the whole chain).
+"""
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .device import DeviceCSR, level0_pattern
+from .krylov import SolverConfig, block_gcro_solve
+from .spai import Preconditioner, SpaiConfig, _factor_from_columns, spai_build
+from .update import UpdateConfig, update_first, update_second
+
+PRECOND_KINDS = ("none", "spai", "spai-update-first", "spai-update-second")
+
+
+@dataclass
+class PrecondPolicy:
+    kind: str = "none"
+    spai: SpaiConfig = field(default_factory=SpaiConfig)
+    update: UpdateConfig = field(default_factory=UpdateConfig)
+    threads: int = 1
+
+    def __post_init__(self):
+        if self.kind not in PRECOND_KINDS:
+            raise ValueError("unknown preconditioner kind %r" % self.kind)
+
+
+class SequencePreconditioner:
+    """Stateful producer of per-system preconditioners (rpmor.py:189-218)."""
+
+    def __init__(self, policy=None):
+        self.policy = policy or PrecondPolicy()
+        self._initial_system = None
+        self._initial_pre = None
+        self._prev_system = None
+        self._prev_pre = None
+
+    def seed(self, A1, P1):
+        """Install an externally built initial pair (the broadcast P1)."""
+        self._initial_system, self._initial_pre = A1, P1
+        self._prev_system, self._prev_pre = A1, P1
+
+    def for_system(self, A):
+        """Returns (preconditioner-or-None, build_seconds, kind_label, stats)."""
+        pol = self.policy
+        if pol.kind == "none":
+            return None, 0.0, "none", None
+        t0 = time.perf_counter()
+        if pol.kind == "spai" or self._initial_pre is None:
+            P, stats = spai_build(A, pol.spai, threads=pol.threads)
+            label = "spai"
+        elif pol.kind == "spai-update-first":
+            P, stats = update_first(self._initial_system, A, self._initial_pre, pol.update)
+            label = "update-first"
+        else:
+            P, stats = update_second(self._prev_system, A, self._prev_pre, pol.update)
+            label = "update-second"
+        seconds = time.perf_counter() - t0
+        if self._initial_pre is None:
+            self._initial_system, self._initial_pre = A, P
+        self._prev_system, self._prev_pre = A, P
+        return P, seconds, label, stats
+
+
+# ---------------------------------------------------------------------------
+# sharding helpers (host logic; tested with gloo on CPU)
+# ---------------------------------------------------------------------------
+
+def owned_systems(n_systems, rank, world, kind="spai-update-first"):
+    """Global sequence indices this rank solves: round-robin for independent
+    systems, the whole chain (replica) for the second approach."""
+    if world <= 1 or kind == "spai-update-second":
+        return list(range(n_systems))
+    return [i for i in range(n_systems) if i % world == rank]
+
+
+def broadcast_values(t, src=0, group=None):
+    """Broadcast a tensor's values from `src` (NCCL for CUDA tensors; the
+    gloo path used by the CPU tests broadcasts a host copy)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t
+    backend = dist.get_backend(group)
+    if t.is_cuda and backend == "nccl":
+        dist.broadcast(t, src, group=group)
+        return t
+    h = t.detach().cpu().contiguous()
+    dist.broadcast(h, src, group=group)
+    t.copy_(h)
+    return t
+
+
+RECORD_FIELDS = ("index", "iterations", "converged", "matvec_count", "precond_apply_count",
+                 "max_final_residual")
+
+
+def gather_records(records, n_systems, group=None):
+    """All-gather the per-system scalar records (sum over ranks of a
+    zero-padded table; each system is owned by exactly one rank)."""
+    import torch.distributed as dist
+    table = np.zeros((n_systems, len(RECORD_FIELDS)), dtype=np.float64)
+    for r in records:
+        table[r["index"]] = [r[f] if f != "index" else r["index"] + 1 for f in RECORD_FIELDS]
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        backend = dist.get_backend(group)
+        t = torch.as_tensor(table)
+        if backend == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, group=group)
+        table = t.cpu().numpy()
+    out = []
+    for row in table:
+        if row[0] == 0:
+            continue
+        d = dict(zip(RECORD_FIELDS, row.tolist()))
+        d["index"] = int(d["index"]) - 1
+        d["iterations"] = int(d["iterations"])
+        d["converged"] = bool(d["converged"])
+        out.append(d)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the driver
+# ---------------------------------------------------------------------------
+
+def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, rank=0, world=1,
+                 group=None, keep_solutions=False, timing=True):
+    """Run the whole parametric sequence; returns (records, info).
+
+    records: one dict per system this rank owns (index, sigma, p, label,
+    iterations, converged, counts, final residuals, optional X).
+    info: phase times from CUDA events (assemble / build / solve seconds,
+    build columns) for this rank.
+    """
+    policy = policy or PrecondPolicy("spai-update-first")
+    solver_cfg = solver_cfg or SolverConfig(tol=1e-8)
+    B = model.rhs if B is None else B
+    Bd = B if torch.is_tensor(B) else torch.as_tensor(np.ascontiguousarray(B, dtype=np.float64),
+                                                       device="cuda")
+    points = [(s, np.atleast_1d(p)) for s in s_grid for p in p_grid]
+    nsys = len(points)
+    mine = owned_systems(nsys, rank, world, policy.kind)
+    seq = SequencePreconditioner(policy)
+    ev = []
+
+    def mark():
+        if not timing:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        ev.append(e)
+        return e
+
+    phases = {"assemble": [], "build": [], "solve": []}
+    build_cols = 0
+    records = []
+    sharded = world > 1 and policy.kind == "spai-update-first"
+    if sharded:
+        # every rank: A1 locally; rank 0 builds P1; broadcast the values
+        t0 = mark()
+        A1 = model.assemble(*points[0])
+        t1 = mark()
+        phases["assemble"].append((t0, t1))
+        if rank == 0:
+            P1, _ = spai_build(A1, policy.spai, threads=policy.threads)
+            build_cols += A1.n
+        else:
+            pat = level0_pattern(A1)
+            vals = torch.empty(pat.nnz, dtype=torch.float64, device=A1.vals.device)
+            P1 = Preconditioner(matrix=_factor_from_columns(pat, vals))
+        t2 = mark()
+        phases["build"].append((t1, t2))
+        broadcast_values(P1.matrix.vals, 0, group)
+        seq.seed(A1, P1)
+    for idx in mine:
+        s, p = points[idx]
+        t0 = mark()
+        if sharded and idx == 0:
+            A = A1
+        else:
+            A = model.assemble(s, p)
+        t1 = mark()
+        if sharded and idx == 0:
+            P, label = P1, "spai"
+        else:
+            P, _, label, _ = seq.for_system(A)
+            build_cols += A.n if P is not None else 0
+        t2 = mark()
+        X, rep = block_gcro_solve(A, Bd, P=P, cfg=solver_cfg)
+        t3 = mark()
+        if timing:
+            phases["assemble"].append((t0, t1))
+            phases["build"].append((t1, t2))
+            phases["solve"].append((t2, t3))
+        rec = {"index": idx, "sigma": float(s), "p": [float(v) for v in p], "label": label,
+               "iterations": rep.iterations, "converged": rep.converged,
+               "matvec_count": rep.matvec_count, "precond_apply_count": rep.precond_apply_count,
+               "final_residuals": np.asarray(rep.final_residuals, dtype=float).tolist(),
+               "max_final_residual": float(np.max(rep.final_residuals)),
+               "launches": getattr(rep, "device_launches", 0)}
+        if keep_solutions:
+            rec["X"] = X
+        records.append(rec)
+    info = {"build_columns": build_cols}
+    if timing:
+        torch.cuda.synchronize()
+        for k, lst in phases.items():
+            info[k + "_s"] = sum(a.elapsed_time(b) for a, b in lst) / 1e3
+    return records, info

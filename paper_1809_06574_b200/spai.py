@@ -1,0 +1,551 @@
+"""Sparse approximate inverse on the B200 -- same API as the reference's
+``pmorprec.spai`` (spai.py:37-373), computed by libpmorb200.
+
+``spai_build`` (spai.py:341-364) runs, entirely on the device:
+  level-0 pattern gather (pmp_pattern_l0)                     spai.py:182-207
+  per-column least squares, tiered by subproblem size
+  (pmp_ls_columns: warp / CTA / global-memory teams)          spai.py:229-292
+  [level 1] selection of columns with resid > ep, two-hop
+  augmentation (pmp_augment) and a second solve pass           spai.py:210-222, :287-290
+  CSC -> CSR of the factor (pmp_permute over a cached
+  transpose plan of the pattern)                               spai.py:295-315
+The per-pattern plan (size tiers of the |J| x |I| subproblems) and the
+transpose are computed once and cached on the pattern, so every later
+build over the same structure -- the SPAI-update sequence -- is a fixed
+list of kernel launches with no host synchronisation.
+"""
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _abi
+from .device import (DeviceCSR, DevicePattern, Structure, _dev, i32, level0_pattern, scratch)
+
+# ---------------------------------------------------------------------------
+# configs and stats (spai.py:131-171)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SpaiConfig:
+    """Knobs of the sparse-approximate-inverse build (spai.py:131-150)."""
+
+    ep: float = 1e-4
+    pattern_level: int = 1
+    max_fill_per_column: int = 80
+
+    def __post_init__(self):
+        if self.ep <= 0:
+            raise ValueError("ep must be positive")
+        if self.pattern_level not in (0, 1):
+            raise ValueError("pattern_level must be 0 or 1")
+
+
+class BuildStats:
+    """Per-column diagnostics of a build (spai.py:153-171).  Device results
+    are copied to the host lazily, on first access."""
+
+    def __init__(self, resid=None, flags=None, augmented=0, t_events=None, seconds=None):
+        self._resid = resid
+        self._flags = flags
+        self._aug = augmented
+        self._events = t_events
+        self._seconds = seconds
+        self._res_host = None
+        self._def = None
+
+    @property
+    def residuals(self):
+        if self._res_host is None:
+            self._res_host = (self._resid.cpu().numpy() if self._resid is not None
+                              else np.zeros(0))
+        return self._res_host
+
+    @property
+    def augmented_columns(self):
+        return int(self._aug)
+
+    @property
+    def rank_deficient_columns(self):
+        if self._def is None:
+            if self._flags is None:
+                self._def = 0
+            else:
+                cnt = torch.zeros(1, dtype=torch.int32, device=self._flags.device)
+                _abi.call("pmp_count_flags", self._flags.numel(), _abi.ptr(self._flags), 1,
+                          _abi.ptr(cnt), _abi.stream())
+                self._def = int(cnt.item())
+        return self._def
+
+    @property
+    def seconds(self):
+        if self._seconds is None and self._events is not None:
+            a, b = self._events
+            b.synchronize()
+            self._seconds = a.elapsed_time(b) / 1e3
+        return float(self._seconds or 0.0)
+
+    def summary(self):
+        res = np.asarray(self.residuals, dtype=float)
+        return {
+            "columns": int(res.size),
+            "max_residual": float(res.max()) if res.size else 0.0,
+            "mean_residual": float(res.mean()) if res.size else 0.0,
+            "augmented_columns": self.augmented_columns,
+            "rank_deficient_columns": self.rank_deficient_columns,
+            "seconds": self.seconds,
+        }
+
+
+# ---------------------------------------------------------------------------
+# preconditioner object (spai.py:37-128)
+# ---------------------------------------------------------------------------
+
+
+def _as_dev_csr(M):
+    if isinstance(M, DeviceCSR):
+        return M
+    return DeviceCSR.from_scipy(M)
+
+
+class Preconditioner:
+    """Right preconditioner: explicit device CSR or factored chain
+    Q * base, applied as successive SpMMs (never materialised;
+    spai.py:37-101)."""
+
+    def __init__(self, matrix=None, q=None, base=None):
+        if matrix is not None:
+            if q is not None or base is not None:
+                raise ValueError("give either an explicit matrix or (q, base)")
+            matrix = _as_dev_csr(matrix)
+            self.matrix, self.q, self.base = matrix, None, None
+        else:
+            if q is None or base is None:
+                raise ValueError("factored form needs both q and base")
+            q = _as_dev_csr(q)
+            if q.shape[0] != base.dim:
+                raise ValueError("factor dimension does not match base preconditioner")
+            self.matrix, self.q, self.base = None, q, base
+
+    @property
+    def kind(self):
+        return "explicit" if self.matrix is not None else "factored"
+
+    @property
+    def dim(self):
+        return (self.matrix if self.matrix is not None else self.q).shape[0]
+
+    @property
+    def depth(self):
+        return 1 if self.matrix is not None else 1 + self.base.depth
+
+    @classmethod
+    def identity(cls, n):
+        return cls(matrix=sp.identity(n, format="csr"))
+
+    def factors(self):
+        """Device factors outermost first: P = f[0] @ ... @ f[-1]."""
+        if self.matrix is not None:
+            return [self.matrix]
+        return [self.q] + self.base.factors()
+
+    def apply_dev(self, X, ldx, s, Y, ldy, tmp):
+        """Y = P X on raw device pointers; ``tmp`` = two scratch tensors of at
+        least n*s doubles (only used for chains)."""
+        f = self.factors()
+        src, lds = X, ldx
+        for i, F in enumerate(reversed(f)):
+            last = i == len(f) - 1
+            dst, ldd = (Y, ldy) if last else (_abi.ptr(tmp[i % 2]), s)
+            F.spmm(src, lds, s, dst, ldd)
+            src, lds = dst, ldd
+
+    def apply(self, V):
+        host = not torch.is_tensor(V)
+        Vd = _block_to_dev(V)
+        n, s = Vd.shape
+        if n != self.dim:
+            raise ValueError("preconditioner is %dx%d, block has %d rows" % (self.dim, self.dim, n))
+        Y = torch.empty_like(Vd)
+        tmp = [torch.empty_like(Vd), torch.empty_like(Vd)] if self.depth > 1 else None
+        self.apply_dev(_abi.ptr(Vd), s, s, _abi.ptr(Y), s, tmp)
+        return Y.cpu().numpy() if host else Y
+
+    def materialize(self):
+        """Explicit sparse matrix of the chain, on the host (diagnostics
+        only, spai.py:91-95)."""
+        mats = [F.to_scipy() for F in self.factors()]
+        out = mats[-1]
+        for M in reversed(mats[:-1]):
+            out = M @ out
+        out = sp.csr_matrix(out)
+        out.eliminate_zeros()
+        return out
+
+
+def _block_to_dev(V):
+    if torch.is_tensor(V):
+        Vd = V.to(device=_dev(), dtype=torch.float64)
+    else:
+        arr = np.asarray(V)
+        if np.iscomplexobj(arr):
+            if np.any(arr.imag != 0):
+                raise NotImplementedError("complex blocks are not supported by the B200 path yet")
+            arr = arr.real
+        Vd = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64), device=_dev())
+    if Vd.dim() == 1:
+        Vd = Vd[:, None]
+    if Vd.dim() != 2:
+        raise ValueError("expected vector or 2-D block")
+    return Vd.contiguous()
+
+
+# ---------------------------------------------------------------------------
+# least-squares planning (size tiers) -- host side, once per pattern
+# ---------------------------------------------------------------------------
+
+_TIERS = ((32, 0, 12 * 1024), (128, 0, 64 * 1024), (256, 0, 200 * 1024), (256, 1, None))
+
+
+def _align16(b):
+    return (b + 15) & ~15
+
+
+def _team_bytes(lcap, mcap, ncap):
+    d = mcap * (ncap + 1) + 4 * (ncap + 1) + 16
+    i = lcap + 3 * (ncap + 1) + 1 + 16
+    return _align16(8 * d) + _align16(4 * i)
+
+
+def _pow2(v):
+    v = np.maximum(np.asarray(v, dtype=np.int64), 1)
+    return (1 << np.ceil(np.log2(v)).astype(np.int64)).astype(np.int64)
+
+
+class _Tier:
+    def __init__(self, team, glob, lcap, mcap, ncap, cols):
+        self.team, self.glob = team, glob
+        self.lcap, self.mcap, self.ncap = int(lcap), int(mcap), int(ncap)
+        self.cols_host = cols
+        self.cols = i32(cols)
+        self.ncols = int(cols.size)
+        self.bytes = _team_bytes(self.lcap, self.mcap, self.ncap)
+
+
+def _split_tiers(cols, lcap, m, nI):
+    """Group columns into launch tiers by the team memory they need."""
+    if cols.size == 0:
+        return []
+    b = _team_bytes(lcap, m, nI)
+    cls = np.full(cols.size, len(_TIERS) - 1)
+    for t in range(len(_TIERS) - 2, -1, -1):
+        cls[b <= _TIERS[t][2]] = t
+    tiers = []
+    for t, (team, glob, limit) in enumerate(_TIERS):
+        sel = np.flatnonzero(cls == t)
+        if sel.size == 0:
+            continue
+        sel = sel[np.argsort(b[sel], kind="stable")]
+        start = 0
+        while start < sel.size:
+            # greedily extend while the running maxima still fit the tier
+            lo, hi = start + 1, sel.size
+            if limit is not None:
+                while lo < hi:
+                    mid = (lo + hi + 1) // 2
+                    s = sel[start:mid]
+                    if _team_bytes(lcap[s].max(), m[s].max(), nI[s].max()) <= limit:
+                        lo = mid
+                    else:
+                        hi = mid - 1
+                end = lo
+            else:
+                end = sel.size
+            s = sel[start:end]
+            s_sorted = s[np.argsort(cols[s], kind="stable")]
+            tiers.append(_Tier(team, glob, lcap[s].max(), m[s].max(), nI[s].max(),
+                               cols[s_sorted]))
+            start = end
+    return tiers
+
+
+def _plan(pattern, sys_colptr, sys_rowidx, t_colptr, t_rowidx, t_key, sys_key, cols_host=None):
+    """Size tiers for solving the listed columns of ``pattern`` against the
+    system (and target) structures; cached on the pattern when all columns
+    are solved."""
+    key = ("plan", sys_key, t_key) if cols_host is None else None
+    if key is not None and key in pattern.cache:
+        return pattern.cache[key]
+    n = pattern.n
+    st = _abi.stream()
+    cols = np.arange(n, dtype=np.int64) if cols_host is None else np.asarray(cols_host, np.int64)
+    ncols = cols.size
+    if ncols == 0:
+        return []
+    dcols = None if cols_host is None else i32(cols)
+    lsize = torch.empty(ncols, dtype=torch.int32, device=_dev())
+    _abi.call("pmp_ls_bound", ncols, _abi.ptr(dcols), _abi.ptr(pattern.iptr),
+              _abi.ptr(pattern.iidx), _abi.ptr(sys_colptr), _abi.ptr(t_colptr),
+              _abi.ptr(lsize), st)
+    L = lsize.cpu().numpy().astype(np.int64)
+    iptr = pattern.iptr.cpu().numpy().astype(np.int64)
+    nI = (iptr[cols + 1] - iptr[cols]).astype(np.int64)
+    lcap = _pow2(L)
+    # plan pass: |J_j| (mode 1) grouped by list capacity
+    msize = torch.zeros(n, dtype=torch.int32, device=_dev())
+    for cap in np.unique(lcap):
+        s = np.flatnonzero(lcap == cap)
+        nc = int(nI[s].max())
+        tb = _team_bytes(int(cap), 0, nc)
+        team, glob = (32, 0) if tb <= 12 * 1024 else ((256, 0) if tb <= 200 * 1024 else (256, 1))
+        dsel = i32(cols[s])
+        ws = _ws_for(glob, tb, s.size)
+        _abi.call("pmp_ls_columns", 1, team, glob, int(cap), 0, nc, int(s.size), _abi.ptr(dsel), n,
+                  _abi.ptr(pattern.iptr), _abi.ptr(pattern.iidx), _abi.ptr(sys_colptr),
+                  _abi.ptr(sys_rowidx), None, _abi.ptr(t_colptr), _abi.ptr(t_rowidx),
+                  None, None, None, None, _abi.ptr(msize), None, None, _abi.ptr(ws),
+                  ws.numel() if ws is not None else 0, st)
+    m = msize.cpu().numpy().astype(np.int64)[cols]
+    tiers = _split_tiers(cols, lcap, m, nI)
+    if key is not None:
+        pattern.cache[key] = tiers
+    return tiers
+
+
+def _ws_for(glob, team_bytes, ncols):
+    if not glob:
+        return None
+    grid = min(ncols, 2 * torch.cuda.get_device_properties(_dev()).multi_processor_count)
+    return scratch().get("ls_global", team_bytes * max(grid, 1))
+
+
+# ---------------------------------------------------------------------------
+# column solves (spai.py:273-338)
+# ---------------------------------------------------------------------------
+
+
+def _csr_plan(pattern):
+    """Transpose plan of a pattern (CSC supports -> CSR factor), cached."""
+    plan = pattern.cache.get("csr")
+    if plan is None:
+        n, nnz = pattern.n, pattern.nnz
+        rowptr = torch.empty(n + 1, dtype=torch.int32, device=_dev())
+        colidx = torch.empty(max(nnz, 1), dtype=torch.int32, device=_dev())
+        perm = torch.empty(max(nnz, 1), dtype=torch.int32, device=_dev())
+        ws = scratch().get("transpose", _abi.lib().pmp_transpose_workspace(n, nnz))
+        _abi.call("pmp_transpose", n, nnz, _abi.ptr(pattern.iptr), _abi.ptr(pattern.iidx), None,
+                  0, _abi.ptr(rowptr), _abi.ptr(colidx), None, _abi.ptr(perm), _abi.ptr(ws),
+                  ws.numel(), _abi.stream())
+        st = Structure(n, rowptr, colidx[:nnz] if nnz else colidx[:0])
+        plan = (st, perm[:nnz] if nnz else perm[:0])
+        pattern.cache["csr"] = plan
+    return plan
+
+
+def _factor_from_columns(pattern, coef):
+    st, perm = _csr_plan(pattern)
+    vals = torch.empty(max(pattern.nnz, 1), dtype=torch.float64, device=_dev())[:pattern.nnz]
+    if pattern.nnz:
+        _abi.call("pmp_permute", pattern.nnz, _abi.ptr(perm), _abi.ptr(coef), _abi.ptr(vals),
+                  _abi.stream())
+    return DeviceCSR(st, vals, symmetric=False)
+
+
+def _run_tiers(tiers, pattern, A_csc, T_csc, coef, resid, flags, mode=0, jptr=None, jidx=None):
+    st = _abi.stream()
+    acolptr, arowidx, avals = A_csc
+    tcolptr, trowidx, tvals = T_csc if T_csc is not None else (None, None, None)
+    for t in tiers:
+        ws = _ws_for(t.glob, t.bytes, t.ncols)
+        _abi.call("pmp_ls_columns", mode, t.team, t.glob, t.lcap, t.mcap, t.ncap, t.ncols,
+                  _abi.ptr(t.cols), pattern.n, _abi.ptr(pattern.iptr), _abi.ptr(pattern.iidx),
+                  _abi.ptr(acolptr), _abi.ptr(arowidx), _abi.ptr(avals), _abi.ptr(tcolptr),
+                  _abi.ptr(trowidx), _abi.ptr(tvals), _abi.ptr(coef), _abi.ptr(resid),
+                  _abi.ptr(flags), None, _abi.ptr(jptr), _abi.ptr(jidx), _abi.ptr(ws),
+                  ws.numel() if ws is not None else 0, st)
+
+
+def _get_tiers(pattern, system, target, cols_host=None):
+    acolptr, arowidx = system.csc_structure()
+    tcolptr = trowidx = tkey = None
+    if target is not None:
+        tcolptr, trowidx = target.csc_structure()
+        tkey = target.structure.key
+    return _plan(pattern, acolptr, arowidx, tcolptr, trowidx, tkey, system.structure.key,
+                 cols_host)
+
+
+def _augment(system, base, cols_dev, ncols, max_fill):
+    """Level-1 supports for the listed columns (spai.py:210-222): returns an
+    n-column pattern whose column j is non-empty iff j was augmented."""
+    n = base.n
+    st = _abi.stream()
+    acolptr, arowidx, avals = system.csc()
+    lsize = torch.empty(ncols, dtype=torch.int32, device=_dev())
+    _abi.call("pmp_ls_bound", ncols, _abi.ptr(cols_dev), _abi.ptr(base.iptr), _abi.ptr(base.iidx),
+              _abi.ptr(acolptr), None, _abi.ptr(lsize), st)
+    L = int(lsize.max().item())
+    lcap = int(_pow2(L))
+    tb = _abi.lib().pmp_augment_team_bytes(lcap)
+    glob = 1 if tb > 200 * 1024 else 0
+    ws = _ws_for(glob, tb, ncols)
+    size = torch.zeros(n, dtype=torch.int32, device=_dev())
+    args_tail = (_abi.ptr(ws), ws.numel() if ws is not None else 0, st)
+    _abi.call("pmp_augment", 0, lcap, glob, ncols, _abi.ptr(cols_dev), int(max_fill),
+              _abi.ptr(base.iptr), _abi.ptr(base.iidx), _abi.ptr(acolptr), _abi.ptr(arowidx),
+              _abi.ptr(avals), _abi.ptr(size), None, None, *args_tail)
+    aptr = torch.empty(n + 1, dtype=torch.int32, device=_dev())
+    sws = scratch().get("scan", _abi.lib().pmp_scan_workspace(n))
+    _abi.call("pmp_scan", n, _abi.ptr(size), _abi.ptr(aptr), _abi.ptr(sws), sws.numel(), st)
+    nnz = int(aptr[n].item())
+    aidx = torch.empty(max(nnz, 1), dtype=torch.int32, device=_dev())
+    _abi.call("pmp_augment", 1, lcap, glob, ncols, _abi.ptr(cols_dev), int(max_fill),
+              _abi.ptr(base.iptr), _abi.ptr(base.iidx), _abi.ptr(acolptr), _abi.ptr(arowidx),
+              _abi.ptr(avals), None, _abi.ptr(aptr), _abi.ptr(aidx), *args_tail)
+    return DevicePattern(n, aptr, aidx, nnz)
+
+
+def solve_columns(system, target, pattern, cfg, events=True):
+    """Device restatement of _run_column_solves + _build_columns
+    (spai.py:273-338): returns (factor DeviceCSR, BuildStats, final pattern,
+    coefficients in pattern order)."""
+    n = system.n
+    st = _abi.stream()
+    ev0 = ev1 = None
+    if events:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    A_csc = system.csc()
+    T_csc = target.csc() if target is not None else None
+    tiers = _get_tiers(pattern, system, target)
+    coef = torch.empty(max(pattern.nnz, 1), dtype=torch.float64, device=_dev())
+    resid = torch.empty(n, dtype=torch.float64, device=_dev())
+    flags = torch.zeros(n, dtype=torch.int32, device=_dev())
+    _run_tiers(tiers, pattern, A_csc, T_csc, coef, resid, flags)
+    final_pat, final_coef, n_aug = pattern, coef, 0
+    if cfg.pattern_level >= 1 and n > 0:
+        sel = torch.empty(n, dtype=torch.int32, device=_dev())
+        cnt = torch.zeros(1, dtype=torch.int32, device=_dev())
+        ws = scratch().get("select", _abi.lib().pmp_select_workspace(n))
+        _abi.call("pmp_select_gt", n, None, _abi.ptr(resid), float(cfg.ep), _abi.ptr(sel),
+                  _abi.ptr(cnt), _abi.ptr(ws), ws.numel(), st)
+        n_aug = int(cnt.item())
+        if n_aug:
+            cols_dev = sel[:n_aug]
+            apat = _augment(system, pattern, cols_dev, n_aug, cfg.max_fill_per_column)
+            atiers = _get_tiers(apat, system, target, cols_dev.cpu().numpy())
+            acoef = torch.empty(max(apat.nnz, 1), dtype=torch.float64, device=_dev())
+            _run_tiers(atiers, apat, A_csc, T_csc, acoef, resid, flags)
+            final_pat, final_coef = _merge(pattern, coef, apat, acoef)
+    if final_pat is pattern:
+        P = _factor_from_columns(pattern, coef)
+    else:
+        P = _factor_from_columns(final_pat, final_coef)
+    if events:
+        ev1.record()
+    stats = BuildStats(resid, flags, n_aug, (ev0, ev1) if events else None)
+    return P, stats, final_pat, final_coef
+
+
+def _merge(base, bcoef, apat, acoef):
+    n = base.n
+    st = _abi.stream()
+    size = torch.empty(n, dtype=torch.int32, device=_dev())
+    _abi.call("pmp_merge_sizes", n, _abi.ptr(base.iptr), _abi.ptr(apat.iptr), _abi.ptr(size), st)
+    optr = torch.empty(n + 1, dtype=torch.int32, device=_dev())
+    sws = scratch().get("scan", _abi.lib().pmp_scan_workspace(n))
+    _abi.call("pmp_scan", n, _abi.ptr(size), _abi.ptr(optr), _abi.ptr(sws), sws.numel(), st)
+    nnz = int(optr[n].item())
+    oidx = torch.empty(max(nnz, 1), dtype=torch.int32, device=_dev())
+    ocoef = torch.empty(max(nnz, 1), dtype=torch.float64, device=_dev())
+    _abi.call("pmp_merge_columns", n, _abi.ptr(base.iptr), _abi.ptr(base.iidx), _abi.ptr(bcoef),
+              _abi.ptr(apat.iptr), _abi.ptr(apat.iidx), _abi.ptr(acoef), _abi.ptr(optr),
+              _abi.ptr(oidx), _abi.ptr(ocoef), st)
+    return DevicePattern(n, optr, oidx, nnz), ocoef
+
+
+# ---------------------------------------------------------------------------
+# public API (spai.py:182-373)
+# ---------------------------------------------------------------------------
+
+
+class SparsityPattern:
+    """Host mirror of sparsecore.SparsityPattern (sparsecore.py:76-99)."""
+
+    def __init__(self, nrows, columns=()):
+        self.nrows = nrows
+        cleaned = []
+        for idx in columns:
+            arr = np.unique(np.asarray(idx, dtype=np.int64))
+            if arr.size and (arr[0] < 0 or arr[-1] >= nrows):
+                raise ValueError("pattern row index out of range [0, %d)" % nrows)
+            cleaned.append(arr)
+        self.columns = cleaned
+
+    @property
+    def ncols(self):
+        return len(self.columns)
+
+    def max_fill(self):
+        return max((len(c) for c in self.columns), default=0)
+
+
+def _to_device_pattern(pattern, n):
+    if isinstance(pattern, DevicePattern):
+        return pattern
+    cols = pattern.columns if isinstance(pattern, SparsityPattern) else pattern
+    if len(cols) != n:
+        raise ValueError("pattern has %d columns, matrix has %d" % (len(cols), n))
+    return DevicePattern.from_columns(n, [np.unique(np.asarray(c, dtype=np.int64)) for c in cols])
+
+
+def spai_pattern(A, level=0, max_fill_per_column=80):
+    """A-priori pattern (spai.py:182-207), computed on the device."""
+    A = _as_dev_csr(A)
+    base = level0_pattern(A)
+    if level == 0:
+        return SparsityPattern(A.n, base.columns())
+    n = A.n
+    cols = torch.arange(n, dtype=torch.int32, device=_dev())
+    apat = _augment(A, base, cols, n, max_fill_per_column)
+    return SparsityPattern(n, apat.columns())
+
+
+def spai_column(A, i, pattern_i):
+    """Least-squares column of the approximate inverse (spai.py:256-270)."""
+    A = _as_dev_csr(A)
+    support = np.unique(np.asarray(pattern_i, dtype=np.int64))
+    if support.size == 0:
+        raise ValueError("column pattern must be nonempty")
+    n = A.n
+    cols = [np.zeros(0, dtype=np.int64)] * n
+    cols[int(i)] = support
+    pat = DevicePattern.from_columns(n, cols)
+    tiers = _get_tiers(pat, A, None, np.array([int(i)]))
+    coef = torch.empty(max(pat.nnz, 1), dtype=torch.float64, device=_dev())
+    resid = torch.empty(n, dtype=torch.float64, device=_dev())
+    flags = torch.zeros(n, dtype=torch.int32, device=_dev())
+    _run_tiers(tiers, pat, A.csc(), None, coef, resid, flags)
+    return (support, coef[:support.size].cpu().numpy(), float(resid[int(i)].item()),
+            bool(flags[int(i)].item()))
+
+
+def spai_build(A, cfg=None, pattern=None, threads=1):
+    """Explicit sparse approximate inverse of A (spai.py:341-364).
+    ``threads`` is accepted for API compatibility (the device build is
+    column-parallel regardless)."""
+    A = _as_dev_csr(A)
+    cfg = cfg or SpaiConfig()
+    if pattern is None:
+        pat = level0_pattern(A)
+        eff = cfg
+    else:
+        pat = _to_device_pattern(pattern, A.n)
+        eff = SpaiConfig(ep=cfg.ep, pattern_level=0, max_fill_per_column=cfg.max_fill_per_column)
+    P, stats, _, _ = solve_columns(A, None, pat, eff)
+    return Preconditioner(matrix=P), stats

@@ -1,0 +1,356 @@
+"""Device parity: the B200 path against the golden outputs of the real
+reference (tests/golden/) and the CPU oracle, through the C-ABI library.
+
+Bars: assembly and patterns bit-exact; SPAI / update
+factors within 1e-10 relative Frobenius (structure equal modulo exact
+zeros); residuals within 1e-12; solves to the 1e-8 relative residual with
+iteration counts within +-2.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import goldens as G  # noqa: E402
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "oracle"))
+import pmor_oracle as orc  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def pm():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1809_06574_b200 as pm
+    from paper_1809_06574_b200 import _abi
+    _abi.load()
+    return pm
+
+
+def _mf(name):
+    return 12 if name == "rand40" else (50 if name == "tridiag9" else 80)
+
+
+# ---------------------------------------------------------------------------
+# assembly (kernel 1): bit-exact
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", list(G.WORKLOAD_CASES))
+def test_assembly_bit_exact(pm, name):
+    from paper_1809_06574_b200.workloads import make_config
+    g = G.load(name + "_assemble")
+    cfg, scale = G.WORKLOAD_CASES[name]
+    W = make_config(cfg, scale=scale)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    i = 0
+    while "asm%d_point" % i in g:
+        pt = g["asm%d_point" % i]
+        A = model.assemble(pt[0], pt[1:]).to_scipy()
+        ref = G.csr(g, "asm%d" % i)
+        assert np.array_equal(A.indptr, ref.indptr)
+        assert np.array_equal(A.indices, ref.indices)
+        assert np.array_equal(A.data, ref.data)
+        i += 1
+
+
+def test_affine_evaluate_bit_exact(pm):
+    rs = np.random.RandomState(3)
+    terms = [sp.random(60, 60, density=0.1, random_state=rs, format="csr") + 3 * sp.identity(60)]
+    terms += [sp.random(60, 60, density=0.05, random_state=rs, format="csr") for _ in range(3)]
+    coeffs = [0.3, 0.0, -1.7]
+    ref = orc.affine_evaluate(terms, coeffs)
+    got = pm.AffineFamily(terms).evaluate(coeffs).to_scipy()
+    assert np.array_equal(got.indptr, ref.indptr)
+    assert np.array_equal(got.indices, ref.indices)
+    assert np.array_equal(got.data, ref.data)
+
+
+def test_assembly_drops_exact_zeros(pm):
+    # K0 and K1 cancel exactly on the off-diagonal at p = -1
+    n = 20
+    K0 = sp.diags([np.ones(n - 1), 4 * np.ones(n), np.ones(n - 1)], (-1, 0, 1)).tocsr()
+    K1 = sp.diags([np.ones(n - 1), np.ones(n - 1)], (-1, 1)).tocsr()
+    M = sp.identity(n, format="csr")
+    model = pm.SecondOrderModel.from_mdk([M], None, [K0, K1], rhs=np.ones((n, 1)))
+    A = model.assemble(0.0, [-1.0]).to_scipy(drop_zeros=False)
+    ref = orc.assemble_mdk([M], None, [K0, K1], 0.0, [-1.0])
+    assert np.array_equal(A.indptr, ref.indptr) and np.array_equal(A.data, ref.data)
+
+
+# ---------------------------------------------------------------------------
+# patterns (kernel 2 + augmentation): bit-exact
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_patterns_bit_exact(pm, name):
+    g = G.load(name)
+    A1 = G.csr(g, "A1")
+    p0 = pm.spai_pattern(A1, level=0)
+    for a, b in zip(p0.columns, G.pattern(g, "pat0")):
+        assert np.array_equal(a, b)
+    if G.has(g, "pat1"):
+        p1 = pm.spai_pattern(A1, level=1, max_fill_per_column=_mf(name))
+        for j, (a, b) in enumerate(zip(p1.columns, G.pattern(g, "pat1"))):
+            assert np.array_equal(a, b), j
+
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_touched_rows_bit_exact(pm, name):
+    """J_j exported by the least-squares kernel (mode 2) == spai.py:237-240."""
+    import torch as th
+    from paper_1809_06574_b200 import _abi
+    from paper_1809_06574_b200.device import DeviceCSR, level0_pattern
+    from paper_1809_06574_b200.spai import _get_tiers, _run_tiers
+    g = G.load(name)
+    for Akey, Tkey, Jkey in (("A1", None, "J0"), ("Al", "A1", "J0u")):
+        if not G.has(g, Jkey):
+            continue
+        A = DeviceCSR.from_scipy(G.csr(g, Akey))
+        T = DeviceCSR.from_scipy(G.csr(g, Tkey)) if Tkey else None
+        pat = level0_pattern(A)
+        Jref = G.pattern(g, Jkey)
+        jptr = np.zeros(len(Jref) + 1, dtype=np.int64)
+        jptr[1:] = np.cumsum([len(c) for c in Jref])
+        jptr_d = th.as_tensor(jptr.astype(np.int32), device="cuda")
+        jidx = th.full((max(int(jptr[-1]), 1),), -1, dtype=th.int32, device="cuda")
+        tiers = _get_tiers(pat, A, T)
+        n = A.n
+        coef = th.empty(max(pat.nnz, 1), dtype=th.float64, device="cuda")
+        resid = th.empty(n, dtype=th.float64, device="cuda")
+        flags = th.zeros(n, dtype=th.int32, device="cuda")
+        _run_tiers(tiers, pat, A.csc(), T.csc() if T else None, coef, resid, flags, mode=2,
+                   jptr=jptr_d, jidx=jidx)
+        got = jidx.cpu().numpy()
+        for j in range(n):
+            assert np.array_equal(got[jptr[j]:jptr[j + 1]], Jref[j]), (Jkey, j)
+
+
+# ---------------------------------------------------------------------------
+# SPAI and update values (kernels 3/4)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", G.CASES)
+def test_spai_and_update_vs_reference(pm, name):
+    g = G.load(name)
+    A1, Al = G.csr(g, "A1"), G.csr(g, "Al")
+    for lvl in (0, 1):
+        if not G.has(g, "P%d" % lvl):
+            continue
+        cfg = pm.SpaiConfig(pattern_level=lvl, max_fill_per_column=_mf(name))
+        P, st = pm.spai_build(A1, cfg)
+        G.compare_factor(P.matrix.to_scipy(), G.csr(g, "P%d" % lvl))
+        assert np.allclose(st.residuals, g["P%d_resid" % lvl], rtol=0, atol=1e-12)
+        assert st.augmented_columns == int(g["P%d_aug" % lvl])
+        assert st.rank_deficient_columns == int(g["P%d_def" % lvl])
+        if not G.has(g, "Q%d" % lvl):
+            continue
+        ucfg = pm.UpdateConfig(pattern_level=lvl, max_fill_per_column=_mf(name))
+        Pu, su = pm.update_first(A1, Al, P, ucfg)
+        assert Pu.kind == "factored" and Pu.depth == 2
+        G.compare_factor(Pu.q.to_scipy(), G.csr(g, "Q%d" % lvl))
+        assert np.allclose(su.residuals, g["Q%d_resid" % lvl], rtol=0, atol=1e-12)
+        assert su.augmented_columns == int(g["Q%d_aug" % lvl])
+
+
+def test_build_deterministic(pm):
+    g = G.load("c3s6")
+    A1 = G.csr(g, "A1")
+    a, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=1))
+    b, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=1))
+    assert np.array_equal(a.matrix.vals.cpu().numpy(), b.matrix.vals.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# reference unit-test assertions on real inputs (test_spai.py, test_update.py)
+# ---------------------------------------------------------------------------
+
+def test_known_answers(pm):
+    P, st = pm.spai_build(sp.identity(6, format="csr"))
+    assert np.allclose(P.matrix.to_scipy().toarray(), np.eye(6), atol=1e-15)
+    assert st.residuals.max() <= 1e-14
+    d = np.array([2.0, 5.0, 0.5, 8.0])
+    P, _ = pm.spai_build(sp.diags(d).tocsr())
+    assert np.allclose(P.matrix.to_scipy().diagonal(), 1 / d, rtol=0, atol=1e-15)
+    sup, vals, resid, dfc = pm.spai_column(sp.diags([2.0, 4.0]).tocsr(), 1, [1])
+    assert abs(vals[0] - 0.25) <= 1e-15 and resid <= 1e-15 and not dfc
+    # degenerate column flagged, not fatal (test_spai.py:170-174)
+    _, st = pm.spai_build(sp.csr_matrix(np.array([[1.0, 0.0], [0.0, 0.0]])),
+                          pm.SpaiConfig(pattern_level=0))
+    assert st.rank_deficient_columns >= 1
+
+
+def test_full_pattern_inverse(pm):
+    rs = np.random.RandomState(17)
+    A = sp.random(50, 50, density=0.08, random_state=rs, format="csr") + 4 * sp.identity(50)
+    P, _ = pm.spai_build(A, pattern=[np.arange(50)] * 50)
+    inv = np.linalg.inv(A.toarray())
+    assert np.linalg.norm(P.matrix.to_scipy().toarray() - inv) <= 1e-10 * np.linalg.norm(inv)
+
+
+def test_update_identity_and_scaling(pm):
+    rs = np.random.RandomState(1)
+    A1 = (sp.random(30, 30, density=0.08, random_state=rs, format="csr")
+          + 4 * sp.identity(30)).tocsr()
+    P1, _ = pm.spai_build(A1)
+    P, st = pm.update_first(A1, A1, P1)
+    assert np.linalg.norm(P.q.to_scipy().toarray() - np.eye(30)) <= 1e-10
+    assert st.residuals.max() <= 1e-10
+    P, _ = pm.update_first(A1, 2.0 * A1, P1)
+    assert np.linalg.norm(P.q.to_scipy().toarray() - 0.5 * np.eye(30)) <= 1e-10
+    V = np.random.default_rng(7).standard_normal((30, 2))
+    direct = P.materialize() @ V
+    assert np.linalg.norm(P.apply(V) - direct) <= 1e-13 * np.linalg.norm(direct)
+    P3, _ = pm.update_second(A1, A1, P)
+    assert P3.depth == 3
+
+
+# ---------------------------------------------------------------------------
+# block GCRO (kernel 5)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["rand40", "tridiag9", "c1s24", "c2s8", "c3s6", "c5n500"])
+def test_block_gcro_vs_reference(pm, name):
+    g = G.load(name)
+    A1, Al, B = G.csr(g, "A1"), G.csr(g, "Al"), g["B"]
+    P0, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))
+    Pu, _ = pm.update_first(A1, Al, P0, pm.UpdateConfig(pattern_level=0))
+    for tag, A, P in (("s1", A1, P0), ("s2", Al, Pu), ("nop", Al, None)):
+        X, rep = pm.block_gcro_solve(A, B, P=P, cfg=pm.SolverConfig(tol=1e-8))
+        assert rep.converged == bool(g[tag + "_conv"])
+        assert abs(rep.iterations - int(g[tag + "_iters"])) <= 2, (tag, rep.iterations,
+                                                                   int(g[tag + "_iters"]))
+        rel = np.linalg.norm(B - A @ X, axis=0) / np.linalg.norm(B, axis=0)
+        assert np.all(rel <= 1e-8), rel
+        assert abs(float(np.max(rep.final_residuals)) - rel.max()) <= 1e-9
+
+
+def test_gcro_known_answers(pm):
+    I5 = sp.identity(5, format="csr")
+    x, rep = pm.gcro_solve(I5, np.arange(1.0, 6.0))
+    assert rep.converged and rep.iterations <= 1 and np.linalg.norm(x - np.arange(1.0, 6.0)) < 1e-12
+    A = sp.diags(np.arange(1.0, 11.0)).tocsr()
+    x, rep = pm.gcro_solve(A, np.ones(10))
+    assert rep.converged and np.linalg.norm(x - 1 / np.arange(1.0, 11.0)) <= 1e-10
+    with pytest.raises(pm.SolverBreakdown):
+        pm.gcro_solve(sp.diags([1.0, 0.0, 0.0]).tocsr(), np.array([1.0, 1.0, 1.0]))
+    with pytest.raises(ValueError):
+        pm.gcro_solve(sp.identity(4, format="csr"), np.ones(5))
+    with pytest.raises(TypeError):
+        pm.apply_preconditioner(np.eye(3), np.ones((3, 1)))
+
+
+def test_block_special_cases(pm):
+    rs = np.random.RandomState(27)
+    A = (sp.random(50, 50, density=0.08, random_state=rs, format="csr")
+         + 4 * sp.identity(50)).tocsr()
+    rng = np.random.default_rng(28)
+    b1, b2 = rng.standard_normal(50), rng.standard_normal(50)
+    X, rep = pm.block_gcro_solve(A, np.column_stack([b1, b2, b1 + b2]))   # rank 2 block
+    assert rep.converged and np.linalg.norm(X[:, 2] - X[:, 0] - X[:, 1]) <= 1e-9
+    X, rep = pm.block_gcro_solve(A, np.column_stack([b1, np.zeros(50)]))  # zero column
+    assert rep.converged and np.all(X[:, 1] == 0) and rep.final_residuals[1] == 0.0
+    Bm = rng.standard_normal((50, 4))
+    Bm[:, 2] *= 1e-6
+    X, rep = pm.block_gcro_solve(A, Bm)                                    # column scales
+    rel = np.linalg.norm(Bm - A @ X, axis=0) / np.linalg.norm(Bm, axis=0)
+    assert rep.converged and np.all(rel <= 1e-10)
+    x, rep = pm.gcro_solve(A, b1, cfg=pm.SolverConfig(max_iters=3))       # not converged
+    assert not rep.converged and rep.iterations == 3 and np.all(np.isfinite(x))
+    x, rep = pm.gcro_solve(A, b1, cfg=pm.SolverConfig(inner_restart=8, outer_space_dim=5))
+    assert rep.converged                                                   # restarts + fold
+    assert np.linalg.norm(b1 - A @ x) / np.linalg.norm(b1) <= 1e-10
+
+
+def test_restart_matches_oracle(pm):
+    """Restarted cycles with outer-space recycling follow the oracle."""
+    rs = np.random.RandomState(9)
+    A = (sp.random(150, 150, density=0.12, random_state=rs, format="csr")
+         + 4 * sp.identity(150)).tocsr()
+    B = np.random.default_rng(10).standard_normal((150, 3))
+    cfg = dict(inner_restart=4, outer_space_dim=5, tol=1e-10)
+    X, rep = pm.block_gcro_solve(A, B, cfg=pm.SolverConfig(**cfg))
+    Xr, info = orc.block_gcro(A, B, None, **cfg)
+    assert rep.converged and info["converged"]
+    assert abs(rep.iterations - info["iterations"]) <= 2, (rep.iterations, info["iterations"])
+
+
+# ---------------------------------------------------------------------------
+# full sequences (driver) vs the oracle
+# ---------------------------------------------------------------------------
+
+def test_c1_sequence_vs_oracle(pm):
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(1)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pol = pm.PrecondPolicy("spai-update-first", spai=pm.SpaiConfig(pattern_level=0),
+                           update=pm.UpdateConfig(pattern_level=0))
+    recs, info = pm.run_sequence(model, W.s_grid, W.p_grid, pol, keep_solutions=True)
+    ref = orc.run_sequence(W, level=0, tol=1e-8)
+    pts = W.points()
+    for r, (idx, Xr, inf, _) in zip(recs, ref):
+        assert r["index"] == idx
+        assert r["converged"] and inf["converged"]
+        assert abs(r["iterations"] - inf["iterations"]) <= 2, (idx, r["iterations"],
+                                                               inf["iterations"])
+        A = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[idx])
+        X = r["X"].cpu().numpy()
+        rel = np.linalg.norm(W.rhs - A @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
+        assert np.all(rel <= 1e-8)
+
+
+@pytest.mark.parametrize("cfg,level", [(2, 0), (3, 0), (3, 1), (4, 0)])
+def test_full_size_sampled_columns(pm, cfg, level):
+    """Full-size configs: every column built on the device, a deterministic
+    sample checked against the oracle (supports bit-exact, values 1e-10)."""
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(cfg)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pts = W.points()
+    A1 = model.assemble(*pts[0])
+    A2 = model.assemble(*pts[1])
+    P1, st = pm.spai_build(A1, pm.SpaiConfig(pattern_level=level))
+    Pu, su = pm.update_first(A1, A2, P1, pm.UpdateConfig(pattern_level=level))
+    A1h, A2h = A1.to_scipy(), A2.to_scipy()
+    cols = np.sort(np.random.default_rng(7).permutation(A1.n)[:300])
+    for F, res, stats in ((P1.matrix, orc.spai_build(A1h, pattern_level=level, columns=cols), st),
+                          (Pu.q, orc.update_factor(A1h, A2h, pattern_level=level, columns=cols),
+                           su)):
+        Fc = F.to_scipy(drop_zeros=False).tocsc()
+        for (j, sup, coef, r, dfc, aug) in res:
+            lo, hi = Fc.indptr[j], Fc.indptr[j + 1]
+            assert np.array_equal(Fc.indices[lo:hi], sup), j
+            err = np.linalg.norm(Fc.data[lo:hi] - coef) / max(np.linalg.norm(coef), 1e-300)
+            assert err <= 1e-10, (j, err)
+            assert abs(stats.residuals[j] - r) <= 1e-12
+
+
+def test_c2_sequence_property(pm):
+    """c2 at full size: every system's true residual <= 1e-8 (recomputed on
+    the host from X) and the first two systems' iterations match the oracle."""
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(2)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pol = pm.PrecondPolicy("spai-update-first", spai=pm.SpaiConfig(pattern_level=0),
+                           update=pm.UpdateConfig(pattern_level=0))
+    s_grid = W.s_grid[:2]
+    recs, info = pm.run_sequence(model, s_grid, W.p_grid[:3], pol, keep_solutions=True)
+    ref = orc.run_sequence(W, level=0, tol=1e-8, systems={0, 1})
+    for r, (idx, Xr, inf, _) in zip(recs[:2], ref):
+        assert abs(r["iterations"] - inf["iterations"]) <= 2
+    pts = [(s, np.atleast_1d(p)) for s in s_grid for p in W.p_grid[:3]]
+    for r in recs:
+        A = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[r["index"]])
+        X = r["X"].cpu().numpy()
+        rel = np.linalg.norm(W.rhs - A @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
+        assert r["converged"] and np.all(rel <= 1e-8)

@@ -1,0 +1,129 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol the
+header declares, the host-side planning / sharding logic, and the
+multi-rank (gloo, world_size 2) broadcast / gather path."""
+
+import os
+import re
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "pmorb200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pmp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_header_symbols():
+    from paper_1809_06574_b200 import _abi
+    lib = _abi.load()
+    names = _header_functions()
+    assert len(names) >= 25
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_abi.EXPORTS)
+    assert lib.pmp_version() == 1
+    # workspace queries are host-only and need no device
+    assert lib.pmp_gram_workspace(1000, 10, 4) >= 256 + 8 * 40
+    assert lib.pmp_ls_team_bytes(32, 64, 25, 7) > 0
+
+
+def test_library_rejects_bad_arguments_without_device():
+    from paper_1809_06574_b200 import _abi
+    lib = _abi.load()
+    assert lib.pmp_spmm(10, None, None, None, 40, None, 40, 1.0, 0.0, None, 0, None, 40,
+                        None) == _abi.PMP_ERR_ARG
+    assert lib.pmp_ls_columns(5, 32, 0, 64, 1, 1, 1, None, 1, None, None, None, None, None,
+                              None, None, None, None, None, None, None, None, None, None, 0,
+                              None) == _abi.PMP_ERR_ARG
+    assert b"bad arguments" in lib.pmp_last_error()
+
+
+def test_team_bytes_formula_matches_library():
+    from paper_1809_06574_b200 import _abi
+    from paper_1809_06574_b200.spai import _team_bytes
+    lib = _abi.load()
+    for l, m, n in ((64, 25, 7), (1024, 125, 27), (4096, 295, 80), (1, 0, 0)):
+        assert lib.pmp_ls_team_bytes(32, l, m, n) == _team_bytes(l, m, n)
+
+
+def test_tier_split_respects_limits():
+    from paper_1809_06574_b200 import spai
+    rng = np.random.default_rng(0)
+    ncol = 5000
+    cols = np.arange(ncol)
+    nI = rng.integers(1, 240, ncol)
+    m = nI * rng.integers(5, 60, ncol)
+    lcap = spai._pow2(m * 3)
+    # patch the device upload for a CPU run
+    orig = spai.i32
+    spai.i32 = lambda a, device=None: np.asarray(a)
+    try:
+        tiers = spai._split_tiers(cols, lcap, m, nI)
+    finally:
+        spai.i32 = orig
+    seen = np.concatenate([t.cols_host for t in tiers])
+    assert np.array_equal(np.sort(seen), cols)
+    for t in tiers:
+        limit = dict(((a, b), c) for a, b, c in spai._TIERS)[(t.team, t.glob)]
+        if limit is not None:
+            assert t.bytes <= limit
+        sel = t.cols_host
+        assert t.mcap == m[sel].max() and t.ncap == nI[sel].max()
+
+
+def test_owned_systems_partition():
+    from paper_1809_06574_b200.sequence import owned_systems
+    for world in (1, 2, 3, 8):
+        got = sorted(i for r in range(world) for i in owned_systems(40, r, world))
+        assert got == list(range(40))
+    assert owned_systems(5, 1, 2, "spai-update-second") == list(range(5))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1809_06574_b200.sequence import (broadcast_values, gather_records,
+                                                owned_systems)
+    vals = torch.arange(10, dtype=torch.float64) if rank == 0 else torch.zeros(10,
+                                                                               dtype=torch.float64)
+    broadcast_values(vals, 0)
+    recs = [{"index": i, "iterations": 10 + i, "converged": True, "matvec_count": 3 * i,
+             "precond_apply_count": 2 * i, "max_final_residual": 1e-9}
+            for i in owned_systems(7, rank, world)]
+    table = gather_records(recs, 7)
+    q.put((rank, vals.tolist(), [(r["index"], r["iterations"]) for r in table]))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_broadcast_and_gather():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, vals, table in out:
+        assert vals == list(range(10))
+        assert table == [(i, 10 + i) for i in range(7)]
