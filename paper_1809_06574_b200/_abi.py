@@ -112,6 +112,49 @@ def stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+# kernel launches issued per ABI call (CUB scans launch an init + a scan
+# kernel; the transpose launches count, scan, fill and sort kernels)
+_LAUNCHES_PER_CALL = {"pmp_scan": 2, "pmp_transpose": 5, "pmp_pattern_l0": 5,
+                      "pmp_pattern_l0_ptr": 3, "pmp_compact_zeros": 4, "pmp_select_gt": 4,
+                      "pmp_augment": 1}
+_NO_LAUNCH = {"pmp_last_error", "pmp_version"}
+
+COUNTERS = {}          # name -> calls (enabled by count_launches())
+_counting = False
+_timed = {}            # name -> list of (start, end) CUDA events
+_timing_names = ()
+
+
+def count_launches(enable=True, timed=()):
+    """Count ABI kernel launches (and optionally bracket the calls named in
+    ``timed`` with CUDA events on the current stream)."""
+    global _counting, _timing_names
+    _counting = enable
+    _timing_names = tuple(timed)
+    COUNTERS.clear()
+    _timed.clear()
+
+
+def launches():
+    return sum(_LAUNCHES_PER_CALL.get(k, 1) * v for k, v in COUNTERS.items()
+               if k not in _NO_LAUNCH)
+
+
+def timed_events():
+    return _timed
+
+
 def call(name, *args):
+    if _counting:
+        COUNTERS[name] = COUNTERS.get(name, 0) + 1
+        if name in _timing_names:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            rc = getattr(lib(), name)(*args)
+            b.record()
+            _timed.setdefault(name, []).append((a, b, args))
+            check(rc, name)
+            return
     rc = getattr(lib(), name)(*args)
     check(rc, name)

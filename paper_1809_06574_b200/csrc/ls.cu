@@ -548,7 +548,8 @@ struct AugParams {
 };
 
 __host__ __device__ inline size_t aug_team_bytes(int lcap) {
-  return align16(((size_t)lcap + 16) * sizeof(double)) + align16(((size_t)lcap + 64 + 16) * sizeof(int));
+  return align16(((size_t)lcap + 16) * sizeof(double)) +
+         align16((2 * (size_t)lcap + 64 + 16) * sizeof(int));
 }
 
 // |A(r, k)| by binary search in CSC column k (0 if structurally absent)
@@ -563,7 +564,8 @@ __device__ void aug_column(const AugParams& P, int c, char* mem, int tid) {
   double* w = reinterpret_cast<double*>(mem);
   double* red = w + P.lcap;
   int* list = reinterpret_cast<int*>(mem + align16(((size_t)P.lcap + 16) * sizeof(double)));
-  int* off = list + P.lcap;  // 64 + 16 ints: misc
+  int* off = list + P.lcap;    // 64 + 16 ints: misc
+  int* keepf = off + 80;       // lcap ints: top-k keep flags
   Team<T> tm{tid, red};
   const int j = P.cols ? P.cols[c] : c;
   const int b0 = P.iptr[j], nb = P.iptr[j + 1] - b0;
@@ -627,10 +629,11 @@ __device__ void aug_column(const AugParams& P, int c, char* mem, int tid) {
         double wt = w[t];
         rank += (wt > wq) || (wt == wq && list[t] < rq);
       }
-      w[q] = rank < room ? 1.0 : -1.0;
+      keepf[q] = rank < room;
     }
     tm.sync();
-    kept = team_compact<T>(list, w, C, tm, off, [](int, int, int, double wv) { return wv >= 0.0; });
+    kept = team_compact<T>(list, w, C, tm, off,
+                           [keepf](int i, int, int, double) { return keepf[i] != 0; });
   }
   if (P.mode == 0) {
     if (tid == 0) P.newsize[j] = nb + kept;

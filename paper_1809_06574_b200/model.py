@@ -68,13 +68,13 @@ class _UnionTerms:
                 self.vals.append(f64(d))
                 self.kinds.append(1)
             else:
-                # slot of every term entry inside the union row
-                pos = np.empty(T.nnz, dtype=np.int64)
-                for i in range(n):
-                    lo, hi = S.indptr[i], S.indptr[i + 1]
-                    tlo, thi = T.indptr[i], T.indptr[i + 1]
-                    if thi > tlo:
-                        pos[tlo:thi] = lo + np.searchsorted(S.indices[lo:hi], T.indices[tlo:thi])
+                # slot of every term entry inside the union pattern: both
+                # patterns are row-major sorted, so global (row, col) keys
+                # are sorted and one searchsorted finds every slot
+                skeys = rows.astype(np.int64) * n + S.indices
+                tkeys = (np.repeat(np.arange(n, dtype=np.int64), np.diff(T.indptr)) * n
+                         + T.indices)
+                pos = np.searchsorted(skeys, tkeys)
                 full = np.zeros(S.nnz)
                 full[pos] = T.data
                 self.vals.append(f64(full))
