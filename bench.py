@@ -191,8 +191,9 @@ def run_ours(args):
     clk.start()
     step_ms = []
     infos = []
-    dominant = ("pmp_ls_columns", "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm")
-    _abi.count_launches(True, timed=dominant)
+    dominant = ("pmp_ls_columns", "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm",
+                "pmp_copy_cols", "pmp_axpby_cols", "pmp_assemble", "pmp_permute")
+    _abi.count_launches(True)
     recs_all = None
     for k in range(args.steps):
         flush.zero_()
@@ -207,10 +208,23 @@ def run_ours(args):
         infos.append(info)
         recs_all = recs
     launches = _abi.launches()
-    timed = _abi.timed_events()
     counters = dict(_abi.COUNTERS)
     _abi.count_launches(False)
     clocks = clk.stop()
+    # one extra, untimed step with CUDA events around every launch of the
+    # candidate kernels (per-kernel device time and share of the step)
+    flush.zero_()
+    barrier()
+    _abi.count_launches(True, timed=dominant)
+    i0 = torch.cuda.Event(enable_timing=True)
+    i1 = torch.cuda.Event(enable_timing=True)
+    i0.record()
+    step()
+    i1.record()
+    barrier()
+    instr_ms = i0.elapsed_time(i1)
+    timed = dict(_abi.timed_events())
+    _abi.count_launches(False)
     t_local = float(np.sum(step_ms))
     t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -224,7 +238,8 @@ def run_ours(args):
     for name, lst in timed.items():
         ms = [a.elapsed_time(b) for a, b, _ in lst]
         kern[name] = {"launches": len(ms), "total_ms": float(np.sum(ms)),
-                      "avg_us": float(np.mean(ms) * 1e3) if ms else 0.0}
+                      "avg_us": float(np.mean(ms) * 1e3) if ms else 0.0,
+                      "share_of_step": float(np.sum(ms)) / instr_ms}
     build_s = float(np.mean([i["build_s"] for i in infos]))
     solve_s = float(np.mean([i["solve_s"] for i in infos]))
     asm_s = float(np.mean([i["assemble_s"] for i in infos]))
@@ -258,6 +273,8 @@ def run_ours(args):
                            "mean": float(np.mean(iters))},
             "converged": conv,
             "gpu_launches": int(launches),
+            "gpu_launches_per_step": int(launches) // args.steps,
+            "abi_calls": counters,
             "kernels": kern,
             "roofline": roof,
             "clocks": clocks,
@@ -298,7 +315,8 @@ def roofline(kern, timed, n, W, model):
         return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": None,
                 "peak_source": which + " (MEASURED_PEAKS.json hbm_gbs)",
-                "share_of_step": None}
+                "launches": len(lst), "avg_us": kern[name]["avg_us"],
+                "share_of_step": kern[name]["share_of_step"]}
     # LS kernel: FP64 flops of the Householder solves
     fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
     return {"kernel": name, "bound": "fp64", "achieved": None, "peak": fp64_peak,

@@ -193,6 +193,25 @@ int pmp_merge_columns(int n, const int32_t* d_base_ptr, const int32_t* d_base_id
                       const int32_t* d_out_ptr, int32_t* d_out_idx, double* d_out_coef,
                       void* stream);
 
+/* ---- host-side small dense algebra of block GCRO (no device) -----------
+ * Rank-revealing QR of the mz x mz TSQR factor rt (row-major, upper): LAPACK
+ * geqp3 semantics with exact column norms; rank = #{|R_kk| > tol |R_00|}
+ * (krylov.py:89-95).  Writes T (mz x rank, row-major) = Pi R11^-1, so the
+ * orthonormal block is Z T, and Rout (rank x mz rows of an mz x mz
+ * row-major buffer) = R[:rank] un-pivoted; *cond = |R_00| / |R_{r-1,r-1}|. */
+int pmp_host_deflate(int mz, const double* h_rt, double tol, int* h_rank, double* h_T,
+                     double* h_Rout, double* h_cond);
+/* Incremental Householder QR least squares for min ||rhs - G Y||
+ * (krylov.py:204-212): appends nnew columns (nrows x nnew, column-major) to
+ * the factorisation held in h_QR (ldq x ldq column-major), h_tau, h_ext,
+ * applies the new reflectors to h_C (ldq x nrhs, column-major, = Q^T rhs),
+ * and writes Y ((ncols_old + nnew) x nrhs, column-major) and the residual
+ * norms.  Returns 1 when R is (near) rank deficient (caller falls back to
+ * a minimum-norm solve). */
+int pmp_host_hls_append(int ldq, int nrhs, int ncols_old, int nnew, int nrows,
+                        const double* h_newcols, double* h_QR, double* h_tau, int* h_ext,
+                        double* h_C, double* h_Y, double* h_resnorm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,9 @@ _SIGS = {
     "pmp_merge_columns": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
                           c_int),
     "pmp_merge_sizes": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                             c_vp, c_vp], c_int),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -117,7 +120,7 @@ def stream():
 _LAUNCHES_PER_CALL = {"pmp_scan": 2, "pmp_transpose": 5, "pmp_pattern_l0": 5,
                       "pmp_pattern_l0_ptr": 3, "pmp_compact_zeros": 4, "pmp_select_gt": 4,
                       "pmp_augment": 1}
-_NO_LAUNCH = {"pmp_last_error", "pmp_version"}
+_NO_LAUNCH = {"pmp_last_error", "pmp_version", "pmp_host_deflate", "pmp_host_hls_append"}
 
 COUNTERS = {}          # name -> calls (enabled by count_launches())
 _counting = False

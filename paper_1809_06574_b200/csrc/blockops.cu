@@ -99,17 +99,25 @@ __global__ void __launch_bounds__(256) k_gram(int n, int kv, const double* __res
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // fixed-order sum over the block partials with 8 independent chains
+  // (b mod 8) so the L2 loads overlap; combined in a fixed tree
+  const int nb = gridDim.x;
   for (int o = tid; o < K; o += 256) {
-    double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(partial + (size_t)b * K + o);
-    Gout[o] = s;
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int b = 0;
+    for (; b + 8 <= nb; b += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += __ldcg(partial + (size_t)(b + u) * K + o);
+    }
+    for (int u = 0; b + u < nb; ++u) a[u] += __ldcg(partial + (size_t)(b + u) * K + o);
+    Gout[o] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
   if (tid == 0) *ticket = 0u;
 }
 
 static int gram_blocks(int n) {
-  int nb = ceil_div(n, 128);
-  if (nb > 296) nb = 296;
+  int nb = ceil_div(n, 1024);
+  if (nb > 148) nb = 148;
   if (nb < 1) nb = 1;
   return nb;
 }
@@ -285,6 +293,143 @@ static void tsqr_geometry(int n, int nz, int* nb, int* chunk, int* sub) {
 
 static size_t tsqr_smem(int nz, int sub) { return sizeof(double) * (64 + (size_t)(nz + sub) * nz); }
 
+// ---------------------------------------------------------------------------
+// 5c' TSQR for nz <= 16 in registers: lane = row of a 32-row tile.  A warp
+// keeps its running R in lanes 0..nz-1 and streams (32 - nz) new rows into
+// lanes nz..31 per tile; one Householder QR of the tile (shfl reductions)
+// leaves the new R on top.  Warp R's are combined pairwise (2 nz <= 32 rows
+// per QR) in a fixed tree inside the block, and the last block combines the
+// block R's the same way, so the result is deterministic.
+// ---------------------------------------------------------------------------
+
+template <int NZ>
+__device__ __forceinline__ void warp_house_qr(double (&a)[NZ], int nz, int lane) {
+#pragma unroll
+  for (int k = 0; k < NZ; ++k) {
+    if (k >= nz) break;
+    const double x = (lane > k) ? a[k] : 0.0;
+    const double xn2 = warp_sum(x * x);
+    const double alpha = __shfl_sync(0xffffffffu, a[k], k);
+    if (xn2 == 0.0) continue;
+    const double beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+    const double tau = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    const double v = (lane > k) ? a[k] * scal : (lane == k ? 1.0 : 0.0);
+#pragma unroll
+    for (int j = k + 1; j < NZ; ++j) {
+      if (j >= nz) break;
+      const double w = warp_sum(v * a[j]);
+      if (lane >= k) a[j] -= tau * w * v;
+    }
+    if (lane == k)
+      a[k] = beta;
+    else if (lane > k)
+      a[k] = 0.0;
+  }
+}
+
+// stack R (lanes 0..nz-1, in registers) on top of the R stored row-major at
+// src (loaded into lanes nz..2nz-1) and re-triangularise
+template <int NZ>
+__device__ __forceinline__ void warp_combine(double (&a)[NZ], int nz, int lane, const double* src) {
+  if (lane >= nz && lane < 2 * nz) {
+#pragma unroll
+    for (int c = 0; c < NZ; ++c)
+      if (c < nz) a[c] = src[(lane - nz) * nz + c];
+  } else if (lane >= 2 * nz) {
+#pragma unroll
+    for (int c = 0; c < NZ; ++c) a[c] = 0.0;
+  }
+  warp_house_qr<NZ>(a, nz, lane);
+}
+
+template <int NZ>
+__device__ __forceinline__ void warp_store_R(const double (&a)[NZ], int nz, int lane, double* dst) {
+  if (lane < nz) {
+#pragma unroll
+    for (int c = 0; c < NZ; ++c)
+      if (c < nz) dst[lane * nz + c] = (c >= lane) ? a[c] : 0.0;
+  }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(256) k_tsqr_warp(int n, int nz, const double* __restrict__ Z,
+                                                   int ldz, int chunk, double* partial,
+                                                   unsigned* ticket, double* Rout) {
+  __shared__ double sR[8][NZ * NZ];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double a[NZ];
+#pragma unroll
+  for (int c = 0; c < NZ; ++c) a[c] = 0.0;
+  // rows of this block, split evenly over its 8 warps
+  const int b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+  const int per = (b1 - b0 + 7) / 8;
+  const int r0 = min(b1, b0 + wid * per), r1 = min(b1, r0 + per);
+  const int fresh = 32 - nz;
+  for (int base = r0; base < r1; base += fresh) {
+    if (lane >= nz) {
+      const int row = base + lane - nz;
+      if (row < r1) {
+        const double* zr = Z + (size_t)row * ldz;
+#pragma unroll
+        for (int c = 0; c < NZ; ++c) a[c] = (c < nz) ? zr[c] : 0.0;
+      } else {
+#pragma unroll
+        for (int c = 0; c < NZ; ++c) a[c] = 0.0;
+      }
+    }
+    warp_house_qr<NZ>(a, nz, lane);
+  }
+  warp_store_R<NZ>(a, nz, lane, sR[wid]);
+  __syncthreads();
+  // tree over the 8 warps: 0+1, 2+3, ... then 0+2, 4+6, then 0+4
+  for (int step = 1; step < 8; step <<= 1) {
+    if ((wid % (2 * step)) == 0) {
+      warp_combine<NZ>(a, nz, lane, sR[wid + step]);
+      warp_store_R<NZ>(a, nz, lane, sR[wid]);
+    }
+    __syncthreads();
+  }
+  double* mine = partial + (size_t)blockIdx.x * nz * nz;
+  for (int q = threadIdx.x; q < nz * nz; q += blockDim.x) mine[q] = sR[0][q];
+  __threadfence();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last block: warp w folds block partials w, w+8, w+16, ... in order,
+  // then the same fixed tree over the 8 warps
+  const int nb = gridDim.x;
+#pragma unroll
+  for (int c = 0; c < NZ; ++c) a[c] = 0.0;
+  for (int b = wid; b < nb; b += 8) {
+    // stage partial b in the warp's smem slot, then combine
+    for (int q = lane; q < nz * nz; q += 32) sR[wid][q] = __ldcg(partial + (size_t)b * nz * nz + q);
+    __syncwarp();
+    warp_combine<NZ>(a, nz, lane, sR[wid]);
+    __syncwarp();
+  }
+  warp_store_R<NZ>(a, nz, lane, sR[wid]);
+  __syncthreads();
+  for (int step = 1; step < 8; step <<= 1) {
+    if ((wid % (2 * step)) == 0) {
+      warp_combine<NZ>(a, nz, lane, sR[wid + step]);
+      warp_store_R<NZ>(a, nz, lane, sR[wid]);
+    }
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < nz * nz; q += blockDim.x) Rout[q] = sR[0][q];
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+static int tsqr_warp_blocks(int n) {
+  int nb = ceil_div(n, 8 * 32 * 4);
+  if (nb > 148) nb = 148;
+  if (nb < 1) nb = 1;
+  return nb;
+}
+
 }  // namespace pmp
 
 using namespace pmp;
@@ -375,6 +520,8 @@ int pmp_tsmm(int n, int kv, const double* V, int ldv, int nc, const double* H, d
 size_t pmp_tsqr_workspace(int n, int nz) {
   int nb, chunk, sub;
   tsqr_geometry(n, nz, &nb, &chunk, &sub);
+  int nbw = tsqr_warp_blocks(n);
+  if (nbw > nb) nb = nbw;
   return 256 + sizeof(double) * (size_t)nb * nz * nz;
 }
 
@@ -387,6 +534,17 @@ int pmp_tsqr_r(int n, int nz, const double* Z, int ldz, double* R, void* ws, siz
   if (bytes < pmp_tsqr_workspace(n, nz)) {
     set_error("pmp_tsqr_r: workspace too small");
     return PMP_ERR_WORKSPACE;
+  }
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(st);
+  if (nz <= 16) {
+    int nb = tsqr_warp_blocks(n);
+    int chunk = ceil_div(n > 0 ? n : 1, nb);
+    double* partial = (double*)((char*)ws + 256);
+    if (nz <= 8)
+      k_tsqr_warp<8><<<nb, 256, 0, stream>>>(n, nz, Z, ldz, chunk, partial, (unsigned*)ws, R);
+    else
+      k_tsqr_warp<16><<<nb, 256, 0, stream>>>(n, nz, Z, ldz, chunk, partial, (unsigned*)ws, R);
+    return cuda_status("pmp_tsqr_r");
   }
   int nb, chunk, sub;
   tsqr_geometry(n, nz, &nb, &chunk, &sub);

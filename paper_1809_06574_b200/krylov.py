@@ -8,11 +8,14 @@ Split of the work:
     update, krylov.py:189-196), the R factor of the rank-revealing QR
     (TSQR, krylov.py:88) and the new basis block Q = Z Pi R^-1 (tall-skinny
     multiply), solution / residual / outer-space updates (krylov.py:221-269);
-  * the tiny dense algebra stays on the host exactly as in the reference:
-    the pivoted QR of the s x s R factor (scipy geqp3, krylov.py:88), the
-    (k + cap) x (k + m) least-squares problem (numpy gelsd, krylov.py:211)
-    and every control-flow decision (restart, deflation rank, stopping,
-    breakdown, outer-space fold and truncation: krylov.py:152-271).
+  * the tiny dense algebra stays on the host, in native code
+    (csrc/hostls.cpp): the pivoted QR of the s x s R factor (geqp3
+    semantics, krylov.py:88) and an incremental Householder QR of the
+    (k + total) x (k + m) projected least-squares problem (the reference
+    re-solves it from scratch with gelsd, krylov.py:211; the minimum-norm
+    gelsd solve is kept as the fallback for a rank-deficient G), plus every
+    control-flow decision (restart, deflation rank, stopping, breakdown,
+    outer-space fold and truncation: krylov.py:152-271).
 One small device->host copy (a few KB) per block step carries all the
 small matrices the host needs; n-sized data never leaves HBM.
 """
@@ -86,19 +89,24 @@ _REORTH_COND = 1e3
 
 
 class _Dev:
-    """Device buffers and kernel wrappers for one block solve."""
+    """Device buffers and direct ctypes handles for one block solve (the
+    inner loop issues ~15 library calls per block step, so the per-call
+    Python overhead is kept to a plain ctypes call)."""
 
     def __init__(self, n, s, cap, kc):
         self.n, self.s, self.cap, self.kc = n, s, cap, kc
         dev = _dev()
-        f = lambda *shape: torch.empty(*shape, dtype=torch.float64, device=dev)
-        self.V = f(max(n * cap, 1))
-        self.C = f(max(n * kc, 1))
-        self.U = f(max(n * kc, 1))
-        self.bufs = {name: f(max(n * s, 1)) for name in
+        f = lambda size: torch.empty(max(size, 1), dtype=torch.float64, device=dev)
+        self.V = f(n * cap)
+        self.C = f(n * kc)
+        self.U = f(n * kc)
+        self.bufs = {name: f(n * s) for name in
                      ("W", "T0", "T1", "T2", "Z", "dX", "Xa", "Rb", "Q")}
-        self.w1 = f(max(n, 1))
-        self.z1 = f(max(n, 1))
+        self.w1 = f(n)
+        self.z1 = f(n)
+        self.ptr = {k: v.data_ptr() for k, v in self.bufs.items()}
+        for name in ("V", "C", "U", "w1", "z1"):
+            self.ptr[name] = getattr(self, name).data_ptr()
         # small device matrices, fetched to the host in one copy
         self.off = {}
         o = 0
@@ -112,44 +120,68 @@ class _Dev:
         self.hin = torch.empty(o, dtype=torch.float64, pin_memory=True)
         self.hm_np = self.hm.numpy()
         self.hin_np = self.hin.numpy()
+        self.smbase = self.sm.data_ptr()
+        self.smp_ = {k: self.smbase + 8 * v for k, v in self.off.items()}
         sc = scratch()
         self.gram_ws = sc.get("gram", _abi.lib().pmp_gram_workspace(n, cap + kc, s), zero=True)
         self.tsqr_ws = sc.get("tsqr", _abi.lib().pmp_tsqr_workspace(n, s), zero=True)
+        self.gws, self.gwb = self.gram_ws.data_ptr(), self.gram_ws.numel()
+        self.tws, self.twb = self.tsqr_ws.data_ptr(), self.tsqr_ws.numel()
         self.st = _abi.stream()
+        self.cstream = torch.cuda.current_stream()
+        L = _abi.lib()
+        self.f_gram, self.f_tsmm, self.f_tsqr = L.pmp_gram, L.pmp_tsmm, L.pmp_tsqr_r
+        self.f_copy, self.f_axpby = L.pmp_copy_cols, L.pmp_axpby_cols
+        self.f_defl, self.f_hls = L.pmp_host_deflate, L.pmp_host_hls_append
+        self.counting = _abi._counting
+        self.timing = _abi._timing_names
         self.launches = 0
+        # host scratch for the deflation helper
+        self.h_rank = np.zeros(1, dtype=np.int32)
+        self.h_cond = np.zeros(1)
+        self.h_T = np.zeros(s * s)
+        self.h_R = np.zeros(s * s)
+
+    def _call(self, name, fn, *args):
+        if self.timing and name in self.timing:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            rc = fn(*args)
+            b.record()
+            _abi._timed.setdefault(name, []).append((a, b, args))
+        else:
+            rc = fn(*args)
+        if rc:
+            _abi.check(rc, name)
+        self.launches += 1
+        if self.counting:
+            _abi.COUNTERS[name] = _abi.COUNTERS.get(name, 0) + 1
 
     def p(self, name, col=0):
-        """Pointer to a buffer (optionally offset by `col` doubles)."""
-        t = self.bufs[name] if name in self.bufs else getattr(self, name)
-        return t.data_ptr() + 8 * col
+        return self.ptr[name] + 8 * col
 
     def smp(self, name):
-        return self.sm.data_ptr() + 8 * self.off[name]
+        return self.smp_[name]
 
     def gram(self, Vp, ldv, kv, Wp, ldw, nw, out):
         if kv == 0 or nw == 0:
             return
-        _abi.call("pmp_gram", self.n, kv, Vp, ldv, nw, Wp, ldw, self.smp(out),
-                  _abi.ptr(self.gram_ws), self.gram_ws.numel(), self.st)
-        self.launches += 1
+        self._call("pmp_gram", self.f_gram, self.n, kv, Vp, ldv, nw, Wp, ldw, self.smp_[out], self.gws,
+                             self.gwb, self.st)
 
     def tsmm(self, Vp, ldv, kv, Hp, nc, alpha, beta, Op, ldo):
         if nc == 0:
             return
         if kv == 0:
             if beta == 0.0:
-                _abi.call("pmp_axpby_cols", self.n, nc, 0.0, Op, ldo, None, 0.0, Op, ldo, None,
-                          self.st)
-                self.launches += 1
+                self._call("pmp_axpby_cols", self.f_axpby, self.n, nc, 0.0, Op, ldo, None, 0.0, Op, ldo, None,
+                                      self.st)
             return
-        _abi.call("pmp_tsmm", self.n, kv, Vp, ldv, nc, Hp, float(alpha), float(beta), Op, ldo,
-                  self.st)
-        self.launches += 1
+        self._call("pmp_tsmm", self.f_tsmm, self.n, kv, Vp, ldv, nc, Hp, alpha, beta, Op, ldo, self.st)
 
     def tsqr(self, Zp, ldz, nz):
-        _abi.call("pmp_tsqr_r", self.n, nz, Zp, ldz, self.smp("RT"), _abi.ptr(self.tsqr_ws),
-                  self.tsqr_ws.numel(), self.st)
-        self.launches += 1
+        self._call("pmp_tsqr_r", self.f_tsqr, self.n, nz, Zp, ldz, self.smp_["RT"], self.tws, self.twb, self.st)
 
     def put(self, name, arr):
         """Stage a small host matrix into the device small buffer."""
@@ -157,53 +189,42 @@ class _Dev:
         o = self.off[name]
         self.hin_np[o:o + a.size] = a
         self.sm[o:o + a.size].copy_(self.hin[o:o + a.size], non_blocking=True)
-        return self.smp(name)
+        return self.smp_[name]
 
-    def fetch(self):
-        self.hm.copy_(self.sm, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+    def fetch(self, upto=None):
+        if upto is None:
+            self.hm.copy_(self.sm, non_blocking=True)
+        else:
+            e = self.off[upto[0]] + upto[1]
+            self.hm[:e].copy_(self.sm[:e], non_blocking=True)
+        self.cstream.synchronize()
 
     def get(self, name, rows, cols):
         o = self.off[name]
-        return self.hm_np[o:o + rows * cols].reshape(rows, cols).copy()
+        return self.hm_np[o:o + rows * cols].reshape(rows, cols)
 
     def copy_cols(self, nc, src, lds, sc, dst, ldd, dc):
-        _abi.call("pmp_copy_cols", self.n, nc, src, lds, _abi.ptr(sc), dst, ldd, _abi.ptr(dc),
-                  self.st)
-        self.launches += 1
+        self._call("pmp_copy_cols", self.f_copy, self.n, nc, src, lds, sc, dst, ldd, dc, self.st)
 
     def axpby(self, nc, alpha, src, lds, sc, beta, dst, ldd, dc):
-        _abi.call("pmp_axpby_cols", self.n, nc, float(alpha), src, lds, _abi.ptr(sc),
-                  float(beta), dst, ldd, _abi.ptr(dc), self.st)
-        self.launches += 1
-
-
-def _deflate(D, Zp, ldz, mz, outp, ldo, tol, report):
-    """Rank-revealing QR of the n x mz block at Zp (krylov.py:79-95):
-    device TSQR R factor, host pivoted QR of R (geqp3), device
-    Q = Z Pi R11^-1 written to outp.  Returns (rank, R[:rank] un-pivoted)."""
-    if mz == 0:
-        return 0, np.zeros((0, 0))
-    D.tsqr(Zp, ldz, mz)
-    D.fetch()
-    return _deflate_finish(D, Zp, ldz, mz, outp, ldo, tol, report)
+        self._call("pmp_axpby_cols", self.f_axpby, self.n, nc, alpha, src, lds, sc, beta, dst, ldd, dc, self.st)
 
 
 def _deflate_finish(D, Zp, ldz, mz, outp, ldo, tol, report):
-    RT = np.triu(D.get("RT", mz, mz))
-    Qs, Rs, piv = scipy.linalg.qr(RT, mode="economic", pivoting=True)
-    d = np.abs(np.diag(Rs))
-    if d.size == 0 or d[0] == 0.0:
+    """Rank-revealing QR of the n x mz block at Zp (krylov.py:79-95) from its
+    TSQR factor (already fetched): host pivoted QR of R, then on the device
+    Q = Z Pi R11^-1 written to outp.  Returns (rank, R[:rank] un-pivoted)."""
+    RT = np.ascontiguousarray(np.triu(D.get("RT", mz, mz)))
+    rc = D.f_defl(mz, RT.ctypes.data, float(tol), D.h_rank.ctypes.data, D.h_T.ctypes.data,
+                  D.h_R.ctypes.data, D.h_cond.ctypes.data)
+    if rc:
+        _abi.check(rc, "pmp_host_deflate")
+    r = int(D.h_rank[0])
+    if r == 0:
         return 0, np.zeros((0, mz))
-    r = int(np.sum(d > tol * d[0]))
-    inv = np.empty_like(piv)
-    inv[piv] = np.arange(piv.size)
-    Rout = Rs[:r][:, inv]
-    R11 = Rs[:r, :r]
-    Rinv = scipy.linalg.solve_triangular(R11, np.eye(r), lower=False)
-    T = np.zeros((mz, r))
-    T[piv[:r], :] = Rinv
-    if d[0] / d[r - 1] > _REORTH_COND:
+    Rout = D.h_R[:r * mz].reshape(r, mz).copy()
+    T = D.h_T[:mz * r]
+    if D.h_cond[0] > _REORTH_COND:
         # Q1 = Z T, then one Cholesky-QR pass restores orthogonality:
         # Q = Q1 R2^-1, R = R2 R
         D.tsmm(Zp, ldz, mz, D.put("T", T), r, 1.0, 0.0, D.p("Q"), D.s)
@@ -221,7 +242,7 @@ def _deflate_finish(D, Zp, ldz, mz, outp, ldo, tol, report):
 
 def _colnorms(D, Wp, ldw, nw):
     D.gram(Wp, ldw, nw, Wp, ldw, nw, "NRM")
-    D.fetch()
+    D.fetch(("NRM", nw * nw))
     g = np.diag(D.get("NRM", nw, nw)).copy()
     return np.sqrt(np.maximum(g, 0.0))
 
@@ -251,6 +272,67 @@ def block_gcro_solve(A, B, P=None, cfg=None):
     return (X.cpu().numpy() if host_out else X), report
 
 
+class _Projected:
+    """The projected least-squares problem of one cycle (krylov.py:171-212),
+    factorised incrementally on the host (pmp_host_hls_append)."""
+
+    def __init__(self, D, k, cap, na, rhs_c, S0, bs):
+        self.D = D
+        self.k, self.na = k, na
+        self.ldq = k + cap
+        self.QR = np.zeros((self.ldq, self.ldq), order="F")
+        self.tau = np.zeros(self.ldq)
+        self.ext = np.zeros(self.ldq, dtype=np.int32)
+        self.C = np.zeros((self.ldq, na), order="F")
+        self.C[:k] = rhs_c
+        self.C[k:k + bs] = S0
+        self.rhs0 = self.C.copy()
+        self.ncols = 0
+        self.Y = np.zeros((na, self.ldq))
+        self.res = np.zeros(na)
+
+    def append(self, Bmat, Hb, q0, q1, total, m):
+        """Append the block columns q0:q1 of G (rows k + total); returns
+        (Y, residual norms) of min ||rhs - G Y||."""
+        k = self.k
+        nrows = k + total
+        sb = q1 - q0
+        first = self.ncols == 0
+        nnew = (k + sb) if first else sb
+        cols = np.zeros((nrows, nnew), order="F")
+        o = 0
+        if first:
+            cols[:k, :k] = np.eye(k)
+            o = k
+        if k:
+            cols[:k, o:o + sb] = Bmat[:, q0:q1]
+        cols[k:, o:o + sb] = Hb[:total, q0:q1]
+        n1 = self.ncols + nnew
+        rc = self.D.f_hls(self.ldq, self.na, self.ncols, nnew, nrows, cols.ctypes.data,
+                          self.QR.ctypes.data, self.tau.ctypes.data, self.ext.ctypes.data,
+                          self.C.ctypes.data, self.Y.ctypes.data, self.res.ctypes.data)
+        self.ncols = n1
+        Y = self.Y.ravel()[:n1 * self.na].reshape(self.na, n1).T.copy()
+        if rc == 1:
+            # (near) rank-deficient G: the reference's minimum-norm gelsd
+            G = _build_G(k, Bmat, Hb, total, m)
+            rhs = self.rhs0[:nrows]
+            Y, _, _, _ = np.linalg.lstsq(G, rhs, rcond=None)
+            return Y, np.linalg.norm(rhs - G @ Y, axis=0)
+        if rc:
+            _abi.check(rc, "pmp_host_hls_append")
+        return Y, self.res.copy()
+
+
+def _build_G(k, Bmat, Hb, total, m):
+    G = np.zeros((k + total, k + m))
+    if k:
+        G[:k, :k] = np.eye(k)
+        G[:k, k:] = Bmat[:, :m]
+    G[k:, k:] = Hb[:total, :m]
+    return G
+
+
 def _solve(A, B, P, cfg):
     n, s = B.shape
     t_start = time.perf_counter()
@@ -258,7 +340,6 @@ def _solve(A, B, P, cfg):
     cap = cfg.inner_restart + 2 * s + 2
     kc = cfg.outer_space_dim + s
     D = _Dev(n, s, cap, kc)
-    st = D.st
     dev = _dev()
     X = torch.zeros(n, s, dtype=torch.float64, device=dev)
     Xt = torch.zeros(n, s, dtype=torch.float64, device=dev)
@@ -270,78 +351,83 @@ def _solve(A, B, P, cfg):
     active = np.flatnonzero(bnorms > 0)
     prev_norms = bnorms.copy()     # ||R[:, j]|| as of the last true residual
     tmp = [D.bufs["T0"], D.bufs["T1"]]
+    chain = P.factors() if P is not None else []
+    spmm = _abi.lib().pmp_spmm
+    T2 = D.p("T2")
 
     def op(Vp, ldv, sb, Wp):
-        if P is not None:
-            P.apply_dev(Vp, ldv, sb, D.p("T2"), s, tmp)
+        # W = A P V: the preconditioner chain right to left, then A
+        # (krylov.py:140-147; spai.py:82-89)
+        src, lds = Vp, ldv
+        for i, F in enumerate(reversed(chain)):
+            dst = T2 if i == len(chain) - 1 else D.p("T%d" % (i % 2))
+            st = F.structure
+            D._call("pmp_spmm", spmm, st.n, st.rowptr.data_ptr(), st.colidx.data_ptr(), F.vals.data_ptr(), sb,
+                       src, lds, 1.0, 0.0, None, 0, dst, s, D.st)
+            src, lds = dst, s
+        st = A.structure
+        D._call("pmp_spmm", spmm, st.n, st.rowptr.data_ptr(), st.colidx.data_ptr(), A.vals.data_ptr(), sb,
+                   src, lds, 1.0, 0.0, None, 0, Wp, s, D.st)
+        if chain:
             report.precond_apply_count += sb
-            A.spmm(D.p("T2"), s, sb, Wp, s)
-        else:
-            A.spmm(Vp, ldv, sb, Wp, s)
         report.matvec_count += sb
 
     k = 0          # outer-space dimension (columns of C / U in use)
     while active.size and report.iterations < cfg.max_iters:
         na = active.size
         act_dev = torch.as_tensor(active.astype(np.int32), device=dev)
+        act_p = act_dev.data_ptr()
         start_rel = _safe_rel(prev_norms[active], bnorms[active])
-        # Ract -> Z buffer (n x na, ld s)
-        D.copy_cols(na, Rp, s, act_dev, D.p("Z"), s, None)
+        # Ract -> Z buffer (n x na, ld s);  Z0 = Ract - C (C^T Ract)
+        D.copy_cols(na, Rp, s, act_p, D.p("Z"), s, None)
         if k:
             D.gram(D.p("C"), kc, k, D.p("Z"), s, na, "G1")
             D.tsmm(D.p("C"), kc, k, D.smp("G1"), na, -1.0, 1.0, D.p("Z"), s)
         D.tsqr(D.p("Z"), s, na)
         D.fetch()
-        rhs_c = D.get("G1", k, na) if k else np.zeros((0, na))
+        rhs_c = D.get("G1", k, na).copy() if k else np.zeros((0, na))
         bs, S0 = _deflate_finish(D, D.p("Z"), s, na, D.p("V"), cap, cfg.deflation_tol, report)
         if bs == 0:
             raise SolverBreakdown(
                 "projected residual block vanished with %d unconverged column(s)" % na)
         Hb = np.zeros((cap, cap))
         Bmat = np.zeros((k, cap))
-        rhs_v = np.zeros((cap, na))
-        rhs_v[:bs] = S0
+        proj = _Projected(D, k, cap, na, rhs_c, S0, bs)
         m = 0
         total = bs
         Y = None
-        G = None
         exhausted = False
         cycle_converged = False
+        bn_act = bnorms[active]
+        Wp = D.p("W")
+        Vp = D.p("V")
+        Cp = D.p("C")
         while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
                and m < cfg.inner_restart):
             q0, q1 = m, total
             sb = q1 - q0
-            Wp = D.p("W")
             op(D.p("V", q0), cap, sb, Wp)
             report.iterations += 1
             if k:
-                D.gram(D.p("C"), kc, k, Wp, s, sb, "G1")
-                D.tsmm(D.p("C"), kc, k, D.smp("G1"), sb, -1.0, 1.0, Wp, s)
-            D.gram(D.p("V"), cap, total, Wp, s, sb, "G2")
-            D.tsmm(D.p("V"), cap, total, D.smp("G2"), sb, -1.0, 1.0, Wp, s)
-            D.gram(D.p("V"), cap, total, Wp, s, sb, "G3")
-            D.tsmm(D.p("V"), cap, total, D.smp("G3"), sb, -1.0, 1.0, Wp, s)
+                D.gram(Cp, kc, k, Wp, s, sb, "G1")
+                D.tsmm(Cp, kc, k, D.smp("G1"), sb, -1.0, 1.0, Wp, s)
+            D.gram(Vp, cap, total, Wp, s, sb, "G2")
+            D.tsmm(Vp, cap, total, D.smp("G2"), sb, -1.0, 1.0, Wp, s)
+            D.gram(Vp, cap, total, Wp, s, sb, "G3")
+            D.tsmm(Vp, cap, total, D.smp("G3"), sb, -1.0, 1.0, Wp, s)
             D.tsqr(Wp, s, sb)
-            D.fetch()
+            D.fetch(("RT", sb * sb))
             if k:
                 Bmat[:, q0:q1] = D.get("G1", k, sb)
             Hb[:total, q0:q1] += D.get("G2", total, sb)
             Hb[:total, q0:q1] += D.get("G3", total, sb)
-            bs_next, Rn = _deflate_finish(D, Wp, s, sb, D.p("V", total), cap, cfg.deflation_tol,
-                                          report)
+            bs_next, Rn = _deflate_finish(D, Wp, s, sb, D.p("V", total), cap,
+                                          cfg.deflation_tol, report)
             Hb[total:total + bs_next, q0:q1] = Rn
             m = total
             total += bs_next
-
-            rows_v = total
-            G = np.zeros((k + rows_v, k + m))
-            if k:
-                G[:k, :k] = np.eye(k)
-                G[:k, k:] = Bmat[:, :m]
-            G[k:, k:] = Hb[:rows_v, :m]
-            rhs = np.vstack([rhs_c, rhs_v[:rows_v]])
-            Y, _, _, _ = np.linalg.lstsq(G, rhs, rcond=None)
-            est = _safe_rel(np.linalg.norm(rhs - G @ Y, axis=0), bnorms[active])
+            Y, rn = proj.append(Bmat, Hb, q0, q1, total, m)
+            est = _safe_rel(rn, bn_act)
             last_rel[active] = est
             report.residual_history.append(last_rel.copy())
             cycle_converged = bool(np.all(est <= cfg.tol))
@@ -351,26 +437,26 @@ def _solve(A, B, P, cfg):
             break
 
         # dXt = V Y_v + U Y_u ; Xt[:, active] += dXt     (krylov.py:221-224)
-        D.tsmm(D.p("V"), cap, m, D.put("H", Y[k:]), na, 1.0, 0.0, D.p("dX"), s)
+        D.tsmm(Vp, cap, m, D.put("H", Y[k:]), na, 1.0, 0.0, D.p("dX"), s)
         if k:
             D.tsmm(D.p("U"), kc, k, D.put("G1", Y[:k]), na, 1.0, 1.0, D.p("dX"), s)
-        D.axpby(na, 1.0, D.p("dX"), s, None, 1.0, Xtp, s, act_dev)
+        D.axpby(na, 1.0, D.p("dX"), s, None, 1.0, Xtp, s, act_p)
         # X = P Xt ; R = B - A X                          (krylov.py:225-233)
-        D.copy_cols(na, Xtp, s, act_dev, D.p("Z"), s, None)
+        D.copy_cols(na, Xtp, s, act_p, D.p("Z"), s, None)
         if P is not None:
             P.apply_dev(D.p("Z"), s, na, D.p("Xa"), s, tmp)
             report.precond_apply_count += na
             xa = D.p("Xa")
         else:
             xa = D.p("Z")
-        D.copy_cols(na, xa, s, None, Xp, s, act_dev)
-        D.copy_cols(na, Bp, s, act_dev, D.p("Rb"), s, None)
+        D.copy_cols(na, xa, s, None, Xp, s, act_p)
+        D.copy_cols(na, Bp, s, act_p, D.p("Rb"), s, None)
         A.spmm(xa, s, na, D.p("Rb"), s, alpha=-1.0, beta=1.0, Y0=D.p("Rb"), ldy0=s)
         report.matvec_count += na
-        D.copy_cols(na, D.p("Rb"), s, None, Rp, s, act_dev)
+        D.copy_cols(na, D.p("Rb"), s, None, Rp, s, act_p)
         tn = _colnorms(D, D.p("Rb"), s, na)
         prev_norms[active] = tn
-        true_rel = _safe_rel(tn, bnorms[active])
+        true_rel = _safe_rel(tn, bn_act)
         last_rel[active] = true_rel
         report.residual_history.append(last_rel.copy())
 
@@ -383,10 +469,11 @@ def _solve(A, B, P, cfg):
         # fold the cycle's directions into the outer space (krylov.py:244-269);
         # skipped when no further cycle can run -- (U, C) are never read again
         if np.any(still) and report.iterations < cfg.max_iters:
+            G = _build_G(k, Bmat, Hb, total, m)
             img = G @ Y
-            D.tsmm(D.p("V"), cap, total, D.put("H", img[k:]), na, 1.0, 0.0, D.p("Rb"), s)
+            D.tsmm(Vp, cap, total, D.put("H", img[k:]), na, 1.0, 0.0, D.p("Rb"), s)
             if k:
-                D.tsmm(D.p("C"), kc, k, D.put("G1", img[:k]), na, 1.0, 1.0, D.p("Rb"), s)
+                D.tsmm(Cp, kc, k, D.put("G1", img[:k]), na, 1.0, 1.0, D.p("Rb"), s)
             kk = k
             for col in range(na):
                 D.copy_cols(1, D.p("Rb", col), s, None, D.p("w1"), 1, None)
@@ -396,8 +483,8 @@ def _solve(A, B, P, cfg):
                     continue
                 if kk:
                     for _ in range(2):
-                        D.gram(D.p("C"), kc, kk, D.p("w1"), 1, 1, "H1")
-                        D.tsmm(D.p("C"), kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("w1"), 1)
+                        D.gram(Cp, kc, kk, D.p("w1"), 1, 1, "H1")
+                        D.tsmm(Cp, kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("w1"), 1)
                         D.tsmm(D.p("U"), kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("z1"), 1)
                 nw = _colnorms(D, D.p("w1"), 1, 1)[0]
                 if nw <= 1e-10 * w0:
