@@ -160,6 +160,23 @@ size_t pmp_tsqr_workspace(int n, int nz);
 int pmp_tsqr_r(int n, int nz, const double* d_z, int ldz, double* d_r, void* d_ws,
                size_t ws_bytes, void* stream);
 
+/* ---- kernel 5b+5c fused: one block-Arnoldi orthogonalisation step -------
+ * (krylov.py:189-202) in one cooperative launch:
+ *   W -= C (C^T W)  [k > 0];  npass x { H = V^T W; W -= V H }  (npass 0 or 2)
+ *   W = Q R by Cholesky-QR2 with symmetric pivoting; Q written to
+ *   V[:, qout : qout + sb].
+ * Outputs (device): outB = C^T W (k x sb), outH1 / outH2 = the two CGS
+ * coefficient blocks (total x sb), outR (sb x sb, row-major, un-pivoted),
+ * *outFlag = 0.  When the pivoted Cholesky finds min|R_kk|/|R_00| <= 1e-5
+ * (too close to the 1e-12 deflation threshold for Cholesky to decide),
+ * *outFlag = 1, V is untouched and W holds the projected block for the
+ * Householder fallback (pmp_tsqr_r + pmp_host_deflate).  sb <= 16. */
+size_t pmp_orth_workspace(int n, int total_max, int k_max, int sb);
+int pmp_orth_step(int n, const double* d_C, int ldc, int k, double* d_V, int ldv, int total,
+                  int npass, double* d_W, int ldw, int sb, int qout, double* d_outB,
+                  double* d_outH1, double* d_outH2, double* d_outR, double* d_outFlag,
+                  void* d_ws, size_t ws_bytes, void* stream);
+
 /* ---- helpers ------------------------------------------------------------ */
 /* dst[:, dst_cols[c]] = src[:, src_cols[c]] for c < nc (NULL = identity). */
 int pmp_copy_cols(int n, int nc, const double* d_src, int lds, const int32_t* d_src_cols,

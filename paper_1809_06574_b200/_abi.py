@@ -65,6 +65,9 @@ _SIGS = {
     "pmp_merge_columns": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
                           c_int),
     "pmp_merge_sizes": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_orth_workspace": ([c_int, c_int, c_int, c_int], c_sz),
+    "pmp_orth_step": ([c_int, c_vp, c_int, c_int, c_vp, c_int, c_int, c_int, c_vp, c_int, c_int,
+                       c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp, c_vp], c_int),

@@ -63,6 +63,7 @@ class SolveReport:
     precond_apply_count: int = 0
     wall_time: float = 0.0
     reorth_passes: int = 0
+    deflation_fallbacks: int = 0
 
     @property
     def final_residuals(self):
@@ -111,7 +112,7 @@ class _Dev:
         self.off = {}
         o = 0
         for name, size in (("G1", kc * s), ("G2", cap * s), ("G3", cap * s), ("RT", s * s),
-                           ("NRM", s * s), ("H", (cap + kc) * s), ("T", s * s),
+                           ("FLAG", 1), ("NRM", s * s), ("H", (cap + kc) * s), ("T", s * s),
                            ("H1", kc + 1)):
             self.off[name] = o
             o += size
@@ -127,12 +128,17 @@ class _Dev:
         self.tsqr_ws = sc.get("tsqr", _abi.lib().pmp_tsqr_workspace(n, s), zero=True)
         self.gws, self.gwb = self.gram_ws.data_ptr(), self.gram_ws.numel()
         self.tws, self.twb = self.tsqr_ws.data_ptr(), self.tsqr_ws.numel()
+        self.fused = s <= 16
+        if self.fused:
+            self.orth_ws = sc.get("orth", _abi.lib().pmp_orth_workspace(n, cap, kc, s))
+            self.ows, self.owb = self.orth_ws.data_ptr(), self.orth_ws.numel()
         self.st = _abi.stream()
         self.cstream = torch.cuda.current_stream()
         L = _abi.lib()
         self.f_gram, self.f_tsmm, self.f_tsqr = L.pmp_gram, L.pmp_tsmm, L.pmp_tsqr_r
         self.f_copy, self.f_axpby = L.pmp_copy_cols, L.pmp_axpby_cols
         self.f_defl, self.f_hls = L.pmp_host_deflate, L.pmp_host_hls_append
+        self.f_orth = L.pmp_orth_step
         self.counting = _abi._counting
         self.timing = _abi._timing_names
         self.launches = 0
@@ -179,6 +185,15 @@ class _Dev:
                                       self.st)
             return
         self._call("pmp_tsmm", self.f_tsmm, self.n, kv, Vp, ldv, nc, Hp, alpha, beta, Op, ldo, self.st)
+
+    def orth(self, k, total, npass, Wp, sb, qout):
+        """Fused C projection + CGS2 + Cholesky-QR2 (pmp_orth_step).  Returns
+        (rank, R rows) after one fetch, falling back to Householder TSQR +
+        host pivoted QR when the kernel flags a near-deficient block."""
+        self._call("pmp_orth_step", self.f_orth, self.n, self.ptr["C"], self.kc, k,
+                   self.ptr["V"], self.cap, total, npass, Wp, self.s, sb, qout,
+                   self.smp_["G1"], self.smp_["G2"], self.smp_["G3"], self.smp_["RT"],
+                   self.smp_["FLAG"], self.ows, self.owb, self.st)
 
     def tsqr(self, Zp, ldz, nz):
         self._call("pmp_tsqr_r", self.f_tsqr, self.n, nz, Zp, ldz, self.smp_["RT"], self.tws, self.twb, self.st)
@@ -238,6 +253,32 @@ def _deflate_finish(D, Zp, ldz, mz, outp, ldo, tol, report):
         return r, R2 @ Rout
     D.tsmm(Zp, ldz, mz, D.put("T", T), r, 1.0, 0.0, outp, ldo)
     return r, Rout
+
+
+def _project_deflate(D, k, total, npass, Wp, sb, qout, tol, report):
+    """W -= C (C^T W); npass x {W -= V (V^T W)}; rank-revealing QR of W with
+    the orthonormal block written to V[:, qout:] (krylov.py:156-165,
+    :189-202).  C^T W, the two CGS coefficient blocks land in the small
+    buffer slots G1, G2, G3 (fetched)."""
+    s, cap, kc = D.s, D.cap, D.kc
+    if D.fused:
+        D.orth(k, total, npass, Wp, sb, qout)
+        D.fetch(("FLAG", 1))
+        if D.get("FLAG", 1, 1)[0, 0] == 0.0:
+            return sb, D.get("RT", sb, sb).copy()
+        report.deflation_fallbacks += 1
+        D.tsqr(Wp, s, sb)
+        D.fetch(("FLAG", 1))
+        return _deflate_finish(D, Wp, s, sb, D.p("V", qout), cap, tol, report)
+    if k:
+        D.gram(D.p("C"), kc, k, Wp, s, sb, "G1")
+        D.tsmm(D.p("C"), kc, k, D.smp("G1"), sb, -1.0, 1.0, Wp, s)
+    for g in ("G2", "G3")[:npass]:
+        D.gram(D.p("V"), cap, total, Wp, s, sb, g)
+        D.tsmm(D.p("V"), cap, total, D.smp(g), sb, -1.0, 1.0, Wp, s)
+    D.tsqr(Wp, s, sb)
+    D.fetch(("FLAG", 1))
+    return _deflate_finish(D, Wp, s, sb, D.p("V", qout), cap, tol, report)
 
 
 def _colnorms(D, Wp, ldw, nw):
@@ -380,13 +421,8 @@ def _solve(A, B, P, cfg):
         start_rel = _safe_rel(prev_norms[active], bnorms[active])
         # Ract -> Z buffer (n x na, ld s);  Z0 = Ract - C (C^T Ract)
         D.copy_cols(na, Rp, s, act_p, D.p("Z"), s, None)
-        if k:
-            D.gram(D.p("C"), kc, k, D.p("Z"), s, na, "G1")
-            D.tsmm(D.p("C"), kc, k, D.smp("G1"), na, -1.0, 1.0, D.p("Z"), s)
-        D.tsqr(D.p("Z"), s, na)
-        D.fetch()
+        bs, S0 = _project_deflate(D, k, 0, 0, D.p("Z"), na, 0, cfg.deflation_tol, report)
         rhs_c = D.get("G1", k, na).copy() if k else np.zeros((0, na))
-        bs, S0 = _deflate_finish(D, D.p("Z"), s, na, D.p("V"), cap, cfg.deflation_tol, report)
         if bs == 0:
             raise SolverBreakdown(
                 "projected residual block vanished with %d unconverged column(s)" % na)
@@ -408,21 +444,12 @@ def _solve(A, B, P, cfg):
             sb = q1 - q0
             op(D.p("V", q0), cap, sb, Wp)
             report.iterations += 1
-            if k:
-                D.gram(Cp, kc, k, Wp, s, sb, "G1")
-                D.tsmm(Cp, kc, k, D.smp("G1"), sb, -1.0, 1.0, Wp, s)
-            D.gram(Vp, cap, total, Wp, s, sb, "G2")
-            D.tsmm(Vp, cap, total, D.smp("G2"), sb, -1.0, 1.0, Wp, s)
-            D.gram(Vp, cap, total, Wp, s, sb, "G3")
-            D.tsmm(Vp, cap, total, D.smp("G3"), sb, -1.0, 1.0, Wp, s)
-            D.tsqr(Wp, s, sb)
-            D.fetch(("RT", sb * sb))
+            bs_next, Rn = _project_deflate(D, k, total, 2, Wp, sb, total, cfg.deflation_tol,
+                                           report)
             if k:
                 Bmat[:, q0:q1] = D.get("G1", k, sb)
             Hb[:total, q0:q1] += D.get("G2", total, sb)
             Hb[:total, q0:q1] += D.get("G3", total, sb)
-            bs_next, Rn = _deflate_finish(D, Wp, s, sb, D.p("V", total), cap,
-                                          cfg.deflation_tol, report)
             Hb[total:total + bs_next, q0:q1] = Rn
             m = total
             total += bs_next
