@@ -115,9 +115,14 @@ __global__ void __launch_bounds__(256) k_gram(int n, int kv, const double* __res
   if (tid == 0) *ticket = 0u;
 }
 
-static int gram_blocks(int n) {
-  int nb = ceil_div(n, 1024);
-  if (nb > 148) nb = 148;
+// enough blocks to cover the SMs with >= 64 rows each, but few enough that
+// the last block's fixed-order pass over the partials stays ~<= 128 KB
+static int gram_blocks(int n, int K) {
+  int nb = ceil_div(n, 64);
+  if (nb > 296) nb = 296;
+  int cap = 16384 / (K > 0 ? K : 1);
+  if (cap < 16) cap = 16;
+  if (nb > cap) nb = cap;
   if (nb < 1) nb = 1;
   return nb;
 }
@@ -461,7 +466,10 @@ int pmp_spmm(int n, const int32_t* rowptr, const int32_t* colidx, const double* 
 }
 
 size_t pmp_gram_workspace(int n, int kv, int nw) {
-  return 256 + sizeof(double) * (size_t)gram_blocks(n) * kv * nw;
+  // any K' <= kv * nw needs gram_blocks(n, K') * K' <= max(16384, 296 * 55) doubles
+  size_t need = (size_t)gram_blocks(n, kv * nw) * kv * nw;
+  if (need < 16384 + 296) need = 16384 + 296;
+  return 256 + sizeof(double) * need;
 }
 
 int pmp_gram(int n, int kv, const double* V, int ldv, int nw, const double* W, int ldw,
@@ -478,7 +486,7 @@ int pmp_gram(int n, int kv, const double* V, int ldv, int nw, const double* W, i
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(st);
   unsigned* ticket = (unsigned*)ws;
   double* partial = (double*)((char*)ws + 256);
-  int nb = gram_blocks(n);
+  int nb = gram_blocks(n, kv * nw);
   int chunk = ceil_div(n > 0 ? n : 1, nb);
   size_t sm = sizeof(double) * kGramRows * (kv + nw);
   int K = kv * nw;

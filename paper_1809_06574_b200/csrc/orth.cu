@@ -7,19 +7,25 @@
 //
 // The reference runs these as separate BLAS/LAPACK calls; on the device
 // each is a tall-skinny reduction whose cost at BASELINE sizes is latency,
-// not bandwidth.  Here every block owns a contiguous row range, keeps its
-// rows of V, C and W in shared memory when they fit (c2: 222 rows x 86
-// columns = 153 KB), and the reductions are two-stage (per-block partials,
-// then a distributed fixed-order reduction) separated by grid-wide
-// barriers, so HBM/L2 is touched once per operand and no host round trip
-// is needed between the passes.
+// not bandwidth.  Here every block owns a contiguous row range and keeps
+// its rows of [C | V], W and Q in shared memory when they fit (c2: 222 rows
+// x 87 columns), so HBM/L2 is read once; the reductions are two-stage
+// (per-block partials, then a distributed fixed-order reduction) separated
+// by grid-wide barriers, so no host round trip happens inside the step.
 //
-// The QR is Cholesky-QR2 with symmetric pivoting: G = W^T W, R1 = chol(G),
-// Q1 = W P R1^-1, R2 = chol(Q1^T Q1), Q = Q1 R2^-1, R = R2 R1 (un-pivoted).
-// When the pivoted Cholesky shows min |R_kk| / |R_00| <= 1e-5 the block is
-// too close to rank deficiency for Cholesky to decide the 1e-12 deflation
-// rank of the reference (krylov.py:92); the kernel then leaves the
-// projected W in global memory and raises a flag, and the host falls back
+// Reduction schedule (3 reductions, 6 grid barriers):
+//   R1: [C | V]^T W           -> B = C^T W, H1 = V^T W
+//       W1 = W - C B - V H1          (C and V are mutually orthogonal, so
+//                                     projecting on [C | V] at once equals
+//                                     the reference's C-then-V order up to
+//                                     rounding, which the second pass cleans)
+//   R2: [V | W1]^T W1         -> H2 = V^T W1, W1^T W1
+//       W2 = W1 - V H2,  G = W1^T W1 - H2^T H2   (= W2^T W2; H2 ~ eps)
+//       R1f = chol(P^T G P) (symmetric pivoting), Q1 = W2 P R1f^-1
+//   R3: Q1^T Q1 -> R2f = chol(.), Q = Q1 R2f^-1, R = R2f R1f (un-pivoted)
+// When the pivoted Cholesky shows min |R_kk| / |R_00| <= 1e-5, Cholesky
+// cannot decide the reference's 1e-12 deflation rank (krylov.py:92): the
+// kernel leaves W2 in global memory, raises a flag, and the host falls back
 // to Householder TSQR + pivoted QR (pmp_tsqr_r + pmp_host_deflate), which
 // reproduce geqp3's rank decision.
 #include <cooperative_groups.h>
@@ -41,55 +47,86 @@ struct OrthParams {
   int ldv, total, npass;
   double* W;
   int ldw, sb;
-  int qout;            // V column receiving the new orthonormal block
+  int qout;  // V column receiving the new orthonormal block
   int rows_per_block;
-  int cached;
-  double* partial;     // gridDim.x * kmax doubles
-  double* Q1;          // n x sb scratch (streaming mode)
-  double* gout;        // reduction results (global): kmax doubles
-  double* outB;        // k x sb      (C^T W)
-  double* outH1;       // total x sb  (first CGS pass)
-  double* outH2;       // total x sb  (second CGS pass)
-  double* outR;        // sb x sb     (R, un-pivoted, row-major)
-  double* outFlag;     // 1 double: 0 ok, 1 fallback needed
+  double* partial;  // gridDim.x * kmax doubles
+  double* Q1g;      // n x sb scratch (streaming mode)
+  double* gout;     // reduction results (global): kmax doubles
+  double* outB;     // k x sb      (C^T W)
+  double* outH1;    // total x sb  (first CGS pass)
+  double* outH2;    // total x sb  (second CGS pass)
+  double* outR;     // sb x sb     (R, un-pivoted, row-major)
+  double* outFlag;  // 1 double: 0 ok, 1 fallback needed
 };
 
-struct OrthSmem {
-  double* Vs;  // rows x total   (cached mode)
-  double* Cs;  // rows x k
-  double* Ws;  // rows x sb
-  double* Qs;  // rows x sb
-  double* G;   // kmax  (reduced matrix)
-  double* A;   // 16 x 16 Cholesky work
-  double* R1;  // 16 x 16
-  double* R2;  // 16 x 16
-  int* piv;    // 16
-  int* piv2;   // 16
-  int* flag;   // 2
+// operand view of this block's rows: columns [0, ka) from a, then from b
+struct Rows {
+  const double* a;
+  int lda, ka;
+  const double* b;
+  int ldb;
+  __device__ __forceinline__ double at(int r, int t) const {
+    return t < ka ? a[(size_t)r * lda + t] : b[(size_t)r * ldb + (t - ka)];
+  }
 };
 
-// partial[b][o] = sum over this block's rows of X[r][t] Y[r][c], o = t*ny + c
-__device__ inline void block_gram(const double* X, int ldx, int kx, const double* Y, int ldy, int ny,
-                                  int nrows, double* partial) {
+__host__ __device__ __forceinline__ int odd_ld(int w) { return w | 1; }
+
+// partial[b][t * ny + c] = sum over this block's rows of X(r, t) Y[r][c].
+// Lanes own columns t (coalesced / conflict-free with odd leading
+// dimensions), warps split the rows; the per-warp sums are combined in a
+// fixed order through smem.
+__device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int ny, int nrows,
+                           double* red, double* partial) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = kx * ny;
   double* part = partial + (size_t)blockIdx.x * K;
-  for (int o = threadIdx.x; o < K; o += kOrthT) {
-    const int t = o / ny, c = o % ny;
-    double a0 = 0.0, a1 = 0.0;
-    int r = 0;
-    for (; r + 1 < nrows; r += 2) {
-      a0 += X[(size_t)r * ldx + t] * Y[(size_t)r * ldy + c];
-      a1 += X[(size_t)(r + 1) * ldx + t] * Y[(size_t)(r + 1) * ldy + c];
+  const int rounds = (kx + 31) / 32;
+  int splits = 8 / rounds;
+  if (splits < 1) splits = 1;
+  for (int job0 = 0; job0 < rounds * splits; job0 += 8) {
+    const int job = job0 + wid;
+    const int rd = job / splits, sp = job % splits;
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    const int t = rd * 32 + lane;
+    if (job < rounds * splits && t < kx) {
+      const int per = (nrows + splits - 1) / splits;
+      const int ra = sp * per, rb = min(nrows, ra + per);
+      for (int r = ra; r < rb; ++r) {
+        const double x = X.at(r, t);
+        const double* y = Y + (size_t)r * ldy;
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < ny) acc[c] += x * y[c];
+      }
     }
-    if (r < nrows) a0 += X[(size_t)r * ldx + t] * Y[(size_t)r * ldy + c];
-    part[o] = a0 + a1;
+    if (job < rounds * splits) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < ny) red[((size_t)(job - job0) * 32 + lane) * ny + c] = acc[c];
+    }
+    __syncthreads();
+    // fixed-order sum over the splits of every round covered by this batch
+    for (int o = threadIdx.x; o < K; o += kOrthT) {
+      const int tt = o / ny, c = o % ny, r2 = tt / 32, ln = tt % 32;
+      const int j0 = r2 * splits;
+      if (j0 >= job0 && j0 < job0 + 8) {
+        double s = 0.0;
+        for (int q = 0; q < splits; ++q) s += red[((size_t)(j0 + q - job0) * 32 + ln) * ny + c];
+        part[o] = s;
+      }
+    }
+    __syncthreads();
   }
 }
 
-// fixed-order distributed reduction of the block partials; every block
-// ends with the full result in smem G (and block 0's slice writes `out`)
-__device__ inline void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, double* G,
-                                   double* out) {
+// distributed fixed-order reduction of the block partials; every block ends
+// with the full K-vector in smem G.  Entries [0, split) are also copied to
+// out, entries [split, K) to out2 (either may be null).
+__device__ void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, double* G,
+                            double* out, int split, double* out2) {
   __threadfence();
   grid.sync();
   const int nb = gridDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -99,7 +136,11 @@ __device__ inline void grid_reduce(cg::grid_group& grid, const OrthParams& P, in
     s = warp_sum(s);
     if (lane == 0) {
       P.gout[o] = s;
-      if (out) out[o] = s;
+      if (o < split) {
+        if (out) out[o] = s;
+      } else if (out2) {
+        out2[o - split] = s;
+      }
     }
   }
   __threadfence();
@@ -108,29 +149,33 @@ __device__ inline void grid_reduce(cg::grid_group& grid, const OrthParams& P, in
   __syncthreads();
 }
 
-// Y[r][c] -= sum_t X[r][t] G[t][c]
-__device__ inline void block_update(const double* X, int ldx, int kx, double* Y, int ldy, int ny,
-                                    int nrows, const double* G) {
-  for (int q = threadIdx.x; q < nrows * ny; q += kOrthT) {
-    const int r = q / ny, c = q % ny;
-    const double* x = X + (size_t)r * ldx;
-    double a0 = 0.0, a1 = 0.0;
-    int t = 0;
-    for (; t + 1 < kx; t += 2) {
-      a0 += x[t] * G[t * ny + c];
-      a1 += x[t + 1] * G[(t + 1) * ny + c];
+// Y[r][c] -= sum_t X(r, t) G[t][c] ; thread per row, all ny outputs
+__device__ void block_update(const Rows& X, int kx, double* Y, int ldy, int ny, int nrows,
+                             const double* G) {
+  for (int r = threadIdx.x; r < nrows; r += kOrthT) {
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int t = 0; t < kx; ++t) {
+      const double x = X.at(r, t);
+      const double* g = G + t * ny;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < ny) acc[c] += x * g[c];
     }
-    if (t < kx) a0 += x[t] * G[t * ny + c];
-    Y[(size_t)r * ldy + c] -= a0 + a1;
+    double* y = Y + (size_t)r * ldy;
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < ny) y[c] -= acc[c];
   }
   __syncthreads();
 }
 
-// Cholesky of the m x m SPD matrix in G (row-major), by warp 0.  With
-// pivot != 0, symmetric pivoting on the largest remaining diagonal.
-// R (m x m, row-major, upper) gets the factor of P^T G P; returns ok.
-__device__ inline bool warp_cholesky(const double* G, int m, double* A, double* R, int* piv,
-                                     bool pivot, double ratio) {
+// Cholesky of the m x m SPD matrix G (row-major) by warp 0; with `pivot`,
+// symmetric pivoting on the largest remaining diagonal.  R (row-major,
+// upper) is the factor of P^T G P; returns ok (and the ratio test).
+__device__ bool warp_cholesky(const double* G, int m, double* A, double* R, int* piv, bool pivot,
+                              double ratio) {
   const int lane = threadIdx.x & 31;
   for (int q = lane; q < m * m; q += 32) {
     A[q] = G[q];
@@ -150,8 +195,6 @@ __device__ inline bool warp_cholesky(const double* G, int m, double* A, double* 
         }
     }
     if (p != k) {
-      // symmetric swap of rows/columns k and p of the trailing matrix, and
-      // of the already computed R columns
       for (int q = lane; q < m; q += 32) {
         double t = A[k * m + q];
         A[k * m + q] = A[p * m + q];
@@ -183,8 +226,9 @@ __device__ inline bool warp_cholesky(const double* G, int m, double* A, double* 
     const double d = sqrt(dkk);
     for (int j = k + lane; j < m; j += 32) R[k * m + j] = (j == k) ? d : A[k * m + j] / d;
     __syncwarp();
-    for (int q = lane; q < (m - k - 1) * (m - k - 1); q += 32) {
-      int i = k + 1 + q / (m - k - 1), j = k + 1 + q % (m - k - 1);
+    const int w = m - k - 1;
+    for (int q = lane; q < w * w; q += 32) {
+      int i = k + 1 + q / w, j = k + 1 + q % w;
       A[i * m + j] -= R[k * m + i] * R[k * m + j];
     }
     __syncwarp();
@@ -193,22 +237,24 @@ __device__ inline bool warp_cholesky(const double* G, int m, double* A, double* 
   return ok;
 }
 
-// Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve), in place allowed
-__device__ inline void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows,
-                                       int m, const double* R, const int* piv) {
+// Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve); thread per row
+__device__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
+                                const double* R, const int* piv) {
   for (int r = threadIdx.x; r < nrows; r += kOrthT) {
     double x[16], y[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
-      if (c < m) x[c] = X[(size_t)r * ldx + (piv ? piv[c] : c)];
+    for (int c = 0; c < 16; ++c) x[c] = (c < m) ? X[(size_t)r * ldx + (piv ? piv[c] : c)] : 0.0;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      if (c >= m) break;
-      double s = x[c];
+      if (c < m) {
+        double s = x[c];
 #pragma unroll
-      for (int a = 0; a < 16; ++a)
-        if (a < c) s -= y[a] * R[a * m + c];
-      y[c] = s / R[c * m + c];
+        for (int a = 0; a < 16; ++a)
+          if (a < c) s -= y[a] * R[a * m + c];
+        y[c] = s / R[c * m + c];
+      } else {
+        y[c] = 0.0;
+      }
     }
 #pragma unroll
     for (int c = 0; c < 16; ++c)
@@ -217,6 +263,7 @@ __device__ inline void block_trsm_rows(const double* X, int ldx, double* Y, int 
   __syncthreads();
 }
 
+template <bool CACHED>
 __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sh[];
@@ -224,113 +271,131 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
   const int r1 = min(P.n, r0 + P.rows_per_block);
   const int nr = max(0, r1 - r0);
   const int sb = P.sb, k = P.k, tot = P.total;
-  const int kmax = max(max(k, tot), sb) * sb;
-  OrthSmem S;
+  const int kx = k + tot;
+  const int kmax = (kx + sb) * sb;
   double* p = sh;
-  S.G = p;
+  double* G = p;
   p += kmax;
-  S.A = p;
+  double* A = p;
   p += 256;
-  S.R1 = p;
+  double* R1 = p;
   p += 256;
-  S.R2 = p;
+  double* R2 = p;
   p += 256;
-  S.piv = reinterpret_cast<int*>(p);
-  S.piv2 = S.piv + 16;
-  p += 16;
-  S.flag = reinterpret_cast<int*>(p);
-  p += 4;
-  // operand views: shared-memory copies of this block's rows, or global
-  const double *Cv = P.C + (size_t)r0 * P.ldc, *Vv = P.V + (size_t)r0 * P.ldv;
-  double* Wv = P.W + (size_t)r0 * P.ldw;
-  int ldc = P.ldc, ldv = P.ldv, ldw = P.ldw;
-  if (P.cached) {
-    S.Vs = p;
-    p += (size_t)nr * tot;
-    S.Cs = p;
-    p += (size_t)nr * k;
-    S.Ws = p;
-    p += (size_t)nr * sb;
-    S.Qs = p;
-    for (int q = threadIdx.x; q < nr * tot; q += kOrthT)
-      S.Vs[q] = Vv[(size_t)(q / tot) * P.ldv + q % tot];
-    for (int q = threadIdx.x; q < nr * k; q += kOrthT)
-      S.Cs[q] = Cv[(size_t)(q / k) * P.ldc + q % k];
+  double* red = p;
+  p += 8 * 32 * 16;
+  int* piv = reinterpret_cast<int*>(p);
+  int* piv2 = piv + 16;
+  int* flag = piv + 32;
+  p += 20;
+  Rows CV;
+  double* Wv;
+  int ldw;
+  double* Q1;
+  int ldq;
+  if (CACHED) {
+    const int ldx = odd_ld(kx);
+    double* Xs = p;
+    p += (size_t)nr * ldx;
+    ldw = odd_ld(sb);
+    Wv = p;
+    p += (size_t)nr * ldw;
+    ldq = ldw;
+    Q1 = p;
+    const double* Cg = P.C + (size_t)r0 * P.ldc;
+    const double* Vg = P.V + (size_t)r0 * P.ldv;
+    const double* Wg = P.W + (size_t)r0 * P.ldw;
+    for (int q = threadIdx.x; q < nr * kx; q += kOrthT) {
+      const int r = q / kx, t = q % kx;
+      Xs[(size_t)r * ldx + t] = t < k ? Cg[(size_t)r * P.ldc + t] : Vg[(size_t)r * P.ldv + t - k];
+    }
     for (int q = threadIdx.x; q < nr * sb; q += kOrthT)
-      S.Ws[q] = Wv[(size_t)(q / sb) * P.ldw + q % sb];
+      Wv[(size_t)(q / sb) * ldw + q % sb] = Wg[(size_t)(q / sb) * P.ldw + q % sb];
+    CV = Rows{Xs, ldx, kx, Xs, ldx};
     __syncthreads();
-    Vv = S.Vs;
-    Cv = S.Cs;
-    Wv = S.Ws;
-    ldv = tot;
-    ldc = k;
-    ldw = sb;
+  } else {
+    CV = Rows{P.C + (size_t)r0 * P.ldc, P.ldc, k, P.V + (size_t)r0 * P.ldv, P.ldv};
+    Wv = P.W + (size_t)r0 * P.ldw;
+    ldw = P.ldw;
+    Q1 = P.Q1g + (size_t)r0 * sb;
+    ldq = sb;
   }
-  double* part = P.partial;
+  const double* Vrows = CACHED ? CV.a + k : P.V + (size_t)r0 * P.ldv;
+  const int ldvr = CACHED ? CV.lda : P.ldv;
+  const Rows Vonly{Vrows, ldvr, tot, Vrows, ldvr};
 
-  // ---- W -= C (C^T W) --------------------------------------------------------
-  if (k > 0) {
-    block_gram(Cv, ldc, k, Wv, ldw, sb, nr, part);
-    grid_reduce(grid, P, k * sb, S.G, P.outB);
-    block_update(Cv, ldc, k, Wv, ldw, sb, nr, S.G);
+  // ---- R1: [C | V]^T W -------------------------------------------------------
+  if (kx > 0) {
+    block_gram(CV, kx, Wv, ldw, sb, nr, red, P.partial);
+    grid_reduce(grid, P, kx * sb, G, P.outB, k * sb, P.npass ? P.outH1 : nullptr);
+    block_update(CV, kx, Wv, ldw, sb, nr, G);
   }
-  // ---- block CGS2 against V[:, :total] -----------------------------------------
-  for (int pass = 0; pass < P.npass && tot > 0; ++pass) {
-    // same fixed-order reduction structure for both passes
-    block_gram(Vv, ldv, tot, Wv, ldw, sb, nr, part);
-    grid_reduce(grid, P, tot * sb, S.G, pass == 0 ? P.outH1 : P.outH2);
-    block_update(Vv, ldv, tot, Wv, ldw, sb, nr, S.G);
+  // ---- R2: [V | W1]^T W1 -----------------------------------------------------
+  const bool second = P.npass >= 2 && tot > 0;
+  const int kv2 = second ? tot : 0;
+  const int kx2 = kv2 + sb;
+  {
+    const Rows VW{Vrows, ldvr, kv2, Wv, ldw};
+    block_gram(VW, kx2, Wv, ldw, sb, nr, red, P.partial);
+    grid_reduce(grid, P, kx2 * sb, G, second ? P.outH2 : nullptr, kv2 * sb, nullptr);
   }
-  // ---- Cholesky-QR2 -------------------------------------------------------------
-  block_gram(Wv, ldw, sb, Wv, ldw, sb, nr, part);
-  grid_reduce(grid, P, sb * sb, S.G, nullptr);
-  if (threadIdx.x < 32) {
-    bool ok = warp_cholesky(S.G, sb, S.A, S.R1, S.piv, true, kCholRatio);
-    if (threadIdx.x == 0) S.flag[0] = ok ? 0 : 1;
+  // G_W = W1^T W1 - H2^T H2 (into R2 as scratch), then W2 = W1 - V H2
+  for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {
+    const int i = q / sb, j = q % sb;
+    double s = G[(size_t)(kv2 + i) * sb + j];
+    for (int t = 0; t < kv2; ++t) s -= G[t * sb + i] * G[t * sb + j];
+    R2[q] = s;
   }
   __syncthreads();
-  // Q1 = W P R1^-1 into a separate view, so W stays intact for a fallback
-  double* Q1 = P.cached ? S.Qs : (P.Q1 + (size_t)r0 * sb);
-  if (!S.flag[0]) {
-    block_trsm_rows(Wv, ldw, Q1, sb, nr, sb, S.R1, S.piv);
-    block_gram(Q1, sb, sb, Q1, sb, sb, nr, part);
+  if (second) block_update(Vonly, tot, Wv, ldw, sb, nr, G);
+  for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {
+    const int i = q / sb, j = q % sb;
+    G[q] = 0.5 * (R2[i * sb + j] + R2[j * sb + i]);
   }
-  // the flag is grid-uniform (every block factors the same reduced G), so
-  // this reduction is reached by all blocks or by none
-  if (!S.flag[0]) {
-    grid_reduce(grid, P, sb * sb, S.G, nullptr);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    bool ok = warp_cholesky(G, sb, A, R1, piv, true, kCholRatio);
+    if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
+  }
+  __syncthreads();
+  if (flag[0] == 0) {
+    block_trsm_rows(Wv, ldw, Q1, ldq, nr, sb, R1, piv);
+    // ---- R3: Q1^T Q1 ---------------------------------------------------------
+    const Rows Qv{Q1, ldq, sb, Q1, ldq};
+    block_gram(Qv, sb, Q1, ldq, sb, nr, red, P.partial);
+    grid_reduce(grid, P, sb * sb, G, nullptr, 0, nullptr);
     if (threadIdx.x < 32) {
-      bool ok = warp_cholesky(S.G, sb, S.A, S.R2, S.piv2, false, 0.0);
-      if (threadIdx.x == 0) S.flag[0] = ok ? 0 : 1;
+      bool ok = warp_cholesky(G, sb, A, R2, piv2, false, 0.0);
+      if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
     }
     __syncthreads();
   }
-  if (S.flag[0]) {
-    // fallback: leave the projected block in global W for the host path
-    if (P.cached)
+  // flag is grid-uniform: every block factored the same reduced matrices
+  if (flag[0]) {
+    if (CACHED)
       for (int q = threadIdx.x; q < nr * sb; q += kOrthT)
-        P.W[(size_t)(r0 + q / sb) * P.ldw + q % sb] = Wv[q];
+        P.W[(size_t)(r0 + q / sb) * P.ldw + q % sb] = Wv[(size_t)(q / sb) * ldw + q % sb];
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.outFlag = 1.0;
     return;
   }
   // Q = Q1 R2^-1 -> V[:, qout : qout + sb]
-  block_trsm_rows(Q1, sb, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, S.R2, nullptr);
+  block_trsm_rows(Q1, ldq, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R2, nullptr);
   if (blockIdx.x == 0) {
     // R = R2 R1 (pivoted column order), un-pivoted: Rout[i, piv[c]] = R[i, c]
     for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {
       const int i = q / sb, c = q % sb;
       double s = 0.0;
-      for (int a = i; a <= c; ++a) s += S.R2[i * sb + a] * S.R1[a * sb + c];
-      P.outR[i * sb + S.piv[c]] = (c >= i) ? s : 0.0;
+      for (int a = i; a <= c; ++a) s += R2[i * sb + a] * R1[a * sb + c];
+      P.outR[i * sb + piv[c]] = (c >= i) ? s : 0.0;
     }
     if (threadIdx.x == 0) *P.outFlag = 0.0;
   }
 }
 
 size_t orth_smem_bytes(int rows, int total, int k, int sb, int cached) {
-  const int kmax = (k > total ? (k > sb ? k : sb) : (total > sb ? total : sb)) * sb;
-  size_t d = (size_t)kmax + 3 * 256 + 16 + 16 + 4;
-  if (cached) d += (size_t)rows * (total + k + 2 * sb);
+  const int kx = k + total;
+  size_t d = (size_t)(kx + sb) * sb + 3 * 256 + 8 * 32 * 16 + 20;
+  if (cached) d += (size_t)rows * (odd_ld(kx) + 2 * odd_ld(sb));
   return d * sizeof(double);
 }
 
@@ -338,8 +403,8 @@ size_t orth_smem_bytes(int rows, int total, int k, int sb, int cached) {
 
 using namespace pmp;
 
-static int orth_geometry(int n, int total, int k, int sb, int* grid, int* rows, int* cached,
-                         size_t* smem) {
+static void orth_geometry(int n, int total, int k, int sb, int* grid, int* rows, int* cached,
+                          size_t* smem) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -352,11 +417,10 @@ static int orth_geometry(int n, int total, int k, int sb, int* grid, int* rows, 
   if (want < g) g = want > 0 ? want : 1;
   int r = (n + g - 1) / g;
   size_t full = orth_smem_bytes(r, total, k, sb, 1);
-  *cached = full <= (size_t)200 * 1024;
+  *cached = full <= (size_t)220 * 1024;
   *smem = *cached ? full : orth_smem_bytes(r, total, k, sb, 0);
   *grid = g;
   *rows = r;
-  return 0;
 }
 
 extern "C" {
@@ -365,8 +429,7 @@ size_t pmp_orth_workspace(int n, int total_max, int k_max, int sb) {
   int g, r, c;
   size_t sm;
   orth_geometry(n, total_max, k_max, sb, &g, &r, &c, &sm);
-  const int kmax = (k_max > total_max ? (k_max > sb ? k_max : sb)
-                                      : (total_max > sb ? total_max : sb)) * sb;
+  const int kmax = (k_max + total_max + sb) * sb;
   return 256 + sizeof(double) * ((size_t)g * kmax + kmax + (size_t)n * sb + 64);
 }
 
@@ -375,7 +438,7 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
                   double* outH2, double* outR, double* outFlag, void* ws, size_t ws_bytes,
                   void* stream) {
   if (n < 1 || sb < 1 || sb > 16 || k < 0 || total < 0 || (k && ldc < k) || ldw < sb ||
-      ldv < qout + sb || (npass && total && ldv < total)) {
+      ldv < qout + sb || (total && ldv < total) || (npass != 0 && npass != 2)) {
     set_error("pmp_orth_step: bad arguments (n=%d k=%d total=%d sb=%d)", n, k, total, sb);
     return PMP_ERR_ARG;
   }
@@ -386,14 +449,15 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
   int g, rows, cached;
   size_t smem;
   orth_geometry(n, total, k, sb, &g, &rows, &cached, &smem);
-  cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  void* fn = cached ? (void*)k_orth<true> : (void*)k_orth<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_orth, kOrthT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kOrthT, smem);
   if (bps < 1) {
     set_error("pmp_orth_step: kernel does not fit on an SM (smem %zu)", smem);
     return PMP_ERR_ARG;
   }
-  const int kmax = (k > total ? (k > sb ? k : sb) : (total > sb ? total : sb)) * sb;
+  const int kmax = (k + total + sb) * sb;
   OrthParams P;
   P.n = n;
   P.C = C;
@@ -408,18 +472,17 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
   P.sb = sb;
   P.qout = qout;
   P.rows_per_block = rows;
-  P.cached = cached;
   double* w = (double*)((char*)ws + 256);
   P.partial = w;
   P.gout = w + (size_t)g * kmax;
-  P.Q1 = P.gout + kmax;
+  P.Q1g = P.gout + kmax;
   P.outB = outB;
   P.outH1 = outH1;
   P.outH2 = outH2;
   P.outR = outR;
   P.outFlag = outFlag;
   void* args[] = {&P};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_orth, dim3(g), dim3(kOrthT), args, smem,
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem,
                                               reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     set_error("pmp_orth_step: %s", cudaGetErrorString(e));

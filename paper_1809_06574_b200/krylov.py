@@ -502,10 +502,13 @@ def _solve(A, B, P, cfg):
             if k:
                 D.tsmm(Cp, kc, k, D.put("G1", img[:k]), na, 1.0, 1.0, D.p("Rb"), s)
             kk = k
+            w0s = _colnorms(D, D.p("Rb"), s, na)      # ||images[:, col]|| for all columns
             for col in range(na):
+                w0 = w0s[col]
+                if w0 == 0.0:
+                    continue
                 D.copy_cols(1, D.p("Rb", col), s, None, D.p("w1"), 1, None)
                 D.copy_cols(1, D.p("dX", col), s, None, D.p("z1"), 1, None)
-                w0 = _colnorms(D, D.p("w1"), 1, 1)[0]
                 if w0 == 0.0:
                     continue
                 if kk:
