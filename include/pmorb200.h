@@ -177,6 +177,18 @@ int pmp_orth_step(int n, const double* d_C, int ldc, int k, double* d_V, int ldv
                   double* d_outH1, double* d_outH2, double* d_outR, double* d_outFlag,
                   void* d_ws, size_t ws_bytes, void* stream);
 
+/* ---- outer-space fold (krylov.py:244-269), one cooperative launch --------
+ * For col = 0..na-1: w = img[:, col], z = dz[:, col]; two passes of
+ * { h = C^T w; w -= C h; z -= U h } against the current C (k columns);
+ * drop when ||w|| <= 1e-10 ||img[:, col]|| (or ||img[:, col]|| == 0), else
+ * append C[:, k] = w / ||w||, U[:, k] = z / ||w||, k++.  Writes out[0] =
+ * final k and out[1 + col] = 1 / 0 (kept).  C, U: n x ldc row-major with
+ * k0 + na <= kc <= ldc. */
+size_t pmp_fold_workspace(int n, int kc);
+int pmp_fold(int n, int na, const double* d_img, int ldi, const double* d_dz, int ldz,
+             double* d_C, double* d_U, int ldc, int kc, int k0, double* d_out, void* d_ws,
+             size_t ws_bytes, void* stream);
+
 /* ---- helpers ------------------------------------------------------------ */
 /* dst[:, dst_cols[c]] = src[:, src_cols[c]] for c < nc (NULL = identity). */
 int pmp_copy_cols(int n, int nc, const double* d_src, int lds, const int32_t* d_src_cols,

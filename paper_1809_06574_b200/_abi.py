@@ -68,6 +68,9 @@ _SIGS = {
     "pmp_orth_workspace": ([c_int, c_int, c_int, c_int], c_sz),
     "pmp_orth_step": ([c_int, c_vp, c_int, c_int, c_vp, c_int, c_int, c_int, c_vp, c_int, c_int,
                        c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
+    "pmp_fold_workspace": ([c_int, c_int], c_sz),
+    "pmp_fold": ([c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_int, c_int, c_vp,
+                  c_vp, c_sz, c_vp], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp, c_vp], c_int),

@@ -102,15 +102,37 @@ __global__ void __launch_bounds__(256) k_gram(int n, int kv, const double* __res
   // fixed-order sum over the block partials with 8 independent chains
   // (b mod 8) so the L2 loads overlap; combined in a fixed tree
   const int nb = gridDim.x;
-  for (int o = tid; o < K; o += 256) {
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int b = 0;
-    for (; b + 8 <= nb; b += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] += __ldcg(partial + (size_t)(b + u) * K + o);
+  // `per` threads share one output (all 256 threads busy even for small K);
+  // each sums a fixed strided subset of the partials, then the subsets are
+  // combined in order through shared memory
+  int per = 256 / K;
+  if (per < 1) per = 1;
+  if (per > 32) per = 32;
+  __shared__ double red[256];
+  for (int o0 = 0; o0 < K; o0 += 256 / per) {
+    const int o = o0 + tid / per, sub = tid % per;
+    double s = 0.0;
+    if (o < K && tid / per < 256 / per) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* pp = partial + o;
+      int b = sub;
+      for (; b + 3 * per < nb; b += 4 * per) {
+        a0 += __ldcg(pp + (size_t)b * K);
+        a1 += __ldcg(pp + (size_t)(b + per) * K);
+        a2 += __ldcg(pp + (size_t)(b + 2 * per) * K);
+        a3 += __ldcg(pp + (size_t)(b + 3 * per) * K);
+      }
+      for (; b < nb; b += per) a0 += __ldcg(pp + (size_t)b * K);
+      s = (a0 + a1) + (a2 + a3);
     }
-    for (int u = 0; b + u < nb; ++u) a[u] += __ldcg(partial + (size_t)(b + u) * K + o);
-    Gout[o] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    red[tid] = s;
+    __syncthreads();
+    if (sub == 0 && o < K && tid / per < 256 / per) {
+      double t = 0.0;
+      for (int q = 0; q < per; ++q) t += red[tid + q];
+      Gout[o] = t;
+    }
+    __syncthreads();
   }
   if (tid == 0) *ticket = 0u;
 }

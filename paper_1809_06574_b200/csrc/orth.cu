@@ -392,6 +392,138 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Outer-space fold (krylov.py:244-269) in one cooperative launch: for each
+// image column, CGS2 against the current C (with the matching U update),
+// the 1e-10 drop test, and the append -- all decisions are grid-uniform, so
+// no host round trip per column.  Norms: ||w||^2 comes with the first
+// projection's reduction, ||w2||^2 = ||w1||^2 - ||h2||^2 with the second
+// (recomputed exactly when that difference cancels).
+// ---------------------------------------------------------------------------
+
+struct FoldParams {
+  int n, na;
+  const double* img;
+  int ldi;
+  const double* dz;
+  int ldz;
+  double* C;
+  double* U;
+  int ldc, kc, k0;
+  int rows_per_block;
+  double* partial;
+  double* gout;
+  double* wz;   // n x 2 scratch (streaming mode)
+  double* out;  // out[0] = final outer dimension, out[1 + col] = kept flag
+};
+
+template <bool CACHED>
+__global__ void __launch_bounds__(kOrthT, 1) k_fold(FoldParams F) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sh[];
+  const int r0 = blockIdx.x * F.rows_per_block;
+  const int r1 = min(F.n, r0 + F.rows_per_block);
+  const int nr = max(0, r1 - r0);
+  const int kc = F.kc;
+  double* p = sh;
+  double* G = p;
+  p += kc + 8;
+  double* red = p;
+  p += 8 * 32 * 16;
+  OrthParams P;  // only the reduction scratch is used by grid_reduce
+  P.partial = F.partial;
+  P.gout = F.gout;
+  double *Cs, *Us, *w, *z;
+  int ldcs;
+  if (CACHED) {
+    ldcs = odd_ld(kc);
+    Cs = p;
+    p += (size_t)nr * ldcs;
+    Us = p;
+    p += (size_t)nr * ldcs;
+    w = p;
+    p += nr;
+    z = p;
+    for (int q = threadIdx.x; q < nr * kc; q += kOrthT) {
+      const int r = q / kc, t = q % kc;
+      if (t < F.k0) {
+        Cs[(size_t)r * ldcs + t] = F.C[(size_t)(r0 + r) * F.ldc + t];
+        Us[(size_t)r * ldcs + t] = F.U[(size_t)(r0 + r) * F.ldc + t];
+      }
+    }
+  } else {
+    ldcs = F.ldc;
+    Cs = F.C + (size_t)r0 * F.ldc;
+    Us = F.U + (size_t)r0 * F.ldc;
+    w = F.wz + (size_t)r0 * 2;
+    z = w + 1;
+  }
+  const int ldwz = CACHED ? 1 : 2;
+  int kk = F.k0;
+  for (int col = 0; col < F.na; ++col) {
+    for (int r = threadIdx.x; r < nr; r += kOrthT) {
+      w[(size_t)r * ldwz] = F.img[(size_t)(r0 + r) * F.ldi + col];
+      z[(size_t)r * ldwz] = F.dz[(size_t)(r0 + r) * F.ldz + col];
+    }
+    __syncthreads();
+    // [C | w]^T w  ->  h1, ||w||^2
+    Rows Cw{Cs, ldcs, kk, w, ldwz};
+    block_gram(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
+    grid_reduce(grid, P, kk + 1, G, nullptr, 0, nullptr);
+    const double w0 = sqrt(G[kk]);
+    if (w0 == 0.0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) F.out[1 + col] = 0.0;
+      continue;
+    }
+    double nw;
+    if (kk > 0) {
+      Rows Conly{Cs, ldcs, kk, Cs, ldcs}, Uonly{Us, ldcs, kk, Us, ldcs};
+      block_update(Conly, kk, w, ldwz, 1, nr, G);
+      block_update(Uonly, kk, z, ldwz, 1, nr, G);
+      block_gram(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
+      grid_reduce(grid, P, kk + 1, G, nullptr, 0, nullptr);
+      double h2 = 0.0;
+      for (int t = 0; t < kk; ++t) h2 += G[t] * G[t];
+      const double w1n2 = G[kk];
+      block_update(Conly, kk, w, ldwz, 1, nr, G);
+      block_update(Uonly, kk, z, ldwz, 1, nr, G);
+      double nw2 = w1n2 - h2;
+      if (!(nw2 > 1e-4 * w1n2)) {
+        // cancellation: recompute ||w2||^2 exactly
+        Rows Wo{w, ldwz, 1, w, ldwz};
+        block_gram(Wo, 1, w, ldwz, 1, nr, red, P.partial);
+        grid_reduce(grid, P, 1, G, nullptr, 0, nullptr);
+        nw2 = G[0];
+      }
+      nw = sqrt(fmax(nw2, 0.0));
+    } else {
+      nw = w0;
+    }
+    const bool keep = !(nw <= 1e-10 * w0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) F.out[1 + col] = keep ? 1.0 : 0.0;
+    if (!keep) continue;
+    const double inv = 1.0 / nw;
+    for (int r = threadIdx.x; r < nr; r += kOrthT) {
+      const double cv = w[(size_t)r * ldwz] * inv, uv = z[(size_t)r * ldwz] * inv;
+      F.C[(size_t)(r0 + r) * F.ldc + kk] = cv;
+      F.U[(size_t)(r0 + r) * F.ldc + kk] = uv;
+      if (CACHED) {
+        Cs[(size_t)r * ldcs + kk] = cv;
+        Us[(size_t)r * ldcs + kk] = uv;
+      }
+    }
+    __syncthreads();
+    ++kk;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) F.out[0] = (double)kk;
+}
+
+size_t fold_smem_bytes(int rows, int kc, int cached) {
+  size_t d = (size_t)kc + 8 + 8 * 32 * 16;
+  if (cached) d += (size_t)rows * (2 * odd_ld(kc) + 2);
+  return d * sizeof(double);
+}
+
 size_t orth_smem_bytes(int rows, int total, int k, int sb, int cached) {
   const int kx = k + total;
   size_t d = (size_t)(kx + sb) * sb + 3 * 256 + 8 * 32 * 16 + 20;
@@ -489,6 +621,59 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
     return PMP_ERR_CUDA;
   }
   return cuda_status("pmp_orth_step");
+}
+
+size_t pmp_fold_workspace(int n, int kc) {
+  int g, r, c;
+  size_t sm;
+  orth_geometry(n, 0, 0, 1, &g, &r, &c, &sm);
+  return 256 + sizeof(double) * ((size_t)g * (kc + 1) + (kc + 1) + 2 * (size_t)n + 64);
+}
+
+int pmp_fold(int n, int na, const double* img, int ldi, const double* dz, int ldz, double* C,
+             double* U, int ldc, int kc, int k0, double* out, void* ws, size_t ws_bytes,
+             void* stream) {
+  if (n < 1 || na < 0 || k0 < 0 || k0 + na > kc || ldc < kc || ldi < na || ldz < na) {
+    set_error("pmp_fold: bad arguments (n=%d na=%d k0=%d kc=%d)", n, na, k0, kc);
+    return PMP_ERR_ARG;
+  }
+  if (ws_bytes < pmp_fold_workspace(n, kc)) {
+    set_error("pmp_fold: workspace too small");
+    return PMP_ERR_WORKSPACE;
+  }
+  int g, rows, c0;
+  size_t sm0;
+  orth_geometry(n, 0, 0, 1, &g, &rows, &c0, &sm0);
+  const int cached = fold_smem_bytes(rows, kc, 1) <= (size_t)220 * 1024;
+  const size_t smem = fold_smem_bytes(rows, kc, cached);
+  void* fn = cached ? (void*)k_fold<true> : (void*)k_fold<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  FoldParams F;
+  F.n = n;
+  F.na = na;
+  F.img = img;
+  F.ldi = ldi;
+  F.dz = dz;
+  F.ldz = ldz;
+  F.C = C;
+  F.U = U;
+  F.ldc = ldc;
+  F.kc = kc;
+  F.k0 = k0;
+  F.rows_per_block = rows;
+  double* w = (double*)((char*)ws + 256);
+  F.partial = w;
+  F.gout = w + (size_t)g * (kc + 1);
+  F.wz = F.gout + (kc + 1);
+  F.out = out;
+  void* args[] = {&F};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem,
+                                              reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error("pmp_fold: %s", cudaGetErrorString(e));
+    return PMP_ERR_CUDA;
+  }
+  return cuda_status("pmp_fold");
 }
 
 }  // extern "C"

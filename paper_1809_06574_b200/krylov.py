@@ -139,6 +139,8 @@ class _Dev:
         self.f_copy, self.f_axpby = L.pmp_copy_cols, L.pmp_axpby_cols
         self.f_defl, self.f_hls = L.pmp_host_deflate, L.pmp_host_hls_append
         self.f_orth = L.pmp_orth_step
+        self.f_fold = L.pmp_fold
+        self.fold_ws = sc.get("fold", L.pmp_fold_workspace(n, kc))
         self.counting = _abi._counting
         self.timing = _abi._timing_names
         self.launches = 0
@@ -194,6 +196,15 @@ class _Dev:
                    self.ptr["V"], self.cap, total, npass, Wp, self.s, sb, qout,
                    self.smp_["G1"], self.smp_["G2"], self.smp_["G3"], self.smp_["RT"],
                    self.smp_["FLAG"], self.ows, self.owb, self.st)
+
+    def fold(self, k, na):
+        """Outer-space fold of the images in Rb / directions in dX
+        (pmp_fold, one cooperative launch); returns the new dimension."""
+        self._call("pmp_fold", self.f_fold, self.n, na, self.ptr["Rb"], self.s, self.ptr["dX"],
+                   self.s, self.ptr["C"], self.ptr["U"], self.kc, self.kc, k, self.smp_["H"],
+                   self.fold_ws.data_ptr(), self.fold_ws.numel(), self.st)
+        self.fetch(("H", 1))
+        return int(round(self.get("H", 1, 1)[0, 0]))
 
     def tsqr(self, Zp, ldz, nz):
         self._call("pmp_tsqr_r", self.f_tsqr, self.n, nz, Zp, ldz, self.smp_["RT"], self.tws, self.twb, self.st)
@@ -501,27 +512,7 @@ def _solve(A, B, P, cfg):
             D.tsmm(Vp, cap, total, D.put("H", img[k:]), na, 1.0, 0.0, D.p("Rb"), s)
             if k:
                 D.tsmm(Cp, kc, k, D.put("G1", img[:k]), na, 1.0, 1.0, D.p("Rb"), s)
-            kk = k
-            w0s = _colnorms(D, D.p("Rb"), s, na)      # ||images[:, col]|| for all columns
-            for col in range(na):
-                w0 = w0s[col]
-                if w0 == 0.0:
-                    continue
-                D.copy_cols(1, D.p("Rb", col), s, None, D.p("w1"), 1, None)
-                D.copy_cols(1, D.p("dX", col), s, None, D.p("z1"), 1, None)
-                if w0 == 0.0:
-                    continue
-                if kk:
-                    for _ in range(2):
-                        D.gram(Cp, kc, kk, D.p("w1"), 1, 1, "H1")
-                        D.tsmm(Cp, kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("w1"), 1)
-                        D.tsmm(D.p("U"), kc, kk, D.smp("H1"), 1, -1.0, 1.0, D.p("z1"), 1)
-                nw = _colnorms(D, D.p("w1"), 1, 1)[0]
-                if nw <= 1e-10 * w0:
-                    continue
-                D.axpby(1, 1.0 / nw, D.p("w1"), 1, None, 0.0, D.p("C", kk), kc, None)
-                D.axpby(1, 1.0 / nw, D.p("z1"), 1, None, 0.0, D.p("U", kk), kc, None)
-                kk += 1
+            kk = D.fold(k, na)
             if kk > cfg.outer_space_dim:
                 drop = kk - cfg.outer_space_dim
                 keep = cfg.outer_space_dim
