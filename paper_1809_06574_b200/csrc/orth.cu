@@ -38,6 +38,7 @@ namespace pmp {
 
 constexpr int kOrthT = 256;
 constexpr double kCholRatio = 1e-5;
+constexpr double kSkipKappa = 4.0;
 
 struct OrthParams {
   int n;
@@ -358,7 +359,14 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
     if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
   }
   __syncthreads();
+  // a well-conditioned block (|R_00| / |R_mm| <= 4) is orthonormal to
+  // ~16 eps after one Cholesky-QR pass: skip the second reduction
+  bool single = false;
   if (flag[0] == 0) {
+    const double kap = fabs(R1[0]) / fabs(R1[(sb - 1) * sb + (sb - 1)]);
+    single = kap <= kSkipKappa;
+  }
+  if (flag[0] == 0 && !single) {
     block_trsm_rows(Wv, ldw, Q1, ldq, nr, sb, R1, piv);
     // ---- R3: Q1^T Q1 ---------------------------------------------------------
     const Rows Qv{Q1, ldq, sb, Q1, ldq};
@@ -378,8 +386,14 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.outFlag = 1.0;
     return;
   }
-  // Q = Q1 R2^-1 -> V[:, qout : qout + sb]
-  block_trsm_rows(Q1, ldq, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R2, nullptr);
+  if (single) {
+    // Q = W P R1^-1 -> V[:, qout : qout + sb], R2 = I
+    block_trsm_rows(Wv, ldw, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R1, piv);
+    for (int q = threadIdx.x; q < sb * sb; q += kOrthT) R2[q] = (q / sb == q % sb) ? 1.0 : 0.0;
+    __syncthreads();
+  } else {
+    block_trsm_rows(Q1, ldq, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R2, nullptr);
+  }
   if (blockIdx.x == 0) {
     // R = R2 R1 (pivoted column order), un-pivoted: Rout[i, piv[c]] = R[i, c]
     for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {

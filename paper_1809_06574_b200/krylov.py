@@ -271,16 +271,16 @@ def _project_deflate(D, k, total, npass, Wp, sb, qout, tol, report):
     the orthonormal block written to V[:, qout:] (krylov.py:156-165,
     :189-202).  C^T W, the two CGS coefficient blocks land in the small
     buffer slots G1, G2, G3 (fetched)."""
+    _project_launch(D, k, total, npass, Wp, sb, qout)
+    return _project_finish(D, Wp, sb, qout, tol, report)
+
+
+def _project_launch(D, k, total, npass, Wp, sb, qout):
+    """Enqueue the projection + QR of one block step (no host sync)."""
     s, cap, kc = D.s, D.cap, D.kc
     if D.fused:
         D.orth(k, total, npass, Wp, sb, qout)
-        D.fetch(("FLAG", 1))
-        if D.get("FLAG", 1, 1)[0, 0] == 0.0:
-            return sb, D.get("RT", sb, sb).copy()
-        report.deflation_fallbacks += 1
-        D.tsqr(Wp, s, sb)
-        D.fetch(("FLAG", 1))
-        return _deflate_finish(D, Wp, s, sb, D.p("V", qout), cap, tol, report)
+        return
     if k:
         D.gram(D.p("C"), kc, k, Wp, s, sb, "G1")
         D.tsmm(D.p("C"), kc, k, D.smp("G1"), sb, -1.0, 1.0, Wp, s)
@@ -288,7 +288,20 @@ def _project_deflate(D, k, total, npass, Wp, sb, qout, tol, report):
         D.gram(D.p("V"), cap, total, Wp, s, sb, g)
         D.tsmm(D.p("V"), cap, total, D.smp(g), sb, -1.0, 1.0, Wp, s)
     D.tsqr(Wp, s, sb)
+
+
+def _project_finish(D, Wp, sb, qout, tol, report):
+    """Fetch the step's small results; finish the rank-revealing QR on the
+    host when the fused kernel could not (or the unfused path is used).
+    Returns (rank, R[:rank] un-pivoted)."""
+    s, cap = D.s, D.cap
     D.fetch(("FLAG", 1))
+    if D.fused:
+        if D.get("FLAG", 1, 1)[0, 0] == 0.0:
+            return sb, D.get("RT", sb, sb).copy()
+        report.deflation_fallbacks += 1
+        D.tsqr(Wp, s, sb)
+        D.fetch(("FLAG", 1))
     return _deflate_finish(D, Wp, s, sb, D.p("V", qout), cap, tol, report)
 
 
@@ -420,9 +433,7 @@ def _solve(A, B, P, cfg):
         st = A.structure
         D._call("pmp_spmm", spmm, st.n, st.rowptr.data_ptr(), st.colidx.data_ptr(), A.vals.data_ptr(), sb,
                    src, lds, 1.0, 0.0, None, 0, Wp, s, D.st)
-        if chain:
-            report.precond_apply_count += sb
-        report.matvec_count += sb
+
 
     k = 0          # outer-space dimension (columns of C / U in use)
     while active.size and report.iterations < cfg.max_iters:
@@ -449,14 +460,22 @@ def _solve(A, B, P, cfg):
         Wp = D.p("W")
         Vp = D.p("V")
         Cp = D.p("C")
+        launched = False   # the current step's kernels are already enqueued
         while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
                and m < cfg.inner_restart):
             q0, q1 = m, total
             sb = q1 - q0
-            op(D.p("V", q0), cap, sb, Wp)
+            if not launched:
+                op(D.p("V", q0), cap, sb, Wp)
+                _project_launch(D, k, total, 2, Wp, sb, total)
+            launched = False
             report.iterations += 1
-            bs_next, Rn = _project_deflate(D, k, total, 2, Wp, sb, total, cfg.deflation_tol,
-                                           report)
+            if chain:
+                report.precond_apply_count += sb
+            report.matvec_count += sb
+            fb0 = report.deflation_fallbacks
+            bs_next, Rn = _project_finish(D, Wp, sb, total, cfg.deflation_tol, report)
+            fast = D.fused and bs_next == sb and report.deflation_fallbacks == fb0
             if k:
                 Bmat[:, q0:q1] = D.get("G1", k, sb)
             Hb[:total, q0:q1] += D.get("G2", total, sb)
@@ -464,6 +483,15 @@ def _solve(A, B, P, cfg):
             Hb[total:total + bs_next, q0:q1] = Rn
             m = total
             total += bs_next
+            # enqueue the next step before the host solves the projected
+            # problem: if that solve declares convergence the speculative
+            # step is simply discarded (it only writes scratch and columns
+            # of V beyond `total`)
+            if (fast and bs_next > 0 and report.iterations < cfg.max_iters
+                    and m < cfg.inner_restart):
+                op(D.p("V", m), cap, bs_next, Wp)
+                _project_launch(D, k, total, 2, Wp, bs_next, total)
+                launched = True
             Y, rn = proj.append(Bmat, Hb, q0, q1, total, m)
             est = _safe_rel(rn, bn_act)
             last_rel[active] = est
