@@ -189,6 +189,32 @@ int pmp_fold(int n, int na, const double* d_img, int ldi, const double* d_dz, in
              double* d_C, double* d_U, int ldc, int kc, int k0, double* d_out, void* d_ws,
              size_t ws_bytes, void* stream);
 
+/* ---- native block-step driver (krylov.py:184-216) ------------------------
+ * Pinned, device-mapped host memory for zero-copy step results. */
+int pmp_host_alloc_mapped(size_t bytes, void** h_ptr);
+int pmp_host_free_mapped(void* h_ptr);
+int pmp_host_device_ptr(void* h_ptr, void** d_ptr);
+/* Spin until *h_flag != sentinel (written last by the step kernel); after
+ * timeout_us, synchronise the stream instead. */
+int pmp_host_wait_flag(const double* h_flag, double sentinel, long long timeout_us, void* stream);
+/* Enqueue one block step: W = A F_0 ... F_{nfac-1} V[:, q0:q0+sb] (host
+ * arrays of the factors' device CSR pointers, outermost first), then
+ * pmp_orth_step with its small outputs at out_small + off* (mapped host
+ * memory); out_small[offFlag] is set to the sentinel -1 first. */
+int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* h_fac_rowptr,
+                  const int32_t* const* h_fac_colidx, const double* const* h_fac_vals,
+                  const int32_t* d_a_rowptr, const int32_t* d_a_colidx, const double* d_a_vals,
+                  double* d_V, int cap, int q0, int sb, double* d_W, double* d_T0, double* d_T1,
+                  double* d_T2, const double* d_C, int kc, int k, int total, double* out_small,
+                  int offB, int offH1, int offH2, int offR, int offFlag, void* d_ws,
+                  size_t ws_bytes, void* stream);
+/* Fold a finished full-rank step into Bmat / Hb (krylov.py:190-200) and the
+ * incremental QR of G (pmp_host_hls_append). */
+int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int offR, int cap,
+                    int k, int q0, int sb, int total, double* h_Bmat, double* h_Hb, int ldq,
+                    int nrhs, int ncols_old, double* h_QR, double* h_tau, int* h_ext,
+                    double* h_C, double* h_Y, double* h_resnorm, double* h_colsbuf);
+
 /* ---- helpers ------------------------------------------------------------ */
 /* dst[:, dst_cols[c]] = src[:, src_cols[c]] for c < nc (NULL = identity). */
 int pmp_copy_cols(int n, int nc, const double* d_src, int lds, const int32_t* d_src_cols,

@@ -71,6 +71,16 @@ _SIGS = {
     "pmp_fold_workspace": ([c_int, c_int], c_sz),
     "pmp_fold": ([c_int, c_int, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_int, c_int, c_int, c_vp,
                   c_vp, c_sz, c_vp], c_int),
+    "pmp_host_alloc_mapped": ([c_sz, c_vp], c_int),
+    "pmp_host_free_mapped": ([c_vp], c_int),
+    "pmp_host_device_ptr": ([c_vp, c_vp], c_int),
+    "pmp_host_wait_flag": ([c_vp, c_dbl, ctypes.c_longlong, c_vp], c_int),
+    "pmp_gcro_step": ([c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
+                       c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp,
+                       c_int, c_int, c_int, c_int, c_int, c_vp, c_sz, c_vp], c_int),
+    "pmp_gcro_absorb": ([c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                         c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                         c_vp], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp, c_vp], c_int),
@@ -126,7 +136,31 @@ def stream():
 _LAUNCHES_PER_CALL = {"pmp_scan": 2, "pmp_transpose": 5, "pmp_pattern_l0": 5,
                       "pmp_pattern_l0_ptr": 3, "pmp_compact_zeros": 4, "pmp_select_gt": 4,
                       "pmp_augment": 1}
-_NO_LAUNCH = {"pmp_last_error", "pmp_version", "pmp_host_deflate", "pmp_host_hls_append"}
+_NO_LAUNCH = {"pmp_last_error", "pmp_version", "pmp_host_deflate", "pmp_host_hls_append",
+              "pmp_host_alloc_mapped", "pmp_host_free_mapped", "pmp_host_device_ptr",
+              "pmp_host_wait_flag", "pmp_gcro_absorb"}
+# pmp_gcro_step launches the SpMM chain (1 + depth) and the orthogonalisation
+_LAUNCHES_PER_CALL["pmp_gcro_step"] = 4
+
+
+class MappedBuffer:
+    """Pinned, device-mapped host memory (zero-copy results of the block
+    step kernels); freed with the object."""
+
+    def __init__(self, ndoubles):
+        import numpy as np
+        p = ctypes.c_void_p()
+        check(lib().pmp_host_alloc_mapped(8 * ndoubles, ctypes.byref(p)), "pmp_host_alloc_mapped")
+        self.ptr = p.value
+        self.array = np.ctypeslib.as_array((ctypes.c_double * ndoubles).from_address(self.ptr))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib().pmp_host_free_mapped(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
 
 COUNTERS = {}          # name -> calls (enabled by count_launches())
 _counting = False

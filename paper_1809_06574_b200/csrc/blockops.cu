@@ -579,7 +579,7 @@ int pmp_tsqr_r(int n, int nz, const double* Z, int ldz, double* R, void* ws, siz
   int nb, chunk, sub;
   tsqr_geometry(n, nz, &nb, &chunk, &sub);
   size_t sm = tsqr_smem(nz, sub);
-  cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  prepare_smem((const void*)k_tsqr, sm, kTsqrT);
   k_tsqr<<<nb, kTsqrT, sm, reinterpret_cast<cudaStream_t>(st)>>>(
       n, nz, Z, ldz, chunk, sub, (double*)((char*)ws + 256), (unsigned*)ws, R);
   return cuda_status("pmp_tsqr_r");

@@ -88,6 +88,44 @@ __device__ __forceinline__ int lower_bound_i(const int* a, int n, int key) {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Raise a kernel's dynamic shared-memory limit (only ever upwards, so any
+// smaller launch stays valid) and return how many blocks of `threads` fit
+// per SM.  Both are cached: the CUDA attribute / occupancy queries cost
+// microseconds of host time, and the block-Krylov loop launches these
+// kernels tens of thousands of times.  One device per process.
+inline int prepare_smem(const void* fn, size_t smem, int threads) {
+  struct Lim {
+    const void* fn;
+    size_t max_smem;
+  };
+  struct Occ {
+    const void* fn;
+    size_t smem;
+    int threads, bps;
+  };
+  static Lim lim[64];
+  static int nlim = 0;
+  static Occ occ[256];
+  static int nocc = 0;
+  for (int i = 0; i < nocc; ++i)
+    if (occ[i].fn == fn && occ[i].smem == smem && occ[i].threads == threads) return occ[i].bps;
+  int li = -1;
+  for (int i = 0; i < nlim; ++i)
+    if (lim[i].fn == fn) li = i;
+  if (li < 0 && nlim < 64) {
+    li = nlim++;
+    lim[li] = {fn, 0};
+  }
+  if (li < 0 || lim[li].max_smem < smem) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (li >= 0) lim[li].max_smem = smem;
+  }
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, threads, smem);
+  if (nocc < 256) occ[nocc++] = {fn, smem, threads, bps};
+  return bps;
+}
+
 inline int next_pow2(int v) {
   int p = 1;
   while (p < v) p <<= 1;

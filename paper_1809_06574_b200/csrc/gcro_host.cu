@@ -1,0 +1,165 @@
+// Native per-step driver of block GCRO (krylov.py:184-216).
+//
+// At BASELINE sizes a block step is ~50 us of device work, so the host side
+// of a step -- launching the operator and the orthogonalisation, waiting for
+// the small results, and folding them into the projected least-squares
+// problem -- must cost about as much or less.  Through Python + numpy it
+// cost ~150 us.  These entry points keep the reference's control flow in
+// the Python caller but make each step two native calls:
+//   pmp_gcro_step   : enqueue W = A P V[:, q0:q0+sb] (chain of SpMMs) and the
+//                     fused orthogonalisation (pmp_orth_step) whose small
+//                     outputs land directly in mapped (zero-copy) host memory;
+//   pmp_gcro_absorb : spin on the step's flag in that memory, then update
+//                     Bmat / Hb (krylov.py:190-202) and append the new block
+//                     columns to the incremental QR of G (pmp_host_hls_append).
+#include <chrono>
+
+#include "common.cuh"
+
+extern "C" {
+
+int pmp_host_alloc_mapped(size_t bytes, void** host) {
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    pmp::set_error("pmp_host_alloc_mapped: %s", cudaGetErrorString(e));
+    return PMP_ERR_CUDA;
+  }
+  *host = p;
+  return PMP_OK;
+}
+
+int pmp_host_free_mapped(void* host) {
+  cudaError_t e = cudaFreeHost(host);
+  if (e != cudaSuccess) {
+    pmp::set_error("pmp_host_free_mapped: %s", cudaGetErrorString(e));
+    return PMP_ERR_CUDA;
+  }
+  return PMP_OK;
+}
+
+// device-side address of mapped host memory (identical under UVA)
+int pmp_host_device_ptr(void* host, void** dev) {
+  cudaError_t e = cudaHostGetDevicePointer(dev, host, 0);
+  if (e != cudaSuccess) {
+    pmp::set_error("pmp_host_device_ptr: %s", cudaGetErrorString(e));
+    return PMP_ERR_CUDA;
+  }
+  return PMP_OK;
+}
+
+// Spin until *flag != sentinel (the kernel writes it last, after a
+// system-scope fence).  After `timeout_us` fall back to synchronising the
+// stream; returns PMP_OK when the flag arrived, PMP_ERR_CUDA otherwise.
+int pmp_host_wait_flag(const double* flag, double sentinel, long long timeout_us, void* stream) {
+  const volatile double* f = flag;
+  auto t0 = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  while (*f == sentinel) {
+    if ((++spins & 1023u) == 0) {
+      auto us = std::chrono::duration_cast<std::chrono::microseconds>(
+                    std::chrono::steady_clock::now() - t0)
+                    .count();
+      if (us > timeout_us) {
+        cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) {
+          pmp::set_error("pmp_host_wait_flag: %s", cudaGetErrorString(e));
+          return PMP_ERR_CUDA;
+        }
+        if (*f == sentinel) {
+          pmp::set_error("pmp_host_wait_flag: stream finished without writing the flag");
+          return PMP_ERR_CUDA;
+        }
+        break;
+      }
+    }
+  }
+  return PMP_OK;
+}
+
+int pmp_spmm(int n, const int32_t* rowptr, const int32_t* colidx, const double* vals, int s,
+             const double* X, int ldx, double alpha, double beta, const double* Y0, int ldy0,
+             double* Y, int ldy, void* st);
+int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, int total, int npass,
+                  double* W, int ldw, int sb, int qout, double* outB, double* outH1,
+                  double* outH2, double* outR, double* outFlag, void* ws, size_t ws_bytes,
+                  void* stream);
+
+int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* fac_rowptr,
+                  const int32_t* const* fac_colidx, const double* const* fac_vals,
+                  const int32_t* a_rowptr, const int32_t* a_colidx, const double* a_vals,
+                  double* V, int cap, int q0, int sb, double* W, double* T0, double* T1,
+                  double* T2, const double* C, int kc, int k, int total, double* out_small,
+                  int offB, int offH1, int offH2, int offR, int offFlag, void* ws,
+                  size_t ws_bytes, void* stream) {
+  // W = A F_0 F_1 ... F_{nfac-1} V[:, q0 : q0 + sb], applied right to left
+  const double* src = V + q0;
+  int lds = cap;
+  double* tmp[2] = {T0, T1};
+  for (int i = nfac - 1; i >= 0; --i) {
+    double* dst = (i == 0) ? T2 : tmp[(nfac - 1 - i) % 2];
+    int rc = pmp_spmm(n, fac_rowptr[i], fac_colidx[i], fac_vals[i], sb, src, lds, 1.0, 0.0,
+                      nullptr, 0, dst, s, stream);
+    if (rc) return rc;
+    src = dst;
+    lds = s;
+  }
+  int rc = pmp_spmm(n, a_rowptr, a_colidx, a_vals, sb, src, lds, 1.0, 0.0, nullptr, 0, W, s,
+                    stream);
+  if (rc) return rc;
+  out_small[offFlag] = -1.0;  // sentinel, overwritten by the kernel's last write
+  return pmp_orth_step(n, C, kc, k, V, cap, total, 2, W, s, sb, total, out_small + offB,
+                       out_small + offH1, out_small + offH2, out_small + offR,
+                       out_small + offFlag, ws, ws_bytes, stream);
+}
+
+int pmp_host_hls_append(int ldq, int nrhs, int ncols_old, int nnew, int nrows,
+                        const double* newcols, double* QR, double* tau, int* ext, double* C,
+                        double* Y, double* resnorm);
+
+// Fold a finished fast-path step (rank == sb) into the projected problem:
+// Bmat[:, q0:q1] = B, Hb[:total, q0:q1] += H1, += H2 (krylov.py:190-196),
+// Hb[total:total+sb, q0:q1] = R (krylov.py:198-200), then append the new
+// block columns of G to its incremental QR (first call also adds the k
+// identity columns).  Hb: cap x cap row-major, Bmat: k x cap row-major.
+// Returns the pmp_host_hls_append code (1 = G rank deficient).
+int pmp_gcro_absorb(const double* small, int offB, int offH1, int offH2, int offR, int cap, int k,
+                    int q0, int sb, int total, double* Bmat, double* Hb, int ldq, int nrhs,
+                    int ncols_old, double* QR, double* tau, int* ext, double* Cq, double* Y,
+                    double* resnorm, double* colsbuf) {
+  const double* B = small + offB;
+  const double* H1 = small + offH1;
+  const double* H2 = small + offH2;
+  const double* R = small + offR;
+  for (int i = 0; i < k; ++i)
+    for (int c = 0; c < sb; ++c) Bmat[(size_t)i * cap + q0 + c] = B[i * sb + c];
+  for (int i = 0; i < total; ++i)
+    for (int c = 0; c < sb; ++c) {
+      double h = Hb[(size_t)i * cap + q0 + c];
+      h += H1[i * sb + c];
+      h += H2[i * sb + c];
+      Hb[(size_t)i * cap + q0 + c] = h;
+    }
+  for (int i = 0; i < sb; ++i)
+    for (int c = 0; c < sb; ++c) Hb[(size_t)(total + i) * cap + q0 + c] = R[i * sb + c];
+  const int tot_new = total + sb;
+  const int nrows = k + tot_new;
+  const bool first = ncols_old == 0;
+  const int nnew = first ? k + sb : sb;
+  // new columns of G (column-major nrows x nnew)
+  for (int q = 0; q < nrows * nnew; ++q) colsbuf[q] = 0.0;
+  int o = 0;
+  if (first) {
+    for (int i = 0; i < k; ++i) colsbuf[i + (size_t)i * nrows] = 1.0;
+    o = k;
+  }
+  for (int c = 0; c < sb; ++c) {
+    double* col = colsbuf + (size_t)(o + c) * nrows;
+    for (int i = 0; i < k; ++i) col[i] = Bmat[(size_t)i * cap + q0 + c];
+    for (int i = 0; i < tot_new; ++i) col[k + i] = Hb[(size_t)i * cap + q0 + c];
+  }
+  return pmp_host_hls_append(ldq, nrhs, ncols_old, nnew, nrows, colsbuf, QR, tau, ext, Cq, Y,
+                             resnorm);
+}
+
+}  // extern "C"

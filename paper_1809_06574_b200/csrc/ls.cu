@@ -695,7 +695,7 @@ static int launch_ls(LsParams P, cudaStream_t st, size_t ws_bytes) {
       set_error("pmp_ls_columns: team needs %zu B of shared memory", sm);
       return PMP_ERR_ARG;
     }
-    cudaFuncSetAttribute(k_ls<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    prepare_smem((const void*)k_ls<T, false>, sm, T * per_block);
     int grid = ceil_div(P.ncols, per_block);
     k_ls<T, false><<<grid, T * per_block, sm, st>>>(P);
   }
@@ -722,7 +722,7 @@ static int launch_aug(AugParams P, cudaStream_t st, size_t ws_bytes) {
       set_error("pmp_augment: team needs %zu B of shared memory", sm);
       return PMP_ERR_ARG;
     }
-    cudaFuncSetAttribute(k_aug<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    prepare_smem((const void*)k_aug<T, false>, sm, T * per_block);
     k_aug<T, false><<<ceil_div(P.ncols, per_block), T * per_block, sm, st>>>(P);
   }
   return cuda_status("pmp_augment");

@@ -144,7 +144,7 @@ __device__ void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, do
       }
     }
   }
-  __threadfence();
+  __threadfence_system();   // outputs may be mapped host memory
   grid.sync();
   for (int o = threadIdx.x; o < K; o += kOrthT) G[o] = __ldcg(P.gout + o);
   __syncthreads();
@@ -383,7 +383,9 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
     if (CACHED)
       for (int q = threadIdx.x; q < nr * sb; q += kOrthT)
         P.W[(size_t)(r0 + q / sb) * P.ldw + q % sb] = Wv[(size_t)(q / sb) * ldw + q % sb];
-    if (blockIdx.x == 0 && threadIdx.x == 0) *P.outFlag = 1.0;
+    __threadfence_system();
+    grid.sync();   // every block's W rows are written back before the flag
+    if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile double*)P.outFlag = 1.0;
     return;
   }
   if (single) {
@@ -402,7 +404,14 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
       for (int a = i; a <= c; ++a) s += R2[i * sb + a] * R1[a * sb + c];
       P.outR[i * sb + piv[c]] = (c >= i) ? s : 0.0;
     }
-    if (threadIdx.x == 0) *P.outFlag = 0.0;
+    // the outputs may live in mapped host memory that the host polls:
+    // make every write visible system-wide before the flag
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *(volatile double*)P.outFlag = 0.0;
+    }
   }
 }
 
@@ -596,9 +605,7 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
   size_t smem;
   orth_geometry(n, total, k, sb, &g, &rows, &cached, &smem);
   void* fn = cached ? (void*)k_orth<true> : (void*)k_orth<false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kOrthT, smem);
+  const int bps = prepare_smem(fn, smem, kOrthT);
   if (bps < 1) {
     set_error("pmp_orth_step: kernel does not fit on an SM (smem %zu)", smem);
     return PMP_ERR_ARG;
@@ -661,7 +668,7 @@ int pmp_fold(int n, int na, const double* img, int ldi, const double* dz, int ld
   const int cached = fold_smem_bytes(rows, kc, 1) <= (size_t)220 * 1024;
   const size_t smem = fold_smem_bytes(rows, kc, cached);
   void* fn = cached ? (void*)k_fold<true> : (void*)k_fold<false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  prepare_smem(fn, smem, kOrthT);
   FoldParams F;
   F.n = n;
   F.na = na;

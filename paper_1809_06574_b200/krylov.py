@@ -20,6 +20,7 @@ One small device->host copy (a few KB) per block step carries all the
 small matrices the host needs; n-sized data never leaves HBM.
 """
 
+import ctypes
 import time
 from dataclasses import dataclass, field
 
@@ -140,6 +141,16 @@ class _Dev:
         self.f_defl, self.f_hls = L.pmp_host_deflate, L.pmp_host_hls_append
         self.f_orth = L.pmp_orth_step
         self.f_fold = L.pmp_fold
+        self.f_step, self.f_wait, self.f_absorb = L.pmp_gcro_step, L.pmp_host_wait_flag, \
+            L.pmp_gcro_absorb
+        # native per-step path: results land in mapped host memory (two
+        # buffers so a speculative next step never overwrites unread ones)
+        self.native = self.fused
+        if self.native:
+            self.mapped = _mapped_pair(o)
+            self.mptr = [b.ptr for b in self.mapped]
+            self.colsbuf = np.zeros((kc + cap) * (kc + s))
+            self._chain_key = None
         self.fold_ws = sc.get("fold", L.pmp_fold_workspace(n, kc))
         self.counting = _abi._counting
         self.timing = _abi._timing_names
@@ -205,6 +216,35 @@ class _Dev:
                    self.fold_ws.data_ptr(), self.fold_ws.numel(), self.st)
         self.fetch(("H", 1))
         return int(round(self.get("H", 1, 1)[0, 0]))
+
+    def step(self, chain, A, q0, sb, k, total, buf):
+        """Enqueue one native block step (pmp_gcro_step) whose small results
+        go to mapped buffer `buf`."""
+        key = tuple(id(F) for F in chain)
+        if key != self._chain_key:
+            nf = len(chain)
+            arr = lambda vals: (ctypes.c_void_p * max(nf, 1))(*vals)
+            self._fr = arr([F.structure.rowptr.data_ptr() for F in chain])
+            self._fc = arr([F.structure.colidx.data_ptr() for F in chain])
+            self._fv = arr([F.vals.data_ptr() for F in chain])
+            self._chain_key = key
+        st = A.structure
+        off = self.off
+        self._call("pmp_gcro_step", self.f_step, self.n, self.s, len(chain), self._fr, self._fc,
+                   self._fv, st.rowptr.data_ptr(), st.colidx.data_ptr(), A.vals.data_ptr(),
+                   self.ptr["V"], self.cap, q0, sb, self.ptr["W"], self.ptr["T0"],
+                   self.ptr["T1"], self.ptr["T2"], self.ptr["C"], self.kc, k, total,
+                   self.mptr[buf], off["G1"], off["G2"], off["G3"], off["RT"], off["FLAG"],
+                   self.ows, self.owb, self.st)
+
+    def wait(self, buf):
+        rc = self.f_wait(self.mptr[buf] + 8 * self.off["FLAG"], -1.0, 60_000_000, self.st)
+        if rc:
+            _abi.check(rc, "pmp_host_wait_flag")
+
+    def mget(self, buf, name, rows, cols):
+        o = self.off[name]
+        return self.mapped[buf].array[o:o + rows * cols].reshape(rows, cols)
 
     def tsqr(self, Zp, ldz, nz):
         self._call("pmp_tsqr_r", self.f_tsqr, self.n, nz, Zp, ldz, self.smp_["RT"], self.tws, self.twb, self.st)
@@ -389,6 +429,45 @@ class _Projected:
         return Y, self.res.copy()
 
 
+    def absorb(self, D, buf, q0, sb, total, Bmat, Hb):
+        """Native fast path: fold a full-rank step (results in mapped buffer
+        `buf`) into Bmat / Hb and the incremental QR (pmp_gcro_absorb)."""
+        k = self.k
+        nnew = (k + sb) if self.ncols == 0 else sb
+        n1 = self.ncols + nnew
+        off = D.off
+        rc = D.f_absorb(D.mptr[buf], off["G1"], off["G2"], off["G3"], off["RT"], D.cap, k, q0,
+                        sb, total, Bmat.ctypes.data, Hb.ctypes.data, self.ldq, self.na,
+                        self.ncols, self.QR.ctypes.data, self.tau.ctypes.data,
+                        self.ext.ctypes.data, self.C.ctypes.data, self.Y.ctypes.data,
+                        self.res.ctypes.data, D.colsbuf.ctypes.data)
+        self.ncols = n1
+        total_new = total + sb
+        m = total
+        if rc == 1:
+            G = _build_G(k, Bmat, Hb, total_new, m)
+            rhs = self.rhs0[:k + total_new]
+            Y, _, _, _ = np.linalg.lstsq(G, rhs, rcond=None)
+            return Y, np.linalg.norm(rhs - G @ Y, axis=0)
+        if rc:
+            _abi.check(rc, "pmp_gcro_absorb")
+        Y = self.Y.ravel()[:n1 * self.na].reshape(self.na, n1).T.copy()
+        return Y, self.res.copy()
+
+
+_MAPPED = {}
+
+
+def _mapped_pair(ndoubles):
+    """Two mapped host buffers of at least `ndoubles`, cached per process."""
+    pair = _MAPPED.get("pair")
+    if pair is None or pair[0].array.size < ndoubles:
+        size = max(ndoubles, 2 * (pair[0].array.size if pair else 0))
+        pair = [_abi.MappedBuffer(size), _abi.MappedBuffer(size)]
+        _MAPPED["pair"] = pair
+    return pair
+
+
 def _build_G(k, Bmat, Hb, total, m):
     G = np.zeros((k + total, k + m))
     if k:
@@ -461,8 +540,56 @@ def _solve(A, B, P, cfg):
         Vp = D.p("V")
         Cp = D.p("C")
         launched = False   # the current step's kernels are already enqueued
+        buf = 0            # mapped result buffer of the pending native step
         while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
-               and m < cfg.inner_restart):
+               and m < cfg.inner_restart and D.native):
+            # native fast path: two library calls per block step
+            q0, q1 = m, total
+            sb = q1 - q0
+            if not launched:
+                D.step(chain, A, q0, sb, k, total, buf)
+            launched = False
+            report.iterations += 1
+            if chain:
+                report.precond_apply_count += sb
+            report.matvec_count += sb
+            D.wait(buf)
+            ms = D.mapped[buf].array
+            if ms[D.off["FLAG"]] == 0.0:
+                bs_next = sb
+                m_new, total_new = total, total + sb
+                # enqueue the next step before the host-side projected solve;
+                # if that solve declares convergence the speculative step is
+                # discarded (it only writes scratch and V columns >= total)
+                if report.iterations < cfg.max_iters and m_new < cfg.inner_restart:
+                    D.step(chain, A, m_new, sb, k, total_new, buf ^ 1)
+                    launched = True
+                Y, rn = proj.absorb(D, buf, q0, sb, total, Bmat, Hb)
+                m, total = m_new, total_new
+                if launched:
+                    buf ^= 1
+            else:
+                # Cholesky could not decide the rank: Householder fallback
+                report.deflation_fallbacks += 1
+                if k:
+                    Bmat[:, q0:q1] = D.mget(buf, "G1", k, sb)
+                Hb[:total, q0:q1] += D.mget(buf, "G2", total, sb)
+                Hb[:total, q0:q1] += D.mget(buf, "G3", total, sb)
+                D.tsqr(Wp, s, sb)
+                D.fetch(("FLAG", 1))
+                bs_next, Rn = _deflate_finish(D, Wp, s, sb, D.p("V", total), cap,
+                                              cfg.deflation_tol, report)
+                Hb[total:total + bs_next, q0:q1] = Rn
+                m = total
+                total += bs_next
+                Y, rn = proj.append(Bmat, Hb, q0, q1, total, m)
+            est = _safe_rel(rn, bn_act)
+            last_rel[active] = est
+            report.residual_history.append(last_rel.copy())
+            cycle_converged = bool(np.all(est <= cfg.tol))
+            exhausted = bs_next == 0
+        while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
+               and m < cfg.inner_restart and not D.native):
             q0, q1 = m, total
             sb = q1 - q0
             if not launched:
