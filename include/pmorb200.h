@@ -199,15 +199,16 @@ int pmp_host_device_ptr(void* h_ptr, void** d_ptr);
 int pmp_host_wait_flag(const double* h_flag, double sentinel, long long timeout_us, void* stream);
 /* Enqueue one block step: W = A F_0 ... F_{nfac-1} V[:, q0:q0+sb] (host
  * arrays of the factors' device CSR pointers, outermost first), then
- * pmp_orth_step with its small outputs at out_small + off* (mapped host
- * memory); out_small[offFlag] is set to the sentinel -1 first. */
+ * pmp_orth_step with its small outputs at d_small + off* (device), mirrored
+ * at the end of the kernel to the same offsets of h_mirror (mapped host
+ * memory, flag written last); h_mirror[offFlag] is set to -1 first. */
 int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* h_fac_rowptr,
                   const int32_t* const* h_fac_colidx, const double* const* h_fac_vals,
                   const int32_t* d_a_rowptr, const int32_t* d_a_colidx, const double* d_a_vals,
                   double* d_V, int cap, int q0, int sb, double* d_W, double* d_T0, double* d_T1,
-                  double* d_T2, const double* d_C, int kc, int k, int total, double* out_small,
-                  int offB, int offH1, int offH2, int offR, int offFlag, void* d_ws,
-                  size_t ws_bytes, void* stream);
+                  double* d_T2, const double* d_C, int kc, int k, int total, double* d_small,
+                  double* h_mirror, int offB, int offH1, int offH2, int offR, int offFlag,
+                  void* d_ws, size_t ws_bytes, void* stream);
 /* Fold a finished full-rank step into Bmat / Hb (krylov.py:190-200) and the
  * incremental QR of G (pmp_host_hls_append). */
 int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int offR, int cap,

@@ -88,6 +88,13 @@ __device__ __forceinline__ int lower_bound_i(const int* a, int n, int key) {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// pmp_orth_step with an optional zero-copy mirror of its small outputs
+// (orth.cu); used by the native block-step driver (gcro_host.cu)
+int orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, int ldv, int total,
+                       int npass, double* W, int ldw, int sb, int qout, double* outB,
+                       double* outH1, double* outH2, double* outR, double* outFlag, void* ws,
+                       size_t ws_bytes, void* stream, const double* dbase, double* mbase);
+
 // Raise a kernel's dynamic shared-memory limit (only ever upwards, so any
 // smaller launch stays valid) and return how many blocks of `threads` fit
 // per SM.  Both are cached: the CUDA attribute / occupancy queries cost

@@ -80,18 +80,14 @@ int pmp_host_wait_flag(const double* flag, double sentinel, long long timeout_us
 int pmp_spmm(int n, const int32_t* rowptr, const int32_t* colidx, const double* vals, int s,
              const double* X, int ldx, double alpha, double beta, const double* Y0, int ldy0,
              double* Y, int ldy, void* st);
-int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, int total, int npass,
-                  double* W, int ldw, int sb, int qout, double* outB, double* outH1,
-                  double* outH2, double* outR, double* outFlag, void* ws, size_t ws_bytes,
-                  void* stream);
 
 int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* fac_rowptr,
                   const int32_t* const* fac_colidx, const double* const* fac_vals,
                   const int32_t* a_rowptr, const int32_t* a_colidx, const double* a_vals,
                   double* V, int cap, int q0, int sb, double* W, double* T0, double* T1,
-                  double* T2, const double* C, int kc, int k, int total, double* out_small,
-                  int offB, int offH1, int offH2, int offR, int offFlag, void* ws,
-                  size_t ws_bytes, void* stream) {
+                  double* T2, const double* C, int kc, int k, int total, double* d_small,
+                  double* mirror, int offB, int offH1, int offH2, int offR, int offFlag,
+                  void* ws, size_t ws_bytes, void* stream) {
   // W = A F_0 F_1 ... F_{nfac-1} V[:, q0 : q0 + sb], applied right to left
   const double* src = V + q0;
   int lds = cap;
@@ -107,10 +103,10 @@ int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* fac_rowptr,
   int rc = pmp_spmm(n, a_rowptr, a_colidx, a_vals, sb, src, lds, 1.0, 0.0, nullptr, 0, W, s,
                     stream);
   if (rc) return rc;
-  out_small[offFlag] = -1.0;  // sentinel, overwritten by the kernel's last write
-  return pmp_orth_step(n, C, kc, k, V, cap, total, 2, W, s, sb, total, out_small + offB,
-                       out_small + offH1, out_small + offH2, out_small + offR,
-                       out_small + offFlag, ws, ws_bytes, stream);
+  mirror[offFlag] = -1.0;  // sentinel, overwritten by the kernel's last write
+  return pmp::orth_step_mirrored(n, C, kc, k, V, cap, total, 2, W, s, sb, total, d_small + offB,
+                                 d_small + offH1, d_small + offH2, d_small + offR,
+                                 d_small + offFlag, ws, ws_bytes, stream, d_small, mirror);
 }
 
 int pmp_host_hls_append(int ldq, int nrhs, int ncols_old, int nnew, int nrows,

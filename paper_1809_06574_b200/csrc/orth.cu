@@ -58,7 +58,34 @@ struct OrthParams {
   double* outH2;    // total x sb  (second CGS pass)
   double* outR;     // sb x sb     (R, un-pivoted, row-major)
   double* outFlag;  // 1 double: 0 ok, 1 fallback needed
+  // optional zero-copy mirror: the small outputs above live at offsets of
+  // one device buffer `dbase`; block 0 copies them to the same offsets of
+  // mapped host memory `mbase` and writes the flag there last
+  const double* dbase;
+  double* mbase;
 };
+
+// block 0, all threads: flag (and, with a mirror, the small results) out
+__device__ void publish(const OrthParams& P, double flag) {
+  if (threadIdx.x == 0) *P.outFlag = flag;
+  if (P.mbase) {
+    const int sb = P.sb;
+    const double* src[4] = {P.outB, P.outH1, P.outH2, P.outR};
+    const int len[4] = {P.k * sb, P.npass ? P.total * sb : 0, P.npass ? P.total * sb : 0,
+                        flag == 0.0 ? sb * sb : 0};
+    for (int a = 0; a < 4; ++a) {
+      if (!src[a] || len[a] == 0) continue;
+      double* dst = P.mbase + (src[a] - P.dbase);
+      for (int q = threadIdx.x; q < len[a]; q += kOrthT) dst[q] = __ldcg(src[a] + q);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *(volatile double*)(P.mbase + (P.outFlag - P.dbase)) = flag;
+    }
+  }
+}
 
 // operand view of this block's rows: columns [0, ka) from a, then from b
 struct Rows {
@@ -144,7 +171,7 @@ __device__ void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, do
       }
     }
   }
-  __threadfence_system();   // outputs may be mapped host memory
+  __threadfence();
   grid.sync();
   for (int o = threadIdx.x; o < K; o += kOrthT) G[o] = __ldcg(P.gout + o);
   __syncthreads();
@@ -383,9 +410,9 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
     if (CACHED)
       for (int q = threadIdx.x; q < nr * sb; q += kOrthT)
         P.W[(size_t)(r0 + q / sb) * P.ldw + q % sb] = Wv[(size_t)(q / sb) * ldw + q % sb];
-    __threadfence_system();
+    __threadfence();
     grid.sync();   // every block's W rows are written back before the flag
-    if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile double*)P.outFlag = 1.0;
+    if (blockIdx.x == 0) publish(P, 1.0);
     return;
   }
   if (single) {
@@ -404,14 +431,8 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
       for (int a = i; a <= c; ++a) s += R2[i * sb + a] * R1[a * sb + c];
       P.outR[i * sb + piv[c]] = (c >= i) ? s : 0.0;
     }
-    // the outputs may live in mapped host memory that the host polls:
-    // make every write visible system-wide before the flag
-    __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      *(volatile double*)P.outFlag = 0.0;
-    }
+    publish(P, 0.0);
   }
 }
 
@@ -592,6 +613,16 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
                   double* W, int ldw, int sb, int qout, double* outB, double* outH1,
                   double* outH2, double* outR, double* outFlag, void* ws, size_t ws_bytes,
                   void* stream) {
+  return pmp::orth_step_mirrored(n, C, ldc, k, V, ldv, total, npass, W, ldw, sb, qout, outB, outH1,
+                                 outH2, outR, outFlag, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+}  // extern "C"
+
+int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, int ldv, int total,
+                            int npass, double* W, int ldw, int sb, int qout, double* outB,
+                            double* outH1, double* outH2, double* outR, double* outFlag, void* ws,
+                            size_t ws_bytes, void* stream, const double* dbase, double* mbase) {
   if (n < 1 || sb < 1 || sb > 16 || k < 0 || total < 0 || (k && ldc < k) || ldw < sb ||
       ldv < qout + sb || (total && ldv < total) || (npass != 0 && npass != 2)) {
     set_error("pmp_orth_step: bad arguments (n=%d k=%d total=%d sb=%d)", n, k, total, sb);
@@ -634,6 +665,8 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
   P.outH2 = outH2;
   P.outR = outR;
   P.outFlag = outFlag;
+  P.dbase = dbase;
+  P.mbase = mbase;
   void* args[] = {&P};
   cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem,
                                               reinterpret_cast<cudaStream_t>(stream));
@@ -643,6 +676,8 @@ int pmp_orth_step(int n, const double* C, int ldc, int k, double* V, int ldv, in
   }
   return cuda_status("pmp_orth_step");
 }
+
+extern "C" {
 
 size_t pmp_fold_workspace(int n, int kc) {
   int g, r, c;

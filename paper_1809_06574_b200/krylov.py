@@ -234,7 +234,8 @@ class _Dev:
                    self._fv, st.rowptr.data_ptr(), st.colidx.data_ptr(), A.vals.data_ptr(),
                    self.ptr["V"], self.cap, q0, sb, self.ptr["W"], self.ptr["T0"],
                    self.ptr["T1"], self.ptr["T2"], self.ptr["C"], self.kc, k, total,
-                   self.mptr[buf], off["G1"], off["G2"], off["G3"], off["RT"], off["FLAG"],
+                   self.smbase, self.mptr[buf], off["G1"], off["G2"], off["G3"], off["RT"],
+                   off["FLAG"],
                    self.ows, self.owb, self.st)
 
     def wait(self, buf):
