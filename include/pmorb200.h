@@ -209,6 +209,18 @@ int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* h_fac_rowptr,
                   double* d_T2, const double* d_C, int kc, int k, int total, double* d_small,
                   double* h_mirror, int offB, int offH1, int offH2, int offR, int offFlag,
                   void* d_ws, size_t ws_bytes, void* stream);
+/* End of a GCRO cycle (krylov.py:221-234), enqueued natively:
+ *   dX = V[:, :m] Yv + U[:, :k] Yu ; Xt[:, act] += dX ; Xa = P Xt[:, act] ;
+ *   X[:, act] = Xa ; Rb = B[:, act] - A Xa ; R[:, act] = Rb ; nrm = Rb^T Rb. */
+int pmp_gcro_cycle_end(int n, int s, int na, const int32_t* d_act, const double* d_V, int cap,
+                       int m, const double* d_Yv, const double* d_U, int kc, int k,
+                       const double* d_Yu, double* d_dX, double* d_Xt, double* d_Z,
+                       double* d_Xa, double* d_X, const double* d_B, double* d_Rb, double* d_R,
+                       int nfac, const int32_t* const* h_fac_rowptr,
+                       const int32_t* const* h_fac_colidx, const double* const* h_fac_vals,
+                       const int32_t* d_a_rowptr, const int32_t* d_a_colidx,
+                       const double* d_a_vals, double* d_T0, double* d_T1, double* d_nrm,
+                       void* d_gram_ws, size_t gram_ws_bytes, void* stream);
 /* Fold a finished full-rank step into Bmat / Hb (krylov.py:190-200) and the
  * incremental QR of G (pmp_host_hls_append). */
 int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int offR, int cap,

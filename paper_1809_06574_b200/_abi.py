@@ -78,6 +78,10 @@ _SIGS = {
     "pmp_gcro_step": ([c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
                        c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp,
                        c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_sz, c_vp], c_int),
+    "pmp_gcro_cycle_end": ([c_int, c_int, c_int, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_int,
+                            c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
+                            c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
+                            c_vp], c_int),
     "pmp_gcro_absorb": ([c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                          c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                          c_vp], c_int),

@@ -109,6 +109,59 @@ int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* fac_rowptr,
                                  d_small + offFlag, ws, ws_bytes, stream, d_small, mirror);
 }
 
+int pmp_tsmm(int n, int kv, const double* V, int ldv, int nc, const double* H, double alpha,
+             double beta, double* Out, int ldo, void* st);
+int pmp_axpby_cols(int n, int nc, double alpha, const double* src, int lds, const int32_t* sc,
+                   double beta, double* dst, int ldd, const int32_t* dc, void* st);
+int pmp_copy_cols(int n, int nc, const double* src, int lds, const int32_t* sc, double* dst,
+                  int ldd, const int32_t* dc, void* st);
+int pmp_gram(int n, int kv, const double* V, int ldv, int nw, const double* W, int ldw,
+             double* G, void* ws, size_t bytes, void* st);
+
+// End of a GCRO cycle (krylov.py:221-234), all on the device:
+//   dX = V[:, :m] Yv + U[:, :k] Yu ; Xt[:, act] += dX
+//   Xa = P Xt[:, act] ; X[:, act] = Xa
+//   Rb = B[:, act] - A Xa ; R[:, act] = Rb ; nrm = Rb^T Rb
+// Blocks are n x s row-major (ld s); Yv (m x na), Yu (k x na), nrm (na x na)
+// are device matrices.
+int pmp_gcro_cycle_end(int n, int s, int na, const int32_t* act, const double* V, int cap, int m,
+                       const double* Yv, const double* U, int kc, int k, const double* Yu,
+                       double* dX, double* Xt, double* Z, double* Xa, double* X, const double* B,
+                       double* Rb, double* R, int nfac, const int32_t* const* fac_rowptr,
+                       const int32_t* const* fac_colidx, const double* const* fac_vals,
+                       const int32_t* a_rowptr, const int32_t* a_colidx, const double* a_vals,
+                       double* T0, double* T1, double* nrm, void* gram_ws, size_t gram_ws_bytes,
+                       void* stream) {
+  int rc;
+  if (m > 0) {
+    if ((rc = pmp_tsmm(n, m, V, cap, na, Yv, 1.0, 0.0, dX, s, stream))) return rc;
+  } else if ((rc = pmp_axpby_cols(n, na, 0.0, dX, s, nullptr, 0.0, dX, s, nullptr, stream))) {
+    return rc;
+  }
+  if (k > 0 && (rc = pmp_tsmm(n, k, U, kc, na, Yu, 1.0, 1.0, dX, s, stream))) return rc;
+  if ((rc = pmp_axpby_cols(n, na, 1.0, dX, s, nullptr, 1.0, Xt, s, act, stream))) return rc;
+  if ((rc = pmp_copy_cols(n, na, Xt, s, act, Z, s, nullptr, stream))) return rc;
+  const double* xa = Z;
+  if (nfac > 0) {
+    const double* src = Z;
+    double* tmp[2] = {T0, T1};
+    for (int i = nfac - 1; i >= 0; --i) {
+      double* dst = (i == 0) ? Xa : tmp[(nfac - 1 - i) % 2];
+      if ((rc = pmp_spmm(n, fac_rowptr[i], fac_colidx[i], fac_vals[i], na, src, s, 1.0, 0.0,
+                         nullptr, 0, dst, s, stream)))
+        return rc;
+      src = dst;
+    }
+    xa = Xa;
+  }
+  if ((rc = pmp_copy_cols(n, na, xa, s, nullptr, X, s, act, stream))) return rc;
+  if ((rc = pmp_copy_cols(n, na, B, s, act, Rb, s, nullptr, stream))) return rc;
+  if ((rc = pmp_spmm(n, a_rowptr, a_colidx, a_vals, na, xa, s, -1.0, 1.0, Rb, s, Rb, s, stream)))
+    return rc;
+  if ((rc = pmp_copy_cols(n, na, Rb, s, nullptr, R, s, act, stream))) return rc;
+  return pmp_gram(n, na, Rb, s, na, Rb, s, nrm, gram_ws, gram_ws_bytes, stream);
+}
+
 int pmp_host_hls_append(int ldq, int nrhs, int ncols_old, int nnew, int nrows,
                         const double* newcols, double* QR, double* tau, int* ext, double* C,
                         double* Y, double* resnorm);

@@ -145,12 +145,13 @@ class _Dev:
             L.pmp_gcro_absorb
         # native per-step path: results land in mapped host memory (two
         # buffers so a speculative next step never overwrites unread ones)
+        self.f_cend = L.pmp_gcro_cycle_end
+        self._chain_key = None
         self.native = self.fused
         if self.native:
             self.mapped = _mapped_pair(o)
             self.mptr = [b.ptr for b in self.mapped]
             self.colsbuf = np.zeros((kc + cap) * (kc + s))
-            self._chain_key = None
         self.fold_ws = sc.get("fold", L.pmp_fold_workspace(n, kc))
         self.counting = _abi._counting
         self.timing = _abi._timing_names
@@ -176,6 +177,17 @@ class _Dev:
         self.launches += 1
         if self.counting:
             _abi.COUNTERS[name] = _abi.COUNTERS.get(name, 0) + 1
+
+    def set_active(self, active):
+        """Active column list on the device without a synchronising
+        pageable copy (pinned staging + async copy); returns its pointer."""
+        if not hasattr(self, "act_d"):
+            self.act_d = torch.empty(self.s, dtype=torch.int32, device=_dev())
+            self.act_h = torch.empty(self.s, dtype=torch.int32, pin_memory=True)
+        na = len(active)
+        self.act_h.numpy()[:na] = active
+        self.act_d[:na].copy_(self.act_h[:na], non_blocking=True)
+        return self.act_d.data_ptr()
 
     def p(self, name, col=0):
         return self.ptr[name] + 8 * col
@@ -220,14 +232,7 @@ class _Dev:
     def step(self, chain, A, q0, sb, k, total, buf):
         """Enqueue one native block step (pmp_gcro_step) whose small results
         go to mapped buffer `buf`."""
-        key = tuple(id(F) for F in chain)
-        if key != self._chain_key:
-            nf = len(chain)
-            arr = lambda vals: (ctypes.c_void_p * max(nf, 1))(*vals)
-            self._fr = arr([F.structure.rowptr.data_ptr() for F in chain])
-            self._fc = arr([F.structure.colidx.data_ptr() for F in chain])
-            self._fv = arr([F.vals.data_ptr() for F in chain])
-            self._chain_key = key
+        self._chain_arrays(chain)
         st = A.structure
         off = self.off
         self._call("pmp_gcro_step", self.f_step, self.n, self.s, len(chain), self._fr, self._fc,
@@ -237,6 +242,28 @@ class _Dev:
                    self.smbase, self.mptr[buf], off["G1"], off["G2"], off["G3"], off["RT"],
                    off["FLAG"],
                    self.ows, self.owb, self.st)
+
+    def _chain_arrays(self, chain):
+        key = tuple(id(F) for F in chain)
+        if key != self._chain_key:
+            nf = len(chain)
+            arr = lambda vals: (ctypes.c_void_p * max(nf, 1))(*vals)
+            self._fr = arr([F.structure.rowptr.data_ptr() for F in chain])
+            self._fc = arr([F.structure.colidx.data_ptr() for F in chain])
+            self._fv = arr([F.vals.data_ptr() for F in chain])
+            self._chain_key = key
+
+    def cycle_end(self, na, act_p, m, hv, k, hu, Xtp, Xp, Bp, Rp, chain, A):
+        """Solution / true-residual update of a finished cycle
+        (pmp_gcro_cycle_end); column norms land in NRM."""
+        self._chain_arrays(chain)
+        st = A.structure
+        self._call("pmp_gcro_cycle_end", self.f_cend, self.n, self.s, na, act_p, self.ptr["V"],
+                   self.cap, m, hv, self.ptr["U"], self.kc, k, hu, self.ptr["dX"], Xtp,
+                   self.ptr["Z"], self.ptr["Xa"], Xp, Bp, self.ptr["Rb"], Rp, len(chain),
+                   self._fr, self._fc, self._fv, st.rowptr.data_ptr(), st.colidx.data_ptr(),
+                   A.vals.data_ptr(), self.ptr["T0"], self.ptr["T1"], self.smp_["NRM"],
+                   self.gws, self.gwb, self.st)
 
     def wait(self, buf):
         rc = self.f_wait(self.mptr[buf] + 8 * self.off["FLAG"], -1.0, 60_000_000, self.st)
@@ -478,19 +505,38 @@ def _build_G(k, Bmat, Hb, total, m):
     return G
 
 
+import os as _os
+
+PROFILE = {}                      # phase -> host seconds (PMP_PROFILE=1)
+_PROF_ON = _os.environ.get("PMP_PROFILE") == "1"
+_last_tick = [0.0]
+
+
+def _tick(name):
+    if _PROF_ON:
+        t = time.perf_counter()
+        acc = PROFILE.setdefault(name, [0.0, 0])
+        acc[0] += t - _last_tick[0]
+        acc[1] += 1
+        _last_tick[0] = t
+
+
 def _solve(A, B, P, cfg):
     n, s = B.shape
     t_start = time.perf_counter()
+    _last_tick[0] = t_start
     report = SolveReport()
     cap = cfg.inner_restart + 2 * s + 2
     kc = cfg.outer_space_dim + s
     D = _Dev(n, s, cap, kc)
+    _tick("setup-alloc")
     dev = _dev()
     X = torch.zeros(n, s, dtype=torch.float64, device=dev)
     Xt = torch.zeros(n, s, dtype=torch.float64, device=dev)
     R = B.clone()
     Xp, Xtp, Rp, Bp = X.data_ptr(), Xt.data_ptr(), R.data_ptr(), B.data_ptr()
     bnorms = _colnorms(D, Bp, s, s)
+    _tick("setup-norms")
     last_rel = np.where(bnorms > 0, 1.0, 0.0)
     report.residual_history.append(last_rel.copy())
     active = np.flatnonzero(bnorms > 0)
@@ -517,9 +563,9 @@ def _solve(A, B, P, cfg):
 
     k = 0          # outer-space dimension (columns of C / U in use)
     while active.size and report.iterations < cfg.max_iters:
+        _tick("setup/cycle-end")
         na = active.size
-        act_dev = torch.as_tensor(active.astype(np.int32), device=dev)
-        act_p = act_dev.data_ptr()
+        act_p = D.set_active(active)
         start_rel = _safe_rel(prev_norms[active], bnorms[active])
         # Ract -> Z buffer (n x na, ld s);  Z0 = Ract - C (C^T Ract)
         D.copy_cols(na, Rp, s, act_p, D.p("Z"), s, None)
@@ -534,6 +580,7 @@ def _solve(A, B, P, cfg):
         m = 0
         total = bs
         Y = None
+        _tick("cycle-start")
         exhausted = False
         cycle_converged = False
         bn_act = bnorms[active]
@@ -542,6 +589,7 @@ def _solve(A, B, P, cfg):
         Cp = D.p("C")
         launched = False   # the current step's kernels are already enqueued
         buf = 0            # mapped result buffer of the pending native step
+        prev_max = float(np.max(start_rel)) if start_rel.size else 0.0
         while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
                and m < cfg.inner_restart and D.native):
             # native fast path: two library calls per block step
@@ -562,7 +610,10 @@ def _solve(A, B, P, cfg):
                 # enqueue the next step before the host-side projected solve;
                 # if that solve declares convergence the speculative step is
                 # discarded (it only writes scratch and V columns >= total)
-                if report.iterations < cfg.max_iters and m_new < cfg.inner_restart:
+                # (skipped when the last estimate is within 20x of tol: this
+                # step will very likely converge, the speculation be wasted)
+                if (report.iterations < cfg.max_iters and m_new < cfg.inner_restart
+                        and prev_max > 20.0 * cfg.tol):
                     D.step(chain, A, m_new, sb, k, total_new, buf ^ 1)
                     launched = True
                 Y, rn = proj.absorb(D, buf, q0, sb, total, Bmat, Hb)
@@ -585,6 +636,7 @@ def _solve(A, B, P, cfg):
                 total += bs_next
                 Y, rn = proj.append(Bmat, Hb, q0, q1, total, m)
             est = _safe_rel(rn, bn_act)
+            prev_max = float(np.max(est)) if est.size else 0.0
             last_rel[active] = est
             report.residual_history.append(last_rel.copy())
             cycle_converged = bool(np.all(est <= cfg.tol))
@@ -627,28 +679,22 @@ def _solve(A, B, P, cfg):
             cycle_converged = bool(np.all(est <= cfg.tol))
             exhausted = bs_next == 0
 
+        _tick("inner")
         if Y is None:
             break
 
         # dXt = V Y_v + U Y_u ; Xt[:, active] += dXt     (krylov.py:221-224)
-        D.tsmm(Vp, cap, m, D.put("H", Y[k:]), na, 1.0, 0.0, D.p("dX"), s)
-        if k:
-            D.tsmm(D.p("U"), kc, k, D.put("G1", Y[:k]), na, 1.0, 1.0, D.p("dX"), s)
-        D.axpby(na, 1.0, D.p("dX"), s, None, 1.0, Xtp, s, act_p)
         # X = P Xt ; R = B - A X                          (krylov.py:225-233)
-        D.copy_cols(na, Xtp, s, act_p, D.p("Z"), s, None)
+        # (one native call enqueues the whole chain; pmp_gcro_cycle_end)
+        hv = D.put("H", Y[k:])
+        hu = D.put("G1", Y[:k]) if k else None
+        D.cycle_end(na, act_p, m, hv, k, hu, Xtp, Xp, Bp, Rp, chain, A)
         if P is not None:
-            P.apply_dev(D.p("Z"), s, na, D.p("Xa"), s, tmp)
             report.precond_apply_count += na
-            xa = D.p("Xa")
-        else:
-            xa = D.p("Z")
-        D.copy_cols(na, xa, s, None, Xp, s, act_p)
-        D.copy_cols(na, Bp, s, act_p, D.p("Rb"), s, None)
-        A.spmm(xa, s, na, D.p("Rb"), s, alpha=-1.0, beta=1.0, Y0=D.p("Rb"), ldy0=s)
         report.matvec_count += na
-        D.copy_cols(na, D.p("Rb"), s, None, Rp, s, act_p)
-        tn = _colnorms(D, D.p("Rb"), s, na)
+        D.fetch(("NRM", na * na))
+        tn = np.sqrt(np.maximum(np.diag(D.get("NRM", na, na)), 0.0))
+        _tick("cycle-end-resid")
         prev_norms[active] = tn
         true_rel = _safe_rel(tn, bn_act)
         last_rel[active] = true_rel
@@ -669,6 +715,7 @@ def _solve(A, B, P, cfg):
             if k:
                 D.tsmm(Cp, kc, k, D.put("G1", img[:k]), na, 1.0, 1.0, D.p("Rb"), s)
             kk = D.fold(k, na)
+            _tick("fold")
             if kk > cfg.outer_space_dim:
                 drop = kk - cfg.outer_space_dim
                 keep = cfg.outer_space_dim
@@ -678,6 +725,7 @@ def _solve(A, B, P, cfg):
             k = kk
         active = active[still]
 
+    _tick("setup/cycle-end")
     report.converged = active.size == 0
     report.wall_time = time.perf_counter() - t_start
     report.device_launches = D.launches

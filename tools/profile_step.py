@@ -59,6 +59,31 @@ def main():
     print("device kernel time %.2f ms (%.0f%% of wall)" % (tot / 1e3, 100 * tot / 1e3 / (wall * 1e3)))
     for t, c, k in rows[:15]:
         print("  %-70s %6d  %9.1f us  %7.2f us/launch" % (k, c, t, t / max(c, 1)))
+    # host wall per phase, synchronising after each (diagnostic only)
+    from paper_1809_06574_b200 import krylov
+    krylov.PROFILE.clear()
+    ph = {"assemble": 0.0, "build": 0.0, "solve": 0.0}
+    pts = [(s, np.atleast_1d(p)) for s in s_grid for p in p_grid]
+    A1 = model.assemble(*pts[0])
+    P1, _ = pm.spai_build(A1, pol.spai)
+    torch.cuda.synchronize()
+    for s_, p_ in pts[1:]:
+        t = time.perf_counter()
+        A = model.assemble(s_, p_)
+        torch.cuda.synchronize()
+        ph["assemble"] += time.perf_counter() - t
+        t = time.perf_counter()
+        P, _ = pm.update_first(A1, A, P1, pol.update)
+        torch.cuda.synchronize()
+        ph["build"] += time.perf_counter() - t
+        t = time.perf_counter()
+        pm.block_gcro_solve(A, Bd, P=P, cfg=cfg)
+        torch.cuda.synchronize()
+        ph["solve"] += time.perf_counter() - t
+    print("host wall per phase (ms, %d systems):" % (len(pts) - 1),
+          {k: round(v * 1e3, 2) for k, v in ph.items()})
+    print("solver phases (ms, count):",
+          {k: (round(v[0] * 1e3, 2), v[1]) for k, v in krylov.PROFILE.items()})
     pr = cProfile.Profile()
     pr.enable()
     pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, timing=False)
