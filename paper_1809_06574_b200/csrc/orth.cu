@@ -104,6 +104,7 @@ __host__ __device__ __forceinline__ int odd_ld(int w) { return w | 1; }
 // Lanes own columns t (coalesced / conflict-free with odd leading
 // dimensions), warps split the rows; the per-warp sums are combined in a
 // fixed order through smem.
+template <int NY>
 __device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int ny, int nrows,
                            double* red, double* partial) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -115,24 +116,26 @@ __device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int 
   for (int job0 = 0; job0 < rounds * splits; job0 += 8) {
     const int job = job0 + wid;
     const int rd = job / splits, sp = job % splits;
-    double acc[16];
+    double acc[NY];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
     const int t = rd * 32 + lane;
     if (job < rounds * splits && t < kx) {
       const int per = (nrows + splits - 1) / splits;
       const int ra = sp * per, rb = min(nrows, ra + per);
+      double xn = ra < rb ? X.at(ra, t) : 0.0;
       for (int r = ra; r < rb; ++r) {
-        const double x = X.at(r, t);
+        const double x = xn;
+        if (r + 1 < rb) xn = X.at(r + 1, t);   // prefetch the next row's operand
         const double* y = Y + (size_t)r * ldy;
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
+        for (int c = 0; c < NY; ++c)
           if (c < ny) acc[c] += x * y[c];
       }
     }
     if (job < rounds * splits) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
+      for (int c = 0; c < NY; ++c)
         if (c < ny) red[((size_t)(job - job0) * 32 + lane) * ny + c] = acc[c];
     }
     __syncthreads();
@@ -178,22 +181,23 @@ __device__ void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, do
 }
 
 // Y[r][c] -= sum_t X(r, t) G[t][c] ; thread per row, all ny outputs
+template <int NY>
 __device__ void block_update(const Rows& X, int kx, double* Y, int ldy, int ny, int nrows,
                              const double* G) {
   for (int r = threadIdx.x; r < nrows; r += kOrthT) {
-    double acc[16];
+    double acc[NY];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
     for (int t = 0; t < kx; ++t) {
       const double x = X.at(r, t);
       const double* g = G + t * ny;
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
+      for (int c = 0; c < NY; ++c)
         if (c < ny) acc[c] += x * g[c];
     }
     double* y = Y + (size_t)r * ldy;
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
+    for (int c = 0; c < NY; ++c)
       if (c < ny) y[c] -= acc[c];
   }
   __syncthreads();
@@ -266,33 +270,37 @@ __device__ bool warp_cholesky(const double* G, int m, double* A, double* R, int*
 }
 
 // Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve); thread per row
+template <int NY>
 __device__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
                                 const double* R, const int* piv) {
+  __shared__ double rinv[16];
+  if (threadIdx.x < m) rinv[threadIdx.x] = 1.0 / R[threadIdx.x * m + threadIdx.x];
+  __syncthreads();
   for (int r = threadIdx.x; r < nrows; r += kOrthT) {
-    double x[16], y[16];
+    double x[NY], y[NY];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) x[c] = (c < m) ? X[(size_t)r * ldx + (piv ? piv[c] : c)] : 0.0;
+    for (int c = 0; c < NY; ++c) x[c] = (c < m) ? X[(size_t)r * ldx + (piv ? piv[c] : c)] : 0.0;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
+    for (int c = 0; c < NY; ++c) {
       if (c < m) {
         double s = x[c];
 #pragma unroll
-        for (int a = 0; a < 16; ++a)
+        for (int a = 0; a < NY; ++a)
           if (a < c) s -= y[a] * R[a * m + c];
-        y[c] = s / R[c * m + c];
+        y[c] = s * rinv[c];
       } else {
         y[c] = 0.0;
       }
     }
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
+    for (int c = 0; c < NY; ++c)
       if (c < m) Y[(size_t)r * ldy + c] = y[c];
   }
   __syncthreads();
 }
 
-template <bool CACHED>
-__global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
+template <bool CACHED, int NY>
+__global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sh[];
   const int r0 = blockIdx.x * P.rows_per_block;
@@ -305,13 +313,13 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
   double* G = p;
   p += kmax;
   double* A = p;
-  p += 256;
+  p += sb * sb;
   double* R1 = p;
-  p += 256;
+  p += sb * sb;
   double* R2 = p;
-  p += 256;
+  p += sb * sb;
   double* red = p;
-  p += 8 * 32 * 16;
+  p += 8 * 32 * sb;
   int* piv = reinterpret_cast<int*>(p);
   int* piv2 = piv + 16;
   int* flag = piv + 32;
@@ -354,9 +362,9 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
 
   // ---- R1: [C | V]^T W -------------------------------------------------------
   if (kx > 0) {
-    block_gram(CV, kx, Wv, ldw, sb, nr, red, P.partial);
+    block_gram<NY>(CV, kx, Wv, ldw, sb, nr, red, P.partial);
     grid_reduce(grid, P, kx * sb, G, P.outB, k * sb, P.npass ? P.outH1 : nullptr);
-    block_update(CV, kx, Wv, ldw, sb, nr, G);
+    block_update<NY>(CV, kx, Wv, ldw, sb, nr, G);
   }
   // ---- R2: [V | W1]^T W1 -----------------------------------------------------
   const bool second = P.npass >= 2 && tot > 0;
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
   const int kx2 = kv2 + sb;
   {
     const Rows VW{Vrows, ldvr, kv2, Wv, ldw};
-    block_gram(VW, kx2, Wv, ldw, sb, nr, red, P.partial);
+    block_gram<NY>(VW, kx2, Wv, ldw, sb, nr, red, P.partial);
     grid_reduce(grid, P, kx2 * sb, G, second ? P.outH2 : nullptr, kv2 * sb, nullptr);
   }
   // G_W = W1^T W1 - H2^T H2 (into R2 as scratch), then W2 = W1 - V H2
@@ -375,7 +383,7 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
     R2[q] = s;
   }
   __syncthreads();
-  if (second) block_update(Vonly, tot, Wv, ldw, sb, nr, G);
+  if (second) block_update<NY>(Vonly, tot, Wv, ldw, sb, nr, G);
   for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {
     const int i = q / sb, j = q % sb;
     G[q] = 0.5 * (R2[i * sb + j] + R2[j * sb + i]);
@@ -394,10 +402,10 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
     single = kap <= kSkipKappa;
   }
   if (flag[0] == 0 && !single) {
-    block_trsm_rows(Wv, ldw, Q1, ldq, nr, sb, R1, piv);
+    block_trsm_rows<NY>(Wv, ldw, Q1, ldq, nr, sb, R1, piv);
     // ---- R3: Q1^T Q1 ---------------------------------------------------------
     const Rows Qv{Q1, ldq, sb, Q1, ldq};
-    block_gram(Qv, sb, Q1, ldq, sb, nr, red, P.partial);
+    block_gram<NY>(Qv, sb, Q1, ldq, sb, nr, red, P.partial);
     grid_reduce(grid, P, sb * sb, G, nullptr, 0, nullptr);
     if (threadIdx.x < 32) {
       bool ok = warp_cholesky(G, sb, A, R2, piv2, false, 0.0);
@@ -417,11 +425,11 @@ __global__ void __launch_bounds__(kOrthT, 1) k_orth(OrthParams P) {
   }
   if (single) {
     // Q = W P R1^-1 -> V[:, qout : qout + sb], R2 = I
-    block_trsm_rows(Wv, ldw, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R1, piv);
+    block_trsm_rows<NY>(Wv, ldw, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R1, piv);
     for (int q = threadIdx.x; q < sb * sb; q += kOrthT) R2[q] = (q / sb == q % sb) ? 1.0 : 0.0;
     __syncthreads();
   } else {
-    block_trsm_rows(Q1, ldq, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R2, nullptr);
+    block_trsm_rows<NY>(Q1, ldq, P.V + (size_t)r0 * P.ldv + P.qout, P.ldv, nr, sb, R2, nullptr);
   }
   if (blockIdx.x == 0) {
     // R = R2 R1 (pivoted column order), un-pivoted: Rout[i, piv[c]] = R[i, c]
@@ -462,7 +470,7 @@ struct FoldParams {
 };
 
 template <bool CACHED>
-__global__ void __launch_bounds__(kOrthT, 1) k_fold(FoldParams F) {
+__global__ void __launch_bounds__(kOrthT, 2) k_fold(FoldParams F) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sh[];
   const int r0 = blockIdx.x * F.rows_per_block;
@@ -512,7 +520,7 @@ __global__ void __launch_bounds__(kOrthT, 1) k_fold(FoldParams F) {
     __syncthreads();
     // [C | w]^T w  ->  h1, ||w||^2
     Rows Cw{Cs, ldcs, kk, w, ldwz};
-    block_gram(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
+    block_gram<1>(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
     grid_reduce(grid, P, kk + 1, G, nullptr, 0, nullptr);
     const double w0 = sqrt(G[kk]);
     if (w0 == 0.0) {
@@ -522,20 +530,20 @@ __global__ void __launch_bounds__(kOrthT, 1) k_fold(FoldParams F) {
     double nw;
     if (kk > 0) {
       Rows Conly{Cs, ldcs, kk, Cs, ldcs}, Uonly{Us, ldcs, kk, Us, ldcs};
-      block_update(Conly, kk, w, ldwz, 1, nr, G);
-      block_update(Uonly, kk, z, ldwz, 1, nr, G);
-      block_gram(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
+      block_update<1>(Conly, kk, w, ldwz, 1, nr, G);
+      block_update<1>(Uonly, kk, z, ldwz, 1, nr, G);
+      block_gram<1>(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
       grid_reduce(grid, P, kk + 1, G, nullptr, 0, nullptr);
       double h2 = 0.0;
       for (int t = 0; t < kk; ++t) h2 += G[t] * G[t];
       const double w1n2 = G[kk];
-      block_update(Conly, kk, w, ldwz, 1, nr, G);
-      block_update(Uonly, kk, z, ldwz, 1, nr, G);
+      block_update<1>(Conly, kk, w, ldwz, 1, nr, G);
+      block_update<1>(Uonly, kk, z, ldwz, 1, nr, G);
       double nw2 = w1n2 - h2;
       if (!(nw2 > 1e-4 * w1n2)) {
         // cancellation: recompute ||w2||^2 exactly
         Rows Wo{w, ldwz, 1, w, ldwz};
-        block_gram(Wo, 1, w, ldwz, 1, nr, red, P.partial);
+        block_gram<1>(Wo, 1, w, ldwz, 1, nr, red, P.partial);
         grid_reduce(grid, P, 1, G, nullptr, 0, nullptr);
         nw2 = G[0];
       }
@@ -570,7 +578,7 @@ size_t fold_smem_bytes(int rows, int kc, int cached) {
 
 size_t orth_smem_bytes(int rows, int total, int k, int sb, int cached) {
   const int kx = k + total;
-  size_t d = (size_t)(kx + sb) * sb + 3 * 256 + 8 * 32 * 16 + 20;
+  size_t d = (size_t)(kx + sb) * sb + 3 * sb * sb + 8 * 32 * sb + 20;
   if (cached) d += (size_t)rows * (odd_ld(kx) + 2 * odd_ld(sb));
   return d * sizeof(double);
 }
@@ -588,15 +596,30 @@ static void orth_geometry(int n, int total, int k, int sb, int* grid, int* rows,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  int g = sms;
-  int want = (n + 31) / 32;
-  if (want < g) g = want > 0 ? want : 1;
-  int r = (n + g - 1) / g;
-  size_t full = orth_smem_bytes(r, total, k, sb, 1);
-  *cached = full <= (size_t)220 * 1024;
-  *smem = *cached ? full : orth_smem_bytes(r, total, k, sb, 0);
-  *grid = g;
-  *rows = r;
+  // two co-resident blocks per SM when the cached rows fit in half the
+  // shared memory (more warps to hide the latency of the row loops, half
+  // the rows per block), otherwise one
+  for (int bps = 2; bps >= 1; --bps) {
+    int g = sms * bps;
+    int want = (n + 31) / 32;
+    if (want < g) g = want > 0 ? want : 1;
+    int r = (n + g - 1) / g;
+    size_t full = orth_smem_bytes(r, total, k, sb, 1);
+    const size_t budget = bps == 2 ? (size_t)110 * 1024 : (size_t)220 * 1024;
+    if (bps == 2 && full > budget) continue;
+    *cached = full <= budget;
+    *smem = *cached ? full : orth_smem_bytes(r, total, k, sb, 0);
+    *grid = g;
+    *rows = r;
+    return;
+  }
+}
+
+static int orth_max_grid() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return 2 * (sms > 0 ? sms : 148);
 }
 
 extern "C" {
@@ -605,6 +628,7 @@ size_t pmp_orth_workspace(int n, int total_max, int k_max, int sb) {
   int g, r, c;
   size_t sm;
   orth_geometry(n, total_max, k_max, sb, &g, &r, &c, &sm);
+  g = orth_max_grid();   // any (total, k) may pick the two-blocks-per-SM grid
   const int kmax = (k_max + total_max + sb) * sb;
   return 256 + sizeof(double) * ((size_t)g * kmax + kmax + (size_t)n * sb + 64);
 }
@@ -635,8 +659,23 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
   int g, rows, cached;
   size_t smem;
   orth_geometry(n, total, k, sb, &g, &rows, &cached, &smem);
-  void* fn = cached ? (void*)k_orth<true> : (void*)k_orth<false>;
-  const int bps = prepare_smem(fn, smem, kOrthT);
+  auto pick = [&](int c) -> void* {
+    if (sb <= 8) return c ? (void*)k_orth<true, 8> : (void*)k_orth<false, 8>;
+    return c ? (void*)k_orth<true, 16> : (void*)k_orth<false, 16>;
+  };
+  void* fn = pick(cached);
+  int bps = prepare_smem(fn, smem, kOrthT);
+  if (bps * (orth_max_grid() / 2) < g) {
+    // the two-blocks-per-SM grid is not co-resident: one block per SM
+    g = orth_max_grid() / 2;
+    if ((n + 31) / 32 < g) g = (n + 31) / 32 > 0 ? (n + 31) / 32 : 1;
+    rows = (n + g - 1) / g;
+    size_t full = orth_smem_bytes(rows, total, k, sb, 1);
+    cached = full <= (size_t)220 * 1024;
+    smem = cached ? full : orth_smem_bytes(rows, total, k, sb, 0);
+    fn = pick(cached);
+    bps = prepare_smem(fn, smem, kOrthT);
+  }
   if (bps < 1) {
     set_error("pmp_orth_step: kernel does not fit on an SM (smem %zu)", smem);
     return PMP_ERR_ARG;
@@ -703,7 +742,10 @@ int pmp_fold(int n, int na, const double* img, int ldi, const double* dz, int ld
   const int cached = fold_smem_bytes(rows, kc, 1) <= (size_t)220 * 1024;
   const size_t smem = fold_smem_bytes(rows, kc, cached);
   void* fn = cached ? (void*)k_fold<true> : (void*)k_fold<false>;
-  prepare_smem(fn, smem, kOrthT);
+  if (prepare_smem(fn, smem, kOrthT) * (orth_max_grid() / 2) < g) {
+    set_error("pmp_fold: grid of %d blocks is not co-resident", g);
+    return PMP_ERR_ARG;
+  }
   FoldParams F;
   F.n = n;
   F.na = na;
