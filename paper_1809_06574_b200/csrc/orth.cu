@@ -719,9 +719,7 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
 extern "C" {
 
 size_t pmp_fold_workspace(int n, int kc) {
-  int g, r, c;
-  size_t sm;
-  orth_geometry(n, 0, 0, 1, &g, &r, &c, &sm);
+  const int g = orth_max_grid();
   return 256 + sizeof(double) * ((size_t)g * (kc + 1) + (kc + 1) + 2 * (size_t)n + 64);
 }
 
@@ -736,9 +734,11 @@ int pmp_fold(int n, int na, const double* img, int ldi, const double* dz, int ld
     set_error("pmp_fold: workspace too small");
     return PMP_ERR_WORKSPACE;
   }
-  int g, rows, c0;
-  size_t sm0;
-  orth_geometry(n, 0, 0, 1, &g, &rows, &c0, &sm0);
+  // one block per SM: the fold is grid-barrier bound (4 barriers per
+  // column), and barrier cost grows with the block count
+  int g = orth_max_grid() / 2;
+  if ((n + 31) / 32 < g) g = (n + 31) / 32 > 0 ? (n + 31) / 32 : 1;
+  const int rows = (n + g - 1) / g;
   const int cached = fold_smem_bytes(rows, kc, 1) <= (size_t)220 * 1024;
   const size_t smem = fold_smem_bytes(rows, kc, cached);
   void* fn = cached ? (void*)k_fold<true> : (void*)k_fold<false>;
