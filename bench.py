@@ -191,8 +191,11 @@ def run_ours(args):
     clk.start()
     step_ms = []
     infos = []
-    dominant = ("pmp_ls_columns", "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm",
-                "pmp_copy_cols", "pmp_axpby_cols", "pmp_assemble", "pmp_permute")
+    # per-kernel device time: "k_orth" = the fused orthogonalisation kernel
+    # inside each native block step (events recorded in the C driver)
+    dominant = ("k_orth", "pmp_ls_columns", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
+                "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm", "pmp_copy_cols",
+                "pmp_axpby_cols", "pmp_assemble", "pmp_permute")
     _abi.count_launches(True)
     recs_all = None
     for k in range(args.steps):
@@ -298,7 +301,10 @@ def roofline(kern, timed, n, W, model):
     lst = timed[name]
     st = model.structure
     nnz = st.nnz
-    if name == "pmp_spmm":
+    if name == "k_orth":
+        # [C | V] rows read once, W read, Q written: 8 n (k + total + 2 sb)
+        byts = [8.0 * a[0] * (a[1] + a[2] + 2 * a[3]) for _, _, a in lst]
+    elif name == "pmp_spmm":
         # 12 B per nnz + 4 (n+1) + 16 n s_b (X gathered once + Y written)
         byts = [12.0 * nnz + 4.0 * (n + 1) + 16.0 * n * a[4] for _, _, a in lst]
     elif name == "pmp_gram":

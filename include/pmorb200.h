@@ -201,14 +201,16 @@ int pmp_host_wait_flag(const double* h_flag, double sentinel, long long timeout_
  * arrays of the factors' device CSR pointers, outermost first), then
  * pmp_orth_step with its small outputs at d_small + off* (device), mirrored
  * at the end of the kernel to the same offsets of h_mirror (mapped host
- * memory, flag written last); h_mirror[offFlag] is set to -1 first. */
+ * memory, flag written last); h_mirror[offFlag] is set to -1 first.
+ * ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the orthogonalisation
+ * kernel alone, for per-kernel timing. */
 int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* h_fac_rowptr,
                   const int32_t* const* h_fac_colidx, const double* const* h_fac_vals,
                   const int32_t* d_a_rowptr, const int32_t* d_a_colidx, const double* d_a_vals,
                   double* d_V, int cap, int q0, int sb, double* d_W, double* d_T0, double* d_T1,
                   double* d_T2, const double* d_C, int kc, int k, int total, double* d_small,
                   double* h_mirror, int offB, int offH1, int offH2, int offR, int offFlag,
-                  void* d_ws, size_t ws_bytes, void* stream);
+                  void* d_ws, size_t ws_bytes, void* stream, void* ev_begin, void* ev_end);
 /* End of a GCRO cycle (krylov.py:221-234), enqueued natively:
  *   dX = V[:, :m] Yv + U[:, :k] Yu ; Xt[:, act] += dX ; Xa = P Xt[:, act] ;
  *   X[:, act] = Xa ; Rb = B[:, act] - A Xa ; R[:, act] = Rb ; nrm = Rb^T Rb. */

@@ -77,7 +77,8 @@ _SIGS = {
     "pmp_host_wait_flag": ([c_vp, c_dbl, ctypes.c_longlong, c_vp], c_int),
     "pmp_gcro_step": ([c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
                        c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp,
-                       c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_sz, c_vp], c_int),
+                       c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_sz, c_vp, c_vp, c_vp],
+                      c_int),
     "pmp_gcro_cycle_end": ([c_int, c_int, c_int, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_int,
                             c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
                             c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,

@@ -87,7 +87,7 @@ int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* fac_rowptr,
                   double* V, int cap, int q0, int sb, double* W, double* T0, double* T1,
                   double* T2, const double* C, int kc, int k, int total, double* d_small,
                   double* mirror, int offB, int offH1, int offH2, int offR, int offFlag,
-                  void* ws, size_t ws_bytes, void* stream) {
+                  void* ws, size_t ws_bytes, void* stream, void* ev_begin, void* ev_end) {
   // W = A F_0 F_1 ... F_{nfac-1} V[:, q0 : q0 + sb], applied right to left
   const double* src = V + q0;
   int lds = cap;
@@ -104,9 +104,13 @@ int pmp_gcro_step(int n, int s, int nfac, const int32_t* const* fac_rowptr,
                     stream);
   if (rc) return rc;
   mirror[offFlag] = -1.0;  // sentinel, overwritten by the kernel's last write
-  return pmp::orth_step_mirrored(n, C, kc, k, V, cap, total, 2, W, s, sb, total, d_small + offB,
-                                 d_small + offH1, d_small + offH2, d_small + offR,
-                                 d_small + offFlag, ws, ws_bytes, stream, d_small, mirror);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (ev_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_begin), st);
+  rc = pmp::orth_step_mirrored(n, C, kc, k, V, cap, total, 2, W, s, sb, total, d_small + offB,
+                               d_small + offH1, d_small + offH2, d_small + offR,
+                               d_small + offFlag, ws, ws_bytes, stream, d_small, mirror);
+  if (ev_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st);
+  return rc;
 }
 
 int pmp_tsmm(int n, int kv, const double* V, int ldv, int nc, const double* H, double alpha,

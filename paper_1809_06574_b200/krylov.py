@@ -241,7 +241,19 @@ class _Dev:
                    self.ptr["T1"], self.ptr["T2"], self.ptr["C"], self.kc, k, total,
                    self.smbase, self.mptr[buf], off["G1"], off["G2"], off["G3"], off["RT"],
                    off["FLAG"],
-                   self.ows, self.owb, self.st)
+                   self.ows, self.owb, self.st, *self._orth_events(k, total, sb))
+
+    def _orth_events(self, k, total, sb):
+        """CUDA events around the orthogonalisation kernel of a native step
+        when per-kernel timing of "k_orth" is requested (bench.py)."""
+        if not (self.timing and "k_orth" in self.timing):
+            return (None, None)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        b.record()          # materialise the underlying cudaEvent_t handles
+        _abi._timed.setdefault("k_orth", []).append((a, b, (self.n, k, total, sb)))
+        return (a.cuda_event, b.cuda_event)
 
     def _chain_arrays(self, chain):
         key = tuple(id(F) for F in chain)
