@@ -512,6 +512,276 @@ __global__ void k_ls(LsParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large columns (dense A(J, I) beyond shared memory, e.g. the power-law
+// config c5: median 2450 x 30, tail 10948 x 230 while each column of A(J, I)
+// holds only ~40 nonzeros): corrected semi-normal equations.  G = M^T M and
+// M^T t come from sparse dot products of the CSC columns (merge
+// intersections), never forming the dense block; pivoted Cholesky of G; one
+// step of iterative refinement on the explicit residual r = t - M z over J
+// (which also gives the reported residual, spai.py:252).  With
+// kappa(M) sqrt(eps) << 1 this matches the Householder solution to ~kappa
+// eps; a (near) rank-deficient G (min R_kk <= 1e-6 R_00) flags the column
+// (flags bit 1) so the host re-solves it with the dense pivoted-QR kernel.
+// ---------------------------------------------------------------------------
+
+__host__ __device__ inline size_t sne_team_bytes(int lcap, int mcap, int ncap) {
+  size_t d = (size_t)mcap + (size_t)ncap * ncap + 5 * (size_t)(ncap + 1) + 16;
+  size_t i = (size_t)lcap + 3 * (size_t)(ncap + 1) + 1 + 16;
+  return align16(d * sizeof(double)) + align16(i * sizeof(int));
+}
+
+// sparse dot of two sorted CSC columns
+__device__ inline double col_dot(const LsParams& P, int a, int b) {
+  int i = P.acolptr[a], ie = P.acolptr[a + 1];
+  int j = P.acolptr[b], je = P.acolptr[b + 1];
+  double s = 0.0;
+  while (i < ie && j < je) {
+    const int ra = P.arowidx[i], rb = P.arowidx[j];
+    if (ra == rb) {
+      s += P.avals[i] * P.avals[j];
+      ++i;
+      ++j;
+    } else if (ra < rb) {
+      ++i;
+    } else {
+      ++j;
+    }
+  }
+  return s;
+}
+
+// dot of CSC column a with the target column j (identity: e_j)
+__device__ inline double col_dot_target(const LsParams& P, int a, int j) {
+  int i = P.acolptr[a], ie = P.acolptr[a + 1];
+  if (!P.tcolptr) {
+    int pos = i + lower_bound_i(P.arowidx + i, ie - i, j);
+    return (pos < ie && P.arowidx[pos] == j) ? P.avals[pos] : 0.0;
+  }
+  int t = P.tcolptr[j], te = P.tcolptr[j + 1];
+  double s = 0.0;
+  while (i < ie && t < te) {
+    const int ra = P.arowidx[i], rt = P.trowidx[t];
+    if (ra == rt) {
+      s += P.avals[i] * P.tvals[t];
+      ++i;
+      ++t;
+    } else if (ra < rt) {
+      ++i;
+    } else {
+      ++t;
+    }
+  }
+  return s;
+}
+
+template <int T>
+__device__ void sne_column(const LsParams& P, int j, char* mem, int tid) {
+  const int lcap = P.lcap, mcap = P.mcap, ncap = P.ncap;
+  double* d = reinterpret_cast<double*>(mem);
+  double* r = d;
+  d += mcap;
+  double* G = d;
+  d += (size_t)ncap * ncap;
+  double* z = d;
+  d += ncap + 1;
+  double* dz = d;
+  d += ncap + 1;
+  double* bt = d;
+  d += ncap + 1;
+  double* gd = d;  // diagonal scratch
+  d += ncap + 1;
+  double* red = d + (ncap + 1);
+  const size_t dbytes =
+      align16(((size_t)mcap + (size_t)ncap * ncap + 5 * (size_t)(ncap + 1) + 16) * sizeof(double));
+  int* ib = reinterpret_cast<int*>(mem + dbytes);
+  LsMem m;
+  m.list = ib;
+  m.sup = ib + lcap;
+  m.perm = m.sup + ncap + 1;
+  m.off = m.perm + ncap + 1;
+  m.misc = m.off + ncap + 2;
+  Team<T> tm{tid, red};
+  const int i0 = P.iptr[j];
+  const int n = P.iptr[j + 1] - i0;
+  int t0, tl;
+  if (P.tcolptr) {
+    t0 = P.tcolptr[j];
+    tl = P.tcolptr[j + 1] - t0;
+  } else {
+    t0 = -1;
+    tl = 1;
+  }
+  for (int c = tid; c < n; c += T) {
+    m.sup[c] = P.iidx[i0 + c];
+    m.perm[c] = c;
+  }
+  tm.sync();
+  int lp2;
+  gather_sorted_rows<T>(P, j, m, n, t0, tl, tm, &lp2);
+  const int mJ = team_compact<T>(m.list, nullptr, lp2, tm, m.misc + 4,
+                                 [](int i, int v, int prev, double) {
+                                   return v != kIntMax && (i == 0 || v != prev);
+                                 });
+  const int* J = m.list;
+  // G = M^T M (upper triangle computed, mirrored), bt = M^T t
+  const int npairs = n * (n + 1) / 2;
+  for (int q = tid; q < npairs; q += T) {
+    // q -> (a, b), a <= b, row-major upper triangle
+    int a = (int)((2.0 * n + 1.0 - sqrt((2.0 * n + 1.0) * (2.0 * n + 1.0) - 8.0 * q)) / 2.0);
+    while (a > 0 && a * n - a * (a - 1) / 2 > q) --a;
+    while ((a + 1) * n - (a + 1) * a / 2 <= q) ++a;
+    const int b = a + (q - (a * n - a * (a - 1) / 2));
+    const double v = col_dot(P, m.sup[a], m.sup[b]);
+    G[a * ncap + b] = v;
+    G[b * ncap + a] = v;
+  }
+  for (int c = tid; c < n; c += T) bt[c] = col_dot_target(P, m.sup[c], j);
+  tm.sync();
+  // pivoted Cholesky in place (upper factor in G's upper triangle; the
+  // permutation acts symmetrically: perm[k] = original column at position k)
+  int ok = 1;
+  const double g00 = 1.0;
+  (void)g00;
+  double r00 = 0.0;
+  for (int k = 0; k < n; ++k) {
+    if (tid == 0) {
+      int p = k;
+      double best = G[k * ncap + k];
+      for (int c = k + 1; c < n; ++c)
+        if (G[c * ncap + c] > best) {
+          best = G[c * ncap + c];
+          p = c;
+        }
+      m.misc[0] = p;
+    }
+    tm.sync();
+    const int p = m.misc[0];
+    if (p != k) {
+      for (int c = tid; c < n; c += T) {  // swap rows k, p
+        double t = G[k * ncap + c];
+        G[k * ncap + c] = G[p * ncap + c];
+        G[p * ncap + c] = t;
+      }
+      tm.sync();
+      for (int c = tid; c < n; c += T) {  // swap columns k, p
+        double t = G[c * ncap + k];
+        G[c * ncap + k] = G[c * ncap + p];
+        G[c * ncap + p] = t;
+      }
+      if (tid == 0) {
+        int t = m.perm[k];
+        m.perm[k] = m.perm[p];
+        m.perm[p] = t;
+      }
+      tm.sync();
+    }
+    const double dkk = G[k * ncap + k];
+    if (k == 0) r00 = sqrt(fmax(dkk, 0.0));
+    if (!(dkk > 0.0) || sqrt(dkk) <= 1e-6 * r00) {
+      ok = 0;
+      break;
+    }
+    const double rkk = sqrt(dkk);
+    for (int c = k + tid; c < n; c += T) gd[c] = (c == k) ? rkk : G[k * ncap + c] / rkk;
+    tm.sync();
+    for (int c = k + tid; c < n; c += T) G[k * ncap + c] = gd[c];
+    const int w = n - k - 1;
+    for (int q = tid; q < w * w; q += T) {
+      const int a = k + 1 + q / w, b = k + 1 + q % w;
+      if (b >= a) {
+        G[a * ncap + b] -= gd[a] * gd[b];
+        if (b != a) G[b * ncap + a] = G[a * ncap + b];
+      }
+    }
+    tm.sync();
+  }
+  if (!ok) {
+    // leave the column to the dense pivoted-QR path
+    if (tid == 0) P.flags[j] = 2;
+    tm.sync();
+    return;
+  }
+  // z = P R^-1 R^-T P^T bt ; two passes: solve, residual, refine
+  for (int pass = 0; pass < 2; ++pass) {
+    double* y = pass == 0 ? z : dz;
+    // rhs (permuted) into y: y = P^T (pass 0: bt, pass 1: M^T r)
+    if (pass == 1) {
+      for (int c = tid; c < n; c += T) {
+        const int k = m.sup[c];
+        double s = 0.0;
+        for (int e = P.acolptr[k]; e < P.acolptr[k + 1]; ++e)
+          s += P.avals[e] * r[lower_bound_i(J, mJ, P.arowidx[e])];
+        bt[c] = s;
+      }
+      tm.sync();
+    }
+    for (int c = tid; c < n; c += T) y[c] = bt[m.perm[c]];
+    tm.sync();
+    if (tid < 32) {
+      // forward (R^T y' = y) then backward (R x = y'), warp 0
+      for (int k = 0; k < n; ++k) {
+        const double yk = y[k] / G[k * ncap + k];
+        __syncwarp();
+        if (tid == 0) y[k] = yk;
+        for (int c = k + 1 + tid; c < n; c += 32) y[c] -= G[k * ncap + c] * yk;
+        __syncwarp();
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        const double yk = y[k] / G[k * ncap + k];
+        __syncwarp();
+        if (tid == 0) y[k] = yk;
+        for (int c = tid; c < k; c += 32) y[c] -= G[c * ncap + k] * yk;
+        __syncwarp();
+      }
+    }
+    tm.sync();
+    // back to support order: gd[perm[c]] = y[c]; accumulate into z (support order)
+    for (int c = tid; c < n; c += T) gd[m.perm[c]] = y[c];
+    tm.sync();
+    if (pass == 0) {
+      for (int c = tid; c < n; c += T) z[c] = gd[c];
+    } else {
+      for (int c = tid; c < n; c += T) z[c] += gd[c];
+    }
+    tm.sync();
+    // explicit residual r = t - M z over J
+    for (int i = tid; i < mJ; i += T) r[i] = 0.0;
+    tm.sync();
+    for (int q = tid; q < tl; q += T) {
+      const int row = (t0 < 0) ? j : P.trowidx[t0 + q];
+      r[lower_bound_i(J, mJ, row)] = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
+    }
+    tm.sync();
+    for (int c = 0; c < n; ++c) {
+      const double zc = z[c];
+      const int k = m.sup[c];
+      for (int e = P.acolptr[k] + tid; e < P.acolptr[k + 1]; e += T)
+        r[lower_bound_i(J, mJ, P.arowidx[e])] -= P.avals[e] * zc;
+      tm.sync();
+    }
+  }
+  double part = 0.0;
+  for (int i = tid; i < mJ; i += T) part += r[i] * r[i];
+  const double rn2 = tm.sum(part);
+  for (int c = tid; c < n; c += T) P.coef[i0 + c] = z[c];
+  if (tid == 0) {
+    P.resid[j] = sqrt(rn2);
+    P.flags[j] = 0;
+  }
+  tm.sync();
+}
+
+template <int T, bool GLOBAL>
+__global__ void k_ls_sne(LsParams P) {
+  extern __shared__ __align__(16) char smem[];
+  char* mem = GLOBAL ? (P.gws + (size_t)blockIdx.x * P.team_bytes) : smem;
+  for (int c = blockIdx.x; c < P.ncols; c += gridDim.x) {
+    const int j = P.cols ? P.cols[c] : c;
+    sne_column<T>(P, j, mem, threadIdx.x);
+  }
+}
+
 __global__ void k_ls_bound(int ncols, const int* cols, const int* iptr, const int* iidx,
                            const int* acolptr, const int* tcolptr, int* lsize) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -735,7 +1005,8 @@ using namespace pmp;
 extern "C" {
 
 size_t pmp_ls_team_bytes(int team, int lcap, int mcap, int ncap) {
-  (void)team;
+  // team == 0 queries the semi-normal-equations (mode 3) layout
+  if (team == 0) return sne_team_bytes(lcap, mcap, ncap);
   return ls_team_bytes(lcap, mcap, ncap);
 }
 
@@ -753,7 +1024,7 @@ int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int n
                    const int32_t* tcolptr, const int32_t* trowidx, const double* tvals,
                    double* coef, double* resid, int32_t* flags, int32_t* msize,
                    const int32_t* jptr, int32_t* jidx, void* ws, size_t ws_bytes, void* st) {
-  if (mode < 0 || mode > 2 || (team != 32 && team != 128 && team != 256) || lcap < 1 ||
+  if (mode < 0 || mode > 3 || (team != 32 && team != 128 && team != 256) || lcap < 1 ||
       mcap < 0 || ncap < 0 || ncols < 0 || (lcap & (lcap - 1))) {
     set_error("pmp_ls_columns: bad arguments (mode=%d team=%d lcap=%d)", mode, team, lcap);
     return PMP_ERR_ARG;
@@ -779,11 +1050,34 @@ int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int n
   P.jptr = jptr;
   P.jidx = jidx;
   P.lcap = lcap;
-  P.mcap = (mode == 0) ? mcap : 0;
+  P.mcap = (mode == 0 || mode == 3) ? mcap : 0;
   P.ncap = ncap;
   P.team_bytes = ls_team_bytes(lcap, P.mcap, ncap);
   P.gws = (char*)ws;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  if (mode == 3) {
+    // large columns: corrected semi-normal equations, CTA of 256 per column
+    P.team_bytes = sne_team_bytes(lcap, mcap, ncap);
+    const size_t tb = P.team_bytes;
+    if (use_global) {
+      int grid = num_sms() * 2;
+      if (grid > ncols) grid = ncols;
+      if ((size_t)grid * tb > ws_bytes) grid = (int)(ws_bytes / tb);
+      if (grid < 1) {
+        set_error("pmp_ls_columns: global workspace too small (%zu < %zu)", ws_bytes, tb);
+        return PMP_ERR_WORKSPACE;
+      }
+      k_ls_sne<256, true><<<grid, 256, 0, s>>>(P);
+    } else {
+      if (tb > 227 * 1024) {
+        set_error("pmp_ls_columns: SNE team needs %zu B of shared memory", tb);
+        return PMP_ERR_ARG;
+      }
+      prepare_smem((const void*)k_ls_sne<256, false>, tb, 256);
+      k_ls_sne<256, false><<<ncols, 256, tb, s>>>(P);
+    }
+    return cuda_status("pmp_ls_columns");
+  }
   if (use_global) {
     if (team == 32) return launch_ls<32, true>(P, s, ws_bytes);
     if (team == 128) return launch_ls<128, true>(P, s, ws_bytes);

@@ -227,20 +227,30 @@ def _pow2(v):
 
 
 class _Tier:
-    def __init__(self, team, glob, lcap, mcap, ncap, cols):
-        self.team, self.glob = team, glob
+    """One launch of pmp_ls_columns.  mode 3 = the semi-normal-equations
+    kernel for columns whose dense block exceeds shared memory."""
+
+    def __init__(self, team, glob, lcap, mcap, ncap, cols, mode=0):
+        self.team, self.glob, self.mode = team, glob, mode
         self.lcap, self.mcap, self.ncap = int(lcap), int(mcap), int(ncap)
         self.cols_host = cols
         self.cols = i32(cols)
         self.ncols = int(cols.size)
-        self.bytes = _team_bytes(self.lcap, self.mcap, self.ncap)
+        self.bytes = (_sne_bytes(self.lcap, self.mcap, self.ncap) if mode == 3
+                      else _team_bytes(self.lcap, self.mcap, self.ncap))
+
+
+def _sne_bytes(lcap, mcap, ncap):
+    d = mcap + ncap * ncap + 5 * (ncap + 1) + 16
+    i = lcap + 3 * (ncap + 1) + 1 + 16
+    return _align16(8 * d) + _align16(4 * i)
 
 
 def _split_tiers(cols, lcap, m, nI):
     """Group columns into launch tiers by the team memory they need."""
     if cols.size == 0:
         return []
-    b = _team_bytes(lcap, m, nI)
+    b = _team_bytes(lcap, _coarse(m), _coarse(nI))   # classify on the padded dims
     cls = np.full(cols.size, len(_TIERS) - 1)
     for t in range(len(_TIERS) - 2, -1, -1):
         cls[b <= _TIERS[t][2]] = t
@@ -249,28 +259,54 @@ def _split_tiers(cols, lcap, m, nI):
         sel = np.flatnonzero(cls == t)
         if sel.size == 0:
             continue
-        sel = sel[np.argsort(b[sel], kind="stable")]
-        start = 0
-        while start < sel.size:
-            # greedily extend while the running maxima still fit the tier
-            lo, hi = start + 1, sel.size
-            if limit is not None:
-                while lo < hi:
-                    mid = (lo + hi + 1) // 2
-                    s = sel[start:mid]
-                    if _team_bytes(lcap[s].max(), m[s].max(), nI[s].max()) <= limit:
-                        lo = mid
-                    else:
-                        hi = mid - 1
-                end = lo
-            else:
-                end = sel.size
-            s = sel[start:end]
-            s_sorted = s[np.argsort(cols[s], kind="stable")]
-            tiers.append(_Tier(team, glob, lcap[s].max(), m[s].max(), nI[s].max(),
-                               cols[s_sorted]))
-            start = end
+        if limit is None:
+            # beyond shared memory: semi-normal equations (mode 3), in shared
+            # memory when its much smaller footprint fits, else global
+            sb_ = _sne_bytes(lcap[sel], m[sel], nI[sel])
+            small = sel[sb_ <= 200 * 1024]
+            large = sel[sb_ > 200 * 1024]
+            if small.size:
+                tiers.append(_tier_from(256, 0, cols, lcap, m, nI, small, mode=3))
+            if large.size:
+                tiers.append(_tier_from(256, 1, cols, lcap, m, nI, large, mode=3))
+            continue
+        # bucket the columns by coarsened dimensions (<= 25 % padding), then
+        # merge buckets in size order while the merged team still fits the
+        # tier: O(n log n) and a handful of launches even for power-law sizes
+        key = np.stack([lcap[sel], _coarse(nI[sel]), _coarse(m[sel])], axis=1)
+        ukeys, inv = np.unique(key, axis=0, return_inverse=True)
+        inv = inv.ravel()
+        gbytes = _team_bytes(ukeys[:, 0], ukeys[:, 2], ukeys[:, 1])
+        order = np.argsort(gbytes, kind="stable")
+        members = [[] for _ in range(len(ukeys))]
+        for i, g in enumerate(inv):
+            members[g].append(sel[i])
+        cur, dims = [], None
+        for g in order:
+            kd = ukeys[g]
+            nd = kd if dims is None else np.maximum(dims, kd)
+            if dims is not None and limit is not None and \
+                    _team_bytes(nd[0], nd[2], nd[1]) > limit:
+                tiers.append(_tier_from(team, glob, cols, lcap, m, nI, cur))
+                cur, nd = [], kd
+            cur.extend(members[g])
+            dims = nd
+        if cur:
+            tiers.append(_tier_from(team, glob, cols, lcap, m, nI, cur))
     return tiers
+
+
+def _coarse(v):
+    """Round up to {1, 1.25, 1.5, 1.75} x 2^k (at least 8)."""
+    v = np.maximum(np.asarray(v, dtype=np.int64), 8)
+    p = 1 << (np.floor(np.log2(v)).astype(np.int64) - 2)
+    return ((v + p - 1) // p) * p
+
+
+def _tier_from(team, glob, cols, lcap, m, nI, idx, mode=0):
+    s = np.asarray(idx, dtype=np.int64)
+    s = s[np.argsort(cols[s], kind="stable")]
+    return _Tier(team, glob, lcap[s].max(), m[s].max(), nI[s].max(), cols[s], mode=mode)
 
 
 def _plan(pattern, sys_colptr, sys_rowidx, t_colptr, t_rowidx, t_key, sys_key, cols_host=None):
@@ -320,7 +356,9 @@ def _ws_for(glob, team_bytes, ncols):
     if not glob:
         return None
     grid = min(ncols, 2 * torch.cuda.get_device_properties(_dev()).multi_processor_count)
-    return scratch().get("ls_global", team_bytes * max(grid, 1))
+    # at most ~4 GB of team memory (the launcher shrinks the grid to fit)
+    grid = max(1, min(grid, (4 << 30) // max(team_bytes, 1)))
+    return scratch().get("ls_global", team_bytes * grid)
 
 
 # ---------------------------------------------------------------------------
@@ -359,14 +397,37 @@ def _run_tiers(tiers, pattern, A_csc, T_csc, coef, resid, flags, mode=0, jptr=No
     st = _abi.stream()
     acolptr, arowidx, avals = A_csc
     tcolptr, trowidx, tvals = T_csc if T_csc is not None else (None, None, None)
+    sne = []
     for t in tiers:
-        ws = _ws_for(t.glob, t.bytes, t.ncols)
-        _abi.call("pmp_ls_columns", mode, t.team, t.glob, t.lcap, t.mcap, t.ncap, t.ncols,
+        tmode = t.mode if mode == 0 else mode
+        if tmode == 3:
+            sne.append(t)
+        tb = t.bytes if tmode == t.mode else _team_bytes(t.lcap, 0, t.ncap)
+        glob = t.glob if tmode == t.mode else 0
+        team = t.team
+        ws = _ws_for(glob, tb, t.ncols)
+        _abi.call("pmp_ls_columns", tmode, team, glob, t.lcap, t.mcap, t.ncap, t.ncols,
                   _abi.ptr(t.cols), pattern.n, _abi.ptr(pattern.iptr), _abi.ptr(pattern.iidx),
                   _abi.ptr(acolptr), _abi.ptr(arowidx), _abi.ptr(avals), _abi.ptr(tcolptr),
                   _abi.ptr(trowidx), _abi.ptr(tvals), _abi.ptr(coef), _abi.ptr(resid),
                   _abi.ptr(flags), None, _abi.ptr(jptr), _abi.ptr(jidx), _abi.ptr(ws),
                   ws.numel() if ws is not None else 0, st)
+    if sne:
+        # columns the semi-normal equations could not certify (near rank
+        # deficient G, flags == 2): dense column-pivoted QR in global memory
+        fl = flags.cpu().numpy()
+        for t in sne:
+            bad = t.cols_host[fl[t.cols_host] == 2]
+            if bad.size == 0:
+                continue
+            d = _Tier(256, 1, t.lcap, t.mcap, t.ncap, bad)
+            ws = _ws_for(1, d.bytes, d.ncols)
+            _abi.call("pmp_ls_columns", 0, 256, 1, d.lcap, d.mcap, d.ncap, d.ncols,
+                      _abi.ptr(d.cols), pattern.n, _abi.ptr(pattern.iptr),
+                      _abi.ptr(pattern.iidx), _abi.ptr(acolptr), _abi.ptr(arowidx),
+                      _abi.ptr(avals), _abi.ptr(tcolptr), _abi.ptr(trowidx), _abi.ptr(tvals),
+                      _abi.ptr(coef), _abi.ptr(resid), _abi.ptr(flags), None, None, None,
+                      _abi.ptr(ws), ws.numel(), st)
 
 
 def _get_tiers(pattern, system, target, cols_host=None):

@@ -334,6 +334,33 @@ def test_full_size_sampled_columns(pm, cfg, level):
             assert abs(stats.residuals[j] - r) <= 1e-12
 
 
+def test_c5_large_columns_semi_normal(pm):
+    """c5 (power-law rows) at n = 2^16: most columns exceed shared memory and
+    go through the semi-normal-equations kernel; sampled columns must match
+    the oracle's gelsy solution (supports bit-exact, values 1e-10)."""
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(5, scale=1 << 16)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pts = W.points()
+    A1 = model.assemble(*pts[0])
+    A2 = model.assemble(*pts[1])
+    P1, st = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))
+    Pu, su = pm.update_first(A1, A2, P1, pm.UpdateConfig(pattern_level=0))
+    A1h, A2h = A1.to_scipy(), A2.to_scipy()
+    cols = np.sort(np.random.default_rng(11).permutation(A1.n)[:120])
+    for F, res, stats in ((P1.matrix, orc.spai_build(A1h, pattern_level=0, columns=cols), st),
+                          (Pu.q, orc.update_factor(A1h, A2h, pattern_level=0, columns=cols),
+                           su)):
+        Fc = F.to_scipy(drop_zeros=False).tocsc()
+        for (j, sup, coef, r, dfc, aug) in res:
+            lo, hi = Fc.indptr[j], Fc.indptr[j + 1]
+            assert np.array_equal(Fc.indices[lo:hi], sup), j
+            err = np.linalg.norm(Fc.data[lo:hi] - coef) / max(np.linalg.norm(coef), 1e-300)
+            assert err <= 1e-10, (j, err)
+            assert abs(stats.residuals[j] - r) <= 1e-12
+
+
 def test_c2_sequence_property(pm):
     """c2 at full size: every system's true residual <= 1e-8 (recomputed on
     the host from X) and the first two systems' iterations match the oracle."""
