@@ -247,7 +247,9 @@ def _sne_bytes(lcap, mcap, ncap):
 
 
 def _split_tiers(cols, lcap, m, nI):
-    """Group columns into launch tiers by the team memory they need."""
+    """Group columns into launch tiers by the team memory they need: dense
+    pivoted-QR teams (warp / 128 / 256 threads, shared memory) while the
+    dense block fits, the semi-normal-equations kernel (mode 3) beyond."""
     if cols.size == 0:
         return []
     b = _team_bytes(lcap, _coarse(m), _coarse(nI))   # classify on the padded dims
@@ -259,41 +261,45 @@ def _split_tiers(cols, lcap, m, nI):
         sel = np.flatnonzero(cls == t)
         if sel.size == 0:
             continue
-        if limit is None:
-            # beyond shared memory: semi-normal equations (mode 3), in shared
-            # memory when its much smaller footprint fits, else global
-            sb_ = _sne_bytes(lcap[sel], m[sel], nI[sel])
-            small = sel[sb_ <= 200 * 1024]
-            large = sel[sb_ > 200 * 1024]
-            if small.size:
-                tiers.append(_tier_from(256, 0, cols, lcap, m, nI, small, mode=3))
-            if large.size:
-                tiers.append(_tier_from(256, 1, cols, lcap, m, nI, large, mode=3))
+        if limit is not None:
+            tiers += _bucket_merge(sel, cols, lcap, m, nI, _team_bytes, limit, team, 0, 0)
             continue
-        # bucket the columns by coarsened dimensions (<= 25 % padding), then
-        # merge buckets in size order while the merged team still fits the
-        # tier: O(n log n) and a handful of launches even for power-law sizes
-        key = np.stack([lcap[sel], _coarse(nI[sel]), _coarse(m[sel])], axis=1)
-        ukeys, inv = np.unique(key, axis=0, return_inverse=True)
-        inv = inv.ravel()
-        gbytes = _team_bytes(ukeys[:, 0], ukeys[:, 2], ukeys[:, 1])
-        order = np.argsort(gbytes, kind="stable")
-        members = [[] for _ in range(len(ukeys))]
-        for i, g in enumerate(inv):
-            members[g].append(sel[i])
-        cur, dims = [], None
-        for g in order:
-            kd = ukeys[g]
-            nd = kd if dims is None else np.maximum(dims, kd)
-            if dims is not None and limit is not None and \
-                    _team_bytes(nd[0], nd[2], nd[1]) > limit:
-                tiers.append(_tier_from(team, glob, cols, lcap, m, nI, cur))
-                cur, nd = [], kd
-            cur.extend(members[g])
-            dims = nd
-        if cur:
-            tiers.append(_tier_from(team, glob, cols, lcap, m, nI, cur))
+        # beyond shared memory: semi-normal equations, in shared memory when
+        # its much smaller footprint fits, else in global memory
+        sb_ = _sne_bytes(lcap[sel], _coarse(m[sel]), _coarse(nI[sel]))
+        small = sel[sb_ <= 200 * 1024]
+        large = sel[sb_ > 200 * 1024]
+        tiers += _bucket_merge(small, cols, lcap, m, nI, _sne_bytes, 200 * 1024, 256, 0, 3)
+        if large.size:
+            tiers.append(_tier_from(256, 1, cols, lcap, m, nI, large, mode=3))
     return tiers
+
+
+def _bucket_merge(sel, cols, lcap, m, nI, bytes_fn, limit, team, glob, mode):
+    """Bucket columns by coarsened dimensions (<= 25 % padding), then merge
+    buckets in size order while the merged team still fits `limit`:
+    O(n log n) and a handful of launches even for power-law sizes."""
+    if sel.size == 0:
+        return []
+    key = np.stack([lcap[sel], _coarse(nI[sel]), _coarse(m[sel])], axis=1)
+    ukeys, inv = np.unique(key, axis=0, return_inverse=True)
+    inv = inv.ravel()
+    gbytes = bytes_fn(ukeys[:, 0], ukeys[:, 2], ukeys[:, 1])
+    order = np.argsort(gbytes, kind="stable")
+    by_group = np.argsort(inv, kind="stable")
+    bounds = np.searchsorted(inv[by_group], np.arange(len(ukeys) + 1))
+    out, cur, dims = [], [], None
+    for g in order:
+        kd = ukeys[g]
+        nd = kd if dims is None else np.maximum(dims, kd)
+        if dims is not None and bytes_fn(nd[0], nd[2], nd[1]) > limit:
+            out.append(_tier_from(team, glob, cols, lcap, m, nI, np.concatenate(cur), mode))
+            cur, nd = [], kd
+        cur.append(sel[by_group[bounds[g]:bounds[g + 1]]])
+        dims = nd
+    if cur:
+        out.append(_tier_from(team, glob, cols, lcap, m, nI, np.concatenate(cur), mode))
+    return out
 
 
 def _coarse(v):
