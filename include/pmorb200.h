@@ -230,6 +230,10 @@ int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int o
                     int nrhs, int ncols_old, double* h_QR, double* h_tau, int* h_ext,
                     double* h_C, double* h_Y, double* h_resnorm, double* h_colsbuf);
 
+/* Micro-benchmark: `iters` cooperative grid barriers over blocks_per_sm x
+ * #SMs CTAs (diagnostic; time with events around the call). */
+int pmp_bench_grid_sync(int blocks_per_sm, int iters, void* stream);
+
 /* ---- helpers ------------------------------------------------------------ */
 /* dst[:, dst_cols[c]] = src[:, src_cols[c]] for c < nc (NULL = identity). */
 int pmp_copy_cols(int n, int nc, const double* d_src, int lds, const int32_t* d_src_cols,

@@ -86,6 +86,7 @@ _SIGS = {
     "pmp_gcro_absorb": ([c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                          c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                          c_vp], c_int),
+    "pmp_bench_grid_sync": ([c_int, c_int, c_vp], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp, c_vp], c_int),

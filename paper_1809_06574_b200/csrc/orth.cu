@@ -570,6 +570,18 @@ __global__ void __launch_bounds__(kOrthT, 2) k_fold(FoldParams F) {
   if (blockIdx.x == 0 && threadIdx.x == 0) F.out[0] = (double)kk;
 }
 
+// micro-benchmark of the grid barrier the cooperative kernels rely on
+__global__ void __launch_bounds__(kOrthT, 2) k_grid_sync_bench(int iters, double* sink) {
+  cg::grid_group grid = cg::this_grid();
+  double acc = threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+    acc += 1.0;
+    __threadfence();
+    grid.sync();
+  }
+  if (acc < 0) *sink = acc;
+}
+
 size_t fold_smem_bytes(int rows, int kc, int cached) {
   size_t d = (size_t)kc + 8 + 8 * 32 * 16;
   if (cached) d += (size_t)rows * (2 * odd_ld(kc) + 2);
@@ -717,6 +729,21 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
 }
 
 extern "C" {
+
+// Enqueue `iters` grid barriers over blocks_per_sm x #SMs CTAs of 256
+// threads (time it with events around the call).
+int pmp_bench_grid_sync(int blocks_per_sm, int iters, void* stream) {
+  int g = orth_max_grid() / 2 * blocks_per_sm;
+  double* sink = nullptr;
+  void* args[] = {&iters, &sink};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_grid_sync_bench, dim3(g), dim3(kOrthT),
+                                              args, 0, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error("pmp_bench_grid_sync: %s", cudaGetErrorString(e));
+    return PMP_ERR_CUDA;
+  }
+  return PMP_OK;
+}
 
 size_t pmp_fold_workspace(int n, int kc) {
   const int g = orth_max_grid();
