@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--systems", type=int, default=0, help="limit #systems (debug)")
+    ap.add_argument("--workers", type=int, default=4,
+                    help="host threads / CUDA streams driving independent systems")
     return ap.parse_args()
 
 
@@ -176,7 +178,7 @@ def run_ours(args):
 
     def step():
         return pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
-                               group=group, timing=True)
+                               group=group, timing=True, workers=args.workers)
 
     def barrier():
         if world > 1:
@@ -222,7 +224,9 @@ def run_ours(args):
     i0 = torch.cuda.Event(enable_timing=True)
     i1 = torch.cuda.Event(enable_timing=True)
     i0.record()
-    step()
+    # single stream, so each event pair brackets one kernel and nothing else
+    pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world, group=group,
+                    timing=True, workers=1)
     i1.record()
     barrier()
     instr_ms = i0.elapsed_time(i1)
@@ -268,7 +272,8 @@ def run_ours(args):
                        "rhs_block": int(W.rhs.shape[1]), "pattern_level": level,
                        "precond": "spai-update-first", "tol": 1e-8,
                        "l2": "flushed before every step (256 MB write)",
-                       "parallelism": "systems round-robin over %d GPU(s)" % world},
+                       "parallelism": "systems round-robin over %d GPU(s), %d concurrent "
+                                      "streams per GPU" % (world, args.workers)},
             "sequence_s": ms_per_step / 1e3,
             "phases_s": {"assemble": asm_s, "build": build_s, "solve": solve_s},
             "spai_update_columns_per_s": cols / build_s if build_s > 0 else None,
@@ -356,7 +361,8 @@ def run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, group, ba
             dv.copy_(hv, non_blocking=True)
         Bd.copy_(Bh, non_blocking=True)
         recs, _ = pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
-                                  group=group, keep_solutions=True, timing=False)
+                                  group=group, keep_solutions=True, timing=False,
+                                  workers=args.workers)
         for i, r in enumerate(recs):
             Xh[i].copy_(r["X"], non_blocking=True)
         e1.record()

@@ -230,6 +230,11 @@ int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int o
                     int nrhs, int ncols_old, double* h_QR, double* h_tau, int* h_ext,
                     double* h_C, double* h_Y, double* h_resnorm, double* h_colsbuf);
 
+/* Route every cooperative launch (pmp_orth_step, pmp_fold, pmp_gcro_step's
+ * orthogonalisation) through one shared stream, with event handoffs to and
+ * from the caller's stream, so concurrent workers never run two grid-barrier
+ * kernels at once.  NULL restores launching on the caller's stream. */
+int pmp_set_coop_stream(void* stream);
 /* Micro-benchmark: `iters` cooperative grid barriers over blocks_per_sm x
  * #SMs CTAs (diagnostic; time with events around the call). */
 int pmp_bench_grid_sync(int blocks_per_sm, int iters, void* stream);

@@ -627,6 +627,29 @@ static void orth_geometry(int n, int total, int k, int sb, int* grid, int* rows,
   }
 }
 
+// Cooperative (grid-barrier) kernels must never be partially resident at the
+// same time: when several host threads drive independent systems on their
+// own streams, every cooperative launch is routed through one shared
+// stream (event handoff both ways), which serialises them while all other
+// kernels of the workers still overlap.
+static cudaStream_t g_coop_stream = nullptr;
+
+static cudaError_t coop_launch(const void* fn, int g, void** args, size_t smem, cudaStream_t user) {
+  if (!g_coop_stream || g_coop_stream == user)
+    return cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem, user);
+  thread_local cudaEvent_t in = nullptr, out = nullptr;
+  if (!in) {
+    cudaEventCreateWithFlags(&in, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&out, cudaEventDisableTiming);
+  }
+  cudaEventRecord(in, user);
+  cudaStreamWaitEvent(g_coop_stream, in, 0);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem, g_coop_stream);
+  cudaEventRecord(out, g_coop_stream);
+  cudaStreamWaitEvent(user, out, 0);
+  return e;
+}
+
 static int orth_max_grid() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -719,8 +742,7 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
   P.dbase = dbase;
   P.mbase = mbase;
   void* args[] = {&P};
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem,
-                                              reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = coop_launch(fn, g, args, smem, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     set_error("pmp_orth_step: %s", cudaGetErrorString(e));
     return PMP_ERR_CUDA;
@@ -729,6 +751,13 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
 }
 
 extern "C" {
+
+// Route every cooperative launch through `stream` (NULL: launch on the
+// caller's stream, the single-worker default).
+int pmp_set_coop_stream(void* stream) {
+  g_coop_stream = reinterpret_cast<cudaStream_t>(stream);
+  return PMP_OK;
+}
 
 // Enqueue `iters` grid barriers over blocks_per_sm x #SMs CTAs of 256
 // threads (time it with events around the call).
@@ -792,8 +821,7 @@ int pmp_fold(int n, int na, const double* img, int ldi, const double* dz, int ld
   F.wz = F.gout + (kc + 1);
   F.out = out;
   void* args[] = {&F};
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem,
-                                              reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = coop_launch(fn, g, args, smem, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     set_error("pmp_fold: %s", cudaGetErrorString(e));
     return PMP_ERR_CUDA;

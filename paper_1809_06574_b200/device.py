@@ -64,10 +64,12 @@ _scratch = {}
 
 
 def scratch():
-    d = torch.cuda.current_device()
-    s = _scratch.get(d)
+    """Scratch of the current (device, stream): concurrent workers on their
+    own streams never share a workspace."""
+    key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    s = _scratch.get(key)
     if s is None:
-        s = _scratch[d] = Scratch()
+        s = _scratch[key] = Scratch()
     return s
 
 

@@ -499,12 +499,14 @@ _MAPPED = {}
 
 
 def _mapped_pair(ndoubles):
-    """Two mapped host buffers of at least `ndoubles`, cached per process."""
-    pair = _MAPPED.get("pair")
+    """Two mapped host buffers of at least `ndoubles`, cached per thread."""
+    import threading
+    key = threading.get_ident()
+    pair = _MAPPED.get(key)
     if pair is None or pair[0].array.size < ndoubles:
         size = max(ndoubles, 2 * (pair[0].array.size if pair else 0))
         pair = [_abi.MappedBuffer(size), _abi.MappedBuffer(size)]
-        _MAPPED["pair"] = pair
+        _MAPPED[key] = pair
     return pair
 
 

@@ -144,14 +144,25 @@ def gather_records(records, n_systems, group=None):
 # ---------------------------------------------------------------------------
 
 def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, rank=0, world=1,
-                 group=None, keep_solutions=False, timing=True):
+                 group=None, keep_solutions=False, timing=True, workers=1):
     """Run the whole parametric sequence; returns (records, info).
 
     records: one dict per system this rank owns (index, sigma, p, label,
     iterations, converged, counts, final residuals, optional X).
-    info: phase times from CUDA events (assemble / build / solve seconds,
-    build columns) for this rank.
+    info: phase times from CUDA events (summed assemble / build / solve
+    seconds; with workers > 1 the phases of different systems overlap) and
+    the number of SPAI / update columns built.
+
+    workers > 1 (first-approach / independent policies): after the initial
+    system (and one update that warms the plan caches), the remaining
+    systems are dealt to `workers` host threads, each driving its own CUDA
+    stream, so the latency-bound block solves of independent systems overlap
+    on the device; grid-barrier kernels are serialised through one shared
+    stream (pmp_set_coop_stream).
     """
+    import threading
+    from . import _abi
+
     policy = policy or PrecondPolicy("spai-update-first")
     solver_cfg = solver_cfg or SolverConfig(tol=1e-8)
     B = model.rhs if B is None else B
@@ -161,20 +172,20 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     nsys = len(points)
     mine = owned_systems(nsys, rank, world, policy.kind)
     seq = SequencePreconditioner(policy)
-    ev = []
+    lock = threading.Lock()
 
     def mark():
         if not timing:
             return None
         e = torch.cuda.Event(enable_timing=True)
         e.record()
-        ev.append(e)
         return e
 
     phases = {"assemble": [], "build": [], "solve": []}
-    build_cols = 0
+    state = {"build_cols": 0}
     records = []
     sharded = world > 1 and policy.kind == "spai-update-first"
+    A1 = P1 = None
     if sharded:
         # every rank: A1 locally; rank 0 builds P1; broadcast the values
         t0 = mark()
@@ -183,7 +194,7 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
         phases["assemble"].append((t0, t1))
         if rank == 0:
             P1, _ = spai_build(A1, policy.spai, threads=policy.threads)
-            build_cols += A1.n
+            state["build_cols"] += A1.n
         else:
             pat = level0_pattern(A1)
             vals = torch.empty(pat.nnz, dtype=torch.float64, device=A1.vals.device)
@@ -192,26 +203,20 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
         phases["build"].append((t1, t2))
         broadcast_values(P1.matrix.vals, 0, group)
         seq.seed(A1, P1)
-    for idx in mine:
+
+    def do_system(idx):
         s, p = points[idx]
         t0 = mark()
-        if sharded and idx == 0:
-            A = A1
-        else:
-            A = model.assemble(s, p)
+        A = A1 if (sharded and idx == 0) else model.assemble(s, p)
         t1 = mark()
         if sharded and idx == 0:
-            P, label = P1, "spai"
+            P, label, cols = P1, "spai", 0
         else:
             P, _, label, _ = seq.for_system(A)
-            build_cols += A.n if P is not None else 0
+            cols = A.n if P is not None else 0
         t2 = mark()
         X, rep = block_gcro_solve(A, Bd, P=P, cfg=solver_cfg)
         t3 = mark()
-        if timing:
-            phases["assemble"].append((t0, t1))
-            phases["build"].append((t1, t2))
-            phases["solve"].append((t2, t3))
         rec = {"index": idx, "sigma": float(s), "p": [float(v) for v in p], "label": label,
                "iterations": rep.iterations, "converged": rep.converged,
                "matvec_count": rep.matvec_count, "precond_apply_count": rep.precond_apply_count,
@@ -220,8 +225,52 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                "launches": getattr(rep, "device_launches", 0)}
         if keep_solutions:
             rec["X"] = X
-        records.append(rec)
-    info = {"build_columns": build_cols}
+        with lock:
+            records.append(rec)
+            state["build_cols"] += cols
+            if timing:
+                phases["assemble"].append((t0, t1))
+                phases["build"].append((t1, t2))
+                phases["solve"].append((t2, t3))
+
+    parallel = workers > 1 and policy.kind in ("spai-update-first", "spai", "none")
+    head = mine[:2] if parallel else mine
+    for idx in head:
+        do_system(idx)
+    rest = mine[len(head):]
+    if rest:
+        main = torch.cuda.current_stream()
+        coop = torch.cuda.Stream()
+        coop.wait_stream(main)
+        streams = [torch.cuda.Stream() for _ in range(min(workers, len(rest)))]
+        for st in streams:
+            st.wait_stream(main)
+        errors = []
+
+        def worker(w):
+            try:
+                with torch.cuda.stream(streams[w]):
+                    for idx in rest[w::len(streams)]:
+                        do_system(idx)
+            except BaseException as e:  # surfaced after join
+                errors.append(e)
+
+        _abi.check(_abi.lib().pmp_set_coop_stream(coop.cuda_stream), "pmp_set_coop_stream")
+        try:
+            threads = [threading.Thread(target=worker, args=(w,)) for w in range(len(streams))]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+        finally:
+            _abi.lib().pmp_set_coop_stream(None)
+        for st in streams:
+            main.wait_stream(st)
+        main.wait_stream(coop)
+        if errors:
+            raise errors[0]
+    records.sort(key=lambda r: r["index"])
+    info = {"build_columns": state["build_cols"]}
     if timing:
         torch.cuda.synchronize()
         for k, lst in phases.items():
