@@ -223,6 +223,44 @@ int pmp_gcro_cycle_end(int n, int s, int na, const int32_t* d_act, const double*
                        const int32_t* d_a_rowptr, const int32_t* d_a_colidx,
                        const double* d_a_vals, double* d_T0, double* d_T1, double* d_nrm,
                        void* d_gram_ws, size_t gram_ws_bytes, void* stream);
+/* State of the native inner loop of one GCRO cycle (pmp_gcro_inner).  The
+ * caller owns every buffer; the loop runs full-rank block steps
+ * (pmp_gcro_step + wait + pmp_gcro_absorb, with the next step launched
+ * speculatively) until
+ *   status 0: all estimates <= tol (cycle converged)
+ *   status 2: m >= inner_restart      status 3: iterations >= max_iters
+ *   status 4: G rank deficient after an absorb (caller: min-norm solve)
+ *   status 5: the pending step needs the Householder deflation fallback
+ * Estimates of each completed step are written row by row to hist. */
+typedef struct PmpGcroInner {
+  int n, s, na, k, cap, kc, ldq;
+  double tol;
+  int max_iters, inner_restart;
+  int nfac;
+  const int32_t* const* fac_rowptr;
+  const int32_t* const* fac_colidx;
+  const double* const* fac_vals;
+  const int32_t* a_rowptr;
+  const int32_t* a_colidx;
+  const double* a_vals;
+  double *V, *W, *T0, *T1, *T2;
+  const double* C;
+  double* d_small;
+  double* mirror[2];
+  int offB, offH1, offH2, offR, offFlag;
+  void* orth_ws;
+  size_t orth_ws_bytes;
+  void* stream;
+  double *Bmat, *Hb, *QR, *tau;
+  int* ext;
+  double *Cq, *Y, *res, *colsbuf;
+  const double* bn;
+  double* hist;
+  int m, total, ncols, iterations, launched, buf;
+  double prev_max;
+  int matvecs, precond_applies, status, steps_done;
+} PmpGcroInner;
+int pmp_gcro_inner(PmpGcroInner* state);
 /* Fold a finished full-rank step into Bmat / Hb (krylov.py:190-200) and the
  * incremental QR of G (pmp_host_hls_append). */
 int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int offR, int cap,

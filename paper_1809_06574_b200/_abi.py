@@ -87,6 +87,7 @@ _SIGS = {
                          c_vp, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                          c_vp], c_int),
     "pmp_bench_grid_sync": ([c_int, c_int, c_vp], c_int),
+    "pmp_gcro_inner": ([c_vp], c_int),
     "pmp_set_coop_stream": ([c_vp], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,

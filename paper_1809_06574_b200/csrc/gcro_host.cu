@@ -215,4 +215,87 @@ int pmp_gcro_absorb(const double* small, int offB, int offH1, int offH2, int off
                              resnorm);
 }
 
+// The inner loop of one GCRO cycle (krylov.py:184-216), natively, for the
+// fast path (every block step full rank, G full rank).  Mirrors the Python
+// loop in krylov._solve exactly: launch (or reuse the speculatively
+// launched) step, wait for its flag, speculate the next step, absorb,
+// estimate, stop on convergence / restart length / max_iters.  Returns to
+// the caller (status 4 / 5) when a step needs the host fallbacks.
+int pmp_gcro_inner(PmpGcroInner* g) {
+  const int na = g->na;
+  g->steps_done = 0;
+  while (true) {
+    if (g->iterations >= g->max_iters) {
+      g->status = 3;
+      return PMP_OK;
+    }
+    if (g->m >= g->inner_restart) {
+      g->status = 2;
+      return PMP_OK;
+    }
+    const int q0 = g->m, sb = g->total - g->m;
+    double* mirror = g->mirror[g->buf];
+    if (!g->launched) {
+      int rc = pmp_gcro_step(g->n, g->s, g->nfac, g->fac_rowptr, g->fac_colidx, g->fac_vals,
+                             g->a_rowptr, g->a_colidx, g->a_vals, g->V, g->cap, q0, sb, g->W,
+                             g->T0, g->T1, g->T2, g->C, g->kc, g->k, g->total, g->d_small, mirror,
+                             g->offB, g->offH1, g->offH2, g->offR, g->offFlag, g->orth_ws,
+                             g->orth_ws_bytes, g->stream, nullptr, nullptr);
+      if (rc) return rc;
+      g->launched = 1;
+    }
+    int rc = pmp_host_wait_flag(mirror + g->offFlag, -1.0, 60000000LL, g->stream);
+    if (rc) return rc;
+    if (mirror[g->offFlag] != 0.0) {
+      g->status = 5;  // deflation fallback: the Python loop takes this step
+      return PMP_OK;
+    }
+    // consume the step
+    g->launched = 0;
+    g->iterations += 1;
+    g->matvecs += sb;
+    if (g->nfac) g->precond_applies += sb;
+    const int m_new = g->total, total_new = g->total + sb;
+    const int cur = g->buf;
+    if (g->iterations < g->max_iters && m_new < g->inner_restart &&
+        g->prev_max > 20.0 * g->tol) {
+      rc = pmp_gcro_step(g->n, g->s, g->nfac, g->fac_rowptr, g->fac_colidx, g->fac_vals,
+                         g->a_rowptr, g->a_colidx, g->a_vals, g->V, g->cap, m_new, sb, g->W,
+                         g->T0, g->T1, g->T2, g->C, g->kc, g->k, total_new, g->d_small,
+                         g->mirror[cur ^ 1], g->offB, g->offH1, g->offH2, g->offR, g->offFlag,
+                         g->orth_ws, g->orth_ws_bytes, g->stream, nullptr, nullptr);
+      if (rc) return rc;
+      g->launched = 1;
+      g->buf = cur ^ 1;
+    }
+    const int nnew = g->ncols == 0 ? g->k + sb : sb;
+    rc = pmp_gcro_absorb(g->mirror[cur], g->offB, g->offH1, g->offH2, g->offR, g->cap, g->k, q0,
+                         sb, g->total, g->Bmat, g->Hb, g->ldq, na, g->ncols, g->QR, g->tau,
+                         g->ext, g->Cq, g->Y, g->res, g->colsbuf);
+    g->ncols += nnew;
+    g->m = m_new;
+    g->total = total_new;
+    if (rc == 1) {
+      g->status = 4;  // G rank deficient: the caller solves min-norm (gelsd)
+      return PMP_OK;
+    }
+    if (rc) return rc;
+    bool conv = true;
+    double mx = 0.0;
+    double* h = g->hist + (size_t)g->steps_done * na;
+    for (int c = 0; c < na; ++c) {
+      const double est = g->bn[c] > 0 ? g->res[c] / g->bn[c] : 0.0;
+      h[c] = est;
+      if (!(est <= g->tol)) conv = false;
+      if (est > mx) mx = est;
+    }
+    g->steps_done += 1;
+    g->prev_max = mx;
+    if (conv) {
+      g->status = 0;
+      return PMP_OK;
+    }
+  }
+}
+
 }  // extern "C"

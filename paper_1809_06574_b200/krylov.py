@@ -277,6 +277,35 @@ class _Dev:
                    A.vals.data_ptr(), self.ptr["T0"], self.ptr["T1"], self.smp_["NRM"],
                    self.gws, self.gwb, self.st)
 
+    def inner_state(self, A, chain):
+        """PmpGcroInner with the solve-constant fields filled (pointers,
+        offsets, stream); the caller sets the per-cycle fields."""
+        if getattr(self, "_inner", None) is None:
+            self._chain_arrays(chain)
+            g = _InnerState()
+            g.n, g.s, g.cap, g.kc, g.ldq = self.n, self.s, self.cap, self.kc, self.kc + self.cap
+            g.nfac = len(chain)
+            g.fac_rowptr = ctypes.cast(self._fr, ctypes.c_void_p)
+            g.fac_colidx = ctypes.cast(self._fc, ctypes.c_void_p)
+            g.fac_vals = ctypes.cast(self._fv, ctypes.c_void_p)
+            st = A.structure
+            g.a_rowptr, g.a_colidx = st.rowptr.data_ptr(), st.colidx.data_ptr()
+            g.a_vals = A.vals.data_ptr()
+            for name in ("V", "W", "T0", "T1", "T2", "C"):
+                setattr(g, name, self.ptr[name])
+            g.d_small = self.smbase
+            g.mirror[0], g.mirror[1] = self.mptr[0], self.mptr[1]
+            g.offB, g.offH1, g.offH2 = self.off["G1"], self.off["G2"], self.off["G3"]
+            g.offR, g.offFlag = self.off["RT"], self.off["FLAG"]
+            g.orth_ws, g.orth_ws_bytes = self.ows, self.owb
+            g.stream = self.st
+            g.colsbuf = self.colsbuf.ctypes.data
+            self.hist = np.zeros((self.cap + 2, self.s))
+            g.hist = self.hist.ctypes.data
+            self.f_inner = _abi.lib().pmp_gcro_inner
+            self._inner = g
+        return self._inner
+
     def wait(self, buf):
         rc = self.f_wait(self.mptr[buf] + 8 * self.off["FLAG"], -1.0, 60_000_000, self.st)
         if rc:
@@ -495,6 +524,113 @@ class _Projected:
         return Y, self.res.copy()
 
 
+# the inner loop runs natively (pmp_gcro_inner) unless PMP_PY_INNER=1 selects
+# the equivalent Python loop (kept for debugging and A/B comparisons)
+NATIVE_INNER = __import__("os").environ.get("PMP_PY_INNER") != "1"
+
+
+class _InnerState(ctypes.Structure):
+    """ctypes mirror of PmpGcroInner (include/pmorb200.h)."""
+    _fields_ = [(f, ctypes.c_int) for f in ("n", "s", "na", "k", "cap", "kc", "ldq")] + [
+        ("tol", ctypes.c_double), ("max_iters", ctypes.c_int), ("inner_restart", ctypes.c_int),
+        ("nfac", ctypes.c_int)] + [
+        (f, ctypes.c_void_p) for f in ("fac_rowptr", "fac_colidx", "fac_vals", "a_rowptr",
+                                       "a_colidx", "a_vals", "V", "W", "T0", "T1", "T2", "C",
+                                       "d_small")] + [
+        ("mirror", ctypes.c_void_p * 2)] + [
+        (f, ctypes.c_int) for f in ("offB", "offH1", "offH2", "offR", "offFlag")] + [
+        ("orth_ws", ctypes.c_void_p), ("orth_ws_bytes", ctypes.c_size_t),
+        ("stream", ctypes.c_void_p)] + [
+        (f, ctypes.c_void_p) for f in ("Bmat", "Hb", "QR", "tau", "ext", "Cq", "Y", "res",
+                                       "colsbuf", "bn", "hist")] + [
+        (f, ctypes.c_int) for f in ("m", "total", "ncols", "iterations", "launched", "buf")] + [
+        ("prev_max", ctypes.c_double)] + [
+        (f, ctypes.c_int) for f in ("matvecs", "precond_applies", "status", "steps_done")]
+
+
+def _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
+                  last_rel, active):
+    """Inner loop of one cycle through pmp_gcro_inner (native, GIL released
+    while it runs); the rare host fallbacks (rank-deficient G: min-norm
+    gelsd; near-deficient block: Householder deflation) are handled here and
+    the native loop resumed.  Returns (m, total, Y, converged, exhausted)."""
+    g = D.inner_state(A, chain)
+    bn = np.ascontiguousarray(bn_act, dtype=np.float64)
+    g.na, g.k, g.m, g.total, g.ncols = na, k, 0, bs, 0
+    g.launched, g.buf, g.prev_max = 0, 0, prev_max
+    g.iterations, g.max_iters, g.inner_restart = report.iterations, cfg.max_iters, \
+        cfg.inner_restart
+    g.tol = cfg.tol
+    g.Bmat, g.Hb = Bmat.ctypes.data, Hb.ctypes.data
+    g.QR, g.tau, g.ext = proj.QR.ctypes.data, proj.tau.ctypes.data, proj.ext.ctypes.data
+    g.Cq, g.Y, g.res = proj.C.ctypes.data, proj.Y.ctypes.data, proj.res.ctypes.data
+    g.bn = bn.ctypes.data
+    Y = None
+    conv = exh = False
+    s, cap = D.s, D.cap
+    while True:
+        g.matvecs = g.precond_applies = 0
+        rc = D.f_inner(ctypes.byref(g))
+        if rc:
+            _abi.check(rc, "pmp_gcro_inner")
+        for i in range(g.steps_done):
+            last_rel[active] = D.hist[i, :na]
+            report.residual_history.append(last_rel.copy())
+        report.iterations = g.iterations
+        report.matvec_count += g.matvecs
+        report.precond_apply_count += g.precond_applies
+        proj.ncols = g.ncols
+        if g.steps_done:
+            Y = proj.Y.ravel()[:g.ncols * na].reshape(na, g.ncols).T.copy()
+        st = g.status
+        if st == 0:
+            conv = True
+            break
+        if st in (2, 3):
+            break
+        if st == 4:
+            # G (near) rank deficient: the reference's minimum-norm gelsd solve
+            G = _build_G(k, Bmat, Hb, g.total, g.m)
+            rhs = proj.rhs0[:k + g.total]
+            Y, _, _, _ = np.linalg.lstsq(G, rhs, rcond=None)
+            rn = np.linalg.norm(rhs - G @ Y, axis=0)
+        else:
+            # st == 5: the pending step needs the Householder deflation
+            q0, q1 = g.m, g.total
+            sb = q1 - q0
+            buf = g.buf
+            report.iterations += 1
+            report.matvec_count += sb
+            if chain:
+                report.precond_apply_count += sb
+            report.deflation_fallbacks += 1
+            if k:
+                Bmat[:, q0:q1] = D.mget(buf, "G1", k, sb)
+            Hb[:q1, q0:q1] += D.mget(buf, "G2", q1, sb)
+            Hb[:q1, q0:q1] += D.mget(buf, "G3", q1, sb)
+            Wp = D.p("W")
+            D.tsqr(Wp, s, sb)
+            D.fetch(("FLAG", 1))
+            bs_next, Rn = _deflate_finish(D, Wp, s, sb, D.p("V", q1), cap, cfg.deflation_tol,
+                                          report)
+            Hb[q1:q1 + bs_next, q0:q1] = Rn
+            m, total = q1, q1 + bs_next
+            Y, rn = proj.append(Bmat, Hb, q0, q1, total, m)
+            g.m, g.total, g.ncols = m, total, proj.ncols
+            g.launched, g.iterations = 0, report.iterations
+            exh = bs_next == 0
+        est = _safe_rel(rn, bn_act)
+        g.prev_max = float(np.max(est)) if est.size else 0.0
+        last_rel[active] = est
+        report.residual_history.append(last_rel.copy())
+        if bool(np.all(est <= cfg.tol)):
+            conv = True
+            break
+        if exh:
+            break
+    return g.m, g.total, Y, conv, exh
+
+
 _MAPPED = {}
 
 
@@ -604,8 +740,12 @@ def _solve(A, B, P, cfg):
         launched = False   # the current step's kernels are already enqueued
         buf = 0            # mapped result buffer of the pending native step
         prev_max = float(np.max(start_rel)) if start_rel.size else 0.0
+        if D.native and NATIVE_INNER:
+            m, total, Y, cycle_converged, exhausted = _native_cycle(
+                D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
+                last_rel, active)
         while (report.iterations < cfg.max_iters and not cycle_converged and not exhausted
-               and m < cfg.inner_restart and D.native):
+               and m < cfg.inner_restart and D.native and not NATIVE_INNER):
             # native fast path: two library calls per block step
             q0, q1 = m, total
             sb = q1 - q0

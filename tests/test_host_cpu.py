@@ -127,3 +127,21 @@ def test_gloo_two_ranks_broadcast_and_gather():
     for rank, vals, table in out:
         assert vals == list(range(10))
         assert table == [(i, 10 + i) for i in range(7)]
+
+
+def test_inner_state_layout_matches_header(tmp_path):
+    """ctypes mirror of PmpGcroInner == the C struct (gcc probe)."""
+    import ctypes
+    import subprocess
+    from paper_1809_06574_b200.krylov import _InnerState as S
+    src = tmp_path / "probe.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pmorb200.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu %zu\\n", sizeof(PmpGcroInner),'
+                   ' offsetof(PmpGcroInner, mirror), offsetof(PmpGcroInner, bn),'
+                   ' offsetof(PmpGcroInner, prev_max), offsetof(PmpGcroInner, steps_done));}\n')
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert [int(v) for v in got] == [ctypes.sizeof(S), S.mirror.offset, S.bn.offset,
+                                     S.prev_max.offset, S.steps_done.offset]
