@@ -557,6 +557,7 @@ def _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, H
     g = D.inner_state(A, chain)
     bn = np.ascontiguousarray(bn_act, dtype=np.float64)
     g.na, g.k, g.m, g.total, g.ncols = na, k, 0, bs, 0
+    g.ldq = proj.ldq                      # leading dimension of this cycle's QR / C / Y
     g.launched, g.buf, g.prev_max = 0, 0, prev_max
     g.iterations, g.max_iters, g.inner_restart = report.iterations, cfg.max_iters, \
         cfg.inner_restart
