@@ -163,7 +163,17 @@ __device__ void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, do
   const int nb = gridDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int o = blockIdx.x + nb * wid; o < K; o += nb * (kOrthT / 32)) {
     double s = 0.0;
-    for (int b = lane; b < nb; b += 32) s += __ldcg(P.partial + (size_t)b * K + o);
+    {
+      // independent loads first, then a fixed-order sum
+      double t0 = 0.0, t1 = 0.0;
+      int b = lane;
+      for (; b + 32 < nb; b += 64) {
+        t0 += __ldcg(P.partial + (size_t)b * K + o);
+        t1 += __ldcg(P.partial + (size_t)(b + 32) * K + o);
+      }
+      if (b < nb) t0 += __ldcg(P.partial + (size_t)b * K + o);
+      s = t0 + t1;
+    }
     s = warp_sum(s);
     if (lane == 0) {
       P.gout[o] = s;
@@ -269,6 +279,102 @@ __device__ bool warp_cholesky(const double* G, int m, double* A, double* R, int*
   return ok;
 }
 
+// Same factorisation held in registers: lane i owns row i (m <= NY <= 32),
+// pivot search by a warp arg-max, row swaps by shuffles, column swaps by
+// register selects -- no shared-memory round trips or __syncwarp chains.
+template <int NY>
+__device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, bool pivot,
+                                  double ratio) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double a[NY];
+#pragma unroll
+  for (int c = 0; c < NY; ++c) a[c] = (lane < m && c < m) ? G[lane * m + c] : 0.0;
+  int pv = lane;
+  bool ok = true;
+  double r00 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NY; ++k) {
+    if (k >= m) break;
+    int p = k;
+    if (pivot) {
+      double dii = 0.0;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c == lane) dii = a[c];
+      double best = (lane >= k && lane < m) ? dii : -1.0;
+      int bi = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(full, best, o);
+        const int oi = __shfl_xor_sync(full, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      p = bi;
+    }
+    if (p != k) {
+      const int src = lane == k ? p : (lane == p ? k : lane);
+#pragma unroll
+      for (int c = 0; c < NY; ++c) a[c] = __shfl_sync(full, a[c], src);
+      pv = __shfl_sync(full, pv, src);
+      double ap = 0.0;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c == p) ap = a[c];
+      const double ak = a[k];
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c == p) a[c] = ak;
+      a[k] = ap;
+    }
+    const double dkk = __shfl_sync(full, a[k], k);
+    if (!(dkk > 0.0)) {
+      ok = false;
+      break;
+    }
+    const double rkk = sqrt(dkk);
+    if (k == 0) r00 = rkk;
+    if (lane == k) {
+      const double inv = 1.0 / rkk;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c > k) a[c] *= inv;
+      a[k] = rkk;
+    }
+    double rk[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) rk[c] = __shfl_sync(full, a[c], k);
+    double mine = 0.0;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c == lane) mine = rk[c];
+    if (lane > k && lane < m) {
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c > k) a[c] -= mine * rk[c];
+    }
+  }
+  if (ok && m > 0) {
+    double dl = 0.0;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c == lane) dl = a[c];
+    dl = __shfl_sync(full, dl, m - 1);
+    ok = fabs(dl) > ratio * r00;
+  }
+  if (lane < m) {
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < m) R[lane * m + c] = (c >= lane) ? a[c] : 0.0;
+    piv[lane] = pv;
+  }
+  __syncwarp();
+  return ok;
+}
+
 // Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve); thread per row
 template <int NY>
 __device__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
@@ -341,9 +447,23 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
     const double* Cg = P.C + (size_t)r0 * P.ldc;
     const double* Vg = P.V + (size_t)r0 * P.ldv;
     const double* Wg = P.W + (size_t)r0 * P.ldw;
-    for (int q = threadIdx.x; q < nr * kx; q += kOrthT) {
-      const int r = q / kx, t = q % kx;
-      Xs[(size_t)r * ldx + t] = t < k ? Cg[(size_t)r * P.ldc + t] : Vg[(size_t)r * P.ldv + t - k];
+    // 4 independent loads in flight per thread before the stores
+    const int tot4 = nr * kx;
+    for (int q0 = threadIdx.x; q0 < tot4; q0 += 4 * kOrthT) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * kOrthT;
+        if (q < tot4) {
+          const int r = q / kx, t = q % kx;
+          v[u] = t < k ? __ldcg(Cg + (size_t)r * P.ldc + t) : __ldcg(Vg + (size_t)r * P.ldv + t - k);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * kOrthT;
+        if (q < tot4) Xs[(size_t)(q / kx) * ldx + q % kx] = v[u];
+      }
     }
     for (int q = threadIdx.x; q < nr * sb; q += kOrthT)
       Wv[(size_t)(q / sb) * ldw + q % sb] = Wg[(size_t)(q / sb) * P.ldw + q % sb];
@@ -376,11 +496,18 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
     grid_reduce(grid, P, kx2 * sb, G, second ? P.outH2 : nullptr, kv2 * sb, nullptr);
   }
   // G_W = W1^T W1 - H2^T H2 (into R2 as scratch), then W2 = W1 - V H2
-  for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {
-    const int i = q / sb, j = q % sb;
-    double s = G[(size_t)(kv2 + i) * sb + j];
-    for (int t = 0; t < kv2; ++t) s -= G[t * sb + i] * G[t * sb + j];
-    R2[q] = s;
+  // (4 threads per entry over strided t, combined in a fixed order)
+  const int n4 = 4 * sb * sb, lim4 = (n4 + 31) & ~31;   // warp-uniform trip count
+  for (int q4 = threadIdx.x; q4 < lim4; q4 += kOrthT) {
+    const bool act = q4 < n4;
+    const int q = q4 >> 2, part = q4 & 3;
+    const int i = act ? q / sb : 0, j = act ? q % sb : 0;
+    double s = 0.0;
+    if (act)
+      for (int t = part; t < kv2; t += 4) s += G[t * sb + i] * G[t * sb + j];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (act && part == 0) R2[q] = G[(size_t)(kv2 + i) * sb + j] - s;
   }
   __syncthreads();
   if (second) block_update<NY>(Vonly, tot, Wv, ldw, sb, nr, G);
@@ -390,7 +517,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    bool ok = warp_cholesky(G, sb, A, R1, piv, true, kCholRatio);
+    bool ok = warp_cholesky_reg<NY>(G, sb, R1, piv, true, kCholRatio);
     if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
   }
   __syncthreads();
@@ -408,7 +535,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
     block_gram<NY>(Qv, sb, Q1, ldq, sb, nr, red, P.partial);
     grid_reduce(grid, P, sb * sb, G, nullptr, 0, nullptr);
     if (threadIdx.x < 32) {
-      bool ok = warp_cholesky(G, sb, A, R2, piv2, false, 0.0);
+      bool ok = warp_cholesky_reg<NY>(G, sb, R2, piv2, false, 0.0);
       if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
     }
     __syncthreads();
