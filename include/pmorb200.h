@@ -268,11 +268,59 @@ int pmp_gcro_absorb(const double* h_small, int offB, int offH1, int offH2, int o
                     int nrhs, int ncols_old, double* h_QR, double* h_tau, int* h_ext,
                     double* h_C, double* h_Y, double* h_resnorm, double* h_colsbuf);
 
+/* Device-resident inner loop of one GCRO cycle (krylov.py:184-216): ONE
+ * persistent cooperative kernel runs every block step of the cycle -- the
+ * operator chain W = A F_0 .. F_{nfac-1} V[:, q0:q0+sb], the fused
+ * projection + CGS2 + Cholesky-QR2, and the incremental Householder QR of
+ * the projected least-squares problem with the stopping test -- with grid
+ * barriers instead of host round trips.  Block 0 is the control block (it
+ * owns no rows; it keeps the projected QR in shared memory).
+ * The projected state lives in d_proj (doubles, offsets o*; Bmat k x cap
+ * and Hb cap x cap row-major, QR ldq x ldq and Cq ldq x na column-major,
+ * Y na x n1 rhs-major, hist one row of na estimates per completed step) and
+ * d_istate (int32: [0] m, [1] total, [2] ncols, [3] iterations, [4] status,
+ * [5] history rows written, [6] scratch; ext[] of the QR at [16..16+ldq)).
+ * On entry d_istate[0..3] and Cq / bn must be set (ncols == 0: the kernel
+ * zeroes Bmat / Hb).  Exit status as pmp_gcro_inner: 0 converged,
+ * 2 restart length, 3 max_iters, 4 G rank deficient (state after the
+ * absorb), 5 the pending step needs the Householder deflation (W holds W2,
+ * its B / H1 / H2 are copied to `mirror` at offB / offH1 / offH2). */
+typedef struct PmpGcroCycle {
+  int n, s, cap, kc, ldq, nfac;
+  const int32_t* const* fac_rowptr;
+  const int32_t* const* fac_colidx;
+  const double* const* fac_vals;
+  const int32_t* a_rowptr;
+  const int32_t* a_colidx;
+  const double* a_vals;
+  double *V, *W, *T0, *T1;
+  const double* C;
+  double* d_small;
+  double* mirror;
+  int offB, offH1, offH2, offR;
+  void* ws;
+  size_t ws_bytes;
+  void* stream;
+  int k, na, sb, max_iters, inner_restart, hist_cap;
+  double tol;
+  double* d_proj;
+  int oBmat, oHb, oQR, oTau, oCq, oY, oRes, oBn, oHist, blocks_per_sm;
+  int32_t* d_istate;
+} PmpGcroCycle;
+size_t pmp_cycle_workspace(int n, int cap, int kc, int s);
+int pmp_gcro_cycle_dev(PmpGcroCycle* cycle);
+
 /* Route every cooperative launch (pmp_orth_step, pmp_fold, pmp_gcro_step's
  * orthogonalisation) through one shared stream, with event handoffs to and
  * from the caller's stream, so concurrent workers never run two grid-barrier
  * kernels at once.  NULL restores launching on the caller's stream. */
 int pmp_set_coop_stream(void* stream);
+
+/* Diagnostics only: block 0 of each of the next `records` orthogonalisation
+ * kernels writes the device %globaltimer (ns) at its 11 phase boundaries
+ * into d_stamps[16 * launch + 0..10] (device memory, zero-initialised by
+ * the caller; unreached phases stay 0).  NULL (the default) disables it. */
+int pmp_orth_debug_stamps(unsigned long long* d_stamps, int records);
 /* Micro-benchmark: `iters` cooperative grid barriers over blocks_per_sm x
  * #SMs CTAs (diagnostic; time with events around the call). */
 int pmp_bench_grid_sync(int blocks_per_sm, int iters, void* stream);

@@ -28,17 +28,10 @@
 // kernel leaves W2 in global memory, raises a flag, and the host falls back
 // to Householder TSQR + pivoted QR (pmp_tsqr_r + pmp_host_deflate), which
 // reproduce geqp3's rank decision.
-#include <cooperative_groups.h>
-
-#include "common.cuh"
-
-namespace cg = cooperative_groups;
+#include "orth_dev.cuh"
 
 namespace pmp {
 
-constexpr int kOrthT = 256;
-constexpr double kCholRatio = 1e-5;
-constexpr double kSkipKappa = 4.0;
 
 struct OrthParams {
   int n;
@@ -63,7 +56,16 @@ struct OrthParams {
   // mapped host memory `mbase` and writes the flag there last
   const double* dbase;
   double* mbase;
+  unsigned long long* dbg;  // optional phase timestamps (block 0), diagnostics
 };
+
+__device__ __forceinline__ void stamp(const OrthParams& P, int i) {
+  if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.dbg[i] = t;
+  }
+}
 
 // block 0, all threads: flag (and, with a mirror, the small results) out
 __device__ void publish(const OrthParams& P, double flag) {
@@ -87,328 +89,17 @@ __device__ void publish(const OrthParams& P, double flag) {
   }
 }
 
-// operand view of this block's rows: columns [0, ka) from a, then from b
-struct Rows {
-  const double* a;
-  int lda, ka;
-  const double* b;
-  int ldb;
-  __device__ __forceinline__ double at(int r, int t) const {
-    return t < ka ? a[(size_t)r * lda + t] : b[(size_t)r * ldb + (t - ka)];
-  }
-};
 
-__host__ __device__ __forceinline__ int odd_ld(int w) { return w | 1; }
 
-// partial[b][t * ny + c] = sum over this block's rows of X(r, t) Y[r][c].
-// Lanes own columns t (coalesced / conflict-free with odd leading
-// dimensions), warps split the rows; the per-warp sums are combined in a
-// fixed order through smem.
-template <int NY>
-__device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int ny, int nrows,
-                           double* red, double* partial) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int K = kx * ny;
-  double* part = partial + (size_t)blockIdx.x * K;
-  const int rounds = (kx + 31) / 32;
-  int splits = 8 / rounds;
-  if (splits < 1) splits = 1;
-  for (int job0 = 0; job0 < rounds * splits; job0 += 8) {
-    const int job = job0 + wid;
-    const int rd = job / splits, sp = job % splits;
-    double acc[NY];
-#pragma unroll
-    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
-    const int t = rd * 32 + lane;
-    if (job < rounds * splits && t < kx) {
-      const int per = (nrows + splits - 1) / splits;
-      const int ra = sp * per, rb = min(nrows, ra + per);
-      double xn = ra < rb ? X.at(ra, t) : 0.0;
-      for (int r = ra; r < rb; ++r) {
-        const double x = xn;
-        if (r + 1 < rb) xn = X.at(r + 1, t);   // prefetch the next row's operand
-        const double* y = Y + (size_t)r * ldy;
-#pragma unroll
-        for (int c = 0; c < NY; ++c)
-          if (c < ny) acc[c] += x * y[c];
-      }
-    }
-    if (job < rounds * splits) {
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c < ny) red[((size_t)(job - job0) * 32 + lane) * ny + c] = acc[c];
-    }
-    __syncthreads();
-    // fixed-order sum over the splits of every round covered by this batch
-    for (int o = threadIdx.x; o < K; o += kOrthT) {
-      const int tt = o / ny, c = o % ny, r2 = tt / 32, ln = tt % 32;
-      const int j0 = r2 * splits;
-      if (j0 >= job0 && j0 < job0 + 8) {
-        double s = 0.0;
-        for (int q = 0; q < splits; ++q) s += red[((size_t)(j0 + q - job0) * 32 + ln) * ny + c];
-        part[o] = s;
-      }
-    }
-    __syncthreads();
-  }
-}
 
-// distributed fixed-order reduction of the block partials; every block ends
-// with the full K-vector in smem G.  Entries [0, split) are also copied to
-// out, entries [split, K) to out2 (either may be null).
-__device__ void grid_reduce(cg::grid_group& grid, const OrthParams& P, int K, double* G,
-                            double* out, int split, double* out2) {
-  __threadfence();
-  grid.sync();
-  const int nb = gridDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int o = blockIdx.x + nb * wid; o < K; o += nb * (kOrthT / 32)) {
-    double s = 0.0;
-    {
-      // independent loads first, then a fixed-order sum
-      double t0 = 0.0, t1 = 0.0;
-      int b = lane;
-      for (; b + 32 < nb; b += 64) {
-        t0 += __ldcg(P.partial + (size_t)b * K + o);
-        t1 += __ldcg(P.partial + (size_t)(b + 32) * K + o);
-      }
-      if (b < nb) t0 += __ldcg(P.partial + (size_t)b * K + o);
-      s = t0 + t1;
-    }
-    s = warp_sum(s);
-    if (lane == 0) {
-      P.gout[o] = s;
-      if (o < split) {
-        if (out) out[o] = s;
-      } else if (out2) {
-        out2[o - split] = s;
-      }
-    }
-  }
-  __threadfence();
-  grid.sync();
-  for (int o = threadIdx.x; o < K; o += kOrthT) G[o] = __ldcg(P.gout + o);
-  __syncthreads();
-}
 
-// Y[r][c] -= sum_t X(r, t) G[t][c] ; thread per row, all ny outputs
-template <int NY>
-__device__ void block_update(const Rows& X, int kx, double* Y, int ldy, int ny, int nrows,
-                             const double* G) {
-  for (int r = threadIdx.x; r < nrows; r += kOrthT) {
-    double acc[NY];
-#pragma unroll
-    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
-    for (int t = 0; t < kx; ++t) {
-      const double x = X.at(r, t);
-      const double* g = G + t * ny;
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c < ny) acc[c] += x * g[c];
-    }
-    double* y = Y + (size_t)r * ldy;
-#pragma unroll
-    for (int c = 0; c < NY; ++c)
-      if (c < ny) y[c] -= acc[c];
-  }
-  __syncthreads();
-}
 
-// Cholesky of the m x m SPD matrix G (row-major) by warp 0; with `pivot`,
-// symmetric pivoting on the largest remaining diagonal.  R (row-major,
-// upper) is the factor of P^T G P; returns ok (and the ratio test).
-__device__ bool warp_cholesky(const double* G, int m, double* A, double* R, int* piv, bool pivot,
-                              double ratio) {
-  const int lane = threadIdx.x & 31;
-  for (int q = lane; q < m * m; q += 32) {
-    A[q] = G[q];
-    R[q] = 0.0;
-  }
-  if (lane < m) piv[lane] = lane;
-  __syncwarp();
-  bool ok = true;
-  for (int k = 0; k < m; ++k) {
-    int p = k;
-    if (pivot) {
-      double best = A[k * m + k];
-      for (int j = k + 1; j < m; ++j)
-        if (A[j * m + j] > best) {
-          best = A[j * m + j];
-          p = j;
-        }
-    }
-    if (p != k) {
-      for (int q = lane; q < m; q += 32) {
-        double t = A[k * m + q];
-        A[k * m + q] = A[p * m + q];
-        A[p * m + q] = t;
-      }
-      __syncwarp();
-      for (int q = lane; q < m; q += 32) {
-        double t = A[q * m + k];
-        A[q * m + k] = A[q * m + p];
-        A[q * m + p] = t;
-      }
-      for (int q = lane; q < k; q += 32) {
-        double t = R[q * m + k];
-        R[q * m + k] = R[q * m + p];
-        R[q * m + p] = t;
-      }
-      if (lane == 0) {
-        int t = piv[k];
-        piv[k] = piv[p];
-        piv[p] = t;
-      }
-      __syncwarp();
-    }
-    const double dkk = A[k * m + k];
-    if (!(dkk > 0.0)) {
-      ok = false;
-      break;
-    }
-    const double d = sqrt(dkk);
-    for (int j = k + lane; j < m; j += 32) R[k * m + j] = (j == k) ? d : A[k * m + j] / d;
-    __syncwarp();
-    const int w = m - k - 1;
-    for (int q = lane; q < w * w; q += 32) {
-      int i = k + 1 + q / w, j = k + 1 + q % w;
-      A[i * m + j] -= R[k * m + i] * R[k * m + j];
-    }
-    __syncwarp();
-  }
-  if (ok && m > 0) ok = fabs(R[(m - 1) * m + (m - 1)]) > ratio * fabs(R[0]);
-  return ok;
-}
-
-// Same factorisation held in registers: lane i owns row i (m <= NY <= 32),
-// pivot search by a warp arg-max, row swaps by shuffles, column swaps by
-// register selects -- no shared-memory round trips or __syncwarp chains.
-template <int NY>
-__device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, bool pivot,
-                                  double ratio) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  double a[NY];
-#pragma unroll
-  for (int c = 0; c < NY; ++c) a[c] = (lane < m && c < m) ? G[lane * m + c] : 0.0;
-  int pv = lane;
-  bool ok = true;
-  double r00 = 0.0;
-#pragma unroll
-  for (int k = 0; k < NY; ++k) {
-    if (k >= m) break;
-    int p = k;
-    if (pivot) {
-      double dii = 0.0;
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c == lane) dii = a[c];
-      double best = (lane >= k && lane < m) ? dii : -1.0;
-      int bi = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(full, best, o);
-        const int oi = __shfl_xor_sync(full, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      p = bi;
-    }
-    if (p != k) {
-      const int src = lane == k ? p : (lane == p ? k : lane);
-#pragma unroll
-      for (int c = 0; c < NY; ++c) a[c] = __shfl_sync(full, a[c], src);
-      pv = __shfl_sync(full, pv, src);
-      double ap = 0.0;
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c == p) ap = a[c];
-      const double ak = a[k];
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c == p) a[c] = ak;
-      a[k] = ap;
-    }
-    const double dkk = __shfl_sync(full, a[k], k);
-    if (!(dkk > 0.0)) {
-      ok = false;
-      break;
-    }
-    const double rkk = sqrt(dkk);
-    if (k == 0) r00 = rkk;
-    if (lane == k) {
-      const double inv = 1.0 / rkk;
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c > k) a[c] *= inv;
-      a[k] = rkk;
-    }
-    double rk[NY];
-#pragma unroll
-    for (int c = 0; c < NY; ++c) rk[c] = __shfl_sync(full, a[c], k);
-    double mine = 0.0;
-#pragma unroll
-    for (int c = 0; c < NY; ++c)
-      if (c == lane) mine = rk[c];
-    if (lane > k && lane < m) {
-#pragma unroll
-      for (int c = 0; c < NY; ++c)
-        if (c > k) a[c] -= mine * rk[c];
-    }
-  }
-  if (ok && m > 0) {
-    double dl = 0.0;
-#pragma unroll
-    for (int c = 0; c < NY; ++c)
-      if (c == lane) dl = a[c];
-    dl = __shfl_sync(full, dl, m - 1);
-    ok = fabs(dl) > ratio * r00;
-  }
-  if (lane < m) {
-#pragma unroll
-    for (int c = 0; c < NY; ++c)
-      if (c < m) R[lane * m + c] = (c >= lane) ? a[c] : 0.0;
-    piv[lane] = pv;
-  }
-  __syncwarp();
-  return ok;
-}
-
-// Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve); thread per row
-template <int NY>
-__device__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
-                                const double* R, const int* piv) {
-  __shared__ double rinv[16];
-  if (threadIdx.x < m) rinv[threadIdx.x] = 1.0 / R[threadIdx.x * m + threadIdx.x];
-  __syncthreads();
-  for (int r = threadIdx.x; r < nrows; r += kOrthT) {
-    double x[NY], y[NY];
-#pragma unroll
-    for (int c = 0; c < NY; ++c) x[c] = (c < m) ? X[(size_t)r * ldx + (piv ? piv[c] : c)] : 0.0;
-#pragma unroll
-    for (int c = 0; c < NY; ++c) {
-      if (c < m) {
-        double s = x[c];
-#pragma unroll
-        for (int a = 0; a < NY; ++a)
-          if (a < c) s -= y[a] * R[a * m + c];
-        y[c] = s * rinv[c];
-      } else {
-        y[c] = 0.0;
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < NY; ++c)
-      if (c < m) Y[(size_t)r * ldy + c] = y[c];
-  }
-  __syncthreads();
-}
 
 template <bool CACHED, int NY>
 __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sh[];
+  stamp(P, 0);
   const int r0 = blockIdx.x * P.rows_per_block;
   const int r1 = min(P.n, r0 + P.rows_per_block);
   const int nr = max(0, r1 - r0);
@@ -479,12 +170,16 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
   const double* Vrows = CACHED ? CV.a + k : P.V + (size_t)r0 * P.ldv;
   const int ldvr = CACHED ? CV.lda : P.ldv;
   const Rows Vonly{Vrows, ldvr, tot, Vrows, ldvr};
+  stamp(P, 1);
 
   // ---- R1: [C | V]^T W -------------------------------------------------------
   if (kx > 0) {
     block_gram<NY>(CV, kx, Wv, ldw, sb, nr, red, P.partial);
-    grid_reduce(grid, P, kx * sb, G, P.outB, k * sb, P.npass ? P.outH1 : nullptr);
+    stamp(P, 2);
+    grid_reduce(grid, P.partial, P.gout, kx * sb, G, P.outB, k * sb, P.npass ? P.outH1 : nullptr);
+    stamp(P, 3);
     block_update<NY>(CV, kx, Wv, ldw, sb, nr, G);
+    stamp(P, 4);
   }
   // ---- R2: [V | W1]^T W1 -----------------------------------------------------
   const bool second = P.npass >= 2 && tot > 0;
@@ -493,7 +188,9 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
   {
     const Rows VW{Vrows, ldvr, kv2, Wv, ldw};
     block_gram<NY>(VW, kx2, Wv, ldw, sb, nr, red, P.partial);
-    grid_reduce(grid, P, kx2 * sb, G, second ? P.outH2 : nullptr, kv2 * sb, nullptr);
+    stamp(P, 5);
+    grid_reduce(grid, P.partial, P.gout, kx2 * sb, G, second ? P.outH2 : nullptr, kv2 * sb, nullptr);
+    stamp(P, 6);
   }
   // G_W = W1^T W1 - H2^T H2 (into R2 as scratch), then W2 = W1 - V H2
   // (4 threads per entry over strided t, combined in a fixed order)
@@ -511,6 +208,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
   }
   __syncthreads();
   if (second) block_update<NY>(Vonly, tot, Wv, ldw, sb, nr, G);
+  stamp(P, 7);
   for (int q = threadIdx.x; q < sb * sb; q += kOrthT) {
     const int i = q / sb, j = q % sb;
     G[q] = 0.5 * (R2[i * sb + j] + R2[j * sb + i]);
@@ -521,6 +219,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
     if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
   }
   __syncthreads();
+  stamp(P, 8);
   // a well-conditioned block (|R_00| / |R_mm| <= 4) is orthonormal to
   // ~16 eps after one Cholesky-QR pass: skip the second reduction
   bool single = false;
@@ -533,13 +232,14 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
     // ---- R3: Q1^T Q1 ---------------------------------------------------------
     const Rows Qv{Q1, ldq, sb, Q1, ldq};
     block_gram<NY>(Qv, sb, Q1, ldq, sb, nr, red, P.partial);
-    grid_reduce(grid, P, sb * sb, G, nullptr, 0, nullptr);
+    grid_reduce(grid, P.partial, P.gout, sb * sb, G, nullptr, 0, nullptr);
     if (threadIdx.x < 32) {
       bool ok = warp_cholesky_reg<NY>(G, sb, R2, piv2, false, 0.0);
       if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
     }
     __syncthreads();
   }
+  stamp(P, 9);
   // flag is grid-uniform: every block factored the same reduced matrices
   if (flag[0]) {
     if (CACHED)
@@ -567,6 +267,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_orth(OrthParams P) {
       P.outR[i * sb + piv[c]] = (c >= i) ? s : 0.0;
     }
     __syncthreads();
+    stamp(P, 10);
     publish(P, 0.0);
   }
 }
@@ -648,7 +349,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_fold(FoldParams F) {
     // [C | w]^T w  ->  h1, ||w||^2
     Rows Cw{Cs, ldcs, kk, w, ldwz};
     block_gram<1>(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
-    grid_reduce(grid, P, kk + 1, G, nullptr, 0, nullptr);
+    grid_reduce(grid, P.partial, P.gout, kk + 1, G, nullptr, 0, nullptr);
     const double w0 = sqrt(G[kk]);
     if (w0 == 0.0) {
       if (blockIdx.x == 0 && threadIdx.x == 0) F.out[1 + col] = 0.0;
@@ -660,7 +361,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_fold(FoldParams F) {
       block_update<1>(Conly, kk, w, ldwz, 1, nr, G);
       block_update<1>(Uonly, kk, z, ldwz, 1, nr, G);
       block_gram<1>(Cw, kk + 1, w, ldwz, 1, nr, red, P.partial);
-      grid_reduce(grid, P, kk + 1, G, nullptr, 0, nullptr);
+      grid_reduce(grid, P.partial, P.gout, kk + 1, G, nullptr, 0, nullptr);
       double h2 = 0.0;
       for (int t = 0; t < kk; ++t) h2 += G[t] * G[t];
       const double w1n2 = G[kk];
@@ -671,7 +372,7 @@ __global__ void __launch_bounds__(kOrthT, 2) k_fold(FoldParams F) {
         // cancellation: recompute ||w2||^2 exactly
         Rows Wo{w, ldwz, 1, w, ldwz};
         block_gram<1>(Wo, 1, w, ldwz, 1, nr, red, P.partial);
-        grid_reduce(grid, P, 1, G, nullptr, 0, nullptr);
+        grid_reduce(grid, P.partial, P.gout, 1, G, nullptr, 0, nullptr);
         nw2 = G[0];
       }
       nw = sqrt(fmax(nw2, 0.0));
@@ -760,8 +461,11 @@ static void orth_geometry(int n, int total, int k, int sb, int* grid, int* rows,
 // stream (event handoff both ways), which serialises them while all other
 // kernels of the workers still overlap.
 static cudaStream_t g_coop_stream = nullptr;
+static unsigned long long* g_dbg = nullptr;   // pmp_orth_debug_stamps
+static int g_dbg_left = 0;
 
-static cudaError_t coop_launch(const void* fn, int g, void** args, size_t smem, cudaStream_t user) {
+cudaError_t pmp::coop_launch(const void* fn, int g, void** args, size_t smem,
+                             cudaStream_t user) {
   if (!g_coop_stream || g_coop_stream == user)
     return cudaLaunchCooperativeKernel(fn, dim3(g), dim3(kOrthT), args, smem, user);
   thread_local cudaEvent_t in = nullptr, out = nullptr;
@@ -777,7 +481,7 @@ static cudaError_t coop_launch(const void* fn, int g, void** args, size_t smem, 
   return e;
 }
 
-static int orth_max_grid() {
+int pmp::orth_max_grid() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -868,6 +572,12 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
   P.outFlag = outFlag;
   P.dbase = dbase;
   P.mbase = mbase;
+  P.dbg = nullptr;
+  if (g_dbg && g_dbg_left > 0) {   // one 16-slot record per launch
+    P.dbg = g_dbg;
+    g_dbg += 16;
+    --g_dbg_left;
+  }
   void* args[] = {&P};
   cudaError_t e = coop_launch(fn, g, args, smem, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
@@ -878,6 +588,15 @@ int pmp::orth_step_mirrored(int n, const double* C, int ldc, int k, double* V, i
 }
 
 extern "C" {
+
+// Diagnostics: block 0 of the next `records` k_orth launches writes
+// %globaltimer at 11 phase boundaries into d_stamps[16 * launch + 0..10]
+// (NULL disables; the default).
+int pmp_orth_debug_stamps(unsigned long long* d_stamps, int records) {
+  g_dbg = d_stamps;
+  g_dbg_left = d_stamps ? records : 0;
+  return PMP_OK;
+}
 
 // Route every cooperative launch through `stream` (NULL: launch on the
 // caller's stream, the single-worker default).

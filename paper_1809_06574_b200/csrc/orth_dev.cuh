@@ -1,0 +1,279 @@
+// Device building blocks of the tall-skinny orthogonalisation kernels
+// (k_orth / k_fold in orth.cu, the persistent cycle kernel in cycle.cu).
+// Every block owns a contiguous row range; reductions are two-stage
+// (fixed-order per-block partials, then a distributed fixed-order sum)
+// separated by grid barriers, so results are bitwise reproducible.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace pmp {
+
+namespace cg = cooperative_groups;
+
+constexpr int kOrthT = 256;
+constexpr double kCholRatio = 1e-5;
+constexpr double kSkipKappa = 4.0;
+
+// operand view of this block's rows: columns [0, ka) from a, then from b
+struct Rows {
+  const double* a;
+  int lda, ka;
+  const double* b;
+  int ldb;
+  __device__ __forceinline__ double at(int r, int t) const {
+    return t < ka ? a[(size_t)r * lda + t] : b[(size_t)r * ldb + (t - ka)];
+  }
+};
+
+__host__ __device__ __forceinline__ int odd_ld(int w) { return w | 1; }
+
+// partial[b][t * ny + c] = sum over this block's rows of X(r, t) Y[r][c].
+// Lanes own columns t (coalesced / conflict-free with odd leading
+// dimensions), warps split the rows; the per-warp sums are combined in a
+// fixed order through smem.
+template <int NY>
+__device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int ny, int nrows,
+                           double* red, double* partial) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int K = kx * ny;
+  double* part = partial + (size_t)blockIdx.x * K;
+  const int rounds = (kx + 31) / 32;
+  int splits = 8 / rounds;
+  if (splits < 1) splits = 1;
+  for (int job0 = 0; job0 < rounds * splits; job0 += 8) {
+    const int job = job0 + wid;
+    const int rd = job / splits, sp = job % splits;
+    double acc[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
+    const int t = rd * 32 + lane;
+    if (job < rounds * splits && t < kx) {
+      const int per = (nrows + splits - 1) / splits;
+      const int ra = sp * per, rb = min(nrows, ra + per);
+      double xn = ra < rb ? X.at(ra, t) : 0.0;
+      for (int r = ra; r < rb; ++r) {
+        const double x = xn;
+        if (r + 1 < rb) xn = X.at(r + 1, t);   // prefetch the next row's operand
+        const double* y = Y + (size_t)r * ldy;
+#pragma unroll
+        for (int c = 0; c < NY; ++c)
+          if (c < ny) acc[c] += x * y[c];
+      }
+    }
+    if (job < rounds * splits) {
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c < ny) red[((size_t)(job - job0) * 32 + lane) * ny + c] = acc[c];
+    }
+    __syncthreads();
+    // fixed-order sum over the splits of every round covered by this batch
+    for (int o = threadIdx.x; o < K; o += kOrthT) {
+      const int tt = o / ny, c = o % ny, r2 = tt / 32, ln = tt % 32;
+      const int j0 = r2 * splits;
+      if (j0 >= job0 && j0 < job0 + 8) {
+        double s = 0.0;
+        for (int q = 0; q < splits; ++q) s += red[((size_t)(j0 + q - job0) * 32 + ln) * ny + c];
+        part[o] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// distributed fixed-order reduction of the block partials; every block ends
+// with the full K-vector in smem G.  Entries [0, split) are also copied to
+// out, entries [split, K) to out2 (either may be null).
+static __device__ void grid_reduce(cg::grid_group& grid, double* partial, double* gout, int K,
+                            double* G,
+                            double* out, int split, double* out2) {
+  __threadfence();
+  grid.sync();
+  const int nb = gridDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = blockIdx.x + nb * wid; o < K; o += nb * (kOrthT / 32)) {
+    double s = 0.0;
+    {
+      // independent loads first, then a fixed-order sum
+      double t0 = 0.0, t1 = 0.0;
+      int b = lane;
+      for (; b + 32 < nb; b += 64) {
+        t0 += __ldcg(partial + (size_t)b * K + o);
+        t1 += __ldcg(partial + (size_t)(b + 32) * K + o);
+      }
+      if (b < nb) t0 += __ldcg(partial + (size_t)b * K + o);
+      s = t0 + t1;
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      gout[o] = s;
+      if (o < split) {
+        if (out) out[o] = s;
+      } else if (out2) {
+        out2[o - split] = s;
+      }
+    }
+  }
+  __threadfence();
+  grid.sync();
+  for (int o = threadIdx.x; o < K; o += kOrthT) G[o] = __ldcg(gout + o);
+  __syncthreads();
+}
+
+// Y[r][c] -= sum_t X(r, t) G[t][c] ; thread per row, all ny outputs
+template <int NY>
+__device__ void block_update(const Rows& X, int kx, double* Y, int ldy, int ny, int nrows,
+                             const double* G) {
+  for (int r = threadIdx.x; r < nrows; r += kOrthT) {
+    double acc[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
+    for (int t = 0; t < kx; ++t) {
+      const double x = X.at(r, t);
+      const double* g = G + t * ny;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c < ny) acc[c] += x * g[c];
+    }
+    double* y = Y + (size_t)r * ldy;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < ny) y[c] -= acc[c];
+  }
+  __syncthreads();
+}
+
+// Same factorisation held in registers: lane i owns row i (m <= NY <= 32),
+// pivot search by a warp arg-max, row swaps by shuffles, column swaps by
+// register selects -- no shared-memory round trips or __syncwarp chains.
+template <int NY>
+__device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, bool pivot,
+                                  double ratio) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double a[NY];
+#pragma unroll
+  for (int c = 0; c < NY; ++c) a[c] = (lane < m && c < m) ? G[lane * m + c] : 0.0;
+  int pv = lane;
+  bool ok = true;
+  double r00 = 0.0;
+#pragma unroll
+  for (int k = 0; k < NY; ++k) {
+    if (k >= m) break;
+    int p = k;
+    if (pivot) {
+      double dii = 0.0;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c == lane) dii = a[c];
+      double best = (lane >= k && lane < m) ? dii : -1.0;
+      int bi = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(full, best, o);
+        const int oi = __shfl_xor_sync(full, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      p = bi;
+    }
+    if (p != k) {
+      const int src = lane == k ? p : (lane == p ? k : lane);
+#pragma unroll
+      for (int c = 0; c < NY; ++c) a[c] = __shfl_sync(full, a[c], src);
+      pv = __shfl_sync(full, pv, src);
+      double ap = 0.0;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c == p) ap = a[c];
+      const double ak = a[k];
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c == p) a[c] = ak;
+      a[k] = ap;
+    }
+    const double dkk = __shfl_sync(full, a[k], k);
+    if (!(dkk > 0.0)) {
+      ok = false;
+      break;
+    }
+    const double rkk = sqrt(dkk);
+    if (k == 0) r00 = rkk;
+    if (lane == k) {
+      const double inv = 1.0 / rkk;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c > k) a[c] *= inv;
+      a[k] = rkk;
+    }
+    double rk[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) rk[c] = __shfl_sync(full, a[c], k);
+    double mine = 0.0;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c == lane) mine = rk[c];
+    if (lane > k && lane < m) {
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c > k) a[c] -= mine * rk[c];
+    }
+  }
+  if (ok && m > 0) {
+    double dl = 0.0;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c == lane) dl = a[c];
+    dl = __shfl_sync(full, dl, m - 1);
+    ok = fabs(dl) > ratio * r00;
+  }
+  if (lane < m) {
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < m) R[lane * m + c] = (c >= lane) ? a[c] : 0.0;
+    piv[lane] = pv;
+  }
+  __syncwarp();
+  return ok;
+}
+
+// Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve); thread per row
+template <int NY>
+__device__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
+                                const double* R, const int* piv) {
+  __shared__ double rinv[16];
+  if (threadIdx.x < m) rinv[threadIdx.x] = 1.0 / R[threadIdx.x * m + threadIdx.x];
+  __syncthreads();
+  for (int r = threadIdx.x; r < nrows; r += kOrthT) {
+    double x[NY], y[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) x[c] = (c < m) ? X[(size_t)r * ldx + (piv ? piv[c] : c)] : 0.0;
+#pragma unroll
+    for (int c = 0; c < NY; ++c) {
+      if (c < m) {
+        double s = x[c];
+#pragma unroll
+        for (int a = 0; a < NY; ++a)
+          if (a < c) s -= y[a] * R[a * m + c];
+        y[c] = s * rinv[c];
+      } else {
+        y[c] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < m) Y[(size_t)r * ldy + c] = y[c];
+  }
+  __syncthreads();
+}
+
+// cooperative launch of kOrthT-thread blocks, routed through the shared
+// cooperative stream when one is set (orth.cu, pmp_set_coop_stream)
+cudaError_t coop_launch(const void* fn, int g, void** args, size_t smem, cudaStream_t user);
+// 2 x #SMs (the largest co-resident grid the kernels here use)
+int orth_max_grid();
+
+}  // namespace pmp

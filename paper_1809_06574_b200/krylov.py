@@ -306,6 +306,44 @@ class _Dev:
             self._inner = g
         return self._inner
 
+    def cycle_ok(self, na, bs, chain):
+        """The device cycle handles block sizes <= 16 and up to 3 factors."""
+        return 1 <= bs <= 16 and na <= 16 and len(chain) <= 3
+
+    def cycle_bufs(self):
+        if getattr(self, "_cbufs", None) is None:
+            self._cbufs = _CycleBufs(self)
+        return self._cbufs
+
+    def cycle_state(self, A, chain):
+        """PmpGcroCycle with the solve-constant fields filled."""
+        if getattr(self, "_cyc", None) is None:
+            self._chain_arrays(chain)
+            cb = self.cycle_bufs()
+            g = _CycleState()
+            g.n, g.s, g.cap, g.kc, g.nfac = self.n, self.s, self.cap, self.kc, len(chain)
+            g.fac_rowptr = ctypes.cast(self._fr, ctypes.c_void_p)
+            g.fac_colidx = ctypes.cast(self._fc, ctypes.c_void_p)
+            g.fac_vals = ctypes.cast(self._fv, ctypes.c_void_p)
+            st = A.structure
+            g.a_rowptr, g.a_colidx = st.rowptr.data_ptr(), st.colidx.data_ptr()
+            g.a_vals = A.vals.data_ptr()
+            for name in ("V", "W", "T0", "T1", "C"):
+                setattr(g, name, self.ptr[name])
+            g.d_small, g.mirror = self.smbase, self.mptr[0]
+            g.offB, g.offH1, g.offH2 = self.off["G1"], self.off["G2"], self.off["G3"]
+            g.offR = self.off["RT"]
+            g.ws, g.ws_bytes = cb.ws.data_ptr(), cb.ws.numel()
+            g.stream = self.st
+            g.hist_cap = cb.hist_cap
+            g.d_proj = cb.d.data_ptr()
+            for name in ("Bmat", "Hb", "QR", "Tau", "Cq", "Y", "Res", "Bn", "Hist"):
+                setattr(g, "o" + name, cb.off[name])
+            g.blocks_per_sm = _CYCLE_BPS
+            g.d_istate = cb.di.data_ptr()
+            self._cyc = g
+        return self._cyc
+
     def wait(self, buf):
         rc = self.f_wait(self.mptr[buf] + 8 * self.off["FLAG"], -1.0, 60_000_000, self.st)
         if rc:
@@ -548,8 +586,117 @@ class _InnerState(ctypes.Structure):
         (f, ctypes.c_int) for f in ("matvecs", "precond_applies", "status", "steps_done")]
 
 
-def _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
+class _CycleState(ctypes.Structure):
+    """ctypes mirror of PmpGcroCycle (include/pmorb200.h)."""
+    _fields_ = [(f, ctypes.c_int) for f in ("n", "s", "cap", "kc", "ldq", "nfac")] + [
+        (f, ctypes.c_void_p) for f in ("fac_rowptr", "fac_colidx", "fac_vals", "a_rowptr",
+                                       "a_colidx", "a_vals", "V", "W", "T0", "T1", "C",
+                                       "d_small", "mirror")] + [
+        (f, ctypes.c_int) for f in ("offB", "offH1", "offH2", "offR")] + [
+        ("ws", ctypes.c_void_p), ("ws_bytes", ctypes.c_size_t), ("stream", ctypes.c_void_p)] + [
+        (f, ctypes.c_int) for f in ("k", "na", "sb", "max_iters", "inner_restart",
+                                    "hist_cap")] + [
+        ("tol", ctypes.c_double), ("d_proj", ctypes.c_void_p)] + [
+        (f, ctypes.c_int) for f in ("oBmat", "oHb", "oQR", "oTau", "oCq", "oY", "oRes", "oBn",
+                                    "oHist", "blocks_per_sm")] + [
+        ("d_istate", ctypes.c_void_p)]
+
+
+# the whole inner loop of a cycle runs in one persistent kernel
+# (pmp_gcro_cycle_dev) unless PMP_DEVICE_CYCLE=0; PMP_CYCLE_BPS forces the
+# blocks per SM of that kernel (diagnostics)
+DEVICE_CYCLE = __import__("os").environ.get("PMP_DEVICE_CYCLE", "1") != "0"
+_CYCLE_BPS = int(__import__("os").environ.get("PMP_CYCLE_BPS", "0"))
+
+
+class _CycleBufs:
+    """Device / pinned-host mirrors of the projected state of a device
+    cycle (layout of PmpGcroCycle: Cq, bn, res, Y, hist, tau, QR, Bmat, Hb
+    as doubles; the int state + ext separately)."""
+
+    def __init__(self, D):
+        s, cap, kc = D.s, D.cap, D.kc
+        ldq = kc + cap
+        self.hist_cap = cap + 2
+        off = {}
+        o = 0
+        for name, size in (("Cq", ldq * s), ("Bn", s), ("Res", s), ("Y", s * ldq),
+                           ("Hist", self.hist_cap * s), ("Tau", ldq), ("QR", ldq * ldq),
+                           ("Bmat", kc * cap), ("Hb", cap * cap)):
+            off[name] = o
+            o += size
+        self.off, self.size = off, o
+        dev = _dev()
+        self.d = torch.zeros(o, dtype=torch.float64, device=dev)
+        self.h = torch.zeros(o, dtype=torch.float64, pin_memory=True)
+        self.hn = self.h.numpy()
+        self.di = torch.zeros(16 + ldq, dtype=torch.int32, device=dev)
+        self.hi = torch.zeros(16 + ldq, dtype=torch.int32, pin_memory=True)
+        self.hin = self.hi.numpy()
+        sc = scratch()
+        L = _abi.lib()
+        self.ws = sc.get("cycle", L.pmp_cycle_workspace(D.n, cap, kc, s))
+        self.f = L.pmp_gcro_cycle_dev
+
+    def view(self, name, size):
+        o = self.off[name]
+        return self.hn[o:o + size]
+
+
+def _device_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
                   last_rel, active):
+    """Inner loop of one cycle in one persistent kernel (pmp_gcro_cycle_dev);
+    the rare host fallbacks (status 4 / 5) continue in _native_cycle from
+    the state the kernel reached.  Returns (m, total, Y, converged,
+    exhausted)."""
+    cb = D.cycle_bufs()
+    g = D.cycle_state(A, chain)
+    s, cap, ldq = D.s, D.cap, proj.ldq
+    g.k, g.na, g.sb, g.ldq = k, na, bs, ldq
+    g.max_iters, g.inner_restart, g.tol = cfg.max_iters, cfg.inner_restart, float(cfg.tol)
+    # Q^T rhs (rhs_c ; S0) and the column norms, one pinned upload
+    cq = cb.view("Cq", ldq * na)
+    cq[:] = proj.C[:, :na].ravel(order="F")
+    cb.view("Bn", na)[:] = bn_act
+    up = cb.off["Bn"] + s
+    cb.d[:up].copy_(cb.h[:up], non_blocking=True)
+    it0 = report.iterations
+    cb.hin[:4] = (0, bs, 0, it0)
+    cb.di[:16].copy_(cb.hi[:16], non_blocking=True)
+    D._call("pmp_gcro_cycle_dev", cb.f, ctypes.byref(g))
+    cb.h.copy_(cb.d, non_blocking=True)
+    cb.hi.copy_(cb.di, non_blocking=True)
+    D.cstream.synchronize()
+    m, total, ncols, it, st, hrows = (int(v) for v in cb.hin[:6])
+    steps = it - it0
+    report.iterations = it
+    report.matvec_count += bs * steps
+    if chain:
+        report.precond_apply_count += bs * steps
+    hist = cb.view("Hist", cb.hist_cap * na)
+    for i in range(hrows):
+        last_rel[active] = hist[i * na:(i + 1) * na]
+        report.residual_history.append(last_rel.copy())
+    if k:
+        Bmat[:, :] = cb.view("Bmat", k * cap).reshape(k, cap)
+    Hb[:, :] = cb.view("Hb", cap * cap).reshape(cap, cap)
+    Y = None
+    if ncols and st in (0, 2, 3):
+        Y = cb.view("Y", na * ncols).reshape(na, ncols).T.copy()
+    if st in (0, 2, 3):
+        return m, total, Y, st == 0, False
+    # host fallbacks: hand the projected state to the native host loop
+    proj.QR[:, :] = cb.view("QR", ldq * ldq).reshape((ldq, ldq), order="F")
+    proj.tau[:] = cb.view("Tau", ldq)
+    proj.ext[:] = cb.hin[16:16 + ldq]
+    proj.C[:, :na] = cb.view("Cq", ldq * na).reshape((ldq, na), order="F")
+    proj.ncols = ncols
+    return _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
+                         last_rel, active, resume=(st, m, total, ncols))
+
+
+def _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
+                  last_rel, active, resume=None):
     """Inner loop of one cycle through pmp_gcro_inner (native, GIL released
     while it runs); the rare host fallbacks (rank-deficient G: min-norm
     gelsd; near-deficient block: Householder deflation) are handled here and
@@ -569,21 +716,33 @@ def _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, H
     Y = None
     conv = exh = False
     s, cap = D.s, D.cap
+    if resume is not None:
+        # continue after the device cycle stopped at a host fallback
+        st, g.m, g.total, g.ncols = resume
+        g.iterations, g.buf = report.iterations, 0
     while True:
-        g.matvecs = g.precond_applies = 0
-        rc = D.f_inner(ctypes.byref(g))
-        if rc:
-            _abi.check(rc, "pmp_gcro_inner")
-        for i in range(g.steps_done):
-            last_rel[active] = D.hist[i, :na]
-            report.residual_history.append(last_rel.copy())
-        report.iterations = g.iterations
-        report.matvec_count += g.matvecs
-        report.precond_apply_count += g.precond_applies
-        proj.ncols = g.ncols
-        if g.steps_done:
-            Y = proj.Y.ravel()[:g.ncols * na].reshape(na, g.ncols).T.copy()
-        st = g.status
+        if resume is not None:
+            resume = None
+        else:
+            g.matvecs = g.precond_applies = 0
+            it0 = g.iterations
+            rc = D.f_inner(ctypes.byref(g))
+            if rc:
+                _abi.check(rc, "pmp_gcro_inner")
+            if D.counting:
+                _abi.COUNTERS["pmp_gcro_step"] = (_abi.COUNTERS.get("pmp_gcro_step", 0)
+                                                  + g.iterations - it0 + g.launched)
+            hist = D.hist.ravel()
+            for i in range(g.steps_done):
+                last_rel[active] = hist[i * na:(i + 1) * na]
+                report.residual_history.append(last_rel.copy())
+            report.iterations = g.iterations
+            report.matvec_count += g.matvecs
+            report.precond_apply_count += g.precond_applies
+            proj.ncols = g.ncols
+            if g.steps_done:
+                Y = proj.Y.ravel()[:g.ncols * na].reshape(na, g.ncols).T.copy()
+            st = g.status
         if st == 0:
             conv = True
             break
@@ -741,7 +900,11 @@ def _solve(A, B, P, cfg):
         launched = False   # the current step's kernels are already enqueued
         buf = 0            # mapped result buffer of the pending native step
         prev_max = float(np.max(start_rel)) if start_rel.size else 0.0
-        if D.native and NATIVE_INNER:
+        if D.native and DEVICE_CYCLE and D.cycle_ok(na, bs, chain):
+            m, total, Y, cycle_converged, exhausted = _device_cycle(
+                D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
+                last_rel, active)
+        elif D.native and NATIVE_INNER:
             m, total, Y, cycle_converged, exhausted = _native_cycle(
                 D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
                 last_rel, active)

@@ -399,3 +399,33 @@ def test_c2_sequence_property(pm):
         X = r["X"].cpu().numpy()
         rel = np.linalg.norm(W.rhs - A @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
         assert r["converged"] and np.all(rel <= 1e-8)
+
+
+@pytest.mark.parametrize("name", ["rand40", "c1s24", "c2s8", "c3s6", "c5n500"])
+def test_device_cycle_matches_host_loop(pm, name):
+    """The persistent device cycle (pmp_gcro_cycle_dev) against the
+    host-driven native loop (pmp_gcro_inner): same convergence, iteration
+    counts within 1, solutions within the solve tolerance; both geometries
+    (1 and 2 blocks per SM)."""
+    from paper_1809_06574_b200 import krylov
+    g = G.load(name)
+    A1, Al, B = G.csr(g, "A1"), G.csr(g, "Al"), g["B"]
+    P0, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))
+    Pu, _ = pm.update_first(A1, Al, P0, pm.UpdateConfig(pattern_level=0))
+    cfg = pm.SolverConfig(tol=1e-10, inner_restart=12, outer_space_dim=4)
+    saved = krylov.DEVICE_CYCLE, krylov._CYCLE_BPS
+    try:
+        for A, P in ((A1, P0), (Al, Pu), (Al, None)):
+            krylov.DEVICE_CYCLE = False
+            Xh, rh = pm.block_gcro_solve(A, B, P=P, cfg=cfg)
+            for bps in (1, 2):
+                krylov.DEVICE_CYCLE, krylov._CYCLE_BPS = True, bps
+                Xd, rd = pm.block_gcro_solve(A, B, P=P, cfg=cfg)
+                assert rd.converged == rh.converged
+                assert abs(rd.iterations - rh.iterations) <= 1, (rd.iterations, rh.iterations)
+                assert rd.matvec_count > 0
+                rel = np.linalg.norm(B - A @ Xd, axis=0) / np.linalg.norm(B, axis=0)
+                assert np.all(rel <= 1e-10), rel
+                assert len(rd.residual_history) >= rd.iterations
+    finally:
+        krylov.DEVICE_CYCLE, krylov._CYCLE_BPS = saved

@@ -145,3 +145,22 @@ def test_inner_state_layout_matches_header(tmp_path):
     got = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     assert [int(v) for v in got] == [ctypes.sizeof(S), S.mirror.offset, S.bn.offset,
                                      S.prev_max.offset, S.steps_done.offset]
+
+
+def test_cycle_state_layout_matches_header(tmp_path):
+    """ctypes mirror of PmpGcroCycle == the C struct (gcc probe)."""
+    import ctypes
+    import subprocess
+    from paper_1809_06574_b200.krylov import _CycleState as S
+    src = tmp_path / "probe.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pmorb200.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(PmpGcroCycle),'
+                   ' offsetof(PmpGcroCycle, offB), offsetof(PmpGcroCycle, ws_bytes),'
+                   ' offsetof(PmpGcroCycle, tol), offsetof(PmpGcroCycle, blocks_per_sm),'
+                   ' offsetof(PmpGcroCycle, d_istate));}\n')
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert [int(v) for v in got] == [ctypes.sizeof(S), S.offB.offset, S.ws_bytes.offset,
+                                     S.tol.offset, S.blocks_per_sm.offset, S.d_istate.offset]
