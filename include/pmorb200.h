@@ -309,6 +309,10 @@ typedef struct PmpGcroCycle {
 } PmpGcroCycle;
 size_t pmp_cycle_workspace(int n, int cap, int kc, int s);
 int pmp_gcro_cycle_dev(PmpGcroCycle* cycle);
+/* Diagnostics only: the next `records` cycle kernels write %globaltimer
+ * stamps of blocks 0 and 1 into d_stamps[4096 * launch + (32 * step + phase)
+ * * 2 + block] (device memory, zero-initialised by the caller). */
+int pmp_cycle_debug_stamps(unsigned long long* d_stamps, int records);
 
 /* Route every cooperative launch (pmp_orth_step, pmp_fold, pmp_gcro_step's
  * orthogonalisation) through one shared stream, with event handoffs to and

@@ -1,5 +1,8 @@
 // Device building blocks of the tall-skinny orthogonalisation kernels
 // (k_orth / k_fold in orth.cu, the persistent cycle kernel in cycle.cu).
+// The heavier ones are __noinline__: the persistent kernel calls them
+// several times per step, and one shared copy keeps its step loop small
+// enough for the instruction cache (inlined, it was ~24k instructions).
 // Every block owns a contiguous row range; reductions are two-stage
 // (fixed-order per-block partials, then a distributed fixed-order sum)
 // separated by grid barriers, so results are bitwise reproducible.
@@ -86,7 +89,7 @@ __device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int 
 // distributed fixed-order reduction of the block partials; every block ends
 // with the full K-vector in smem G.  Entries [0, split) are also copied to
 // out, entries [split, K) to out2 (either may be null).
-static __device__ void grid_reduce(cg::grid_group& grid, double* partial, double* gout, int K,
+static __device__ __noinline__ void grid_reduce(cg::grid_group& grid, double* partial, double* gout, int K,
                             double* G,
                             double* out, int split, double* out2) {
   __threadfence();
@@ -94,8 +97,23 @@ static __device__ void grid_reduce(cg::grid_group& grid, double* partial, double
   const int nb = gridDim.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int o = blockIdx.x + nb * wid; o < K; o += nb * (kOrthT / 32)) {
     double s = 0.0;
-    {
-      // independent loads first, then a fixed-order sum
+    if (nb <= 512) {
+      // every load in flight at once (one L2 round trip), then the same
+      // fixed-order sum as below: t0 over even, t1 over odd strides of 32
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int b = lane + 32 * u;
+        v[u] = b < nb ? __ldcg(partial + (size_t)b * K + o) : 0.0;
+      }
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; u += 2) {
+        t0 += v[u];
+        t1 += v[u + 1];
+      }
+      s = t0 + t1;
+    } else {
       double t0 = 0.0, t1 = 0.0;
       int b = lane;
       for (; b + 32 < nb; b += 64) {
@@ -144,11 +162,87 @@ __device__ void block_update(const Rows& X, int kx, double* Y, int ldy, int ny, 
   __syncthreads();
 }
 
+// Pivoted Cholesky of the m x m SPD matrix A (row-major, shared memory,
+// destroyed) by one warp with rolled loops: lane i owns row i.  R (row-major,
+// upper) is the factor of P^T A P, piv the permutation.  Small code on
+// purpose: the persistent cycle kernel runs it once per block step, and
+// the fully unrolled register version is large enough to miss in the
+// instruction cache every time.  Returns ok (all pivots positive and the
+// last >= ratio x the first).
+static __device__ __noinline__ bool warp_cholesky_smem(double* A, int m, double* R, int* piv, bool pivot,
+                                                double ratio) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  if (lane < m) piv[lane] = lane;
+  for (int q = lane; q < m * m; q += 32) R[q] = 0.0;
+  __syncwarp();
+  bool ok = true;
+  double r00 = 0.0;
+  for (int k = 0; k < m; ++k) {
+    int p = k;
+    if (pivot) {
+      // packed (diagonal bits, 31 - lane) key: ties within 32 ulp go to the
+      // lowest row; a negative diagonal counts as 0 (a failing pivot)
+      long long key = (lane >= k && lane < m)
+                          ? ((__double_as_longlong(fmax(A[lane * m + lane], 0.0)) & ~31LL) |
+                             (31 - lane))
+                          : -1LL;
+      for (int o = 16; o > 0; o >>= 1) {
+        const long long other = __shfl_xor_sync(full, key, o);
+        key = other > key ? other : key;
+      }
+      p = 31 - (int)(key & 31);
+    }
+    if (p != k) {
+      if (lane < m) {
+        const double t = A[k * m + lane];
+        A[k * m + lane] = A[p * m + lane];
+        A[p * m + lane] = t;
+      }
+      __syncwarp();
+      if (lane < m) {
+        const double t = A[lane * m + k];
+        A[lane * m + k] = A[lane * m + p];
+        A[lane * m + p] = t;
+      }
+      if (lane < k) {
+        const double t = R[lane * m + k];
+        R[lane * m + k] = R[lane * m + p];
+        R[lane * m + p] = t;
+      }
+      if (lane == 0) {
+        const int t = piv[k];
+        piv[k] = piv[p];
+        piv[p] = t;
+      }
+      __syncwarp();
+    }
+    const double dkk = A[k * m + k];
+    if (!(dkk > 0.0)) {
+      ok = false;
+      break;
+    }
+    const double inv = rsqrt(dkk);
+    const double rkk = dkk * inv;
+    if (k == 0) r00 = rkk;
+    if (lane >= k && lane < m) R[k * m + lane] = lane == k ? rkk : A[k * m + lane] * inv;
+    __syncwarp();
+    if (lane > k && lane < m) {
+      const double ri = R[k * m + lane];
+      for (int c = k + 1; c < m; ++c) A[lane * m + c] -= ri * R[k * m + c];
+    }
+    __syncwarp();
+  }
+  if (ok && m > 0) ok = fabs(R[(m - 1) * m + (m - 1)]) > ratio * r00;
+  __syncwarp();
+  return ok;
+}
+
 // Same factorisation held in registers: lane i owns row i (m <= NY <= 32),
 // pivot search by a warp arg-max, row swaps by shuffles, column swaps by
 // register selects -- no shared-memory round trips or __syncwarp chains.
 template <int NY>
-__device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, bool pivot,
+__device__ __noinline__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, bool pivot,
                                   double ratio) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -167,18 +261,21 @@ __device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, b
 #pragma unroll
       for (int c = 0; c < NY; ++c)
         if (c == lane) dii = a[c];
-      double best = (lane >= k && lane < m) ? dii : -1.0;
-      int bi = lane;
+      // arg-max as one 64-bit key: the diagonal's bits (order-preserving for
+      // non-negative doubles) with the low 5 mantissa bits replaced by
+      // 31 - lane, so (near-)ties within 32 ulp go to the lowest lane
+      // (a negative diagonal counts as 0: still a valid, failing pivot;
+      // lanes outside [k, m) get key -1, below every valid key)
+      long long key = (lane >= k && lane < m)
+                          ? ((__double_as_longlong(fmax(dii, 0.0)) & ~31LL) | (31 - lane))
+                          : -1LL;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(full, best, o);
-        const int oi = __shfl_xor_sync(full, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
+      for (int o = NY / 2; o > 0; o >>= 1) {
+        const long long ok = __shfl_xor_sync(full, key, o);
+        key = ok > key ? ok : key;
       }
-      p = bi;
+      // lanes >= NY reduced their own group: take lane 0's (warp-uniform)
+      p = 31 - (int)(__shfl_sync(full, key, 0) & 31);
     }
     if (p != k) {
       const int src = lane == k ? p : (lane == p ? k : lane);
@@ -200,10 +297,10 @@ __device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, b
       ok = false;
       break;
     }
-    const double rkk = sqrt(dkk);
+    const double inv = rsqrt(dkk);
+    const double rkk = dkk * inv;
     if (k == 0) r00 = rkk;
     if (lane == k) {
-      const double inv = 1.0 / rkk;
 #pragma unroll
       for (int c = 0; c < NY; ++c)
         if (c > k) a[c] *= inv;
@@ -242,7 +339,7 @@ __device__ bool warp_cholesky_reg(const double* G, int m, double* R, int* piv, b
 
 // Y[r][:] = X[r][piv] R^-1 (row-vector triangular solve); thread per row
 template <int NY>
-__device__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
+__device__ __noinline__ void block_trsm_rows(const double* X, int ldx, double* Y, int ldy, int nrows, int m,
                                 const double* R, const int* piv) {
   __shared__ double rinv[16];
   if (threadIdx.x < m) rinv[threadIdx.x] = 1.0 / R[threadIdx.x * m + threadIdx.x];

@@ -306,9 +306,10 @@ class _Dev:
             self._inner = g
         return self._inner
 
-    def cycle_ok(self, na, bs, chain):
-        """The device cycle handles block sizes <= 16 and up to 3 factors."""
-        return 1 <= bs <= 16 and na <= 16 and len(chain) <= 3
+    def cycle_ok(self, na, bs, chain, restart):
+        """The device cycle handles block sizes <= 16, up to 3 factors and
+        restart lengths with restart + block <= 96."""
+        return 1 <= bs <= 16 and na <= 16 and len(chain) <= 3 and restart + bs <= 96
 
     def cycle_bufs(self):
         if getattr(self, "_cbufs", None) is None:
@@ -630,8 +631,12 @@ class _CycleBufs:
         self.d = torch.zeros(o, dtype=torch.float64, device=dev)
         self.h = torch.zeros(o, dtype=torch.float64, pin_memory=True)
         self.hn = self.h.numpy()
-        self.di = torch.zeros(16 + ldq, dtype=torch.int32, device=dev)
-        self.hi = torch.zeros(16 + ldq, dtype=torch.int32, pin_memory=True)
+        # int state: [0..5] m, total, ncols, iterations, status, history
+        # rows; [7..9] step / done / barrier flags; [16 + j] decision of
+        # step j (-1 = not yet posted)
+        self.nint = 16 + 128
+        self.di = torch.zeros(self.nint, dtype=torch.int32, device=dev)
+        self.hi = torch.zeros(self.nint, dtype=torch.int32, pin_memory=True)
         self.hin = self.hi.numpy()
         sc = scratch()
         L = _abi.lib()
@@ -661,8 +666,10 @@ def _device_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, H
     up = cb.off["Bn"] + s
     cb.d[:up].copy_(cb.h[:up], non_blocking=True)
     it0 = report.iterations
+    cb.hin[:16] = 0
     cb.hin[:4] = (0, bs, 0, it0)
-    cb.di[:16].copy_(cb.hi[:16], non_blocking=True)
+    cb.hin[16:] = -1
+    cb.di.copy_(cb.hi, non_blocking=True)
     D._call("pmp_gcro_cycle_dev", cb.f, ctypes.byref(g))
     cb.h.copy_(cb.d, non_blocking=True)
     cb.hi.copy_(cb.di, non_blocking=True)
@@ -685,12 +692,16 @@ def _device_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, H
         Y = cb.view("Y", na * ncols).reshape(na, ncols).T.copy()
     if st in (0, 2, 3):
         return m, total, Y, st == 0, False
-    # host fallbacks: hand the projected state to the native host loop
-    proj.QR[:, :] = cb.view("QR", ldq * ldq).reshape((ldq, ldq), order="F")
-    proj.tau[:] = cb.view("Tau", ldq)
-    proj.ext[:] = cb.hin[16:16 + ldq]
-    proj.C[:, :na] = cb.view("Cq", ldq * na).reshape((ldq, na), order="F")
-    proj.ncols = ncols
+    # host fallbacks: re-factor G (block columns absorbed so far) on the
+    # host and hand the cycle to the native host loop
+    proj.C[:, :] = proj.rhs0
+    proj.QR[:, :] = 0.0
+    proj.tau[:] = 0.0
+    proj.ext[:] = 0
+    proj.ncols = 0
+    if m:
+        proj.append(Bmat, Hb, 0, m, total, m)
+    ncols = proj.ncols
     return _native_cycle(D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
                          last_rel, active, resume=(st, m, total, ncols))
 
@@ -900,7 +911,7 @@ def _solve(A, B, P, cfg):
         launched = False   # the current step's kernels are already enqueued
         buf = 0            # mapped result buffer of the pending native step
         prev_max = float(np.max(start_rel)) if start_rel.size else 0.0
-        if D.native and DEVICE_CYCLE and D.cycle_ok(na, bs, chain):
+        if D.native and DEVICE_CYCLE and D.cycle_ok(na, bs, chain, cfg.inner_restart):
             m, total, Y, cycle_converged, exhausted = _device_cycle(
                 D, A, chain, cfg, report, k, na, bs, bn_act, prev_max, Bmat, Hb, proj,
                 last_rel, active)
