@@ -50,8 +50,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--systems", type=int, default=0, help="limit #systems (debug)")
-    ap.add_argument("--workers", type=int, default=4,
-                    help="host threads / CUDA streams driving independent systems")
+    ap.add_argument("--workers", type=int, default=1,
+                    help="host threads / CUDA streams driving independent systems "
+                         "(per-system path, --batch 1)")
+    ap.add_argument("--batch", type=int, default=4,
+                    help="systems per persistent solve launch (1 = per-system path)")
     return ap.parse_args()
 
 
@@ -178,7 +181,8 @@ def run_ours(args):
 
     def step():
         return pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
-                               group=group, timing=True, workers=args.workers)
+                               group=group, timing=True, workers=args.workers,
+                               batch=args.batch)
 
     def barrier():
         if world > 1:
@@ -195,7 +199,7 @@ def run_ours(args):
     infos = []
     # per-kernel device time: "k_orth" = the fused orthogonalisation kernel
     # inside each native block step (events recorded in the C driver)
-    dominant = ("k_orth", "pmp_ls_columns", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
+    dominant = ("pmp_solve_batch", "k_orth", "pmp_ls_columns", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
                 "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm", "pmp_copy_cols",
                 "pmp_axpby_cols", "pmp_assemble", "pmp_permute")
     _abi.count_launches(True)
@@ -225,8 +229,8 @@ def run_ours(args):
     i1 = torch.cuda.Event(enable_timing=True)
     i0.record()
     # single stream, so each event pair brackets one kernel and nothing else
-    pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world, group=group,
-                    timing=True, workers=1)
+    recs_i, _ = pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
+                                group=group, timing=True, workers=1, batch=args.batch)
     i1.record()
     barrier()
     instr_ms = i0.elapsed_time(i1)
@@ -254,7 +258,7 @@ def run_ours(args):
     iters = [r["iterations"] for r in recs_all]
     conv = all(r["converged"] for r in recs_all)
 
-    roof = roofline(kern, timed, n, W, model)
+    roof = roofline(kern, timed, n, W, model, recs_i)
 
     e2e = None
     if not args.no_e2e:
@@ -272,8 +276,9 @@ def run_ours(args):
                        "rhs_block": int(W.rhs.shape[1]), "pattern_level": level,
                        "precond": "spai-update-first", "tol": 1e-8,
                        "l2": "flushed before every step (256 MB write)",
-                       "parallelism": "systems round-robin over %d GPU(s), %d concurrent "
-                                      "streams per GPU" % (world, args.workers)},
+                       "parallelism": "systems round-robin over %d GPU(s); %s" % (
+                           world, ("%d systems per persistent solve launch" % args.batch)
+                           if args.batch > 1 else "%d concurrent streams" % args.workers)},
             "sequence_s": ms_per_step / 1e3,
             "phases_s": {"assemble": asm_s, "build": build_s, "solve": solve_s},
             "spai_update_columns_per_s": cols / build_s if build_s > 0 else None,
@@ -296,9 +301,10 @@ def run_ours(args):
     return line
 
 
-def roofline(kern, timed, n, W, model):
-    """Dominant kernel vs its roofline.  Candidates: the batched LS kernel
-    (FP64 pipe; flops) and the n-sized Krylov kernels (HBM; bytes)."""
+def roofline(kern, timed, n, W, model, recs=None):
+    """Dominant kernel vs its roofline.  Candidates: the persistent solve
+    kernel and the n-sized Krylov kernels (HBM; algorithmic bytes) and the
+    batched LS kernel (FP64 pipe)."""
     hbm, which = peaks()
     if not kern:
         return None
@@ -306,7 +312,13 @@ def roofline(kern, timed, n, W, model):
     lst = timed[name]
     st = model.structure
     nnz = st.nnz
-    if name == "k_orth":
+    if name == "pmp_solve_batch":
+        # the kernel accumulates its algorithmic bytes per system (solve.cu:
+        # operator matrices once per application, [C | V] once per block
+        # step, the n x s blocks it gathers / writes)
+        tot = sum(r.get("algorithmic_bytes") or 0.0 for r in (recs or []))
+        byts = [tot / max(len(lst), 1)] * len(lst)
+    elif name == "k_orth":
         # [C | V] rows read once, W read, Q written: 8 n (k + total + 2 sb)
         byts = [8.0 * a[0] * (a[1] + a[2] + 2 * a[3]) for _, _, a in lst]
     elif name == "pmp_spmm":
@@ -362,7 +374,7 @@ def run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, group, ba
         Bd.copy_(Bh, non_blocking=True)
         recs, _ = pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
                                   group=group, keep_solutions=True, timing=False,
-                                  workers=args.workers)
+                                  workers=args.workers, batch=args.batch)
         for i, r in enumerate(recs):
             Xh[i].copy_(r["X"], non_blocking=True)
         e1.record()

@@ -314,6 +314,45 @@ int pmp_gcro_cycle_dev(PmpGcroCycle* cycle);
  * * 2 + block] (device memory, zero-initialised by the caller). */
 int pmp_cycle_debug_stamps(unsigned long long* d_stamps, int records);
 
+/* Whole block-GCRO solves on the device (krylov.py:105-275), `groups`
+ * independent systems per launch (one group of gsz blocks each; query
+ * pmp_solve_geometry).  One PmpSysDesc per system, in DEVICE memory at
+ * d_sys: the factor chain (nfac CSR factors, applied right to left), A, the
+ * right-hand side block B (n x s) and the output X (n x s).  Each system
+ * gets wsz doubles of d_ws and isz ints of d_istate (offsets below, in
+ * doubles, inside one system's block; p* offsets inside its projected-
+ * state block at oProj).  Per system the int state reports: [144] active
+ * columns left (0 = converged), [146] iterations, [147] status (0 ok,
+ * 10 = needs the host path: deflation, rank-deficient projected problem or
+ * an ambiguous drop test), [148] rows of the residual log (s doubles per
+ * row at oLog), [149] matvecs, [150] preconditioner applications. */
+typedef struct PmpSysDesc {
+  const int32_t* fac_rowptr[3];
+  const int32_t* fac_colidx[3];
+  const double* fac_vals[3];
+  const int32_t* a_rowptr;
+  const int32_t* a_colidx;
+  const double* a_vals;
+  const double* B;
+  double* X;
+} PmpSysDesc;
+typedef struct PmpSolveBatch {
+  int n, s, cap, kc, outer_dim, inner_restart, max_iters, nfac;
+  int groups, gsz, rows_per_block, hist_cap, log_cap, isz;
+  double tol;
+  const PmpSysDesc* d_sys;
+  double* d_ws;
+  size_t wsz;
+  int32_t* d_istate;
+  size_t oV, oC, oU, oW, oT0, oT1, oQ1, oXt, oR, oDX, oRB, oZ, oPart, oGout, oSbuf, oProj, oLog,
+      oAux;
+  int pBmat, pHb, pCq, pY, pRes, pBn, pHist;
+  void* stream;
+} PmpSolveBatch;
+int pmp_solve_geometry(int n, int s, int cap, int kc, int inner_restart, int groups, int* gsz,
+                       int* rows_per_block, int* cached, size_t* smem_bytes);
+int pmp_solve_batch(PmpSolveBatch* batch);
+
 /* Route every cooperative launch (pmp_orth_step, pmp_fold, pmp_gcro_step's
  * orthogonalisation) through one shared stream, with event handoffs to and
  * from the caller's stream, so concurrent workers never run two grid-barrier

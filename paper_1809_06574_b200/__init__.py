@@ -13,7 +13,7 @@ and torch.distributed.  There is no CPU fallback.
 
 from .device import DeviceCSR, DevicePattern, Structure
 from .krylov import (SolveReport, SolverBreakdown, SolverConfig, apply_preconditioner,
-                     block_gcro_solve, gcro_solve)
+                     block_gcro_solve, block_gcro_solve_batch, gcro_solve)
 from .model import AffineFamily, SecondOrderModel, evaluate, pmor_l_sequence
 from .sequence import PrecondPolicy, SequencePreconditioner, run_sequence
 from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, spai_build,

@@ -91,6 +91,9 @@ _SIGS = {
     "pmp_cycle_workspace": ([c_int, c_int, c_int, c_int], c_sz),
     "pmp_gcro_cycle_dev": ([c_vp], c_int),
     "pmp_cycle_debug_stamps": ([c_vp, c_int], c_int),
+    "pmp_solve_geometry": ([c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp],
+                           c_int),
+    "pmp_solve_batch": ([c_vp], c_int),
     "pmp_set_coop_stream": ([c_vp], c_int),
     "pmp_orth_debug_stamps": ([c_vp, c_int], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
@@ -151,7 +154,7 @@ _LAUNCHES_PER_CALL = {"pmp_scan": 2, "pmp_transpose": 5, "pmp_pattern_l0": 5,
 _NO_LAUNCH = {"pmp_last_error", "pmp_version", "pmp_host_deflate", "pmp_host_hls_append",
               "pmp_host_alloc_mapped", "pmp_host_free_mapped", "pmp_host_device_ptr",
               "pmp_host_wait_flag", "pmp_gcro_absorb", "pmp_orth_debug_stamps",
-              "pmp_cycle_debug_stamps",
+              "pmp_cycle_debug_stamps", "pmp_solve_geometry",
               "pmp_cycle_workspace"}
 # pmp_gcro_step launches the SpMM chain (1 + depth) and the orthogonalisation
 _LAUNCHES_PER_CALL["pmp_gcro_step"] = 4

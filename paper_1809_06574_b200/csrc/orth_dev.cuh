@@ -1,8 +1,10 @@
 // Device building blocks of the tall-skinny orthogonalisation kernels
 // (k_orth / k_fold in orth.cu, the persistent cycle kernel in cycle.cu).
-// The heavier ones are __noinline__: the persistent kernel calls them
-// several times per step, and one shared copy keeps its step loop small
-// enough for the instruction cache (inlined, it was ~24k instructions).
+// The heavier ones are __noinline__ (operands by value): the persistent
+// kernels call them several times per step, and inlined copies made the
+// step loop (~25k instructions, 400 KB) overflow the SM's instruction cache
+// -- every step then re-fetched its code from L2, ~700 cycles per 128-byte
+// line (measured: the 8 x 8 Cholesky took 37k cycles in situ vs 9k alone).
 // Every block owns a contiguous row range; reductions are two-stage
 // (fixed-order per-block partials, then a distributed fixed-order sum)
 // separated by grid barriers, so results are bitwise reproducible.
@@ -11,6 +13,10 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+
+#ifndef PMP_GRAM_INLINE
+#define PMP_GRAM_INLINE __forceinline__
+#endif
 
 namespace pmp {
 
@@ -38,11 +44,11 @@ __host__ __device__ __forceinline__ int odd_ld(int w) { return w | 1; }
 // dimensions), warps split the rows; the per-warp sums are combined in a
 // fixed order through smem.
 template <int NY>
-__device__ void block_gram(const Rows& X, int kx, const double* Y, int ldy, int ny, int nrows,
-                           double* red, double* partial) {
+__device__ PMP_GRAM_INLINE void block_gram(const Rows X, int kx, const double* Y, int ldy, int ny, int nrows,
+                           double* red, double* partial, int slot = -1) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int K = kx * ny;
-  double* part = partial + (size_t)blockIdx.x * K;
+  double* part = partial + (size_t)(slot < 0 ? (int)blockIdx.x : slot) * K;
   const int rounds = (kx + 31) / 32;
   int splits = 8 / rounds;
   if (splits < 1) splits = 1;
@@ -141,7 +147,7 @@ static __device__ __noinline__ void grid_reduce(cg::grid_group& grid, double* pa
 
 // Y[r][c] -= sum_t X(r, t) G[t][c] ; thread per row, all ny outputs
 template <int NY>
-__device__ void block_update(const Rows& X, int kx, double* Y, int ldy, int ny, int nrows,
+__device__ PMP_GRAM_INLINE void block_update(const Rows X, int kx, double* Y, int ldy, int ny, int nrows,
                              const double* G) {
   for (int r = threadIdx.x; r < nrows; r += kOrthT) {
     double acc[NY];

@@ -1,0 +1,826 @@
+// Whole block-GCRO solves on the device, several systems per launch
+// (krylov.py:105-275 end to end).
+//
+// k_cycle (cycle.cu) moved the inner loop of a cycle onto the device; the
+// cycle boundaries -- projecting the residual block against the outer space
+// and orthonormalising it (krylov.py:156-169), the solution / true residual
+// update (krylov.py:221-234) and the outer-space fold (krylov.py:244-269) --
+// still cost host round trips, and one system at a time leaves most of the
+// GPU idle (every phase is latency bound).  k_solve runs complete solves:
+// the grid is split into groups of blocks, one independent system per
+// group (the sequence driver solves the systems of a parameter sweep in
+// batches), each group = one control block (the projected least-squares
+// problem, as in k_cycle) + worker blocks that own row ranges.
+//
+// Per cycle (group-local barriers only):
+//   Z = R[:, act]; Z -= C (C^T Z); Cholesky-QR2 -> V[:, :na], S0 = R
+//   inner loop (worker_inner / ctl_run, cycle_dev.cuh)
+//   dX = V Y_v + U Y_u; Xt[:, act] += dX; X[:, act] = P Xt[:, act];
+//   R[:, act] = B[:, act] - A X[:, act]; true residual norms; stop test
+//   fold: images = V G_v Y + C G_c Y, block CGS2 against C (2 reductions),
+//   Cholesky with the reference's drop test (|w2| > 1e-10 |w|), one or two
+//   Cholesky-QR passes -> new C / U columns; keep the last outer_dim.
+// Every decision the fast path cannot take exactly the way the reference
+// does (rank-deficient blocks: krylov.py:79-95 deflation, a rank-deficient
+// projected problem, a drop test inside the cancellation band) ends the
+// group with status PMP_SOLVE_FALLBACK and the host re-solves that system
+// on the host-driven path.
+#include "cycle_dev.cuh"
+
+namespace pmp {
+
+struct SysDesc {
+  const int32_t* frp[3];
+  const int32_t* fci[3];
+  const double* fva[3];
+  const int32_t* arp;
+  const int32_t* aci;
+  const double* ava;
+  const double* B;
+  double* X;
+};
+
+struct SolveArgs {
+  int n, s, cap, kc, outer_dim, inner_restart, max_iters, nfac;
+  int gsz, rows_per_block, ldx, hist_cap, log_cap, isz;
+  double tol;
+  const SysDesc* sys;
+  double* ws;
+  size_t wsz;
+  int* ist;
+  size_t oV, oC, oU, oW, oT0, oT1, oQ1, oXt, oR, oDX, oRB, oZ, oPart, oGout, oSbuf, oProj, oLog,
+      oAux;
+  int pBmat, pHb, pCq, pY, pRes, pBn, pHist;  // offsets inside the projected-state block
+  unsigned long long* dbg;  // diagnostics (group 0): stamps at (32 it + phase) * 2 + block
+};
+
+// solve-level int state (after the cycle-level [0, 144))
+enum {
+  kNa = 144,
+  kK = 145,
+  kIt = 146,
+  kStatus = 147,
+  kLogRows = 148,
+  kMatvecs = 149,
+  kPrec = 150,
+  kGbar = 151,
+  kFold = 152,
+  kAct = 160,  // active columns (<= 16)
+};
+
+constexpr int PMP_SOLVE_OK = 0, PMP_SOLVE_FALLBACK = 10;
+
+// barrier over every block of the group (control block included)
+__device__ __forceinline__ void gbar(WBar& g) { wbar(g); }
+
+__device__ __forceinline__ int ldv(const int* p) { return *(volatile const int*)p; }
+
+// diagnostics: cycle-level phase stamps of group 0's lead worker
+__device__ __forceinline__ void sstamp(const SolveArgs& A, int grp, int cyc, int ph) {
+#ifdef PMP_STAMPS
+  if (A.dbg && grp == 0 && blockIdx.x == 1 && threadIdx.x == 0 && cyc < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.dbg[((size_t)(48 + cyc) * 32 + ph) * 2 + 1] = t;
+  }
+#else
+  (void)A;
+  (void)grp;
+  (void)cyc;
+  (void)ph;
+#endif
+}
+
+// one row of [w | z] (columns keep[a], or 0..nk-1 when keep is null) times
+// T^-1 (upper, ld ldt) -> yw / yz; register arrays with static indices
+template <int NY>
+__device__ __forceinline__ void fold_rowsolve(const double* w, const double* z, const int* keep,
+                                              int nk, const double* T, int ldt, double* yw_out,
+                                              double* yz_out) {
+  double yw[NY], yz[NY];
+#pragma unroll
+  for (int a = 0; a < NY; ++a) {
+    yw[a] = 0.0;
+    yz[a] = 0.0;
+    if (a < nk) {
+      const int col = keep ? keep[a] : a;
+      double vw = w[col], vz = z[col];
+#pragma unroll
+      for (int b = 0; b < NY; ++b)
+        if (b < a) {
+          vw -= yw[b] * T[b * ldt + a];
+          vz -= yz[b] * T[b * ldt + a];
+        }
+      yw[a] = vw / T[a * ldt + a];
+      yz[a] = vz / T[a * ldt + a];
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NY; ++a)
+    if (a < nk) {
+      yw_out[a] = yw[a];
+      yz_out[a] = yz[a];
+    }
+}
+
+template <bool CACHED, int NY>
+#ifndef PMP_MINB
+#define PMP_MINB 2
+#endif
+__global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
+  extern __shared__ __align__(16) double sh[];
+  const int grp = blockIdx.x / A.gsz, lb = blockIdx.x % A.gsz;
+  const bool ctl = lb == 0;
+  const bool lead = lb == 1;
+  const int wi = lb - 1, nw = A.gsz - 1;
+  const SysDesc D = A.sys[grp];
+  double* ws = A.ws + (size_t)grp * A.wsz;
+  int* ist = A.ist + (size_t)grp * A.isz;
+  const int n = A.n, s = A.s, cap = A.cap, kc = A.kc;
+  const int r0 = ctl ? 0 : wi * A.rows_per_block;
+  const int r1 = ctl ? 0 : min(n, r0 + A.rows_per_block);
+  const int nr = max(0, r1 - r0);
+
+  const int kmax = (kc + cap + s) * s;
+  double* p = sh;
+  double* G = p;
+  p += kmax;
+  double* R1 = p;
+  p += s * s;
+  double* R2 = p;
+  p += s * s;
+  double* red = p;
+  p += 8 * 32 * s;
+  int* piv = reinterpret_cast<int*>(p);
+  int* piv2 = piv + 16;
+  int* flag = piv + 32;
+  p += 20;
+  double* region = p;
+
+  double* V = ws + A.oV;
+  double* C = ws + A.oC;
+  double* U = ws + A.oU;
+  double* W = ws + A.oW;
+  double* Xt = ws + A.oXt;
+  double* Rr = ws + A.oR;
+  double* DX = ws + A.oDX;
+  double* RB = ws + A.oRB;
+  double* Z = ws + A.oZ;
+  double* partial = ws + A.oPart;
+  double* gout = ws + A.oGout;
+  double* proj = ws + A.oProj;
+  double* logp = ws + A.oLog;
+  double* aux = ws + A.oAux;
+  double* bn = aux;          // s: |B[:, c]|
+  double* pn = aux + 16;     // s: |R[:, c]| at the last true residual
+  double* lrel = aux + 32;   // s: last relative residual row
+  double* img = aux + 64;    // (kc + cap) x s: G Y (fold images), row-major ld s
+  int* act = ist + kAct;
+
+  // the per-group argument block lives in SHARED memory: as a local struct
+  // it sat in the (L1-starved) stack and every field read in the step loop
+  // became an L2 round trip
+  __shared__ CycleArgs L;
+  __shared__ int acts[16];
+  if (threadIdx.x == 0) {
+  L.n = n;
+  L.s = s;
+  L.cap = cap;
+  L.kc = kc;
+  L.nfac = A.nfac;
+  for (int i = 0; i < 3; ++i) {
+    L.frp[i] = D.frp[i];
+    L.fci[i] = D.fci[i];
+    L.fva[i] = D.fva[i];
+  }
+  L.arp = D.arp;
+  L.aci = D.aci;
+  L.ava = D.ava;
+  L.V = V;
+  L.W = W;
+  L.T0 = ws + A.oT0;
+  L.T1 = ws + A.oT1;
+  L.C = C;
+  L.small = nullptr;
+  L.mirror = nullptr;
+  L.offB = L.offH1 = L.offH2 = L.offR = 0;
+  L.partial = partial;
+  L.gout = gout;
+  L.Q1g = ws + A.oQ1;
+  L.sbuf = ws + A.oSbuf;
+  L.rows_per_block = A.rows_per_block;
+  L.ldx = A.ldx;
+  L.max_iters = A.max_iters;
+  L.inner_restart = A.inner_restart;
+  L.hist_cap = A.hist_cap;
+  L.tol = A.tol;
+  L.proj = proj;
+  L.oBmat = A.pBmat;
+  L.oHb = A.pHb;
+  L.oQR = 0;
+  L.oTau = 0;
+  L.oCq = A.pCq;
+  L.oY = A.pY;
+  L.oRes = A.pRes;
+  L.oBn = A.pBn;
+  L.oHist = A.pHist;
+  L.ist = ist;
+  L.dbg = nullptr;
+  }
+  __syncthreads();
+
+  WBar wb{ist + 9, nw, 0, wi};
+  WBar gb{ist + kGbar, A.gsz, 0, lb};
+  const int slot = lb;  // partial slot of a worker (1 .. nw)
+
+  // ---- setup: X = Xt = 0, R = B, column norms of B -----------------------------
+  if (!ctl) {
+    for (int q = threadIdx.x; q < nr * s; q += kOrthT) {
+      const size_t o = (size_t)r0 * s + q;
+      D.X[o] = 0.0;
+      Xt[o] = 0.0;
+      Rr[o] = D.B[o];
+    }
+    const double* Bv = D.B + (size_t)r0 * s;
+    const Rows BB{Bv, s, s, Bv, s};
+    block_gram<NY>(BB, s, Bv, s, s, nr, red, partial, slot);
+    wreduce(wb, partial, gout, s * s, G, nullptr, 0, nullptr);
+    if (lead && threadIdx.x == 0) {
+      int na = 0;
+      for (int c = 0; c < s; ++c) {
+        const double b = sqrt(fmax(G[c * s + c], 0.0));
+        if (c == 0) aux[48] = 0.0;
+        bn[c] = b;
+        pn[c] = b;
+        lrel[c] = b > 0.0 ? 1.0 : 0.0;
+        logp[c] = lrel[c];
+        if (b > 0.0) act[na++] = c;
+      }
+      ist[kNa] = na;
+      ist[kK] = 0;
+      ist[kIt] = 0;
+      ist[kStatus] = PMP_SOLVE_OK;
+      ist[kLogRows] = 1;
+      ist[kMatvecs] = 0;
+      ist[kPrec] = 0;
+    }
+  }
+  gbar(gb);
+
+  int cyc = 0;
+  while (true) {
+    const int na = ldv(ist + kNa), k = ldv(ist + kK);
+    int it = ldv(ist + kIt);
+    const int it0 = it;
+    if (na == 0 || it >= A.max_iters || ldv(ist + kStatus) != PMP_SOLVE_OK) break;
+    const int ldq = k + cap;
+    if (threadIdx.x == 0) {
+      L.k = k;
+      L.na = na;
+      L.sb = na;
+      L.ldq = ldq;
+      L.nblk = (A.inner_restart + na - 1) / na + 1;
+      // (diagnostic stamps of group 0, indexed by the global iteration)
+      L.dbg = (A.dbg && grp == 0 && !ctl && it < 48) ? A.dbg + (size_t)it * 32 * 2 : nullptr;
+      for (int c = 0; c < na; ++c) acts[c] = ldv(act + c);
+    }
+    __syncthreads();
+
+    // ---- cycle start: Z = R[:, act] - C (C^T R[:, act]); QR -> V[:, :na] -------
+    sstamp(A, grp, cyc, 0);
+    if (!ctl) {
+      double* Zw = W + (size_t)r0 * s;
+      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
+        const int r = q / na, c = q % na;
+        Zw[(size_t)r * s + c] = Rr[(size_t)(r0 + r) * s + acts[c]];
+      }
+      __syncthreads();
+      const StepBuf sbf = step_buf(L, 0);
+      if (k > 0) {
+        const Rows CV{C + (size_t)r0 * kc, kc, k, C + (size_t)r0 * kc, kc};
+        block_gram<NY>(CV, k, Zw, s, na, nr, red, partial, slot);
+        wreduce(wb, partial, gout, k * na, G, sbf.B, k * na, nullptr);
+        block_update<NY>(CV, k, Zw, s, na, nr, G);
+      }
+      {
+        const Rows ZZ{Zw, s, na, Zw, s};
+        block_gram<NY>(ZZ, na, Zw, s, na, nr, red, partial, slot);
+        wreduce(wb, partial, gout, na * na, G, nullptr, 0, nullptr);
+      }
+      for (int q = threadIdx.x; q < na * na; q += kOrthT) {
+        const int i = q / na, j = q % na;
+        R2[q] = 0.5 * (G[i * na + j] + G[j * na + i]);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const bool ok = warp_cholesky_smem(R2, na, R1, piv, true, kCholRatio);
+        if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
+      }
+      __syncthreads();
+      bool single = false;
+      if (flag[0] == 0) single = fabs(R1[0]) / fabs(R1[(na - 1) * na + (na - 1)]) <= kSkipKappa;
+      double* Q1 = L.Q1g + (size_t)r0 * na;
+      if (flag[0] == 0 && !single) {
+        block_trsm_rows<NY>(Zw, s, Q1, na, nr, na, R1, piv);
+        const Rows Qv{Q1, na, na, Q1, na};
+        block_gram<NY>(Qv, na, Q1, na, na, nr, red, partial, slot);
+        wreduce(wb, partial, gout, na * na, G, nullptr, 0, nullptr);
+        if (threadIdx.x < 32) {
+          const bool ok = warp_cholesky_smem(G, na, R2, piv2, false, 0.0);
+          if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
+        }
+        __syncthreads();
+      }
+      if (flag[0]) {
+        if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+      } else {
+        double* Vr = V + (size_t)r0 * cap;
+        if (single)
+          block_trsm_rows<NY>(Zw, s, Vr, cap, nr, na, R1, piv);
+        else
+          block_trsm_rows<NY>(Q1, na, Vr, cap, nr, na, R2, nullptr);
+        if (lead) {
+          // S0 = R2 R1 (pivoted order), un-pivoted
+          for (int q = threadIdx.x; q < na * na; q += kOrthT) {
+            const int i = q / na, c = q % na;
+            double t = 0.0;
+            if (single) {
+              t = R1[i * na + c];
+            } else {
+              for (int a = i; a <= c; ++a) t += R2[i * na + a] * R1[a * na + c];
+            }
+            sbf.R[i * na + piv[c]] = (c >= i) ? t : 0.0;
+          }
+          if (threadIdx.x == 0) {
+            ist[0] = 0;
+            ist[1] = na;
+            ist[2] = 0;
+            ist[3] = it;
+            ist[7] = 0;
+            ist[8] = 0;
+          }
+        }
+        if (CACHED) {
+          double* Xs = region;
+          const int kx0 = k + na;
+          for (int q = threadIdx.x; q < nr * kx0; q += kOrthT) {
+            const int r = q / kx0, t = q % kx0;
+            Xs[(size_t)r * A.ldx + t] = t < k ? C[(size_t)(r0 + r) * kc + t]
+                                              : Vr[(size_t)r * cap + t - k];
+          }
+        }
+      }
+    }
+    sstamp(A, grp, cyc, 1);
+    gbar(gb);
+    sstamp(A, grp, cyc, 2);
+    if (ldv(ist + kStatus) != PMP_SOLVE_OK) break;
+
+    // ---- control block: projected problem of the cycle ---------------------------
+    if (ctl) {
+      const Ctl S = ctl_layout(region, na, L.nblk, ldq, na);
+      const StepBuf sbf = step_buf(L, 0);
+      for (int q = threadIdx.x; q < ldq * na; q += kOrthT) {
+        const int c = q / ldq, i = q % ldq;
+        double v = 0.0;
+        if (i < k)
+          v = __ldcg(sbf.B + i * na + c);
+        else if (i < k + na)
+          v = __ldcg(sbf.R + (i - k) * na + c);
+        S.Cq[q] = v;
+      }
+      for (int c = threadIdx.x; c < na; c += kOrthT) S.bn[c] = bn[acts[c]];
+      if (threadIdx.x == 0) {
+        S.misc[0] = k > 0 ? 1.0 : 0.0;
+        S.misc[1] = k > 0 ? 1.0 : INFINITY;
+        S.misc[3] = 0.0;
+      }
+      for (int q = threadIdx.x; q < k * cap; q += kOrthT) proj[A.pBmat + q] = 0.0;
+      for (int q = threadIdx.x; q < cap * cap; q += kOrthT) proj[A.pHb + q] = 0.0;
+      for (int q = threadIdx.x; q < 128; q += kOrthT) ist[16 + q] = -1;
+      __syncthreads();
+    }
+    gbar(gb);
+
+    // ---- inner loop ---------------------------------------------------------------
+    if (ctl) {
+      const Ctl S = ctl_layout(region, na, L.nblk, ldq, na);
+      ctl_run<NY>(L, S);
+      // the cycle's estimate rows -> the full-width log; fold images G Y
+      const int hrow = ldv(ist + 5), m = ldv(ist + 0), total = ldv(ist + 1), st = ldv(ist + 4);
+      if (threadIdx.x == 0) {
+        int lr = ldv(ist + kLogRows);
+        for (int h = 0; h < hrow && lr < A.log_cap; ++h, ++lr) {
+          for (int c = 0; c < na; ++c) lrel[acts[c]] = proj[A.pHist + (size_t)h * na + c];
+          for (int c = 0; c < s; ++c) logp[(size_t)lr * s + c] = lrel[c];
+        }
+        ist[kLogRows] = lr;
+      }
+      if (st != 4 && st != 5 && m > 0) {
+        // img = G Y: rows [0, k) = Y_u + Bmat Y_v, rows [k, k + total) = Hb Y_v
+        const int n1 = k + m;
+        const double* Y = proj + A.pY;
+        for (int q = threadIdx.x; q < (k + total) * na; q += kOrthT) {
+          const int i = q / na, c = q % na;
+          const double* y = Y + (size_t)c * n1;
+          double v;
+          if (i < k) {
+            v = y[i];
+            const double* brow = proj + A.pBmat + (size_t)i * cap;
+            for (int t = 0; t < m; ++t) v += brow[t] * y[k + t];
+          } else {
+            v = 0.0;
+            const double* hrow_ = proj + A.pHb + (size_t)(i - k) * cap;
+            for (int t = 0; t < m; ++t) v += hrow_[t] * y[k + t];
+          }
+          img[(size_t)i * s + c] = v;
+        }
+      }
+      __syncthreads();
+    } else {
+      int m = 0, total = na, ncols = 0, status = 0;
+      const int ldw = CACHED ? odd_ld(na) : s;
+      double* Wv = CACHED ? region + (size_t)nr * A.ldx : W + (size_t)r0 * s;
+      WSmem wsm{G, R1, R2, red, piv, piv2, flag, region, Wv, L.Q1g + (size_t)r0 * na, ldw};
+      worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
+      sstamp(A, grp, cyc, 3);
+    }
+    gbar(gb);
+    sstamp(A, grp, cyc, 4);
+    {
+      const int st = ldv(ist + 4);
+      if (st == 4 || st == 5) {
+        if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+        break;
+      }
+    }
+    const int m = ldv(ist + 0), total = ldv(ist + 1), it_new = ldv(ist + 3);
+    if (m == 0) break;  // no step ran (iteration budget): nothing to fold in
+
+    // ---- cycle end: dX, X, true residuals (workers) -----------------------------------
+    if (!ctl) {
+      const int n1 = k + m;
+      // Y (rhs-major na x n1) -> smem G as row-major n1 x na
+      const double* Yg = proj + A.pY;
+      for (int q = threadIdx.x; q < n1 * na; q += kOrthT) {
+        const int t = q / na, c = q % na;
+        G[q] = __ldcg(Yg + (size_t)c * n1 + t);
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
+        const int r = q / na, c = q % na;
+        const size_t row = (size_t)(r0 + r);
+        double d = 0.0;
+        const double* vr = V + row * cap;
+        for (int t = 0; t < m; ++t) d += vr[t] * G[(k + t) * na + c];
+        const double* ur = U + row * kc;
+        for (int t = 0; t < k; ++t) d += ur[t] * G[t * na + c];
+        DX[row * s + c] = d;
+        const double xt = Xt[row * s + acts[c]] + d;
+        Xt[row * s + acts[c]] = xt;
+        Z[row * s + c] = xt;
+      }
+      // Xa = P Z (factor chain right to left)
+      const double* src = Z;
+      for (int f = A.nfac - 1; f >= 0; --f) {
+        wbar(wb);
+        double* dst = ((A.nfac - 1 - f) & 1) ? L.T1 : L.T0;
+        spmm_rows<NY>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr);
+        src = dst;
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
+        const int r = q / na, c = q % na;
+        const size_t row = (size_t)(r0 + r);
+        D.X[row * s + acts[c]] = src[row * s + c];
+      }
+      wbar(wb);
+      // Rb = B[:, act] - A Xa -> R[:, act], RB
+      spmm_rows<NY>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr);
+      __syncthreads();
+      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
+        const int r = q / na, c = q % na;
+        const size_t row = (size_t)(r0 + r);
+        const double rb = D.B[row * s + acts[c]] - RB[row * s + c];
+        RB[row * s + c] = rb;
+        Rr[row * s + acts[c]] = rb;
+      }
+      __syncthreads();
+      const double* RBr = RB + (size_t)r0 * s;
+      const Rows RR{RBr, s, na, RBr, s};
+      block_gram<NY>(RR, na, RBr, s, na, nr, red, partial, slot);
+      wreduce(wb, partial, gout, na * na, G, nullptr, 0, nullptr);
+      if (lead && threadIdx.x == 0) {
+        const int steps = it_new - it0;
+        // algorithmic HBM bytes of the cycle's block steps (roofline):
+        // every operator matrix once (12 B / nonzero + row pointers), the
+        // gathered and written n x na blocks, [C | V] once per step
+        double mb = 0.0;
+        for (int f = 0; f < A.nfac; ++f)
+          mb += 12.0 * __ldg(D.frp[f] + n) + 4.0 * (n + 1) + 16.0 * n * na;
+        mb += 12.0 * __ldg(D.arp + n) + 4.0 * (n + 1) + 16.0 * n * na;
+        double by = 0.0;
+        for (int j = 0; j < steps; ++j) by += mb + 8.0 * n * (k + na * (j + 1)) + 32.0 * n * na;
+        aux[48] += by;
+        ist[kIt] = it_new;
+        ist[kMatvecs] += na * steps + na;
+        if (A.nfac) ist[kPrec] += na * steps + na;
+        int lr = ist[kLogRows];
+        int still = 0;
+        for (int c = 0; c < na; ++c) {
+          const double tn = sqrt(fmax(G[c * na + c], 0.0));
+          const int col = acts[c];
+          pn[col] = tn;
+          const double rel = bn[col] > 0.0 ? tn / bn[col] : 0.0;
+          lrel[col] = rel;
+          if (rel > A.tol) act[still++] = col;
+        }
+        if (lr < A.log_cap) {
+          for (int c = 0; c < s; ++c) logp[(size_t)lr * s + c] = lrel[c];
+          ++lr;
+        }
+        ist[kLogRows] = lr;
+        ist[kNa] = still;
+        // fold only when another cycle can run (krylov.py:244)
+        ist[kFold] = (still > 0 && it_new < A.max_iters) ? 1 : 0;
+      }
+    }
+    sstamp(A, grp, cyc, 5);
+    gbar(gb);
+    sstamp(A, grp, cyc, 6);
+    if (!ldv(ist + kFold)) {
+      ++cyc;
+      continue;
+    }
+
+    // ---- fold (workers): images -> block CGS2 against C -> new C / U columns ---------
+    if (!ctl) {
+      // RB = V[:, :total] img_v + C[:, :k] img_c  (own rows)
+      for (int q = threadIdx.x; q < (k + total) * na; q += kOrthT) G[q] = __ldcg(img + (size_t)(q / na) * s + q % na);
+      __syncthreads();
+      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
+        const int r = q / na, c = q % na;
+        const size_t row = (size_t)(r0 + r);
+        double d = 0.0;
+        const double* vr = V + row * cap;
+        for (int t = 0; t < total; ++t) d += vr[t] * G[(k + t) * na + c];
+        const double* cr = C + row * kc;
+        for (int t = 0; t < k; ++t) d += cr[t] * G[t * na + c];
+        RB[row * s + c] = d;
+      }
+      __syncthreads();
+      double* Wr = RB + (size_t)r0 * s;
+      double* Zr = DX + (size_t)r0 * s;
+      const Rows Cr{C + (size_t)r0 * kc, kc, k, Wr, s};
+      const Rows Conly{C + (size_t)r0 * kc, kc, k, C + (size_t)r0 * kc, kc};
+      const Rows Uonly{U + (size_t)r0 * kc, kc, k, U + (size_t)r0 * kc, kc};
+      // pass 1: [C | W]^T W -> H1, M0 = W^T W
+      block_gram<NY>(Cr, k + na, Wr, s, na, nr, red, partial, slot);
+      wreduce(wb, partial, gout, (k + na) * na, G, nullptr, 0, nullptr);
+      double* w0 = R1;  // |w_c| (before any projection)
+      for (int c = threadIdx.x; c < na; c += kOrthT) w0[c] = sqrt(fmax(G[(k + c) * na + c], 0.0));
+      double* Mf = R2;  // na x na: W2^T W2 (built below)
+      if (k > 0) {
+        block_update<NY>(Conly, k, Wr, s, na, nr, G);
+        block_update<NY>(Uonly, k, Zr, s, na, nr, G);
+        // pass 2: [C | W1]^T W1 -> H2, M1; M = M1 - H2^T H2
+        block_gram<NY>(Cr, k + na, Wr, s, na, nr, red, partial, slot);
+        wreduce(wb, partial, gout, (k + na) * na, G, nullptr, 0, nullptr);
+        for (int q = threadIdx.x; q < na * na; q += kOrthT) {
+          const int i = q / na, j = q % na;
+          double h = 0.0;
+          for (int t = 0; t < k; ++t) h += G[t * na + i] * G[t * na + j];
+          Mf[q] = G[(k + i) * na + j] - h;
+        }
+        __syncthreads();
+        block_update<NY>(Conly, k, Wr, s, na, nr, G);
+        block_update<NY>(Uonly, k, Zr, s, na, nr, G);
+      } else {
+        for (int q = threadIdx.x; q < na * na; q += kOrthT) Mf[q] = G[q];
+        __syncthreads();
+      }
+      // sequential drop test + Cholesky of the kept columns (thread 0; tiny)
+      __shared__ int s_keep[16];
+      __shared__ int s_nk, s_amb;
+      double* T = G;  // nk x nk upper (row-major), reuse of the reduction buffer
+      if (threadIdx.x == 0) {
+        int nk = 0, amb = 0;
+        for (int j = 0; j < na; ++j) {
+          if (w0[j] == 0.0) continue;
+          // d = M_jj - sum over kept i of T_ij^2, with T_ij for the kept i
+          double tcol[16];
+          double d = Mf[j * na + j];
+          for (int a = 0; a < nk; ++a) {
+            const int i = s_keep[a];
+            double v = Mf[i * na + j];
+            for (int b = 0; b < a; ++b) v -= T[b * 16 + a] * tcol[b];
+            v /= T[a * 16 + a];
+            tcol[a] = v;
+            d -= v * v;
+          }
+          const double mjj = Mf[j * na + j];
+          if (!(d > 1e-4 * mjj)) {
+            // cancellation: the reference's exact recomputation decides
+            amb = 1;
+            break;
+          }
+          const double nwj = sqrt(d);
+          if (!(nwj > 1e-10 * w0[j])) continue;
+          for (int a = 0; a < nk; ++a) T[a * 16 + nk] = tcol[a];
+          T[nk * 16 + nk] = nwj;
+          s_keep[nk++] = j;
+        }
+        s_nk = nk;
+        s_amb = amb;
+      }
+      __syncthreads();
+      const int nk = s_nk;
+      if (s_amb) {
+        if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+      } else if (nk > 0) {
+        // Q = W2[:, keep] T^-1 and the directions alike (own rows), in place
+        // into the next C / U columns
+        double tmin = INFINITY, tmax = 0.0;
+        for (int a = 0; a < nk; ++a) {
+          tmin = fmin(tmin, T[a * 16 + a]);
+          tmax = fmax(tmax, T[a * 16 + a]);
+        }
+        for (int r = threadIdx.x; r < nr; r += kOrthT) {
+          const size_t row = (size_t)(r0 + r);
+          fold_rowsolve<NY>(RB + row * s, DX + row * s, s_keep, nk, T, 16,
+                            C + row * kc + k, U + row * kc + k);
+        }
+        __syncthreads();
+        if (!(tmax <= kSkipKappa * tmin)) {
+          // second Cholesky-QR pass over the new columns
+          const Rows Qn{C + (size_t)r0 * kc + k, kc, nk, C + (size_t)r0 * kc + k, kc};
+          block_gram<NY>(Qn, nk, C + (size_t)r0 * kc + k, kc, nk, nr, red, partial, slot);
+          wreduce(wb, partial, gout, nk * nk, G, nullptr, 0, nullptr);
+          if (threadIdx.x < 32) {
+            const bool ok = warp_cholesky_smem(G, nk, R1, piv2, false, 0.0);
+            if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
+          }
+          __syncthreads();
+          if (flag[0]) {
+            if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+          } else {
+            for (int r = threadIdx.x; r < nr; r += kOrthT) {
+              const size_t row = (size_t)(r0 + r);
+              fold_rowsolve<NY>(C + row * kc + k, U + row * kc + k, nullptr, nk, R1, nk,
+                                C + row * kc + k, U + row * kc + k);
+            }
+          }
+        }
+      }
+      // truncation: keep the last outer_dim columns (krylov.py:267-269)
+      const int kk = k + nk;
+      if (!s_amb && kk > A.outer_dim) {
+        const int drop = kk - A.outer_dim;
+        for (int r = threadIdx.x; r < nr; r += kOrthT) {
+          const size_t row = (size_t)(r0 + r);
+          for (int t = 0; t < A.outer_dim; ++t) {
+            C[row * kc + t] = C[row * kc + t + drop];
+            U[row * kc + t] = U[row * kc + t + drop];
+          }
+        }
+      }
+      if (lead && threadIdx.x == 0 && !s_amb) ist[kK] = kk > A.outer_dim ? A.outer_dim : kk;
+    }
+    sstamp(A, grp, cyc, 7);
+    gbar(gb);
+    sstamp(A, grp, cyc, 8);
+    ++cyc;
+  }
+}
+
+}  // namespace pmp
+
+// cycle.cu
+namespace pmp {
+size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached);
+}
+
+using namespace pmp;
+
+static size_t solve_smem_bytes(int rows, int ldx, int kc, int cap, int s, int restart,
+                               int cached) {
+  size_t d = (size_t)(kc + cap + s) * s + 2 * (size_t)s * s + 8 * 32 * (size_t)s + 20;
+  d += cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
+  return d * sizeof(double);
+}
+
+static void* solve_kernel(int s, int cached) {
+  if (s <= 8) return cached ? (void*)k_solve<true, 8> : (void*)k_solve<false, 8>;
+  return cached ? (void*)k_solve<true, 16> : (void*)k_solve<false, 16>;
+}
+
+extern "C" {
+
+int pmp_solve_geometry(int n, int s, int cap, int kc, int restart, int groups, int* gsz,
+                       int* rows, int* cached, size_t* smem) {
+  const int sms = orth_max_grid() / 2;
+  const int ldx = odd_ld(kc + cap);
+  if (groups < 1 || s < 1 || s > 16) return PMP_ERR_ARG;
+  const int order[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
+  for (int a = 0; a < 4; ++a) {
+    const int bps = order[a][0], cach = order[a][1];
+    const int g = bps * sms / groups;
+    if (g < 2) continue;
+    int workers = g - 1;
+    const int need = (n + 31) / 32;
+    if (need < workers) workers = need;
+    const int r = (n + workers - 1) / workers;
+    const size_t sm = solve_smem_bytes(r, ldx, kc, cap, s, restart, cach);
+    if (sm > (size_t)(bps == 2 ? 110 : 220) * 1024) continue;
+    // registers may cap residency below what shared memory allows
+    if (prepare_smem(solve_kernel(s, cach), sm, kOrthT) < bps) continue;
+    *gsz = workers + 1;
+    *rows = r;
+    *cached = cach;
+    *smem = sm;
+    return PMP_OK;
+  }
+  return PMP_ERR_ARG;
+}
+
+int pmp_solve_batch(PmpSolveBatch* b) {
+  if (!b || b->groups < 1 || b->s < 1 || b->s > 16 || b->nfac < 0 || b->nfac > 3 ||
+      b->inner_restart + b->s > 96 || b->outer_dim < 0 || b->outer_dim + b->s > b->kc) {
+    set_error("pmp_solve_batch: bad arguments");
+    return PMP_ERR_ARG;
+  }
+  int gsz, rows, cached;
+  size_t smem;
+  if (pmp_solve_geometry(b->n, b->s, b->cap, b->kc, b->inner_restart, b->groups, &gsz, &rows,
+                         &cached, &smem) != PMP_OK) {
+    set_error("pmp_solve_batch: no co-resident geometry (n=%d s=%d groups=%d)", b->n, b->s,
+              b->groups);
+    return PMP_ERR_ARG;
+  }
+  if (gsz != b->gsz || rows != b->rows_per_block) {
+    set_error("pmp_solve_batch: geometry mismatch (query pmp_solve_geometry first)");
+    return PMP_ERR_ARG;
+  }
+  void* fn = solve_kernel(b->s, cached);
+  const int occ = prepare_smem(fn, smem, kOrthT);
+  if (occ * (orth_max_grid() / 2) < gsz * b->groups) {
+    set_error("pmp_solve_batch: grid not co-resident (%d blocks/SM)", occ);
+    return PMP_ERR_ARG;
+  }
+  SolveArgs A;
+  A.n = b->n;
+  A.s = b->s;
+  A.cap = b->cap;
+  A.kc = b->kc;
+  A.outer_dim = b->outer_dim;
+  A.inner_restart = b->inner_restart;
+  A.max_iters = b->max_iters;
+  A.nfac = b->nfac;
+  A.gsz = gsz;
+  A.rows_per_block = rows;
+  A.ldx = odd_ld(b->kc + b->cap);
+  A.hist_cap = b->hist_cap;
+  A.log_cap = b->log_cap;
+  A.isz = b->isz;
+  A.tol = b->tol;
+  A.sys = reinterpret_cast<const SysDesc*>(b->d_sys);
+  A.ws = b->d_ws;
+  A.wsz = b->wsz;
+  A.ist = b->d_istate;
+  A.oV = b->oV;
+  A.oC = b->oC;
+  A.oU = b->oU;
+  A.oW = b->oW;
+  A.oT0 = b->oT0;
+  A.oT1 = b->oT1;
+  A.oQ1 = b->oQ1;
+  A.oXt = b->oXt;
+  A.oR = b->oR;
+  A.oDX = b->oDX;
+  A.oRB = b->oRB;
+  A.oZ = b->oZ;
+  A.oPart = b->oPart;
+  A.oGout = b->oGout;
+  A.oSbuf = b->oSbuf;
+  A.oProj = b->oProj;
+  A.oLog = b->oLog;
+  A.oAux = b->oAux;
+  A.pBmat = b->pBmat;
+  A.pHb = b->pHb;
+  A.pCq = b->pCq;
+  A.pY = b->pY;
+  A.pRes = b->pRes;
+  A.pBn = b->pBn;
+  A.pHist = b->pHist;
+  A.dbg = cycle_dbg_take();
+  void* args[] = {&A};
+  cudaError_t e = coop_launch(fn, gsz * b->groups, args, smem,
+                              reinterpret_cast<cudaStream_t>(b->stream));
+  if (e != cudaSuccess) {
+    set_error("pmp_solve_batch: %s", cudaGetErrorString(e));
+    return PMP_ERR_CUDA;
+  }
+  return cuda_status("pmp_solve_batch");
+}
+
+}  // extern "C"

@@ -1084,3 +1084,192 @@ def gcro_solve(A, b, P=None, cfg=None):
         X, report = block_gcro_solve(A, b[:, None], P=P, cfg=cfg)
     report.residual_history = [float(r[0]) for r in report.residual_history]
     return X[:, 0], report
+
+
+# ---------------------------------------------------------------------------
+# whole solves on the device, several systems per launch (pmp_solve_batch)
+# ---------------------------------------------------------------------------
+
+class _SysDesc(ctypes.Structure):
+    """ctypes mirror of PmpSysDesc (include/pmorb200.h)."""
+    _fields_ = [("fac_rowptr", ctypes.c_void_p * 3), ("fac_colidx", ctypes.c_void_p * 3),
+                ("fac_vals", ctypes.c_void_p * 3)] + [
+        (f, ctypes.c_void_p) for f in ("a_rowptr", "a_colidx", "a_vals", "B", "X")]
+
+
+class _SolveBatchArgs(ctypes.Structure):
+    """ctypes mirror of PmpSolveBatch (include/pmorb200.h)."""
+    _fields_ = [(f, ctypes.c_int) for f in (
+        "n", "s", "cap", "kc", "outer_dim", "inner_restart", "max_iters", "nfac", "groups",
+        "gsz", "rows_per_block", "hist_cap", "log_cap", "isz")] + [
+        ("tol", ctypes.c_double), ("d_sys", ctypes.c_void_p), ("d_ws", ctypes.c_void_p),
+        ("wsz", ctypes.c_size_t), ("d_istate", ctypes.c_void_p)] + [
+        (f, ctypes.c_size_t) for f in ("oV", "oC", "oU", "oW", "oT0", "oT1", "oQ1", "oXt", "oR",
+                                       "oDX", "oRB", "oZ", "oPart", "oGout", "oSbuf", "oProj",
+                                       "oLog", "oAux")] + [
+        (f, ctypes.c_int) for f in ("pBmat", "pHb", "pCq", "pY", "pRes", "pBn", "pHist")] + [
+        ("stream", ctypes.c_void_p)]
+
+
+_SOLVE_ISZ = 256
+_SOLVE_FALLBACK = 10
+
+
+def _solve_layout(n, s, cap, kc, gsz, hist_cap, log_cap):
+    """Per-system workspace layout of pmp_solve_batch (offsets in doubles)."""
+    def al(x):
+        return (x + 31) // 32 * 32
+    ldq = kc + cap
+    kmax = (kc + cap + s) * s
+    proj = {}
+    o = 0
+    for name, size in (("pCq", ldq * s), ("pBn", s), ("pRes", s), ("pY", s * ldq),
+                       ("pHist", hist_cap * s), ("pBmat", kc * cap), ("pHb", cap * cap)):
+        proj[name] = o
+        o += al(size)
+    proj_size = o
+    off = {}
+    o = 0
+    for name, size in (("oV", n * cap), ("oC", n * kc), ("oU", n * kc)) + tuple(
+            (nm, n * s) for nm in ("oW", "oT0", "oT1", "oQ1", "oXt", "oR", "oDX", "oRB", "oZ")) + (
+            ("oPart", (gsz + 1) * kmax), ("oGout", kmax), ("oSbuf", 2 * (kc + 2 * cap + s) * s),
+            ("oProj", proj_size), ("oLog", log_cap * s), ("oAux", 64 + (kc + cap) * s)):
+        off[name] = o
+        o += al(size)
+    return off, proj, o
+
+
+def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
+    """Solve A_i X_i = B for every (A_i, P_i) in ``systems`` (krylov.py:105-275
+    for each), ``groups`` systems at a time in one persistent kernel
+    (pmp_solve_batch).  B is an n x s CUDA tensor shared by all systems.
+    Returns [(X_i, SolveReport_i)] in order.  Systems the device path hands
+    back (status 10: deflation / rank-deficient projected problem / an
+    ambiguous drop test) are re-solved on the host-driven path."""
+    cfg = cfg or SolverConfig()
+    Bd = _block_to_dev(B)
+    n, s = Bd.shape
+    if not systems:
+        return []
+    groups = groups or BATCH_GROUPS
+    groups = max(1, min(groups, len(systems)))
+    L = _abi.lib()
+    cap = cfg.inner_restart + 2 * s + 2
+    kc = cfg.outer_space_dim + s
+    ok = (s <= 16 and cfg.inner_restart + s <= 96 and cfg.outer_space_dim + s <= kc)
+    chains = []
+    for A, P in systems:
+        if P is not None and not isinstance(P, Preconditioner):
+            raise TypeError("P must be a Preconditioner or None")
+        chains.append(P.factors() if P is not None else [])
+    nfacs = {len(c) for c in chains}
+    if not ok or len(nfacs) != 1 or max(nfacs) > 3:
+        return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
+    nfac = nfacs.pop()
+    gsz = ctypes.c_int()
+    rows = ctypes.c_int()
+    cached = ctypes.c_int()
+    smem = ctypes.c_size_t()
+    while groups > 1 and L.pmp_solve_geometry(n, s, cap, kc, cfg.inner_restart, groups,
+                                              ctypes.byref(gsz), ctypes.byref(rows),
+                                              ctypes.byref(cached), ctypes.byref(smem)):
+        groups -= 1
+    rc = L.pmp_solve_geometry(n, s, cap, kc, cfg.inner_restart, groups, ctypes.byref(gsz),
+                              ctypes.byref(rows), ctypes.byref(cached), ctypes.byref(smem))
+    if rc:
+        return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
+    hist_cap = cap + 2
+    log_cap = 2 * cfg.max_iters + 4
+    off, poff, wsz = _solve_layout(n, s, cap, kc, gsz.value, hist_cap, log_cap)
+    dev = _dev()
+    sc = scratch()
+    ws = sc.get("solve_ws", 8 * wsz * groups).view(torch.float64)
+    ist = sc.get("solve_ist", 4 * _SOLVE_ISZ * groups).view(torch.int32)
+    sysd = (_SysDesc * groups)()
+    d_sys = torch.empty(ctypes.sizeof(sysd), dtype=torch.uint8, device=dev)
+    h_sys = torch.empty(ctypes.sizeof(sysd), dtype=torch.uint8, pin_memory=True)
+    h_ist = torch.empty(_SOLVE_ISZ * groups, dtype=torch.int32, pin_memory=True)
+    args = _SolveBatchArgs()
+    args.n, args.s, args.cap, args.kc = n, s, cap, kc
+    args.outer_dim, args.inner_restart, args.max_iters = (cfg.outer_space_dim,
+                                                          cfg.inner_restart, cfg.max_iters)
+    args.nfac, args.groups, args.gsz, args.rows_per_block = nfac, groups, gsz.value, rows.value
+    args.hist_cap, args.log_cap, args.isz, args.tol = hist_cap, log_cap, _SOLVE_ISZ, float(cfg.tol)
+    args.d_sys, args.d_ws, args.wsz = d_sys.data_ptr(), ws.data_ptr(), wsz
+    args.d_istate = ist.data_ptr()
+    for k_, v in off.items():
+        setattr(args, k_, v)
+    for k_, v in poff.items():
+        setattr(args, k_, v)
+    args.stream = _abi.stream()
+    out = [None] * len(systems)
+    fallback = []
+    stream = torch.cuda.current_stream()
+    for b0 in range(0, len(systems), groups):
+        chunk = list(range(b0, min(len(systems), b0 + groups)))
+        ng = len(chunk)
+        Xs = []
+        keep = []   # device operands must outlive the launch
+        for g, i in enumerate(chunk):
+            A, P = systems[i]
+            A = _as_dev_csr(A)
+            keep.append(A)
+            st = A.structure
+            d = sysd[g]
+            for j, F in enumerate(chains[i]):
+                fs = F.structure
+                d.fac_rowptr[j] = fs.rowptr.data_ptr()
+                d.fac_colidx[j] = fs.colidx.data_ptr()
+                d.fac_vals[j] = F.vals.data_ptr()
+            d.a_rowptr, d.a_colidx, d.a_vals = (st.rowptr.data_ptr(), st.colidx.data_ptr(),
+                                                A.vals.data_ptr())
+            X = torch.empty(n, s, dtype=torch.float64, device=dev)
+            Xs.append(X)
+            d.B, d.X = Bd.data_ptr(), X.data_ptr()
+        ctypes.memmove(h_sys.data_ptr(), ctypes.addressof(sysd), ctypes.sizeof(sysd))
+        d_sys.copy_(h_sys, non_blocking=True)
+        ist.zero_()
+        args.groups = ng
+        if _abi._counting:
+            _abi.COUNTERS["pmp_solve_batch"] = _abi.COUNTERS.get("pmp_solve_batch", 0) + 1
+        if _abi._timing_names and "pmp_solve_batch" in _abi._timing_names:
+            ea = torch.cuda.Event(enable_timing=True)
+            eb = torch.cuda.Event(enable_timing=True)
+            ea.record()
+            _abi.check(L.pmp_solve_batch(ctypes.byref(args)), "pmp_solve_batch")
+            eb.record()
+            _abi._timed.setdefault("pmp_solve_batch", []).append((ea, eb, (n, s, ng)))
+        else:
+            _abi.check(L.pmp_solve_batch(ctypes.byref(args)), "pmp_solve_batch")
+        h_ist.copy_(ist.view(-1)[:_SOLVE_ISZ * groups], non_blocking=True)
+        logs = []
+        stream.synchronize()
+        hi = h_ist.numpy()
+        for g, i in enumerate(chunk):
+            st = hi[g * _SOLVE_ISZ:(g + 1) * _SOLVE_ISZ]
+            if st[147] == _SOLVE_FALLBACK:
+                fallback.append(i)
+                continue
+            rows_ = int(st[148])
+            base = g * wsz + off["oLog"]
+            logs.append((g, i, rows_, base))
+        for g, i, rows_, base in logs:
+            st = hi[g * _SOLVE_ISZ:(g + 1) * _SOLVE_ISZ]
+            rep = SolveReport()
+            hist = ws[base:base + rows_ * s].view(rows_, s).cpu().numpy()
+            rep.residual_history = [row.copy() for row in hist]
+            rep.iterations = int(st[146])
+            rep.converged = int(st[144]) == 0
+            rep.matvec_count = int(st[149])
+            rep.precond_apply_count = int(st[150])
+            rep.device_launches = 1
+            rep.algorithmic_bytes = float(ws[g * wsz + off["oAux"] + 48].item())
+            out[i] = (Xs[g], rep)
+    for i in fallback:
+        A, P = systems[i]
+        out[i] = block_gcro_solve(A, Bd, P=P, cfg=cfg)
+    return out
+
+
+# systems per persistent solve launch (PMP_BATCH_GROUPS overrides)
+BATCH_GROUPS = int(_os.environ.get("PMP_BATCH_GROUPS", "4"))

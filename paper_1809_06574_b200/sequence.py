@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from .device import DeviceCSR, level0_pattern
-from .krylov import SolverConfig, block_gcro_solve
+from . import krylov as _krylov
+from .krylov import SolverConfig, block_gcro_solve, block_gcro_solve_batch
 from .spai import Preconditioner, SpaiConfig, _factor_from_columns, spai_build
 from .update import UpdateConfig, update_first, update_second
 
@@ -144,7 +145,7 @@ def gather_records(records, n_systems, group=None):
 # ---------------------------------------------------------------------------
 
 def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, rank=0, world=1,
-                 group=None, keep_solutions=False, timing=True, workers=1):
+                 group=None, keep_solutions=False, timing=True, workers=1, batch=None):
     """Run the whole parametric sequence; returns (records, info).
 
     records: one dict per system this rank owns (index, sigma, p, label,
@@ -152,6 +153,12 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     info: phase times from CUDA events (summed assemble / build / solve
     seconds; with workers > 1 the phases of different systems overlap) and
     the number of SPAI / update columns built.
+
+    batch > 1 (the default, PMP_BATCH_GROUPS; first-approach / independent
+    policies): systems are assembled and preconditioned ``batch`` at a time
+    and each chunk is solved by ONE persistent device launch, one block
+    group per system (block_gcro_solve_batch).  batch=1 keeps the per-system
+    path below.
 
     workers > 1 (first-approach / independent policies): after the initial
     system (and one update that warms the plan caches), the remaining
@@ -233,6 +240,50 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                 phases["build"].append((t1, t2))
                 phases["solve"].append((t2, t3))
 
+    if batch is None:
+        batch = _krylov.BATCH_GROUPS if workers <= 1 else 0
+    batched = batch > 1 and policy.kind in ("spai-update-first", "spai", "none")
+    if batched:
+        # assemble + precondition a chunk of systems, then solve the chunk in
+        # one persistent launch (one block group per system)
+        todo = [i for i in mine if not (sharded and i == 0)]
+        if sharded and 0 in mine:
+            do_system(0)
+        for c0 in range(0, len(todo), batch):
+            chunk = todo[c0:c0 + batch]
+            built = []
+            for idx in chunk:
+                s, p = points[idx]
+                t0 = mark()
+                A = model.assemble(s, p)
+                t1 = mark()
+                P, _, label, _ = seq.for_system(A)
+                t2 = mark()
+                built.append((idx, A, P, label, t0, t1, t2))
+            t3 = mark()
+            res = block_gcro_solve_batch([(A, P) for _, A, P, _, _, _, _ in built], Bd,
+                                         cfg=solver_cfg, groups=batch)
+            t4 = mark()
+            for (idx, A, P, label, t0, t1, t2), (X, rep) in zip(built, res):
+                s, p = points[idx]
+                rec = {"index": idx, "sigma": float(s), "p": [float(v) for v in p],
+                       "label": label, "iterations": rep.iterations,
+                       "converged": rep.converged, "matvec_count": rep.matvec_count,
+                       "precond_apply_count": rep.precond_apply_count,
+                       "final_residuals": np.asarray(rep.final_residuals, dtype=float).tolist(),
+                       "max_final_residual": float(np.max(rep.final_residuals)),
+                       "launches": getattr(rep, "device_launches", 0),
+                       "algorithmic_bytes": getattr(rep, "algorithmic_bytes", None)}
+                if keep_solutions:
+                    rec["X"] = X
+                records.append(rec)
+                state["build_cols"] += A.n if P is not None else 0
+                if timing:
+                    phases["assemble"].append((t0, t1))
+                    phases["build"].append((t1, t2))
+            if timing:
+                phases["solve"].append((t3, t4))
+        mine = []
     parallel = workers > 1 and policy.kind in ("spai-update-first", "spai", "none")
     head = mine[:2] if parallel else mine
     for idx in head:

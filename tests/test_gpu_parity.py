@@ -317,8 +317,10 @@ def test_concurrent_workers_bitwise_identical(pm):
                                          rhs=W.rhs)
     pol = pm.PrecondPolicy("spai-update-first", spai=pm.SpaiConfig(pattern_level=0),
                            update=pm.UpdateConfig(pattern_level=0))
-    r1, _ = pm.run_sequence(model, W.s_grid, W.p_grid, pol, keep_solutions=True, workers=1)
-    r3, _ = pm.run_sequence(model, W.s_grid, W.p_grid, pol, keep_solutions=True, workers=3)
+    r1, _ = pm.run_sequence(model, W.s_grid, W.p_grid, pol, keep_solutions=True, workers=1,
+                            batch=1)
+    r3, _ = pm.run_sequence(model, W.s_grid, W.p_grid, pol, keep_solutions=True, workers=3,
+                            batch=1)
     assert [r["index"] for r in r1] == [r["index"] for r in r3]
     for a, b in zip(r1, r3):
         assert a["iterations"] == b["iterations"]
@@ -434,3 +436,29 @@ def test_device_cycle_matches_host_loop(pm, name):
                 assert len(rd.residual_history) >= rd.iterations
     finally:
         krylov.DEVICE_CYCLE, krylov._CYCLE_BPS = saved
+
+
+@pytest.mark.parametrize("name", ["c1s24", "c2s8", "c3s6", "c5n500"])
+def test_solve_batch_matches_single(pm, name):
+    """Whole solves on the device, several systems per launch
+    (block_gcro_solve_batch): every system's residual <= tol (recomputed on
+    the host), iterations within 2 of the single-system path, histories
+    end at the true residual."""
+    import torch
+    g = G.load(name)
+    A1, Al, B = G.csr(g, "A1"), G.csr(g, "Al"), g["B"]
+    P0, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))
+    Pu, _ = pm.update_first(A1, Al, P0, pm.UpdateConfig(pattern_level=0))
+    cfg = pm.SolverConfig(tol=1e-8)
+    Bd = torch.as_tensor(B, device="cuda")
+    for systems in ([(A1, P0), (Al, P0)], [(Al, Pu), (A1, Pu), (Al, Pu)]):
+        for groups in (1, 2, 3):
+            res = pm.block_gcro_solve_batch(systems, Bd, cfg=cfg, groups=groups)
+            for (A, P), (X, rep) in zip(systems, res):
+                Xh, rh = pm.block_gcro_solve(A, B, P=P, cfg=cfg)
+                assert rep.converged == rh.converged
+                assert abs(rep.iterations - rh.iterations) <= 2, (rep.iterations, rh.iterations)
+                Xn = X.cpu().numpy()
+                rel = np.linalg.norm(B - A @ Xn, axis=0) / np.linalg.norm(B, axis=0)
+                assert np.all(rel <= 1e-8), rel
+                assert abs(float(np.max(rep.final_residuals)) - rel.max()) <= 1e-9

@@ -164,3 +164,31 @@ def test_cycle_state_layout_matches_header(tmp_path):
     got = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     assert [int(v) for v in got] == [ctypes.sizeof(S), S.offB.offset, S.ws_bytes.offset,
                                      S.tol.offset, S.blocks_per_sm.offset, S.d_istate.offset]
+
+
+def test_solve_batch_layout_matches_header(tmp_path):
+    """ctypes mirrors of PmpSysDesc / PmpSolveBatch == the C structs."""
+    import ctypes
+    import subprocess
+    from paper_1809_06574_b200.krylov import _SolveBatchArgs as S, _SysDesc as D
+    src = tmp_path / "probe.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pmorb200.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(PmpSysDesc),'
+                   ' offsetof(PmpSysDesc, B), sizeof(PmpSolveBatch),'
+                   ' offsetof(PmpSolveBatch, tol), offsetof(PmpSolveBatch, oV),'
+                   ' offsetof(PmpSolveBatch, pBmat), offsetof(PmpSolveBatch, stream));}\n')
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert [int(v) for v in got] == [ctypes.sizeof(D), D.B.offset, ctypes.sizeof(S), S.tol.offset,
+                                     S.oV.offset, S.pBmat.offset, S.stream.offset]
+
+
+def test_solve_layout_disjoint():
+    from paper_1809_06574_b200.krylov import _solve_layout
+    off, proj, total = _solve_layout(1000, 8, 68, 18, 74, 70, 2004)
+    starts = sorted(off.values())
+    assert starts[0] == 0 and all(b > a for a, b in zip(starts, starts[1:]))
+    assert total > max(starts)
+    assert all(v % 32 == 0 for v in off.values())

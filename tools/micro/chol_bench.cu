@@ -1,5 +1,5 @@
 // Micro-benchmark (diagnostic): cost of the small serial pieces of the
-// persistent cycle kernel, run in isolation on one block.
+// persistent cycle kernel, run in isolation.
 #include <cstdio>
 #include "../../paper_1809_06574_b200/csrc/orth_dev.cuh"
 
@@ -11,45 +11,62 @@ int orth_max_grid() { return 296; }
 }
 using namespace pmp;
 
-__global__ void k_bench(int m, int reps, long long* out) {
-  __shared__ double G[256], A[256], R[256];
-  __shared__ int piv[32];
+__device__ __noinline__ bool chol_generic(double* A, int m, double* R, int* piv) {
+  return warp_cholesky_smem(A, m, R, piv, true, 1e-5);
+}
+
+__global__ void k_bench(int m, int reps, long long* out, int mode, const double* Gin) {
+  extern __shared__ double dyn[];
+  double* G = dyn;
+  double* A = dyn + 256;
+  double* R = dyn + 512;
+  int* piv = reinterpret_cast<int*>(dyn + 768);
   const int t = threadIdx.x;
   for (int q = t; q < m * m; q += blockDim.x) {
     const int i = q / m, j = q % m;
-    G[q] = (i == j ? m + 1.0 : 0.0) + 1.0 / (1.0 + i + j);
+    G[q] = Gin ? Gin[q] : (i == j ? m + 1.0 : 0.0) + 1.0 / (1.0 + i + j);
   }
   __syncthreads();
-  long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  long long best = 1LL << 60;
   for (int r = 0; r < reps; ++r) {
     for (int q = t; q < m * m; q += blockDim.x) A[q] = G[q];
     __syncthreads();
-    if (r == reps - 1) t0 = clock64();
-    if (t < 32) warp_cholesky_smem(A, m, R, piv, true, 1e-5);
+    if (t < 32) {
+      const long long c0 = clock64();
+      bool ok = mode == 0 ? warp_cholesky_smem(A, m, R, piv, true, 1e-5) : chol_generic(A, m, R, piv);
+      const long long c1 = clock64();
+      if (t == 0 && ok && c1 - c0 < best) best = c1 - c0;
+    }
     __syncthreads();
-    if (r == reps - 1) t1 = clock64();
-    if (t < 32) warp_cholesky_reg<8>(G, m, R, piv, true, 1e-5);
-    __syncthreads();
-    if (r == reps - 1) t2 = clock64();
-    __syncthreads();
-    if (r == reps - 1) t3 = clock64();
   }
-  if (t == 0) {
-    out[0] = t1 - t0;
-    out[1] = t2 - t1;
-    out[2] = t3 - t2;
-  }
+  if (t == 0) out[blockIdx.x] = best;
 }
 
-int main() {
-  long long* d;
-  cudaMalloc(&d, 64);
-  long long h[8];
-  for (int reps : {1, 2, 10}) {
-    k_bench<<<1, 256>>>(8, reps, d);
-    cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
-    printf("reps %d: chol_smem %lld cycles, chol_reg %lld cycles, syncthreads %lld cycles\n", reps,
-           h[0], h[1], h[2]);
+int main(int argc, char** argv) {
+  double* gin = nullptr;
+  if (argc > 1) {
+    double h[64];
+    FILE* f = fopen(argv[1], "rb");
+    if (f && fread(h, 8, 64, f) == 64) {
+      cudaMalloc(&gin, 512);
+      cudaMemcpy(gin, h, 512, cudaMemcpyHostToDevice);
+    }
+    if (f) fclose(f);
   }
+  long long* d;
+  cudaMalloc(&d, 8 * 1024);
+  long long h[1024];
+  cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int mode = 0; mode < 2; ++mode)
+    for (int blocks : {1, 148, 296}) {
+      for (size_t sm : {(size_t)8 * 1024, (size_t)100 * 1024}) {
+        k_bench<<<blocks, 256, sm>>>(8, 5, d, mode, gin);
+        cudaMemcpy(h, d, 8 * blocks, cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int b = 0; b < blocks; ++b) mx = h[b] > mx ? h[b] : mx;
+        printf("mode %d blocks %d smem %zuKB: chol %lld cycles (block 0), max %lld\n", mode,
+               blocks, sm / 1024, h[0], mx);
+      }
+    }
   return 0;
 }
