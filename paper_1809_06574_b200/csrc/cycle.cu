@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(kOrthT, 2) k_cycle(CycleArgs P) {
 
   // ---- workers -----------------------------------------------------------------
   const int ldx = P.ldx;
-  const int ldw = CACHED ? odd_ld(sb) : P.s;
+  const int ldw = odd_ld(sb);  // W rows live in shared memory in both modes
   double* Xs = region;
-  double* Wv = CACHED ? region + (size_t)nr * ldx : P.W + (size_t)r0 * P.s;
+  double* Wv = region + (CACHED ? (size_t)nr * ldx : 0);
   double* Q1 = P.Q1g + (size_t)r0 * sb;
   WBar wb{P.ist + 9, (int)gridDim.x - 1, 0, (int)blockIdx.x - 1};
 
@@ -111,9 +111,9 @@ int cycle_nblk(int restart, int sb) { return (restart + sb - 1) / sb + 1; }
 size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached) {
   const size_t nb = cycle_nblk(restart, sb);
   size_t ctl = nb * 4 * sb * sb + (size_t)sb * sb * nb * (nb + 1) / 2 + (size_t)ldq * na +
-               (size_t)sb * ldq + sb * sb + 8 * 96 + 32 + 8 + 16 + 16 +
+               (size_t)sb * ldq + sb * sb + 16 * 96 + 32 + 8 + 16 + 16 +
                (size_t)(2 * sb + 1) * (3 * sb + na) + (size_t)2 * ldq * sb + 8;
-  size_t work = cached ? (size_t)rows * (ldx + odd_ld(sb)) : 0;
+  size_t work = (size_t)rows * ((cached ? ldx : 0) + odd_ld(sb));
   return ctl > work ? ctl : work;
 }
 

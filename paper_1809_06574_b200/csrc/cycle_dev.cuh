@@ -125,7 +125,7 @@ struct Ctl {
   double* Cq;    // ldq x na, column-major (Q^T rhs)
   double* cols;  // b x ldq: the step's new columns of G
   double* Rr;    // b x b: R of the step's orthonormalisation (un-pivoted)
-  double* ybuf;  // 8 x 96: back substitution
+  double* ybuf;  // 16 x 96: back substitution (one row per right-hand side)
   double* v;     // 32: current reflector
   double* misc;  // [0] max |R_jj| [1] min |R_jj| [2] tau [3] NaN seen
   double* bn;    // 16: column norms of the right-hand sides
@@ -151,7 +151,7 @@ static __device__ __forceinline__ Ctl ctl_layout(double* region, int sb, int nbl
   S.Rr = q;
   q += sb * sb;
   S.ybuf = q;
-  q += 8 * 96;
+  q += 16 * 96;
   S.v = q;
   q += 32;
   S.misc = q;
@@ -355,8 +355,8 @@ static __device__ void ctl_solve_y(const CycleArgs& P, const Ctl& S, int m) {
     rinv[i] = 1.0 / S.Rp[rp_off(q, b) + (size_t)c * (q + 1) * b + i];
   }
   __syncthreads();
-  double* y = S.ybuf + (size_t)wid * 96;
   for (int r = wid; r < P.na; r += kOrthT / 32) {
+    double* y = S.ybuf + (size_t)r * 96;
     const double* cr = S.Cq + (size_t)r * ldq + k;
     double c[3];
 #pragma unroll
@@ -375,15 +375,29 @@ static __device__ void ctl_solve_y(const CycleArgs& P, const Ctl& S, int m) {
       }
     }
     __syncwarp();
-    for (int i = lane; i < k; i += 32) {
-      double s = 0.0;
-      const double* brow = P.proj + P.oBmat + (size_t)i * P.cap;
-      for (int t = 0; t < m; ++t) s += __ldcg(brow + t) * y[t];
-      P.proj[P.oY + (size_t)r * n1 + i] = S.Cq[(size_t)r * ldq + i] - s;
-    }
     for (int i = lane; i < m; i += 32) P.proj[P.oY + (size_t)r * n1 + k + i] = y[i];
-    __syncwarp();
   }
+  __syncthreads();
+  // y_top = c_top - Bmat y_H, Bmat staged into the (now free) packed-R space
+  const size_t rp_cap = (size_t)b * b * P.nblk * (P.nblk + 1) / 2;
+  const bool staged = (size_t)k * m <= rp_cap;
+  double* Bs = S.Rp;
+  if (staged)
+    for (int x = threadIdx.x; x < k * m; x += kOrthT)
+      Bs[x] = __ldcg(P.proj + P.oBmat + (size_t)(x / m) * P.cap + x % m);
+  __syncthreads();
+  for (int x = threadIdx.x; x < k * P.na; x += kOrthT) {
+    const int i = x / P.na, r = x % P.na;
+    const double* y = S.ybuf + (size_t)r * 96;
+    double s = 0.0;
+    if (staged) {
+      for (int t = 0; t < m; ++t) s += Bs[(size_t)i * m + t] * y[t];
+    } else {
+      for (int t = 0; t < m; ++t) s += __ldcg(P.proj + P.oBmat + (size_t)i * P.cap + t) * y[t];
+    }
+    P.proj[P.oY + (size_t)r * n1 + i] = S.Cq[(size_t)r * ldq + i] - s;
+  }
+  __syncthreads();
 }
 
 // barrier over the worker blocks only (the control block runs on its own):
@@ -691,9 +705,8 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     if (flag[0]) {
       // grid-uniform: Cholesky cannot decide the rank -> host Householder
       // (unless the previous step already converged / was deficient)
-      if (CACHED)
-        for (int qq = threadIdx.x; qq < nr * sb; qq += kOrthT)
-          P.W[(size_t)(r0 + qq / sb) * P.s + qq % sb] = Wv[(size_t)(qq / sb) * ldw + qq % sb];
+      for (int qq = threadIdx.x; qq < nr * sb; qq += kOrthT)
+        P.W[(size_t)(r0 + qq / sb) * P.s + qq % sb] = Wv[(size_t)(qq / sb) * ldw + qq % sb];
       status = 5;
       if (q > 0) {
         const int d = wait_flag(P.ist + 16 + q - 1, 0);

@@ -62,10 +62,25 @@ __device__ PMP_GRAM_INLINE void block_gram(const Rows X, int kx, const double* Y
     if (job < rounds * splits && t < kx) {
       const int per = (nrows + splits - 1) / splits;
       const int ra = sp * per, rb = min(nrows, ra + per);
-      double xn = ra < rb ? X.at(ra, t) : 0.0;
-      for (int r = ra; r < rb; ++r) {
-        const double x = xn;
-        if (r + 1 < rb) xn = X.at(r + 1, t);   // prefetch the next row's operand
+      // rows in batches of 4: the X loads of a batch are all in flight
+      // before its FMAs (row order, hence the sums, unchanged)
+      const double* xa = t < X.ka ? X.a + t : X.b + (t - X.ka);
+      const int ldxr = t < X.ka ? X.lda : X.ldb;
+      int r = ra;
+      for (; r + 4 <= rb; r += 4) {
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = xa[(size_t)(r + u) * ldxr];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* y = Y + (size_t)(r + u) * ldy;
+#pragma unroll
+          for (int c = 0; c < NY; ++c)
+            if (c < ny) acc[c] += x[u] * y[c];
+        }
+      }
+      for (; r < rb; ++r) {
+        const double x = xa[(size_t)r * ldxr];
         const double* y = Y + (size_t)r * ldy;
 #pragma unroll
         for (int c = 0; c < NY; ++c)
@@ -149,12 +164,26 @@ static __device__ __noinline__ void grid_reduce(cg::grid_group& grid, double* pa
 template <int NY>
 __device__ PMP_GRAM_INLINE void block_update(const Rows X, int kx, double* Y, int ldy, int ny, int nrows,
                              const double* G) {
+  const int ka = min(kx, X.ka);
   for (int r = threadIdx.x; r < nrows; r += kOrthT) {
     double acc[NY];
 #pragma unroll
     for (int c = 0; c < NY; ++c) acc[c] = 0.0;
-    for (int t = 0; t < kx; ++t) {
-      const double x = X.at(r, t);
+    // the two column segments separately (no per-element branch), unrolled
+    // so several row loads are in flight
+    const double* xa = X.a + (size_t)r * X.lda;
+#pragma unroll 4
+    for (int t = 0; t < ka; ++t) {
+      const double x = xa[t];
+      const double* g = G + t * ny;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c < ny) acc[c] += x * g[c];
+    }
+    const double* xb = X.b + (size_t)r * X.ldb - X.ka;
+#pragma unroll 4
+    for (int t = ka; t < kx; ++t) {
+      const double x = xb[t];
       const double* g = G + t * ny;
 #pragma unroll
       for (int c = 0; c < NY; ++c)

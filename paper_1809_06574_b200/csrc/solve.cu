@@ -389,6 +389,16 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
           v = __ldcg(sbf.R + (i - k) * na + c);
         S.Cq[q] = v;
       }
+      // the fold images start from rhs0 = [rhs_c; S0; 0] (img = rhs0 - Q [0; t])
+      for (int q = threadIdx.x; q < (k + cap) * na; q += kOrthT) {
+        const int i = q / na, c = q % na;
+        double v = 0.0;
+        if (i < k)
+          v = __ldcg(sbf.B + i * na + c);
+        else if (i < k + na)
+          v = __ldcg(sbf.R + (i - k) * na + c);
+        img[(size_t)i * s + c] = v;
+      }
       for (int c = threadIdx.x; c < na; c += kOrthT) S.bn[c] = bn[acts[c]];
       if (threadIdx.x == 0) {
         S.misc[0] = k > 0 ? 1.0 : 0.0;
@@ -408,39 +418,68 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       ctl_run<NY>(L, S);
       // the cycle's estimate rows -> the full-width log; fold images G Y
       const int hrow = ldv(ist + 5), m = ldv(ist + 0), total = ldv(ist + 1), st = ldv(ist + 4);
-      if (threadIdx.x == 0) {
-        int lr = ldv(ist + kLogRows);
-        for (int h = 0; h < hrow && lr < A.log_cap; ++h, ++lr) {
-          for (int c = 0; c < na; ++c) lrel[acts[c]] = proj[A.pHist + (size_t)h * na + c];
-          for (int c = 0; c < s; ++c) logp[(size_t)lr * s + c] = lrel[c];
+      {
+        // the cycle's estimate rows -> full-width log rows (thread per column)
+        const int lr0 = ldv(ist + kLogRows);
+        const int nh = min(hrow, A.log_cap - lr0);
+        for (int col = threadIdx.x; col < s; col += kOrthT) {
+          int pos = -1;
+          for (int c = 0; c < na; ++c)
+            if (acts[c] == col) pos = c;
+          double last = lrel[col];
+          for (int h = 0; h < nh; ++h) {
+            if (pos >= 0) last = proj[A.pHist + (size_t)h * na + pos];
+            logp[(size_t)(lr0 + h) * s + col] = last;
+          }
+          lrel[col] = last;
         }
-        ist[kLogRows] = lr;
+        __syncthreads();
+        if (threadIdx.x == 0) ist[kLogRows] = lr0 + max(nh, 0);
       }
       if (st != 4 && st != 5 && m > 0) {
-        // img = G Y: rows [0, k) = Y_u + Bmat Y_v, rows [k, k + total) = Hb Y_v
-        const int n1 = k + m;
-        const double* Y = proj + A.pY;
-        for (int q = threadIdx.x; q < (k + total) * na; q += kOrthT) {
-          const int i = q / na, c = q % na;
-          const double* y = Y + (size_t)c * n1;
-          double v;
-          if (i < k) {
-            v = y[i];
-            const double* brow = proj + A.pBmat + (size_t)i * cap;
-            for (int t = 0; t < m; ++t) v += brow[t] * y[k + t];
-          } else {
-            v = 0.0;
-            const double* hrow_ = proj + A.pHb + (size_t)(i - k) * cap;
-            for (int t = 0; t < m; ++t) v += hrow_[t] * y[k + t];
+        // fold images G Y = rhs0 - (rhs0 - G Y), and the least-squares
+        // residual rhs0 - G Y = Q [0; t] with t the tail of Q^T rhs0: apply
+        // the steps' window transforms Q_p = M_p^T backwards (cheap, all in
+        // shared memory) instead of multiplying G (global) by Y
+        const int nrows = k + total, n1 = k + m, nq = m / na, b2 = 2 * na;
+        double* z = S.cols;  // na x ldq, column-major
+        for (int x = threadIdx.x; x < na * ldq; x += kOrthT) {
+          const int i = x % ldq;
+          z[x] = (i >= n1 && i < nrows) ? S.Cq[x] : 0.0;
+        }
+        __syncthreads();
+        const int nout = na * b2;
+        for (int pq = nq - 1; pq >= 0; --pq) {
+          const double* M = S.Mq + (size_t)pq * b2 * b2;
+          const int w0 = k + pq * na;
+          double o[2] = {0.0, 0.0};
+          for (int u = 0; u < 2; ++u) {
+            const int x = threadIdx.x + u * kOrthT;
+            if (x < nout) {
+              const int c = x / b2, i = x % b2;
+              const double* zc = z + (size_t)c * ldq + w0;
+              double t = 0.0;
+              for (int j = 0; j < b2; ++j) t += M[i * b2 + j] * zc[j];
+              o[u] = t;
+            }
           }
-          img[(size_t)i * s + c] = v;
+          __syncthreads();
+          for (int u = 0; u < 2; ++u) {
+            const int x = threadIdx.x + u * kOrthT;
+            if (x < nout) z[(size_t)(x / b2) * ldq + w0 + x % b2] = o[u];
+          }
+          __syncthreads();
+        }
+        for (int x = threadIdx.x; x < nrows * na; x += kOrthT) {
+          const int i = x / na, c = x % na;
+          img[(size_t)i * s + c] -= z[(size_t)c * ldq + i];
         }
       }
       __syncthreads();
     } else {
       int m = 0, total = na, ncols = 0, status = 0;
-      const int ldw = CACHED ? odd_ld(na) : s;
-      double* Wv = CACHED ? region + (size_t)nr * A.ldx : W + (size_t)r0 * s;
+      const int ldw = odd_ld(na);  // W rows in shared memory in both modes
+      double* Wv = region + (CACHED ? (size_t)nr * A.ldx : 0);
       WSmem wsm{G, R1, R2, red, piv, piv2, flag, region, Wv, L.Q1g + (size_t)r0 * na, ldw};
       worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
       sstamp(A, grp, cyc, 3);
@@ -471,9 +510,12 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         const int r = q / na, c = q % na;
         const size_t row = (size_t)(r0 + r);
         double d = 0.0;
-        const double* vr = V + row * cap;
+        // (V rows from the block's shared-memory copy when cached)
+        const double* vr = CACHED ? region + (size_t)r * A.ldx + k : V + row * cap;
+#pragma unroll 4
         for (int t = 0; t < m; ++t) d += vr[t] * G[(k + t) * na + c];
         const double* ur = U + row * kc;
+#pragma unroll 4
         for (int t = 0; t < k; ++t) d += ur[t] * G[t * na + c];
         DX[row * s + c] = d;
         const double xt = Xt[row * s + acts[c]] + d;
@@ -562,9 +604,11 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         const int r = q / na, c = q % na;
         const size_t row = (size_t)(r0 + r);
         double d = 0.0;
-        const double* vr = V + row * cap;
+        const double* vr = CACHED ? region + (size_t)r * A.ldx + k : V + row * cap;
+#pragma unroll 4
         for (int t = 0; t < total; ++t) d += vr[t] * G[(k + t) * na + c];
-        const double* cr = C + row * kc;
+        const double* cr = CACHED ? region + (size_t)r * A.ldx : C + row * kc;
+#pragma unroll 4
         for (int t = 0; t < k; ++t) d += cr[t] * G[t * na + c];
         RB[row * s + c] = d;
       }
