@@ -317,7 +317,7 @@ int pmp_cycle_debug_stamps(unsigned long long* d_stamps, int records);
 /* Whole block-GCRO solves on the device (krylov.py:105-275), `groups`
  * independent systems per launch (one group of gsz blocks each; query
  * pmp_solve_geometry).  One PmpSysDesc per system, in DEVICE memory at
- * d_sys: the factor chain (nfac CSR factors, applied right to left), A, the
+ * d_sys: the factor chain (nfac <= 3 CSR factors, applied right to left), A, the
  * right-hand side block B (n x s) and the output X (n x s).  Each system
  * gets wsz doubles of d_ws and isz ints of d_istate (offsets below, in
  * doubles, inside one system's block; p* offsets inside its projected-
@@ -327,6 +327,7 @@ int pmp_cycle_debug_stamps(unsigned long long* d_stamps, int records);
  * an ambiguous drop test), [148] rows of the residual log (s doubles per
  * row at oLog), [149] matvecs, [150] preconditioner applications. */
 typedef struct PmpSysDesc {
+  int nfac;
   const int32_t* fac_rowptr[3];
   const int32_t* fac_colidx[3];
   const double* fac_vals[3];
@@ -337,7 +338,7 @@ typedef struct PmpSysDesc {
   double* X;
 } PmpSysDesc;
 typedef struct PmpSolveBatch {
-  int n, s, cap, kc, outer_dim, inner_restart, max_iters, nfac;
+  int n, s, cap, kc, outer_dim, inner_restart, max_iters;
   int groups, gsz, rows_per_block, hist_cap, log_cap, isz;
   double tol;
   const PmpSysDesc* d_sys;

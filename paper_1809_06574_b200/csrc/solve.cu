@@ -30,6 +30,7 @@
 namespace pmp {
 
 struct SysDesc {
+  int nfac;  // factors in this system's preconditioner chain (0 .. 3)
   const int32_t* frp[3];
   const int32_t* fci[3];
   const double* fva[3];
@@ -41,7 +42,7 @@ struct SysDesc {
 };
 
 struct SolveArgs {
-  int n, s, cap, kc, outer_dim, inner_restart, max_iters, nfac;
+  int n, s, cap, kc, outer_dim, inner_restart, max_iters;
   int gsz, rows_per_block, ldx, hist_cap, log_cap, isz;
   double tol;
   const SysDesc* sys;
@@ -65,6 +66,7 @@ enum {
   kPrec = 150,
   kGbar = 151,
   kFold = 152,
+  kReason = 153,  // fallback reason: 1 cycle-start QR, 2/3 inner status 4/5, 4/5 fold
   kAct = 160,  // active columns (<= 16)
 };
 
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   L.s = s;
   L.cap = cap;
   L.kc = kc;
-  L.nfac = A.nfac;
+  L.nfac = D.nfac;
   for (int i = 0; i < 3; ++i) {
     L.frp[i] = D.frp[i];
     L.fci[i] = D.fci[i];
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         __syncthreads();
       }
       if (flag[0]) {
-        if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+        if (lead && threadIdx.x == 0) { ist[kStatus] = PMP_SOLVE_FALLBACK; ist[kReason] = 1; }
       } else {
         double* Vr = V + (size_t)r0 * cap;
         if (single)
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
     {
       const int st = ldv(ist + 4);
       if (st == 4 || st == 5) {
-        if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+        if (lead && threadIdx.x == 0) { ist[kStatus] = PMP_SOLVE_FALLBACK; ist[kReason] = st == 4 ? 2 : 3; }
         break;
       }
     }
@@ -524,9 +526,9 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       }
       // Xa = P Z (factor chain right to left)
       const double* src = Z;
-      for (int f = A.nfac - 1; f >= 0; --f) {
+      for (int f = D.nfac - 1; f >= 0; --f) {
         wbar(wb);
-        double* dst = ((A.nfac - 1 - f) & 1) ? L.T1 : L.T0;
+        double* dst = ((D.nfac - 1 - f) & 1) ? L.T1 : L.T0;
         spmm_rows<NY>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr);
         src = dst;
       }
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         // every operator matrix once (12 B / nonzero + row pointers), the
         // gathered and written n x na blocks, [C | V] once per step
         double mb = 0.0;
-        for (int f = 0; f < A.nfac; ++f)
+        for (int f = 0; f < D.nfac; ++f)
           mb += 12.0 * __ldg(D.frp[f] + n) + 4.0 * (n + 1) + 16.0 * n * na;
         mb += 12.0 * __ldg(D.arp + n) + 4.0 * (n + 1) + 16.0 * n * na;
         double by = 0.0;
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         aux[48] += by;
         ist[kIt] = it_new;
         ist[kMatvecs] += na * steps + na;
-        if (A.nfac) ist[kPrec] += na * steps + na;
+        if (D.nfac) ist[kPrec] += na * steps + na;
         int lr = ist[kLogRows];
         int still = 0;
         for (int c = 0; c < na; ++c) {
@@ -680,7 +682,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       __syncthreads();
       const int nk = s_nk;
       if (s_amb) {
-        if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+        if (lead && threadIdx.x == 0) { ist[kStatus] = PMP_SOLVE_FALLBACK; ist[kReason] = 4; }
       } else if (nk > 0) {
         // Q = W2[:, keep] T^-1 and the directions alike (own rows), in place
         // into the next C / U columns
@@ -706,7 +708,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
           }
           __syncthreads();
           if (flag[0]) {
-            if (lead && threadIdx.x == 0) ist[kStatus] = PMP_SOLVE_FALLBACK;
+            if (lead && threadIdx.x == 0) { ist[kStatus] = PMP_SOLVE_FALLBACK; ist[kReason] = 5; }
           } else {
             for (int r = threadIdx.x; r < nr; r += kOrthT) {
               const size_t row = (size_t)(r0 + r);
@@ -788,7 +790,7 @@ int pmp_solve_geometry(int n, int s, int cap, int kc, int restart, int groups, i
 }
 
 int pmp_solve_batch(PmpSolveBatch* b) {
-  if (!b || b->groups < 1 || b->s < 1 || b->s > 16 || b->nfac < 0 || b->nfac > 3 ||
+  if (!b || b->groups < 1 || b->s < 1 || b->s > 16 || 
       b->inner_restart + b->s > 96 || b->outer_dim < 0 || b->outer_dim + b->s > b->kc) {
     set_error("pmp_solve_batch: bad arguments");
     return PMP_ERR_ARG;
@@ -819,7 +821,6 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   A.outer_dim = b->outer_dim;
   A.inner_restart = b->inner_restart;
   A.max_iters = b->max_iters;
-  A.nfac = b->nfac;
   A.gsz = gsz;
   A.rows_per_block = rows;
   A.ldx = odd_ld(b->kc + b->cap);

@@ -1092,7 +1092,8 @@ def gcro_solve(A, b, P=None, cfg=None):
 
 class _SysDesc(ctypes.Structure):
     """ctypes mirror of PmpSysDesc (include/pmorb200.h)."""
-    _fields_ = [("fac_rowptr", ctypes.c_void_p * 3), ("fac_colidx", ctypes.c_void_p * 3),
+    _fields_ = [("nfac", ctypes.c_int), ("fac_rowptr", ctypes.c_void_p * 3),
+                ("fac_colidx", ctypes.c_void_p * 3),
                 ("fac_vals", ctypes.c_void_p * 3)] + [
         (f, ctypes.c_void_p) for f in ("a_rowptr", "a_colidx", "a_vals", "B", "X")]
 
@@ -1100,7 +1101,7 @@ class _SysDesc(ctypes.Structure):
 class _SolveBatchArgs(ctypes.Structure):
     """ctypes mirror of PmpSolveBatch (include/pmorb200.h)."""
     _fields_ = [(f, ctypes.c_int) for f in (
-        "n", "s", "cap", "kc", "outer_dim", "inner_restart", "max_iters", "nfac", "groups",
+        "n", "s", "cap", "kc", "outer_dim", "inner_restart", "max_iters", "groups",
         "gsz", "rows_per_block", "hist_cap", "log_cap", "isz")] + [
         ("tol", ctypes.c_double), ("d_sys", ctypes.c_void_p), ("d_ws", ctypes.c_void_p),
         ("wsz", ctypes.c_size_t), ("d_istate", ctypes.c_void_p)] + [
@@ -1113,6 +1114,10 @@ class _SolveBatchArgs(ctypes.Structure):
 
 _SOLVE_ISZ = 256
 _SOLVE_FALLBACK = 10
+# reason code -> count of systems handed back to the host path (diagnostics:
+# 1 cycle-start QR needs deflation, 2 projected problem rank deficient,
+# 3 block step needs deflation, 4 fold drop test ambiguous, 5 fold CholQR)
+FALLBACK_REASONS = {}
 
 
 def _solve_layout(n, s, cap, kc, gsz, hist_cap, log_cap):
@@ -1162,10 +1167,8 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
         if P is not None and not isinstance(P, Preconditioner):
             raise TypeError("P must be a Preconditioner or None")
         chains.append(P.factors() if P is not None else [])
-    nfacs = {len(c) for c in chains}
-    if not ok or len(nfacs) != 1 or max(nfacs) > 3:
+    if not ok or max(len(c) for c in chains) > 3:
         return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
-    nfac = nfacs.pop()
     gsz = ctypes.c_int()
     rows = ctypes.c_int()
     cached = ctypes.c_int()
@@ -1193,7 +1196,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     args.n, args.s, args.cap, args.kc = n, s, cap, kc
     args.outer_dim, args.inner_restart, args.max_iters = (cfg.outer_space_dim,
                                                           cfg.inner_restart, cfg.max_iters)
-    args.nfac, args.groups, args.gsz, args.rows_per_block = nfac, groups, gsz.value, rows.value
+    args.groups, args.gsz, args.rows_per_block = groups, gsz.value, rows.value
     args.hist_cap, args.log_cap, args.isz, args.tol = hist_cap, log_cap, _SOLVE_ISZ, float(cfg.tol)
     args.d_sys, args.d_ws, args.wsz = d_sys.data_ptr(), ws.data_ptr(), wsz
     args.d_istate = ist.data_ptr()
@@ -1216,6 +1219,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
             keep.append(A)
             st = A.structure
             d = sysd[g]
+            d.nfac = len(chains[i])
             for j, F in enumerate(chains[i]):
                 fs = F.structure
                 d.fac_rowptr[j] = fs.rowptr.data_ptr()
@@ -1249,6 +1253,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
             st = hi[g * _SOLVE_ISZ:(g + 1) * _SOLVE_ISZ]
             if st[147] == _SOLVE_FALLBACK:
                 fallback.append(i)
+                FALLBACK_REASONS[int(st[153])] = FALLBACK_REASONS.get(int(st[153]), 0) + 1
                 continue
             rows_ = int(st[148])
             base = g * wsz + off["oLog"]

@@ -451,7 +451,8 @@ def test_solve_batch_matches_single(pm, name):
     Pu, _ = pm.update_first(A1, Al, P0, pm.UpdateConfig(pattern_level=0))
     cfg = pm.SolverConfig(tol=1e-8)
     Bd = torch.as_tensor(B, device="cuda")
-    for systems in ([(A1, P0), (Al, P0)], [(Al, Pu), (A1, Pu), (Al, Pu)]):
+    for systems in ([(A1, P0), (Al, P0)], [(Al, Pu), (A1, Pu), (Al, Pu)],
+                    [(A1, P0), (Al, Pu), (Al, None)]):    # mixed chain lengths
         for groups in (1, 2, 3):
             res = pm.block_gcro_solve_batch(systems, Bd, cfg=cfg, groups=groups)
             for (A, P), (X, rep) in zip(systems, res):
