@@ -333,10 +333,20 @@ def roofline(kern, timed, n, W, model, recs=None):
     else:
         byts = None
     ms = np.array([a.elapsed_time(b) for a, b, _ in lst])
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                         "ncu_traffic.json")))
+        if name in tj:
+            # DRAM bytes of one launch from the committed ncu --set full capture
+            traffic = tj[name]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
     if byts is not None:
         ach = float(np.sum(byts) / (np.sum(ms) / 1e3) / 1e9)
         return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm,
-                "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": float(np.mean(byts)),
                 "peak_source": which + " (MEASURED_PEAKS.json hbm_gbs)",
                 "launches": len(lst), "avg_us": kern[name]["avg_us"],
                 "share_of_step": kern[name]["share_of_step"]}
