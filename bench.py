@@ -199,7 +199,7 @@ def run_ours(args):
     infos = []
     # per-kernel device time: "k_orth" = the fused orthogonalisation kernel
     # inside each native block step (events recorded in the C driver)
-    dominant = ("pmp_solve_batch", "k_orth", "pmp_ls_columns", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
+    dominant = ("pmp_solve_batch", "k_orth", "pmp_ls_columns", "pmp_ls_columns_planned", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
                 "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm", "pmp_copy_cols",
                 "pmp_axpby_cols", "pmp_assemble", "pmp_permute")
     _abi.count_launches(True)

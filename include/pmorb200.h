@@ -121,6 +121,23 @@ int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int n
                    const int32_t* d_jptr, int32_t* d_jidx, void* d_ws, size_t ws_bytes,
                    void* stream);
 
+/* Same least squares with the per-column symbolic work (the sorted J, the
+ * positions of every A(J, I) entry and target entry) recorded once and
+ * replayed: every system of a parameter sweep shares one CSR structure, so
+ * only the values change between updates.  mode 4 solves and records into
+ * d_plan at d_plan_ptr[c] (c = position in the column list; size of column
+ * c: 4 + |I_j| + 2 * (pmp_ls_bound's list length)); mode 5 solves from the
+ * record (A / T values may differ, structures must be the recorded ones).
+ * Results are bitwise those of mode 0. */
+int pmp_ls_columns_planned(int mode, int team, int use_global, int lcap, int mcap, int ncap,
+                           int ncols, const int32_t* d_cols, int n, const int32_t* d_iptr,
+                           const int32_t* d_iidx, const int32_t* d_acolptr,
+                           const int32_t* d_arowidx, const double* d_avals,
+                           const int32_t* d_tcolptr, const int32_t* d_trowidx,
+                           const double* d_tvals, double* d_coef, double* d_resid,
+                           int32_t* d_flags, int32_t* d_plan, const int32_t* d_plan_ptr,
+                           void* d_ws, size_t ws_bytes, void* stream);
+
 /* ---- level-1 augmentation (_augmented_column, spai.py:210-222) ----------
  * Weights w_r = sum over k ascending of |a_rk| |a_kj| (no FMA; scipy's
  * csc_matmat order); candidates outside the base support

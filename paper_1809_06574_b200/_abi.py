@@ -44,6 +44,9 @@ _SIGS = {
     "pmp_ls_columns": ([c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp,
                         c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                         c_vp, c_sz, c_vp], c_int),
+    "pmp_ls_columns_planned": ([c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_int,
+                                c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_augment_team_bytes": ([c_int], c_sz),
     "pmp_augment": ([c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                      c_vp, c_vp, c_vp, c_sz, c_vp], c_int),

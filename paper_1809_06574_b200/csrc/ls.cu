@@ -26,7 +26,8 @@
 namespace pmp {
 
 struct LsParams {
-  int mode;  // 0 solve, 1 plan (|J|), 2 export J
+  int mode;  // 0 solve, 1 plan (|J|), 2 export J, 3 SNE, 4 solve + record the
+             // symbolic plan, 5 solve from a recorded plan
   int ncols;
   const int* cols;
   int n;
@@ -47,6 +48,12 @@ struct LsParams {
   int lcap, mcap, ncap;
   size_t team_bytes;
   char* gws;
+  // symbolic plan of the listed columns (modes 4 / 5): per column c at
+  // plan + plan_ptr[c]: |J|, tot (entries of A(:, I_j)), tl, off[0..|I_j|],
+  // then (value index, pos | col << 16) for the tot A entries and the tl
+  // target entries (value index -1 for the identity target)
+  int* plan;
+  const int* plan_ptr;
 };
 
 // team memory layout --------------------------------------------------------
@@ -228,7 +235,7 @@ __device__ inline int gather_sorted_rows(const LsParams& P, int j, const LsMem& 
 }
 
 template <int T>
-__device__ void ls_column(const LsParams& P, int j, char* mem, int tid) {
+__device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid) {
   LsMem m = ls_carve(mem, P.lcap, P.mcap, P.ncap);
   Team<T> tm{tid, m.red};
   const int i0 = P.iptr[j];
@@ -242,16 +249,25 @@ __device__ void ls_column(const LsParams& P, int j, char* mem, int tid) {
     tl = 1;
   }
   for (int c = tid; c < nI; c += T) m.sup[c] = P.iidx[i0 + c];
-  tm.sync();
-
-  int lp2;
-  const int L = gather_sorted_rows<T>(P, j, m, nI, t0, tl, tm, &lp2);
-  (void)L;
-  const int mJ = team_compact<T>(m.list, nullptr, lp2, tm, m.misc + 4,
-                                 [](int i, int v, int prev, double) {
-                                   return v != kIntMax && (i == 0 || v != prev);
-                                 });
+  int* pl = (P.mode >= 4) ? P.plan + P.plan_ptr[cpos] : nullptr;
+  int mJ;
   const int* J = m.list;
+  if (P.mode == 5) {
+    // the recorded symbolic work of this column (same structure): no gather,
+    // sort or searches
+    for (int c = tid; c <= nI; c += T) m.off[c] = pl[3 + c];
+    tm.sync();
+    mJ = pl[0];
+  } else {
+    tm.sync();
+    int lp2;
+    const int L = gather_sorted_rows<T>(P, j, m, nI, t0, tl, tm, &lp2);
+    (void)L;
+    mJ = team_compact<T>(m.list, nullptr, lp2, tm, m.misc + 4,
+                         [](int i, int v, int prev, double) {
+                           return v != kIntMax && (i == 0 || v != prev);
+                         });
+  }
 
   if (P.mode == 1) {
     if (tid == 0) P.msize[j] = mJ;
@@ -289,8 +305,21 @@ __device__ void ls_column(const LsParams& P, int j, char* mem, int tid) {
   for (int c = tid; c <= n; c += T) m.perm[c] = c;
   tm.sync();
   // scatter A(J, I) (off[] still holds the per-column prefix) and the target
-  {
-    const int tot = m.off[n];
+  const int tot = m.off[n];
+  int* ent = pl ? pl + 4 + n : nullptr;  // (value index, pos | col << 16) pairs
+  if (P.mode == 5) {
+    for (int q = tid; q < tot + tl; q += T) {
+      const int e = ent[2 * q], pc = ent[2 * q + 1];
+      const int pos = pc & 0xffff, col = pc >> 16;
+      M[pos + (size_t)col * mm] = q < tot ? P.avals[e] : (e < 0 ? 1.0 : P.tvals[e]);
+    }
+  } else {
+    if (pl && tid == 0) {
+      pl[0] = mJ;
+      pl[1] = tot;
+      pl[2] = tl;
+    }
+    for (int c = tid; pl && c <= n; c += T) pl[3 + c] = m.off[c];
     for (int q = tid; q < tot + tl; q += T) {
       if (q < tot) {
         int lo = 0, hi = n;
@@ -304,11 +333,20 @@ __device__ void ls_column(const LsParams& P, int j, char* mem, int tid) {
         int e = P.acolptr[m.sup[lo]] + (q - m.off[lo]);
         int pos = lower_bound_i(J, mm, P.arowidx[e]);
         M[pos + (size_t)lo * mm] = P.avals[e];
+        if (ent) {
+          ent[2 * q] = e;
+          ent[2 * q + 1] = pos | (lo << 16);
+        }
       } else {
         int qq = q - tot;
         int r = (t0 < 0) ? j : P.trowidx[t0 + qq];
         double v = (t0 < 0) ? 1.0 : P.tvals[t0 + qq];
-        M[lower_bound_i(J, mm, r) + (size_t)n * mm] = v;
+        const int pos = lower_bound_i(J, mm, r);
+        M[pos + (size_t)n * mm] = v;
+        if (ent) {
+          ent[2 * q] = (t0 < 0) ? -1 : t0 + qq;
+          ent[2 * q + 1] = pos | (n << 16);
+        }
       }
     }
   }
@@ -476,17 +514,33 @@ __device__ void ls_column(const LsParams& P, int j, char* mem, int tid) {
   double* res = M;  // reuse
   for (int i = tid; i < mm; i += T) res[i] = 0.0;
   tm.sync();
-  for (int q = tid; q < tl; q += T) {
-    int r = (t0 < 0) ? j : P.trowidx[t0 + q];
-    res[lower_bound_i(J, mm, r)] = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
-  }
-  tm.sync();
-  for (int c = 0; c < n; ++c) {
-    const double zc = m.w[c];
-    const int k = m.sup[c];
-    const int lo = P.acolptr[k], hi = P.acolptr[k + 1];
-    for (int e = lo + tid; e < hi; e += T) res[lower_bound_i(J, mm, P.arowidx[e])] -= P.avals[e] * zc;
+  if (ent) {
+    // same updates in the same order, positions from the plan
+    for (int q = tid; q < tl; q += T) {
+      const int e = ent[2 * (tot + q)];
+      res[ent[2 * (tot + q) + 1] & 0xffff] = e < 0 ? 1.0 : P.tvals[e];
+    }
     tm.sync();
+    for (int c = 0; c < n; ++c) {
+      const double zc = m.w[c];
+      for (int q = m.off[c] + tid; q < m.off[c + 1]; q += T)
+        res[ent[2 * q + 1] & 0xffff] -= P.avals[ent[2 * q]] * zc;
+      tm.sync();
+    }
+  } else {
+    for (int q = tid; q < tl; q += T) {
+      int r = (t0 < 0) ? j : P.trowidx[t0 + q];
+      res[lower_bound_i(J, mm, r)] = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
+    }
+    tm.sync();
+    for (int c = 0; c < n; ++c) {
+      const double zc = m.w[c];
+      const int k = m.sup[c];
+      const int lo = P.acolptr[k], hi = P.acolptr[k + 1];
+      for (int e = lo + tid; e < hi; e += T)
+        res[lower_bound_i(J, mm, P.arowidx[e])] -= P.avals[e] * zc;
+      tm.sync();
+    }
   }
   double part = 0.0;
   for (int i = tid; i < mm; i += T) part += res[i] * res[i];
@@ -508,7 +562,7 @@ __global__ void k_ls(LsParams P) {
   char* mem = GLOBAL ? (P.gws + (size_t)blockIdx.x * P.team_bytes) : (smem + (size_t)team * P.team_bytes);
   for (int c = blockIdx.x * per_block + team; c < P.ncols; c += gridDim.x * per_block) {
     const int j = P.cols ? P.cols[c] : c;
-    ls_column<T>(P, j, mem, tid);
+    ls_column<T>(P, j, c, mem, tid);
   }
 }
 
@@ -1018,19 +1072,23 @@ int pmp_ls_bound(int ncols, const int32_t* cols, const int32_t* iptr, const int3
   return cuda_status("pmp_ls_bound");
 }
 
-int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int ncap, int ncols,
-                   const int32_t* cols, int n, const int32_t* iptr, const int32_t* iidx,
-                   const int32_t* acolptr, const int32_t* arowidx, const double* avals,
-                   const int32_t* tcolptr, const int32_t* trowidx, const double* tvals,
-                   double* coef, double* resid, int32_t* flags, int32_t* msize,
-                   const int32_t* jptr, int32_t* jidx, void* ws, size_t ws_bytes, void* st) {
-  if (mode < 0 || mode > 3 || (team != 32 && team != 128 && team != 256) || lcap < 1 ||
-      mcap < 0 || ncap < 0 || ncols < 0 || (lcap & (lcap - 1))) {
+static int ls_columns(int mode, int team, int use_global, int lcap, int mcap, int ncap, int ncols,
+                      const int32_t* cols, int n, const int32_t* iptr, const int32_t* iidx,
+                      const int32_t* acolptr, const int32_t* arowidx, const double* avals,
+                      const int32_t* tcolptr, const int32_t* trowidx, const double* tvals,
+                      double* coef, double* resid, int32_t* flags, int32_t* msize,
+                      const int32_t* jptr, int32_t* jidx, int32_t* plan, const int32_t* plan_ptr,
+                      void* ws, size_t ws_bytes, void* st) {
+  if (mode < 0 || mode > 5 || (team != 32 && team != 128 && team != 256) || lcap < 1 ||
+      mcap < 0 || ncap < 0 || ncols < 0 || (lcap & (lcap - 1)) ||
+      (mode >= 4 && (!plan || !plan_ptr || mcap >= 65536 || ncap >= 32768))) {
     set_error("pmp_ls_columns: bad arguments (mode=%d team=%d lcap=%d)", mode, team, lcap);
     return PMP_ERR_ARG;
   }
   if (ncols == 0) return PMP_OK;
   LsParams P;
+  P.plan = plan;
+  P.plan_ptr = plan_ptr;
   P.mode = mode;
   P.ncols = ncols;
   P.cols = cols;
@@ -1050,7 +1108,7 @@ int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int n
   P.jptr = jptr;
   P.jidx = jidx;
   P.lcap = lcap;
-  P.mcap = (mode == 0 || mode == 3) ? mcap : 0;
+  P.mcap = (mode == 0 || mode >= 3) ? mcap : 0;
   P.ncap = ncap;
   P.team_bytes = ls_team_bytes(lcap, P.mcap, ncap);
   P.gws = (char*)ws;
@@ -1086,6 +1144,37 @@ int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int n
   if (team == 32) return launch_ls<32, false>(P, s, ws_bytes);
   if (team == 128) return launch_ls<128, false>(P, s, ws_bytes);
   return launch_ls<256, false>(P, s, ws_bytes);
+}
+
+int pmp_ls_columns(int mode, int team, int use_global, int lcap, int mcap, int ncap, int ncols,
+                   const int32_t* cols, int n, const int32_t* iptr, const int32_t* iidx,
+                   const int32_t* acolptr, const int32_t* arowidx, const double* avals,
+                   const int32_t* tcolptr, const int32_t* trowidx, const double* tvals,
+                   double* coef, double* resid, int32_t* flags, int32_t* msize,
+                   const int32_t* jptr, int32_t* jidx, void* ws, size_t ws_bytes, void* st) {
+  if (mode > 3) {
+    set_error("pmp_ls_columns: bad arguments (modes 4 / 5 need pmp_ls_columns_planned)");
+    return PMP_ERR_ARG;
+  }
+  return ls_columns(mode, team, use_global, lcap, mcap, ncap, ncols, cols, n, iptr, iidx, acolptr,
+                    arowidx, avals, tcolptr, trowidx, tvals, coef, resid, flags, msize, jptr, jidx,
+                    nullptr, nullptr, ws, ws_bytes, st);
+}
+
+int pmp_ls_columns_planned(int mode, int team, int use_global, int lcap, int mcap, int ncap,
+                           int ncols, const int32_t* cols, int n, const int32_t* iptr,
+                           const int32_t* iidx, const int32_t* acolptr, const int32_t* arowidx,
+                           const double* avals, const int32_t* tcolptr, const int32_t* trowidx,
+                           const double* tvals, double* coef, double* resid, int32_t* flags,
+                           int32_t* plan, const int32_t* plan_ptr, void* ws, size_t ws_bytes,
+                           void* st) {
+  if (mode != 4 && mode != 5) {
+    set_error("pmp_ls_columns_planned: mode must be 4 (record) or 5 (replay)");
+    return PMP_ERR_ARG;
+  }
+  return ls_columns(mode, team, use_global, lcap, mcap, ncap, ncols, cols, n, iptr, iidx, acolptr,
+                    arowidx, avals, tcolptr, trowidx, tvals, coef, resid, flags, nullptr, nullptr,
+                    nullptr, plan, plan_ptr, ws, ws_bytes, st);
 }
 
 size_t pmp_augment_team_bytes(int lcap) { return aug_team_bytes(lcap); }

@@ -353,6 +353,11 @@ def _plan(pattern, sys_colptr, sys_rowidx, t_colptr, t_rowidx, t_key, sys_key, c
                   ws.numel() if ws is not None else 0, st)
     m = msize.cpu().numpy().astype(np.int64)[cols]
     tiers = _split_tiers(cols, lcap, m, nI)
+    # per-column sizes of a symbolic plan record (pmp_ls_columns_planned)
+    pos = {int(c): i for i, c in enumerate(cols)} if cols_host is not None else None
+    for t in tiers:
+        idx = t.cols_host if pos is None else np.array([pos[int(c)] for c in t.cols_host])
+        t.plan_sizes = 4 + nI[idx] + 2 * L[idx]
     if key is not None:
         pattern.cache[key] = tiers
     return tiers
@@ -412,6 +417,19 @@ def _run_tiers(tiers, pattern, A_csc, T_csc, coef, resid, flags, mode=0, jptr=No
         glob = t.glob if tmode == t.mode else 0
         team = t.team
         ws = _ws_for(glob, tb, t.ncols)
+        if tmode == 0 and _plan_ok(t):
+            # record the symbolic work on the first solve of this tier, replay
+            # it on every later one (same structures, new values)
+            pmode = 5 if t.plan_ready else 4
+            _abi.call("pmp_ls_columns_planned", pmode, team, glob, t.lcap, t.mcap, t.ncap,
+                      t.ncols, _abi.ptr(t.cols), pattern.n, _abi.ptr(pattern.iptr),
+                      _abi.ptr(pattern.iidx), _abi.ptr(acolptr), _abi.ptr(arowidx),
+                      _abi.ptr(avals), _abi.ptr(tcolptr), _abi.ptr(trowidx), _abi.ptr(tvals),
+                      _abi.ptr(coef), _abi.ptr(resid), _abi.ptr(flags), _abi.ptr(t.plan),
+                      _abi.ptr(t.plan_ptr), _abi.ptr(ws), ws.numel() if ws is not None else 0,
+                      st)
+            t.plan_ready = True
+            continue
         _abi.call("pmp_ls_columns", tmode, team, glob, t.lcap, t.mcap, t.ncap, t.ncols,
                   _abi.ptr(t.cols), pattern.n, _abi.ptr(pattern.iptr), _abi.ptr(pattern.iidx),
                   _abi.ptr(acolptr), _abi.ptr(arowidx), _abi.ptr(avals), _abi.ptr(tcolptr),
@@ -434,6 +452,32 @@ def _run_tiers(tiers, pattern, A_csc, T_csc, coef, resid, flags, mode=0, jptr=No
                       _abi.ptr(avals), _abi.ptr(tcolptr), _abi.ptr(trowidx), _abi.ptr(tvals),
                       _abi.ptr(coef), _abi.ptr(resid), _abi.ptr(flags), None, None, None,
                       _abi.ptr(ws), ws.numel(), st)
+
+
+# symbolic plan records: per-column int32 records up to this many ints per tier
+_PLAN_MAX_INTS = 1 << 30
+USE_LS_PLANS = __import__("os").environ.get("PMP_LS_PLANS", "1") != "0"
+
+
+def _plan_ok(t):
+    """Allocate (once) the plan record of a dense-QR tier; False when the
+    tier cannot use one (sizes beyond the record's 16-bit fields, too big)."""
+    if not USE_LS_PLANS or t.mode != 0 or getattr(t, "plan_sizes", None) is None:
+        return False
+    if getattr(t, "plan", None) is not None:
+        return True
+    if t.mcap >= 65536 or t.ncap >= 32768:
+        return False
+    sizes = np.asarray(t.plan_sizes, dtype=np.int64)
+    total = int(sizes.sum())
+    if total <= 0 or total >= _PLAN_MAX_INTS:
+        return False
+    ptr = np.zeros(sizes.size, dtype=np.int64)
+    ptr[1:] = np.cumsum(sizes)[:-1]
+    t.plan_ptr = i32(ptr)
+    t.plan = torch.empty(total, dtype=torch.int32, device=_dev())
+    t.plan_ready = False
+    return True
 
 
 def _get_tiers(pattern, system, target, cols_host=None):

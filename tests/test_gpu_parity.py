@@ -463,3 +463,31 @@ def test_solve_batch_matches_single(pm, name):
                 rel = np.linalg.norm(B - A @ Xn, axis=0) / np.linalg.norm(B, axis=0)
                 assert np.all(rel <= 1e-8), rel
                 assert abs(float(np.max(rep.final_residuals)) - rel.max()) <= 1e-9
+
+
+def test_ls_plan_replay_bitwise(pm):
+    """SPAI / update columns solved from a recorded symbolic plan (second and
+    later builds on the same structures) are bitwise the first build's."""
+    from paper_1809_06574_b200 import spai
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(2, scale=12)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pts = W.points()
+    A1 = model.assemble(*pts[0])
+    P1, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))        # records
+    P1b, _ = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))       # replays
+    assert torch.equal(P1.matrix.vals, P1b.matrix.vals)
+    outs = []
+    for pt in pts[1:4]:
+        A = model.assemble(*pt)
+        Pu, su = pm.update_first(A1, A, P1, pm.UpdateConfig(pattern_level=0))
+        saved = spai.USE_LS_PLANS
+        spai.USE_LS_PLANS = False
+        try:
+            Pr, sr = pm.update_first(A1, A, P1, pm.UpdateConfig(pattern_level=0))
+        finally:
+            spai.USE_LS_PLANS = saved
+        assert torch.equal(Pu.q.vals, Pr.q.vals)
+        assert np.array_equal(np.asarray(su.residuals), np.asarray(sr.residuals))
+        outs.append(Pu)
