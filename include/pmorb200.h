@@ -365,6 +365,18 @@ typedef struct PmpSolveBatch {
   size_t oV, oC, oU, oW, oT0, oT1, oQ1, oXt, oR, oDX, oRB, oZ, oPart, oGout, oSbuf, oProj, oLog,
       oAux;
   int pBmat, pHb, pCq, pY, pRes, pBn, pHist;
+  /* queue of systems: d_sys holds nsys descriptors; `groups` block groups
+   * solve them, each taking the next unsolved system when it finishes one
+   * (d_queue: one int32 of scratch, reset by the call).  Per system i:
+   * d_result[8 i + 0..6] = status (0 ok, 10 host fallback), fallback reason,
+   * iterations, columns still active (0 = converged), residual-log rows,
+   * matvec count, preconditioner-apply count; d_result_log[i (1 + log_cap s)]
+   * = algorithmic HBM bytes of its block steps, then the residual log
+   * (log rows x s, row-major). */
+  int nsys;
+  int32_t* d_queue;
+  int32_t* d_result;
+  double* d_result_log;
   void* stream;
 } PmpSolveBatch;
 int pmp_solve_geometry(int n, int s, int cap, int kc, int inner_restart, int groups, int* gsz,

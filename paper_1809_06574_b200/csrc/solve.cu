@@ -53,6 +53,10 @@ struct SolveArgs {
       oAux;
   int pBmat, pHb, pCq, pY, pRes, pBn, pHist;  // offsets inside the projected-state block
   unsigned long long* dbg;  // diagnostics (group 0): stamps at (32 it + phase) * 2 + block
+  int nsys, groups;          // systems in the queue, concurrent block groups
+  int* queue;                // next-system counter (zeroed at launch)
+  int* rint;                 // nsys x PMP_SOLVE_RSZ ints: per-system record
+  double* rdbl;              // nsys x (1 + log_cap * s): algorithmic bytes, residual log
 };
 
 // solve-level int state (after the cycle-level [0, 144))
@@ -67,8 +71,13 @@ enum {
   kGbar = 151,
   kFold = 152,
   kReason = 153,  // fallback reason: 1 cycle-start QR, 2/3 inner status 4/5, 4/5 fold
+  kNext = 154,    // the group's next system (taken from the queue by the control block)
   kAct = 160,  // active columns (<= 16)
 };
+
+// per-system record (PmpSolveBatch::d_result): status, reason, iterations,
+// active columns left, log rows, matvecs, preconditioner applies
+enum { rStatus = 0, rReason, rIt, rNa, rLogRows, rMatvecs, rPrec, PMP_SOLVE_RSZ = 8 };
 
 constexpr int PMP_SOLVE_OK = 0, PMP_SOLVE_FALLBACK = 10;
 
@@ -135,7 +144,6 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   const bool ctl = lb == 0;
   const bool lead = lb == 1;
   const int wi = lb - 1, nw = A.gsz - 1;
-  const SysDesc D = A.sys[grp];
   double* ws = A.ws + (size_t)grp * A.wsz;
   int* ist = A.ist + (size_t)grp * A.isz;
   const int n = A.n, s = A.s, cap = A.cap, kc = A.kc;
@@ -184,6 +192,15 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   // became an L2 round trip
   __shared__ CycleArgs L;
   __shared__ int acts[16];
+  WBar wb{ist + 9, nw, 0, wi};
+  WBar gb{ist + kGbar, A.gsz, 0, lb};
+  const int slot = lb;  // partial slot of a worker (1 .. nw)
+
+  // groups take systems from a queue: the first `groups` statically, the
+  // rest in completion order (no group idles while a launch has systems
+  // left; a launch lasts ~ the mean, not the max, of its solves)
+  for (int sys = grp; sys < A.nsys;) {
+  const SysDesc D = A.sys[sys];
   if (threadIdx.x == 0) {
   L.n = n;
   L.s = s;
@@ -231,10 +248,6 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   }
   __syncthreads();
 
-  WBar wb{ist + 9, nw, 0, wi};
-  WBar gb{ist + kGbar, A.gsz, 0, lb};
-  const int slot = lb;  // partial slot of a worker (1 .. nw)
-
   // ---- setup: X = Xt = 0, R = B, column norms of B -----------------------------
   if (!ctl) {
     for (int q = threadIdx.x; q < nr * s; q += kOrthT) {
@@ -265,6 +278,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       ist[kLogRows] = 1;
       ist[kMatvecs] = 0;
       ist[kPrec] = 0;
+      ist[kReason] = 0;
     }
   }
   gbar(gb);
@@ -737,6 +751,29 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
     sstamp(A, grp, cyc, 8);
     ++cyc;
   }
+
+  // ---- system done: its record, then the next system from the queue ------------
+  gbar(gb);
+  if (lead) {
+    int* rec = A.rint + (size_t)sys * PMP_SOLVE_RSZ;
+    double* rd = A.rdbl + (size_t)sys * (1 + (size_t)A.log_cap * s);
+    const int lr = ldv(ist + kLogRows);
+    if (threadIdx.x == 0) {
+      rec[rStatus] = ldv(ist + kStatus);
+      rec[rReason] = ldv(ist + kReason);
+      rec[rIt] = ldv(ist + kIt);
+      rec[rNa] = ldv(ist + kNa);
+      rec[rLogRows] = lr;
+      rec[rMatvecs] = ldv(ist + kMatvecs);
+      rec[rPrec] = ldv(ist + kPrec);
+      rd[0] = __ldcg(aux + 48);
+    }
+    for (int q = threadIdx.x; q < lr * s; q += kOrthT) rd[1 + q] = __ldcg(logp + q);
+  }
+  if (ctl && threadIdx.x == 0) ist[kNext] = A.groups + atomicAdd(A.queue, 1);
+  gbar(gb);
+  sys = ldv(ist + kNext);
+  }
 }
 
 }  // namespace pmp
@@ -790,7 +827,8 @@ int pmp_solve_geometry(int n, int s, int cap, int kc, int restart, int groups, i
 }
 
 int pmp_solve_batch(PmpSolveBatch* b) {
-  if (!b || b->groups < 1 || b->s < 1 || b->s > 16 || 
+  if (!b || b->groups < 1 || b->nsys < 1 || !b->d_queue || !b->d_result || !b->d_result_log ||
+      b->s < 1 || b->s > 16 || 
       b->inner_restart + b->s > 96 || b->outer_dim < 0 || b->outer_dim + b->s > b->kc) {
     set_error("pmp_solve_batch: bad arguments");
     return PMP_ERR_ARG;
@@ -809,7 +847,7 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   }
   void* fn = solve_kernel(b->s, cached);
   const int occ = prepare_smem(fn, smem, kOrthT);
-  if (occ * (orth_max_grid() / 2) < gsz * b->groups) {
+  if (occ * (orth_max_grid() / 2) < gsz * (b->groups < b->nsys ? b->groups : b->nsys)) {
     set_error("pmp_solve_batch: grid not co-resident (%d blocks/SM)", occ);
     return PMP_ERR_ARG;
   }
@@ -858,8 +896,16 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   A.pBn = b->pBn;
   A.pHist = b->pHist;
   A.dbg = cycle_dbg_take();
+  A.nsys = b->nsys;
+  A.groups = b->groups < b->nsys ? b->groups : b->nsys;
+  A.queue = b->d_queue;
+  A.rint = b->d_result;
+  A.rdbl = b->d_result_log;
+  if (cudaMemsetAsync(A.queue, 0, sizeof(int), reinterpret_cast<cudaStream_t>(b->stream)) !=
+      cudaSuccess)
+    return cuda_status("pmp_solve_batch");
   void* args[] = {&A};
-  cudaError_t e = coop_launch(fn, gsz * b->groups, args, smem,
+  cudaError_t e = coop_launch(fn, gsz * A.groups, args, smem,
                               reinterpret_cast<cudaStream_t>(b->stream));
   if (e != cudaSuccess) {
     set_error("pmp_solve_batch: %s", cudaGetErrorString(e));

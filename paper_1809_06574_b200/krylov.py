@@ -1109,10 +1109,12 @@ class _SolveBatchArgs(ctypes.Structure):
                                        "oDX", "oRB", "oZ", "oPart", "oGout", "oSbuf", "oProj",
                                        "oLog", "oAux")] + [
         (f, ctypes.c_int) for f in ("pBmat", "pHb", "pCq", "pY", "pRes", "pBn", "pHist")] + [
-        ("stream", ctypes.c_void_p)]
+        ("nsys", ctypes.c_int), ("d_queue", ctypes.c_void_p), ("d_result", ctypes.c_void_p),
+        ("d_result_log", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
 _SOLVE_ISZ = 256
+_SOLVE_RSZ = 8       # ints per system record (PmpSolveBatch::d_result)
 _SOLVE_FALLBACK = 10
 # reason code -> count of systems handed back to the host path (diagnostics:
 # 1 cycle-start QR needs deflation, 2 projected problem rank deficient,
@@ -1146,18 +1148,21 @@ def _solve_layout(n, s, cap, kc, gsz, hist_cap, log_cap):
 
 def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     """Solve A_i X_i = B for every (A_i, P_i) in ``systems`` (krylov.py:105-275
-    for each), ``groups`` systems at a time in one persistent kernel
-    (pmp_solve_batch).  B is an n x s CUDA tensor shared by all systems.
-    Returns [(X_i, SolveReport_i)] in order.  Systems the device path hands
-    back (status 10: deflation / rank-deficient projected problem / an
-    ambiguous drop test) are re-solved on the host-driven path."""
+    for each) in ONE persistent kernel (pmp_solve_batch): ``groups`` block
+    groups share the GPU, each solving one system at a time and taking the
+    next unsolved one from a device queue when it finishes.  B is an n x s
+    CUDA tensor shared by all systems.  Returns [(X_i, SolveReport_i)] in
+    order.  Systems the device path hands back (status 10: deflation /
+    rank-deficient projected problem / an ambiguous drop test) are
+    re-solved on the host-driven path."""
     cfg = cfg or SolverConfig()
     Bd = _block_to_dev(B)
     n, s = Bd.shape
     if not systems:
         return []
+    nsys = len(systems)
     groups = groups or BATCH_GROUPS
-    groups = max(1, min(groups, len(systems)))
+    groups = max(1, min(groups, nsys))
     L = _abi.lib()
     cap = cfg.inner_restart + 2 * s + 2
     kc = cfg.outer_space_dim + s
@@ -1188,10 +1193,12 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     sc = scratch()
     ws = sc.get("solve_ws", 8 * wsz * groups).view(torch.float64)
     ist = sc.get("solve_ist", 4 * _SOLVE_ISZ * groups).view(torch.int32)
-    sysd = (_SysDesc * groups)()
+    rlen = 1 + log_cap * s
+    rint = sc.get("solve_rint", 4 * (_SOLVE_RSZ * nsys + 1)).view(torch.int32)
+    rdbl = sc.get("solve_rdbl", 8 * rlen * nsys).view(torch.float64)
+    sysd = (_SysDesc * nsys)()
     d_sys = torch.empty(ctypes.sizeof(sysd), dtype=torch.uint8, device=dev)
     h_sys = torch.empty(ctypes.sizeof(sysd), dtype=torch.uint8, pin_memory=True)
-    h_ist = torch.empty(_SOLVE_ISZ * groups, dtype=torch.int32, pin_memory=True)
     args = _SolveBatchArgs()
     args.n, args.s, args.cap, args.kc = n, s, cap, kc
     args.outer_dim, args.inner_restart, args.max_iters = (cfg.outer_space_dim,
@@ -1204,72 +1211,77 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
         setattr(args, k_, v)
     for k_, v in poff.items():
         setattr(args, k_, v)
+    args.nsys = nsys
+    args.d_result = rint.data_ptr()
+    args.d_queue = rint.data_ptr() + 4 * _SOLVE_RSZ * nsys
+    args.d_result_log = rdbl.data_ptr()
     args.stream = _abi.stream()
-    out = [None] * len(systems)
-    fallback = []
     stream = torch.cuda.current_stream()
-    for b0 in range(0, len(systems), groups):
-        chunk = list(range(b0, min(len(systems), b0 + groups)))
-        ng = len(chunk)
-        Xs = []
-        keep = []   # device operands must outlive the launch
-        for g, i in enumerate(chunk):
-            A, P = systems[i]
-            A = _as_dev_csr(A)
-            keep.append(A)
-            st = A.structure
-            d = sysd[g]
-            d.nfac = len(chains[i])
-            for j, F in enumerate(chains[i]):
-                fs = F.structure
-                d.fac_rowptr[j] = fs.rowptr.data_ptr()
-                d.fac_colidx[j] = fs.colidx.data_ptr()
-                d.fac_vals[j] = F.vals.data_ptr()
-            d.a_rowptr, d.a_colidx, d.a_vals = (st.rowptr.data_ptr(), st.colidx.data_ptr(),
-                                                A.vals.data_ptr())
-            X = torch.empty(n, s, dtype=torch.float64, device=dev)
-            Xs.append(X)
-            d.B, d.X = Bd.data_ptr(), X.data_ptr()
-        ctypes.memmove(h_sys.data_ptr(), ctypes.addressof(sysd), ctypes.sizeof(sysd))
-        d_sys.copy_(h_sys, non_blocking=True)
-        ist.zero_()
-        args.groups = ng
-        if _abi._counting:
-            _abi.COUNTERS["pmp_solve_batch"] = _abi.COUNTERS.get("pmp_solve_batch", 0) + 1
-        if _abi._timing_names and "pmp_solve_batch" in _abi._timing_names:
-            ea = torch.cuda.Event(enable_timing=True)
-            eb = torch.cuda.Event(enable_timing=True)
-            ea.record()
-            _abi.check(L.pmp_solve_batch(ctypes.byref(args)), "pmp_solve_batch")
-            eb.record()
-            _abi._timed.setdefault("pmp_solve_batch", []).append((ea, eb, (n, s, ng)))
+    Xs = []
+    keep = []   # device operands must outlive the launch
+    for i, (A, P) in enumerate(systems):
+        A = _as_dev_csr(A)
+        keep.append(A)
+        st = A.structure
+        d = sysd[i]
+        d.nfac = len(chains[i])
+        for j, F in enumerate(chains[i]):
+            fs = F.structure
+            d.fac_rowptr[j] = fs.rowptr.data_ptr()
+            d.fac_colidx[j] = fs.colidx.data_ptr()
+            d.fac_vals[j] = F.vals.data_ptr()
+        d.a_rowptr, d.a_colidx, d.a_vals = (st.rowptr.data_ptr(), st.colidx.data_ptr(),
+                                            A.vals.data_ptr())
+        X = torch.empty(n, s, dtype=torch.float64, device=dev)
+        Xs.append(X)
+        d.B, d.X = Bd.data_ptr(), X.data_ptr()
+    ctypes.memmove(h_sys.data_ptr(), ctypes.addressof(sysd), ctypes.sizeof(sysd))
+    d_sys.copy_(h_sys, non_blocking=True)
+    ist.zero_()
+    if _abi._counting:
+        _abi.COUNTERS["pmp_solve_batch"] = _abi.COUNTERS.get("pmp_solve_batch", 0) + 1
+    if _abi._timing_names and "pmp_solve_batch" in _abi._timing_names:
+        ea = torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
+        ea.record()
+        _abi.check(L.pmp_solve_batch(ctypes.byref(args)), "pmp_solve_batch")
+        eb.record()
+        _abi._timed.setdefault("pmp_solve_batch", []).append((ea, eb, (n, s, nsys)))
+    else:
+        _abi.check(L.pmp_solve_batch(ctypes.byref(args)), "pmp_solve_batch")
+    h_rint = torch.empty(_SOLVE_RSZ * nsys, dtype=torch.int32, pin_memory=True)
+    h_rint.copy_(rint[:_SOLVE_RSZ * nsys], non_blocking=True)
+    stream.synchronize()
+    recs = h_rint.numpy().reshape(nsys, _SOLVE_RSZ).copy()
+    out = [None] * nsys
+    fallback = []
+    done = []
+    for i in range(nsys):
+        if recs[i, 0] == _SOLVE_FALLBACK:
+            fallback.append(i)
+            FALLBACK_REASONS[int(recs[i, 1])] = FALLBACK_REASONS.get(int(recs[i, 1]), 0) + 1
         else:
-            _abi.check(L.pmp_solve_batch(ctypes.byref(args)), "pmp_solve_batch")
-        h_ist.copy_(ist.view(-1)[:_SOLVE_ISZ * groups], non_blocking=True)
-        logs = []
-        stream.synchronize()
-        hi = h_ist.numpy()
-        for g, i in enumerate(chunk):
-            st = hi[g * _SOLVE_ISZ:(g + 1) * _SOLVE_ISZ]
-            if st[147] == _SOLVE_FALLBACK:
-                fallback.append(i)
-                FALLBACK_REASONS[int(st[153])] = FALLBACK_REASONS.get(int(st[153]), 0) + 1
-                continue
-            rows_ = int(st[148])
-            base = g * wsz + off["oLog"]
-            logs.append((g, i, rows_, base))
-        for g, i, rows_, base in logs:
-            st = hi[g * _SOLVE_ISZ:(g + 1) * _SOLVE_ISZ]
+            done.append(i)
+    if done:
+        # one gather + one D2H for every solved system's bytes and residual log
+        rv = rdbl[:rlen * nsys].view(nsys, rlen)
+        parts = [rv[i, :1 + int(recs[i, 4]) * s] for i in done]
+        flat = torch.cat(parts).cpu().numpy()
+        o = 0
+        for i in done:
+            rows_ = int(recs[i, 4])
+            seg = flat[o:o + 1 + rows_ * s]
+            o += seg.size
             rep = SolveReport()
-            hist = ws[base:base + rows_ * s].view(rows_, s).cpu().numpy()
+            hist = seg[1:].reshape(rows_, s)
             rep.residual_history = [row.copy() for row in hist]
-            rep.iterations = int(st[146])
-            rep.converged = int(st[144]) == 0
-            rep.matvec_count = int(st[149])
-            rep.precond_apply_count = int(st[150])
+            rep.iterations = int(recs[i, 2])
+            rep.converged = int(recs[i, 3]) == 0
+            rep.matvec_count = int(recs[i, 5])
+            rep.precond_apply_count = int(recs[i, 6])
             rep.device_launches = 1
-            rep.algorithmic_bytes = float(ws[g * wsz + off["oAux"] + 48].item())
-            out[i] = (Xs[g], rep)
+            rep.algorithmic_bytes = float(seg[0])
+            out[i] = (Xs[i], rep)
     for i in fallback:
         A, P = systems[i]
         out[i] = block_gcro_solve(A, Bd, P=P, cfg=cfg)

@@ -83,8 +83,11 @@ class _UnionTerms:
         if not self.symmetric:
             self.structure.csc()
 
-    def run(self, recipe, mode, s):
-        """recipe: list of (term index, group, first, coef)."""
+    def run(self, recipe, mode, s, zc=None):
+        """recipe: list of (term index, group, first, coef).  With ``zc`` (a
+        one-element int32 device slice, zeroed by the caller) the exact-zero
+        count is left there and no host synchronisation happens: the caller
+        checks it and calls ``finish``."""
         st = self.structure
         nt = len(recipe)
         ptrs = (ctypes_array_vp([self.vals[t].data_ptr() for t, _, _, _ in recipe]))
@@ -93,8 +96,10 @@ class _UnionTerms:
         first = np.array([f for _, _, f, _ in recipe], dtype=np.int32)
         coef = np.array([c for _, _, _, c in recipe], dtype=np.float64)
         out = torch.empty(max(st.nnz, 1), dtype=torch.float64, device=_dev())[:st.nnz]
-        zc = scratch().get("zero_count", 4, zero=False)[:4].view(torch.int32)
-        zc.zero_()
+        deferred = zc is not None
+        if not deferred:
+            zc = scratch().get("zero_count", 4, zero=False)[:4].view(torch.int32)
+            zc.zero_()
         perm = out_perm = None
         if not self.symmetric:
             perm = st.csc()[2]
@@ -103,10 +108,15 @@ class _UnionTerms:
                   first.ctypes.data, coef.ctypes.data, mode, float(s), _abi.ptr(self.rowid),
                   _abi.ptr(st.colidx), _abi.ptr(out), _abi.ptr(perm), _abi.ptr(out_perm),
                   _abi.ptr(zc), _abi.stream())
-        nz = int(zc.item())
-        if nz:
-            return _compacted(st, out)
-        A = DeviceCSR(st, out, symmetric=self.symmetric)
+        if deferred:
+            return (out, out_perm)
+        return self.finish((out, out_perm), int(zc.item()))
+
+    def finish(self, raw, zero_count):
+        out, out_perm = raw
+        if zero_count:
+            return _compacted(self.structure, out)
+        A = DeviceCSR(self.structure, out, symmetric=self.symmetric)
         if out_perm is not None:
             A._csc_vals = out_perm
         return A
@@ -193,6 +203,27 @@ class SecondOrderModel:
     def assemble(self, s, pvals):
         """(s^2 M(p) + s D(p)) + K(p) as a device CSR, bit-identical to the
         reference's canonical CSR (rpmor.py:92-107)."""
+        u, recipe, s = self._recipe(s, pvals)
+        return u.run(recipe, 0, s)
+
+    def assemble_many(self, points):
+        """assemble(s, p) for every (s, p) in ``points`` with ONE host
+        synchronisation (the exact-zero counts of all systems are read
+        together), so a window of systems is enqueued without stalling the
+        device between them."""
+        points = list(points)
+        if not points:
+            return []
+        zc = torch.zeros(len(points), dtype=torch.int32, device=_dev())
+        raws = []
+        for i, (s, p) in enumerate(points):
+            u, recipe, sv = self._recipe(s, p)
+            raws.append(u.run(recipe, 0, sv, zc=zc[i:i + 1]))
+        counts = zc.cpu().numpy()
+        u = self._union()
+        return [u.finish(r, int(c)) for r, c in zip(raws, counts)]
+
+    def _recipe(self, s, pvals):
         if self.family is not None:
             raise ValueError("affine-form models are evaluated at expansion points; "
                              "use family.evaluate")
@@ -209,7 +240,7 @@ class SecondOrderModel:
                 if c != 0:
                     recipe.append((t + i + 1, g, 0, c))
             t += len(ts)
-        return u.run(recipe, 0, s)
+        return u, recipe, s
 
 
 class AffineFamily:

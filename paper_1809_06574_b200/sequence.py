@@ -144,8 +144,23 @@ def gather_records(records, n_systems, group=None):
 # the driver
 # ---------------------------------------------------------------------------
 
+# HBM budget for one solve window (operators + preconditioner factors + X)
+WINDOW_BYTES = int(__import__("os").environ.get("PMP_WINDOW_BYTES", str(24 << 30)))
+
+
+def _window_systems(model, B):
+    """Systems per solve window: every system's A (values), its update factor
+    (indices + values) and X stay resident until the window's launch ends."""
+    n, s = B.shape
+    nnz = getattr(model, "union_nnz", None)
+    if nnz is None:
+        nnz = 27 * n
+    per = 8 * nnz + 12 * nnz + 8 * n * s + 64 * n
+    return max(1, WINDOW_BYTES // per)
+
 def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, rank=0, world=1,
-                 group=None, keep_solutions=False, timing=True, workers=1, batch=None):
+                 group=None, keep_solutions=False, timing=True, workers=1, batch=None,
+                 window=None):
     """Run the whole parametric sequence; returns (records, info).
 
     records: one dict per system this rank owns (index, sigma, p, label,
@@ -155,10 +170,13 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     the number of SPAI / update columns built.
 
     batch > 1 (the default, PMP_BATCH_GROUPS; first-approach / independent
-    policies): systems are assembled and preconditioned ``batch`` at a time
-    and each chunk is solved by ONE persistent device launch, one block
-    group per system (block_gcro_solve_batch).  batch=1 keeps the per-system
-    path below.
+    policies): a window of systems is assembled and preconditioned (all
+    launches asynchronous, no host synchronisation), then solved by ONE
+    persistent device launch in which ``batch`` block groups take the
+    window's systems from a device queue (block_gcro_solve_batch).  The
+    window is every remaining system, capped so the window's operators,
+    preconditioners and solutions stay under WINDOW_BYTES of HBM (``window``
+    overrides).  batch=1 keeps the per-system path below.
 
     workers > 1 (first-approach / independent policies): after the initial
     system (and one update that warms the plan caches), the remaining
@@ -249,22 +267,27 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
         todo = [i for i in mine if not (sharded and i == 0)]
         if sharded and 0 in mine:
             do_system(0)
-        for c0 in range(0, len(todo), batch):
-            chunk = todo[c0:c0 + batch]
+        if window is None:
+            window = _window_systems(model, Bd)
+        window = max(batch, int(window))
+        for c0 in range(0, len(todo), window):
+            chunk = todo[c0:c0 + window]
             built = []
-            for idx in chunk:
-                s, p = points[idx]
-                t0 = mark()
-                A = model.assemble(s, p)
-                t1 = mark()
+            t0 = mark()
+            As = model.assemble_many([points[idx] for idx in chunk])
+            t1 = mark()
+            for j, (idx, A) in enumerate(zip(chunk, As)):
+                ta = mark()
                 P, _, label, _ = seq.for_system(A)
                 t2 = mark()
-                built.append((idx, A, P, label, t0, t1, t2))
+                # (the window's assembly is one phase: charge it to the first system)
+                built.append((idx, A, P, label, t0 if j == 0 else ta, t1 if j == 0 else ta, t2,
+                              ta))
             t3 = mark()
-            res = block_gcro_solve_batch([(A, P) for _, A, P, _, _, _, _ in built], Bd,
+            res = block_gcro_solve_batch([(b[1], b[2]) for b in built], Bd,
                                          cfg=solver_cfg, groups=batch)
             t4 = mark()
-            for (idx, A, P, label, t0, t1, t2), (X, rep) in zip(built, res):
+            for (idx, A, P, label, t0, t1, t2, ta), (X, rep) in zip(built, res):
                 s, p = points[idx]
                 rec = {"index": idx, "sigma": float(s), "p": [float(v) for v in p],
                        "label": label, "iterations": rep.iterations,
@@ -279,8 +302,9 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                 records.append(rec)
                 state["build_cols"] += A.n if P is not None else 0
                 if timing:
-                    phases["assemble"].append((t0, t1))
-                    phases["build"].append((t1, t2))
+                    if t0 is not ta:
+                        phases["assemble"].append((t0, t1))
+                    phases["build"].append((ta, t2))
             if timing:
                 phases["solve"].append((t3, t4))
         mine = []
