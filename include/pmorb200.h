@@ -138,6 +138,25 @@ int pmp_ls_columns_planned(int mode, int team, int use_global, int lcap, int mca
                            int32_t* d_flags, int32_t* d_plan, const int32_t* d_plan_ptr,
                            void* d_ws, size_t ws_bytes, void* stream);
 
+/* Several systems that share the plan's structures (the SPAI updates of a
+ * parameter sweep: same pattern, same A_l structure, same target A1):
+ * system q's values are h_avals[q], its outputs h_coef[q] / h_resid[q] /
+ * h_flags[q] -- HOST arrays of nsys DEVICE pointers.  mode 4 records the
+ * plan on system 0 and replays it for the others, mode 5 replays for all.
+ * Small columns (the segmented register tier: |J| <= 32, |I| <= 15) are
+ * solved for up to PMP_LS_MAX_SYSTEMS systems per launch; other tiers one
+ * launch per system.  Results are bitwise those of pmp_ls_columns_planned
+ * per system. */
+#define PMP_LS_MAX_SYSTEMS 64
+int pmp_ls_columns_multi(int mode, int team, int use_global, int lcap, int mcap, int ncap,
+                         int ncols, const int32_t* d_cols, int n, const int32_t* d_iptr,
+                         const int32_t* d_iidx, const int32_t* d_acolptr,
+                         const int32_t* d_arowidx, int nsys, const double* const* h_avals,
+                         const int32_t* d_tcolptr, const int32_t* d_trowidx,
+                         const double* d_tvals, double* const* h_coef, double* const* h_resid,
+                         int32_t* const* h_flags, int32_t* d_plan, const int32_t* d_plan_ptr,
+                         void* d_ws, size_t ws_bytes, void* stream);
+
 /* ---- level-1 augmentation (_augmented_column, spai.py:210-222) ----------
  * Weights w_r = sum over k ascending of |a_rk| |a_kj| (no FMA; scipy's
  * csc_matmat order); candidates outside the base support

@@ -18,6 +18,7 @@ from .model import AffineFamily, SecondOrderModel, evaluate, pmor_l_sequence
 from .sequence import PrecondPolicy, SequencePreconditioner, run_sequence
 from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, spai_build,
                    spai_column, spai_pattern)
-from .update import UpdateConfig, SequenceStep, sequence_precondition, update_first, update_second
+from .update import (UpdateConfig, SequenceStep, sequence_precondition, update_first,
+                     update_first_many, update_second)
 
 __version__ = "0.1.0"

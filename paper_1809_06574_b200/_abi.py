@@ -40,6 +40,9 @@ _SIGS = {
     "pmp_pattern_l0": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_pattern_l0_ptr": ([c_int, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_ls_team_bytes": ([c_int, c_int, c_int, c_int], c_sz),
+    "pmp_ls_columns_multi": ([c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp,
+                              c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                              c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_ls_bound": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_ls_columns": ([c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp,
                         c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
@@ -198,9 +201,21 @@ def count_launches(enable=True, timed=()):
     _timed.clear()
 
 
+def lib_seg_enabled():
+    """The library's segmented least-squares tier is on (PMP_LS_REG != 0)."""
+    return os.environ.get("PMP_LS_REG", "1")[:1] != "0"
+
+
+def note_launches(k):
+    """Record launches an ABI call made beyond one (calls whose launch count
+    depends on their arguments, e.g. pmp_ls_columns_multi)."""
+    if _counting:
+        COUNTERS["_extra"] = COUNTERS.get("_extra", 0) + int(k)
+
+
 def launches():
-    return sum(_LAUNCHES_PER_CALL.get(k, 1) * v for k, v in COUNTERS.items()
-               if k not in _NO_LAUNCH)
+    return sum((1 if k == "_extra" else _LAUNCHES_PER_CALL.get(k, 1)) * v
+               for k, v in COUNTERS.items() if k not in _NO_LAUNCH)
 
 
 def timed_events():

@@ -20,6 +20,7 @@
 // (columns whose dense block exceeds shared memory).  All reductions are
 // fixed-order, so results are bitwise reproducible.
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -27,7 +28,7 @@ namespace pmp {
 
 struct LsParams {
   int mode;  // 0 solve, 1 plan (|J|), 2 export J, 3 SNE, 4 solve + record the
-             // symbolic plan, 5 solve from a recorded plan
+             // symbolic plan, 5 solve from a recorded plan, 6 record only
   int ncols;
   const int* cols;
   int n;
@@ -54,6 +55,18 @@ struct LsParams {
   // target entries (value index -1 for the identity target)
   int* plan;
   const int* plan_ptr;
+};
+
+// several systems sharing the plan's structures (segmented tier): their
+// values and outputs, passed by value in the kernel parameters (no device
+// pointer arrays); nsys <= 1 uses LsParams' avals / coef / resid / flags
+constexpr int kLsMaxSys = PMP_LS_MAX_SYSTEMS;
+struct LsMulti {
+  int nsys;
+  const double* avals[kLsMaxSys];
+  double* coef[kLsMaxSys];
+  double* resid[kLsMaxSys];
+  int* flags[kLsMaxSys];
 };
 
 // team memory layout --------------------------------------------------------
@@ -234,6 +247,133 @@ __device__ inline int gather_sorted_rows(const LsParams& P, int j, const LsMem& 
   return L;
 }
 
+// rank (gelsy rcond = eps) and the minimum-norm / back-substituted solution
+// of the factored column block M (ld mm, R on top, Q^T t in column n):
+// z -> m.w (original support order), rank -> m.misc[1].  Warp 0 works.
+template <int T>
+__device__ void ls_rank_solve(const LsMem& m, double* M, int mm, int n, int K, int tid) {
+  if (tid < 32) {
+    const int lane = tid;
+    int r = 0;
+    const double r00 = K > 0 ? fabs(M[0]) : 0.0;
+    if (r00 > 0.0) {
+      r = 1;
+      while (r < K && fabs(M[r + (size_t)r * mm]) > DBL_EPSILON * r00) ++r;
+    }
+    double* y = m.z;  // y[0..n)
+    for (int i = lane; i < n; i += 32) y[i] = (i < r) ? M[i + (size_t)n * mm] : 0.0;
+    __syncwarp();
+    if (r < n) {
+      // RZ: annihilate R[i, r:n] for i = r-1 .. 0 (dtzrzf)
+      for (int i = r - 1; i >= 0; --i) {
+        double s2 = 0.0;
+        for (int c = r + lane; c < n; c += 32) {
+          double v = M[i + (size_t)c * mm];
+          s2 += v * v;
+        }
+        s2 = warp_sum(s2);
+        double alpha = M[i + (size_t)i * mm];
+        double tz = 0.0, scal = 0.0, beta = alpha;
+        if (s2 > 0.0) {
+          beta = -copysign(hypot(alpha, sqrt(s2)), alpha);
+          tz = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        __syncwarp();
+        if (tz != 0.0) {
+          for (int c = r + lane; c < n; c += 32) M[i + (size_t)c * mm] *= scal;
+          __syncwarp();
+          if (lane == 0) M[i + (size_t)i * mm] = beta;
+          // rows l < i: w = R[l,i] + sum_c R[l,c] v_c
+          for (int l = lane; l < i; l += 32) {
+            double wl = M[l + (size_t)i * mm];
+            for (int c = r; c < n; ++c) wl += M[l + (size_t)c * mm] * M[i + (size_t)c * mm];
+            M[l + (size_t)i * mm] -= tz * wl;
+            for (int c = r; c < n; ++c) M[l + (size_t)c * mm] -= tz * wl * M[i + (size_t)c * mm];
+          }
+        }
+        if (lane == 0) m.tau[i] = tz;
+        __syncwarp();
+      }
+    }
+    // back substitution on the leading r x r triangle (column oriented)
+    for (int k = r - 1; k >= 0; --k) {
+      double zk = y[k] / M[k + (size_t)k * mm];
+      __syncwarp();
+      if (lane == 0) y[k] = zk;
+      for (int i = lane; i < k; i += 32) y[i] -= M[i + (size_t)k * mm] * zk;
+      __syncwarp();
+    }
+    if (r < n) {
+      // x = H_{r-1} ... H_0 [y; 0]
+      for (int i = 0; i < r; ++i) {
+        double tz = m.tau[i];
+        if (tz == 0.0) continue;
+        double s = 0.0;
+        for (int c = r + lane; c < n; c += 32) s += M[i + (size_t)c * mm] * y[c];
+        s = warp_sum(s) + y[i];
+        __syncwarp();
+        if (lane == 0) y[i] -= tz * s;
+        for (int c = r + lane; c < n; c += 32) y[c] -= tz * s * M[i + (size_t)c * mm];
+        __syncwarp();
+      }
+    }
+    // un-permute into w[] (original support order)
+    for (int k = lane; k < n; k += 32) m.w[m.perm[k]] = y[k];
+    if (lane == 0) m.misc[1] = r;
+  }
+}
+
+// explicit residual t - A(J, I) z (spai.py:252) and the column's outputs;
+// the caller synchronised the team after the solve
+template <int T>
+__device__ void ls_residual_store(const LsParams& P, const LsMem& m, const int* J, int mm, int n,
+                                  int i0, int j, int t0, int tl, int tot, const int* ent,
+                                  int tid) {
+  Team<T> tm{tid, m.red};
+  const int rank = m.misc[1];
+  double* res = m.M;  // reuse
+  for (int i = tid; i < mm; i += T) res[i] = 0.0;
+  tm.sync();
+  if (ent) {
+    // same updates in the same order, positions from the plan
+    for (int q = tid; q < tl; q += T) {
+      const int e = ent[2 * (tot + q)];
+      res[ent[2 * (tot + q) + 1] & 0xffff] = e < 0 ? 1.0 : P.tvals[e];
+    }
+    tm.sync();
+    for (int c = 0; c < n; ++c) {
+      const double zc = m.w[c];
+      for (int q = m.off[c] + tid; q < m.off[c + 1]; q += T)
+        res[ent[2 * q + 1] & 0xffff] -= P.avals[ent[2 * q]] * zc;
+      tm.sync();
+    }
+  } else {
+    for (int q = tid; q < tl; q += T) {
+      int r = (t0 < 0) ? j : P.trowidx[t0 + q];
+      res[lower_bound_i(J, mm, r)] = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
+    }
+    tm.sync();
+    for (int c = 0; c < n; ++c) {
+      const double zc = m.w[c];
+      const int k = m.sup[c];
+      const int lo = P.acolptr[k], hi = P.acolptr[k + 1];
+      for (int e = lo + tid; e < hi; e += T)
+        res[lower_bound_i(J, mm, P.arowidx[e])] -= P.avals[e] * zc;
+      tm.sync();
+    }
+  }
+  double part = 0.0;
+  for (int i = tid; i < mm; i += T) part += res[i] * res[i];
+  const double rn2 = tm.sum(part);
+  for (int c = tid; c < n; c += T) P.coef[i0 + c] = m.w[c];
+  if (tid == 0) {
+    P.resid[j] = sqrt(rn2);
+    P.flags[j] = (rank < n) ? 1 : 0;
+  }
+  tm.sync();
+}
+
 template <int T>
 __device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid) {
   LsMem m = ls_carve(mem, P.lcap, P.mcap, P.ncap);
@@ -351,6 +491,7 @@ __device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid
     }
   }
   tm.sync();
+  if (P.mode == 6) return;  // symbolic record only (the register tier solves)
 
   // ---- column-pivoted Householder QR ----------------------------------------
   const int K = mm < n ? mm : n;
@@ -436,121 +577,9 @@ __device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid
     }
   }
 
-  // ---- rank (gelsy rcond = eps) and solve: warp 0 ---------------------------
-  if (tid < 32) {
-    const int lane = tid;
-    int r = 0;
-    const double r00 = K > 0 ? fabs(M[0]) : 0.0;
-    if (r00 > 0.0) {
-      r = 1;
-      while (r < K && fabs(M[r + (size_t)r * mm]) > DBL_EPSILON * r00) ++r;
-    }
-    double* y = m.z;  // y[0..n)
-    for (int i = lane; i < n; i += 32) y[i] = (i < r) ? M[i + (size_t)n * mm] : 0.0;
-    __syncwarp();
-    if (r < n) {
-      // RZ: annihilate R[i, r:n] for i = r-1 .. 0 (dtzrzf)
-      for (int i = r - 1; i >= 0; --i) {
-        double s2 = 0.0;
-        for (int c = r + lane; c < n; c += 32) {
-          double v = M[i + (size_t)c * mm];
-          s2 += v * v;
-        }
-        s2 = warp_sum(s2);
-        double alpha = M[i + (size_t)i * mm];
-        double tz = 0.0, scal = 0.0, beta = alpha;
-        if (s2 > 0.0) {
-          beta = -copysign(hypot(alpha, sqrt(s2)), alpha);
-          tz = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
-        }
-        __syncwarp();
-        if (tz != 0.0) {
-          for (int c = r + lane; c < n; c += 32) M[i + (size_t)c * mm] *= scal;
-          __syncwarp();
-          if (lane == 0) M[i + (size_t)i * mm] = beta;
-          // rows l < i: w = R[l,i] + sum_c R[l,c] v_c
-          for (int l = lane; l < i; l += 32) {
-            double wl = M[l + (size_t)i * mm];
-            for (int c = r; c < n; ++c) wl += M[l + (size_t)c * mm] * M[i + (size_t)c * mm];
-            M[l + (size_t)i * mm] -= tz * wl;
-            for (int c = r; c < n; ++c) M[l + (size_t)c * mm] -= tz * wl * M[i + (size_t)c * mm];
-          }
-        }
-        if (lane == 0) m.tau[i] = tz;
-        __syncwarp();
-      }
-    }
-    // back substitution on the leading r x r triangle (column oriented)
-    for (int k = r - 1; k >= 0; --k) {
-      double zk = y[k] / M[k + (size_t)k * mm];
-      __syncwarp();
-      if (lane == 0) y[k] = zk;
-      for (int i = lane; i < k; i += 32) y[i] -= M[i + (size_t)k * mm] * zk;
-      __syncwarp();
-    }
-    if (r < n) {
-      // x = H_{r-1} ... H_0 [y; 0]
-      for (int i = 0; i < r; ++i) {
-        double tz = m.tau[i];
-        if (tz == 0.0) continue;
-        double s = 0.0;
-        for (int c = r + lane; c < n; c += 32) s += M[i + (size_t)c * mm] * y[c];
-        s = warp_sum(s) + y[i];
-        __syncwarp();
-        if (lane == 0) y[i] -= tz * s;
-        for (int c = r + lane; c < n; c += 32) y[c] -= tz * s * M[i + (size_t)c * mm];
-        __syncwarp();
-      }
-    }
-    // un-permute into w[] (original support order)
-    for (int k = lane; k < n; k += 32) m.w[m.perm[k]] = y[k];
-    if (lane == 0) m.misc[1] = r;
-  }
+  ls_rank_solve<T>(m, M, mm, n, K, tid);
   tm.sync();
-  const int rank = m.misc[1];
-
-  // ---- explicit residual t - A(J, I) z (spai.py:252) -------------------------
-  double* res = M;  // reuse
-  for (int i = tid; i < mm; i += T) res[i] = 0.0;
-  tm.sync();
-  if (ent) {
-    // same updates in the same order, positions from the plan
-    for (int q = tid; q < tl; q += T) {
-      const int e = ent[2 * (tot + q)];
-      res[ent[2 * (tot + q) + 1] & 0xffff] = e < 0 ? 1.0 : P.tvals[e];
-    }
-    tm.sync();
-    for (int c = 0; c < n; ++c) {
-      const double zc = m.w[c];
-      for (int q = m.off[c] + tid; q < m.off[c + 1]; q += T)
-        res[ent[2 * q + 1] & 0xffff] -= P.avals[ent[2 * q]] * zc;
-      tm.sync();
-    }
-  } else {
-    for (int q = tid; q < tl; q += T) {
-      int r = (t0 < 0) ? j : P.trowidx[t0 + q];
-      res[lower_bound_i(J, mm, r)] = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
-    }
-    tm.sync();
-    for (int c = 0; c < n; ++c) {
-      const double zc = m.w[c];
-      const int k = m.sup[c];
-      const int lo = P.acolptr[k], hi = P.acolptr[k + 1];
-      for (int e = lo + tid; e < hi; e += T)
-        res[lower_bound_i(J, mm, P.arowidx[e])] -= P.avals[e] * zc;
-      tm.sync();
-    }
-  }
-  double part = 0.0;
-  for (int i = tid; i < mm; i += T) part += res[i] * res[i];
-  const double rn2 = tm.sum(part);
-  for (int c = tid; c < n; c += T) P.coef[i0 + c] = m.w[c];
-  if (tid == 0) {
-    P.resid[j] = sqrt(rn2);
-    P.flags[j] = (rank < n) ? 1 : 0;
-  }
-  tm.sync();
+  ls_residual_store<T>(P, m, J, mm, n, i0, j, t0, tl, tot, ent, tid);
 }
 
 template <int T, bool GLOBAL>
@@ -563,6 +592,315 @@ __global__ void k_ls(LsParams P) {
   for (int c = blockIdx.x * per_block + team; c < P.ncols; c += gridDim.x * per_block) {
     const int j = P.cols ? P.cols[c] : c;
     ls_column<T>(P, j, c, mem, tid);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Segmented register tier for columns with a plan (modes 4 / 5) whose dense
+// block is small: |J| <= MR rows, |I| < SEG columns (c1 13 x 5, c2/c4 25 x 7,
+// their boundary columns).  A warp solves 32 / SEG columns at once, one
+// SEG-lane segment per column and ONE LANE PER COLUMN of [A(J, I) | t]:
+// lane c keeps column c (all its rows) in registers, so norms, reflector
+// applications and updates are lane-local FMA chains; only the pivot choice
+// (3-4 shuffle steps) and the reflector broadcast (one shuffle per row) cross
+// lanes.  Same algorithm as ls_column: column pivoting on the trailing norms
+// (largest, earliest position on ties), LAPACK dlarfg reflectors, rank by
+// |R_kk| > eps |R_00|, column-oriented back substitution, explicit residual
+// over the original block in the original support order.  Columns that turn
+// out rank deficient (or |J| < |I|) are finished by the whole warp with the
+// team-memory RZ code (ls_rank_solve / ls_residual_store).
+//
+// Several systems per launch (nsys > 1): problem g = sys * ncols + c solves
+// column c of the shared plan against system sys's values (sys_avals[sys])
+// into sys_coef / sys_resid / sys_flags[sys] -- one launch builds the SPAI
+// updates of a whole window of systems that share their structures.
+// ---------------------------------------------------------------------------
+
+// double reciprocal / square root without libm slow-path calls: hardware
+// approximations refined by Newton steps to ~1 ulp (finite, normal inputs)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+__device__ __forceinline__ double sqrt_nr(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  const double s = x * r;
+  return fma(fma(-s, s, x), 0.5 * r, s);
+}
+
+template <int MR, int SEG>
+struct SegLayout {
+  static constexpr int kTile = MR * SEG + 8;  // original block [MR][SEG] (+pad: bank spread)
+  // R rows 0..SEG-1 (ld SEG; the reflector buffer during the QR), then z /
+  // Q^T t (SEG), the position -> column map (SEG ints), +1 pad so the
+  // segments' broadcast reads fall in different banks
+  static constexpr int kRyMain = SEG * SEG > MR ? SEG * SEG : MR;
+  static constexpr int kRy = kRyMain + SEG + SEG / 2 + 1;
+  static constexpr int kPPW = 32 / SEG;
+  __host__ __device__ static size_t gen_bytes() { return ls_team_bytes(1, MR, SEG); }
+  __host__ __device__ static size_t warp_bytes() {
+    return align16((size_t)kPPW * (kTile + kRy) * sizeof(double) + 16) + gen_bytes();
+  }
+};
+
+template <int MR, int SEG>
+__global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMulti S) {
+  using Lay = SegLayout<MR, SEG>;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int PPW = Lay::kPPW;
+  extern __shared__ __align__(16) char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int seg = lane / SEG, sl = lane % SEG;
+  char* wmem = smem + (size_t)wid * Lay::warp_bytes();
+  double* A = reinterpret_cast<double*>(wmem) + (size_t)seg * (Lay::kTile + Lay::kRy);
+  double* RY = A + Lay::kTile;
+  double* Z = RY + Lay::kRyMain;
+  int* wflag = reinterpret_cast<int*>(reinterpret_cast<double*>(wmem) +
+                                      (size_t)PPW * (Lay::kTile + Lay::kRy));
+  const LsMem gm = ls_carve(wmem + Lay::warp_bytes() - Lay::gen_bytes(), 1, MR, SEG);
+
+  const int nsys = S.nsys > 0 ? S.nsys : 1;
+  const long long total = (long long)P.ncols * nsys;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + wid) * PPW; base < total;
+       base += nwarps * PPW) {
+    const long long g = base + seg;
+    const bool valid = g < total;
+    int sys = 0, c = 0;
+    if (valid) {
+      sys = (int)(g / P.ncols);
+      c = (int)(g - (long long)sys * P.ncols);
+    }
+    const double* avals = nsys > 1 ? S.avals[sys] : P.avals;
+    double* coef = nsys > 1 ? S.coef[sys] : P.coef;
+    double* resid = nsys > 1 ? S.resid[sys] : P.resid;
+    int* flags = nsys > 1 ? S.flags[sys] : P.flags;
+    int j = 0, i0 = 0, n = 0, mm = 0, tot = 0, tl = 0, t0 = -1;
+    const int* pl = nullptr;
+    if (valid) {
+      j = P.cols ? P.cols[c] : c;
+      i0 = P.iptr[j];
+      n = P.iptr[j + 1] - i0;
+      pl = P.plan + P.plan_ptr[c];
+      mm = pl[0];
+      tot = pl[1];
+      tl = pl[2];
+      t0 = P.tcolptr ? P.tcolptr[j] : -1;
+    }
+    const bool degen = valid && (n == 0 || mm == 0);
+    bool fast = valid && !degen;
+    const int* ent = fast ? pl + 4 + n : nullptr;
+
+    // ---- original block [A(J, I) | t] -> tile (row-major, ld SEG) -> registers
+    if (fast)
+      for (int i = 0; i < mm; ++i) A[i * SEG + sl] = 0.0;
+    __syncwarp();
+    if (fast)
+      for (int q = sl; q < tot + tl; q += SEG) {
+        const int e = ent[2 * q], pc = ent[2 * q + 1];
+        A[(pc & 0xffff) * SEG + (pc >> 16)] =
+            q < tot ? avals[e] : (e < 0 ? 1.0 : P.tvals[e]);
+      }
+    __syncwarp();
+    double a[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) a[i] = (fast && i < mm) ? A[i * SEG + sl] : 0.0;
+    const bool iscol = fast && sl < n;
+    const bool isrhs = fast && sl == n;
+    int mypos = sl;  // current position of this lane's column (pivoting)
+    const int K = mm < n ? mm : n;
+
+    // ---- column-pivoted Householder QR ------------------------------------
+#pragma unroll
+    for (int k = 0; k < SEG - 1; ++k) {
+      const bool act = fast && k < K;
+      // trailing norms over rows k.. (rows > k summed first: the pivot's
+      // dlarfg needs that part alone)
+      double sgt = 0.0;
+#pragma unroll
+      for (int i = k + 1; i < MR; ++i) sgt += a[i] * a[i];
+      const bool cand = act && iscol && mypos >= k;
+      double bv = cand ? a[k] * a[k] + sgt : -1.0;
+      int bp = cand ? mypos : 0x7fffffff;
+      int bl = sl;
+#pragma unroll
+      for (int o = 1; o < SEG; o <<= 1) {
+        const double ov = __shfl_xor_sync(FULL, bv, o);
+        const int op = __shfl_xor_sync(FULL, bp, o);
+        const int ol = __shfl_xor_sync(FULL, bl, o);
+        if (ov > bv || (ov == bv && op < bp)) {
+          bv = ov;
+          bp = op;
+          bl = ol;
+        }
+      }
+      // swap positions k <-> bp
+      if (act) {
+        if (sl == bl)
+          mypos = k;
+        else if (iscol && mypos == k)
+          mypos = bp;
+      }
+      // dlarfg on the pivot lane's column, rows k..
+      double tau = 0.0, scal = 0.0;
+      if (act && sl == bl) {
+        const double alpha = a[k];
+        if (sgt > 0.0) {
+          // (call-free sqrt / reciprocal: a libm slow-path call here would
+          // spill the register-resident column around every step)
+          const double beta = -copysign(sqrt_nr(fma(alpha, alpha, sgt)), alpha);
+          tau = (beta - alpha) * rcp_nr(beta);
+          scal = rcp_nr(alpha - beta);
+          a[k] = beta;
+        }
+        if (tau != 0.0) {
+#pragma unroll
+          for (int i = k + 1; i < MR; ++i) a[i] *= scal;
+        }
+      }
+      tau = __shfl_sync(FULL, tau, seg * SEG + bl);
+      // the reflector v (rows > k) -> the segment's broadcast buffer
+      if (act && sl == bl) {
+#pragma unroll
+        for (int i = k + 1; i < MR; ++i) RY[i] = a[i];
+      }
+      __syncwarp();
+      // w = a[k] + sum_{i > k} v_i a[i];  a -= tau w v  (columns right of the
+      // pivot and the right-hand side)
+      if (act && tau != 0.0 && ((iscol && mypos > k) || isrhs)) {
+        double w = 0.0;
+#pragma unroll
+        for (int i = k + 1; i < MR; ++i) w += RY[i] * a[i];
+        w += a[k];
+        a[k] -= tau * w;
+        // re-read v (volatile) instead of holding all of it in registers:
+        // that doubles the live set and spills the column
+        const volatile double* vv = RY;
+#pragma unroll
+        for (int i = k + 1; i < MR; ++i) a[i] -= tau * w * vv[i];
+      }
+      __syncwarp();
+    }
+
+    // ---- R, Q^T t -> smem; rank and back substitution (segment leader) ------
+    if (iscol) {
+#pragma unroll
+      for (int i = 0; i < SEG - 1; ++i)
+        if (i < n) RY[i * SEG + mypos] = a[i];
+      reinterpret_cast<int*>(Z + SEG)[mypos] = sl;
+    }
+    if (isrhs) {
+#pragma unroll
+      for (int i = 0; i < SEG - 1; ++i)
+        if (i < n) Z[i] = a[i];
+    }
+    __syncwarp();
+    if (fast && sl == 0) {
+      int r = 0;
+      const double r00 = K > 0 ? fabs(RY[0]) : 0.0;
+      if (r00 > 0.0) {
+        r = 1;
+        while (r < K && fabs(RY[r * SEG + r]) > DBL_EPSILON * r00) ++r;
+      }
+      if (r == n) {
+        for (int k = r - 1; k >= 0; --k) {
+          const double zk = Z[k] / RY[k * SEG + k];
+          Z[k] = zk;
+          for (int i = 0; i < k; ++i) Z[i] -= RY[i * SEG + k] * zk;
+        }
+      } else {
+        fast = false;  // (leader only; shared below)
+      }
+      wflag[seg] = fast ? 0 : 1;
+    }
+    __syncwarp();
+    if (valid && !degen) fast = wflag[seg] == 0;
+
+    // ---- coefficients (original support order) and the explicit residual
+    //      t - A(J, I) z over the original block, columns in support order --
+    double zo = 0.0;
+    if (fast && iscol) zo = Z[mypos];
+    __syncwarp();
+    if (fast && iscol) {
+      RY[sl] = zo;
+      coef[i0 + sl] = zo;
+    }
+    if (degen)
+      for (int q = sl; q < n; q += SEG) coef[i0 + q] = 0.0;
+    __syncwarp();
+    double part = 0.0;
+    if (fast) {
+      for (int i = sl; i < mm; i += SEG) {
+        double res = A[i * SEG + n];
+        for (int cc = 0; cc < n; ++cc) res -= A[i * SEG + cc] * RY[cc];
+        part += res * res;
+      }
+    } else if (degen) {
+      for (int q = sl; q < tl; q += SEG) {
+        const double v = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
+        part += v * v;
+      }
+    }
+#pragma unroll
+    for (int o = SEG >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    if ((fast || degen) && sl == 0) {
+      resid[j] = sqrt(part);
+      flags[j] = 0;
+    }
+
+    // ---- rank-deficient columns: the whole warp, team-memory RZ path --------
+    // (from the segment's R rows and Q^T t in shared memory: the RZ solve
+    // reads rows < |I| only, the residual the plan and the values)
+    const bool defic = valid && !degen && !fast;
+    unsigned need = __ballot_sync(FULL, defic && sl == 0);
+    while (need) {
+      const int L = __ffs(need) - 1;
+      need &= need - 1;
+      const int ss = L / SEG;
+      const int mm_s = __shfl_sync(FULL, mm, L), n_s = __shfl_sync(FULL, n, L);
+      const int K_s = mm_s < n_s ? mm_s : n_s;
+      const int i0_s = __shfl_sync(FULL, i0, L), j_s = __shfl_sync(FULL, j, L);
+      const int t0_s = __shfl_sync(FULL, t0, L), tl_s = __shfl_sync(FULL, tl, L);
+      const int tot_s = __shfl_sync(FULL, tot, L), sys_s = __shfl_sync(FULL, sys, L);
+      const int* pl_s = reinterpret_cast<const int*>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(pl), L));
+      __syncwarp();
+      const double* RYs = reinterpret_cast<double*>(wmem) + (size_t)ss * (Lay::kTile + Lay::kRy) +
+                          Lay::kTile;
+      const double* Zs = RYs + Lay::kRyMain;
+      const int* perm_s = reinterpret_cast<const int*>(Zs + SEG);
+      const int rows_s = K_s;
+      for (int q = lane; q < rows_s * n_s; q += 32) {
+        const int i = q % rows_s, cq = q / rows_s;
+        gm.M[i + cq * mm_s] = RYs[i * SEG + cq];
+      }
+      for (int q = lane; q < rows_s; q += 32) gm.M[q + n_s * mm_s] = Zs[q];
+      for (int q = lane; q < n_s; q += 32) gm.perm[q] = perm_s[q];
+      for (int q = lane; q <= n_s; q += 32) gm.off[q] = pl_s[3 + q];
+      __syncwarp();
+      LsParams Q = P;
+      if (nsys > 1) {
+        Q.avals = S.avals[sys_s];
+        Q.coef = S.coef[sys_s];
+        Q.resid = S.resid[sys_s];
+        Q.flags = S.flags[sys_s];
+      }
+      ls_rank_solve<32>(gm, gm.M, mm_s, n_s, K_s, lane);
+      __syncwarp();
+      ls_residual_store<32>(Q, gm, nullptr, mm_s, n_s, i0_s, j_s, t0_s, tl_s, tot_s,
+                            pl_s + 4 + n_s, lane);
+      __syncwarp();
+    }
   }
 }
 
@@ -999,6 +1337,16 @@ static int num_sms() {
   return g_num_sms;
 }
 
+// PMP_LS_REG=0 disables the register warp tier (A/B experiments)
+static bool ls_reg_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PMP_LS_REG");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on != 0;
+}
+
 template <int T, bool G>
 static int launch_ls(LsParams P, cudaStream_t st, size_t ws_bytes) {
   const size_t tb = P.team_bytes;
@@ -1024,6 +1372,31 @@ static int launch_ls(LsParams P, cudaStream_t st, size_t ws_bytes) {
     k_ls<T, false><<<grid, T * per_block, sm, st>>>(P);
   }
   return cuda_status("pmp_ls_columns");
+}
+
+template <int MR, int SEG>
+static int launch_seg(const LsParams& P, const LsMulti& S, cudaStream_t st) {
+  const size_t wb = SegLayout<MR, SEG>::warp_bytes();
+  const size_t sm = 8 * wb;
+  prepare_smem((const void*)k_ls_seg<MR, SEG>, sm, 256);
+  const long long total = (long long)P.ncols * (S.nsys > 0 ? S.nsys : 1);
+  const long long per_block = 8LL * (32 / SEG);
+  long long grid = (total + per_block - 1) / per_block;
+  const long long cap = (long long)num_sms() * 64;
+  if (grid > cap) grid = cap;
+  k_ls_seg<MR, SEG><<<(int)grid, 256, sm, st>>>(P, S);
+  return cuda_status("pmp_ls_columns");
+}
+
+static int launch_ls_seg(const LsParams& P, const LsMulti& S, int mcap, int ncap,
+                         cudaStream_t st) {
+  if (ncap <= 7) return mcap <= 16 ? launch_seg<16, 8>(P, S, st) : launch_seg<32, 8>(P, S, st);
+  return mcap <= 16 ? launch_seg<16, 16>(P, S, st) : launch_seg<32, 16>(P, S, st);
+}
+
+static bool seg_eligible(int mode, int team, int use_global, int mcap, int ncap) {
+  return (mode == 4 || mode == 5) && team == 32 && !use_global && mcap <= 32 && ncap <= 15 &&
+         ls_reg_enabled();
 }
 
 template <int T, bool G>
@@ -1136,6 +1509,20 @@ static int ls_columns(int mode, int team, int use_global, int lcap, int mcap, in
     }
     return cuda_status("pmp_ls_columns");
   }
+  if (seg_eligible(mode, team, use_global, mcap, ncap)) {
+    // small columns with a plan: segmented register tier.  A recording call
+    // first records the plan only (mode 6), so the first and every replayed
+    // build of a structure compute bitwise the same numbers.
+    if (mode == 4) {
+      P.mode = 6;
+      const int rc = launch_ls<32, false>(P, s, ws_bytes);
+      if (rc != PMP_OK) return rc;
+    }
+    P.mode = 5;
+    LsMulti S;
+    S.nsys = 1;
+    return launch_ls_seg(P, S, mcap, ncap, s);
+  }
   if (use_global) {
     if (team == 32) return launch_ls<32, true>(P, s, ws_bytes);
     if (team == 128) return launch_ls<128, true>(P, s, ws_bytes);
@@ -1175,6 +1562,88 @@ int pmp_ls_columns_planned(int mode, int team, int use_global, int lcap, int mca
   return ls_columns(mode, team, use_global, lcap, mcap, ncap, ncols, cols, n, iptr, iidx, acolptr,
                     arowidx, avals, tcolptr, trowidx, tvals, coef, resid, flags, nullptr, nullptr,
                     nullptr, plan, plan_ptr, ws, ws_bytes, st);
+}
+
+int pmp_ls_columns_multi(int mode, int team, int use_global, int lcap, int mcap, int ncap,
+                         int ncols, const int32_t* cols, int n, const int32_t* iptr,
+                         const int32_t* iidx, const int32_t* acolptr, const int32_t* arowidx,
+                         int nsys, const double* const* h_avals, const int32_t* tcolptr,
+                         const int32_t* trowidx, const double* tvals, double* const* h_coef,
+                         double* const* h_resid, int32_t* const* h_flags, int32_t* plan,
+                         const int32_t* plan_ptr, void* ws, size_t ws_bytes, void* st) {
+  if ((mode != 4 && mode != 5) || nsys < 0 || (nsys > 0 && (!h_avals || !h_coef || !h_resid ||
+                                                            !h_flags))) {
+    set_error("pmp_ls_columns_multi: bad arguments (mode=%d nsys=%d)", mode, nsys);
+    return PMP_ERR_ARG;
+  }
+  if (nsys == 0 || ncols == 0) return PMP_OK;
+  int first = 0;
+  if (mode == 4 || !seg_eligible(mode, team, use_global, mcap, ncap)) {
+    // record on the first system (or no segmented tier): one system per call
+    const int rc = ls_columns(mode, team, use_global, lcap, mcap, ncap, ncols, cols, n, iptr,
+                              iidx, acolptr, arowidx, h_avals[0], tcolptr, trowidx, tvals,
+                              h_coef[0], h_resid[0], h_flags[0], nullptr, nullptr, nullptr, plan,
+                              plan_ptr, ws, ws_bytes, st);
+    if (rc != PMP_OK) return rc;
+    first = 1;
+    if (!seg_eligible(5, team, use_global, mcap, ncap)) {
+      for (int q = 1; q < nsys; ++q) {
+        const int r2 = ls_columns(5, team, use_global, lcap, mcap, ncap, ncols, cols, n, iptr,
+                                  iidx, acolptr, arowidx, h_avals[q], tcolptr, trowidx, tvals,
+                                  h_coef[q], h_resid[q], h_flags[q], nullptr, nullptr, nullptr,
+                                  plan, plan_ptr, ws, ws_bytes, st);
+        if (r2 != PMP_OK) return r2;
+      }
+      return PMP_OK;
+    }
+  }
+  // the replays: segmented tier, up to PMP_LS_MAX_SYSTEMS systems per launch
+  LsParams P;
+  P.plan = plan;
+  P.plan_ptr = plan_ptr;
+  P.mode = 5;
+  P.ncols = ncols;
+  P.cols = cols;
+  P.n = n;
+  P.iptr = iptr;
+  P.iidx = iidx;
+  P.acolptr = acolptr;
+  P.arowidx = arowidx;
+  P.avals = nullptr;
+  P.tcolptr = tcolptr;
+  P.trowidx = trowidx;
+  P.tvals = tvals;
+  P.coef = nullptr;
+  P.resid = nullptr;
+  P.flags = nullptr;
+  P.msize = nullptr;
+  P.jptr = nullptr;
+  P.jidx = nullptr;
+  P.lcap = lcap;
+  P.mcap = mcap;
+  P.ncap = ncap;
+  P.team_bytes = 0;
+  P.gws = nullptr;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(st);
+  for (int q0 = first; q0 < nsys; q0 += kLsMaxSys) {
+    LsMulti S;
+    S.nsys = nsys - q0 < kLsMaxSys ? nsys - q0 : kLsMaxSys;
+    for (int q = 0; q < S.nsys; ++q) {
+      S.avals[q] = h_avals[q0 + q];
+      S.coef[q] = h_coef[q0 + q];
+      S.resid[q] = h_resid[q0 + q];
+      S.flags[q] = h_flags[q0 + q];
+    }
+    if (S.nsys == 1) {
+      P.avals = S.avals[0];
+      P.coef = S.coef[0];
+      P.resid = S.resid[0];
+      P.flags = S.flags[0];
+    }
+    const int rc = launch_ls_seg(P, S, mcap, ncap, s);
+    if (rc != PMP_OK) return rc;
+  }
+  return PMP_OK;
 }
 
 size_t pmp_augment_team_bytes(int lcap) { return aug_team_bytes(lcap); }

@@ -28,7 +28,7 @@ from .device import DeviceCSR, level0_pattern
 from . import krylov as _krylov
 from .krylov import SolverConfig, block_gcro_solve, block_gcro_solve_batch
 from .spai import Preconditioner, SpaiConfig, _factor_from_columns, spai_build
-from .update import UpdateConfig, update_first, update_second
+from .update import UpdateConfig, update_first, update_first_many, update_second
 
 PRECOND_KINDS = ("none", "spai", "spai-update-first", "spai-update-second")
 
@@ -80,6 +80,27 @@ class SequencePreconditioner:
             self._initial_system, self._initial_pre = A, P
         self._prev_system, self._prev_pre = A, P
         return P, seconds, label, stats
+
+    def for_systems(self, systems):
+        """for_system over a list; under the first approach the updates of
+        systems sharing a structure are built together (update_first_many,
+        bitwise the one-at-a-time results)."""
+        systems = list(systems)
+        out = []
+        if self.policy.kind == "spai-update-first" and systems:
+            if self._initial_pre is None:
+                out.append(self.for_system(systems[0]))
+                systems = systems[1:]
+            if systems:
+                t0 = time.perf_counter()
+                res = update_first_many(self._initial_system, systems, self._initial_pre,
+                                        self.policy.update)
+                seconds = (time.perf_counter() - t0) / len(systems)
+                for P, stats in res:
+                    out.append((P, seconds, "update-first", stats))
+                self._prev_system, self._prev_pre = systems[-1], res[-1][0]
+            return out
+        return [self.for_system(A) for A in systems]
 
 
 # ---------------------------------------------------------------------------
@@ -276,13 +297,15 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
             t0 = mark()
             As = model.assemble_many([points[idx] for idx in chunk])
             t1 = mark()
-            for j, (idx, A) in enumerate(zip(chunk, As)):
-                ta = mark()
-                P, _, label, _ = seq.for_system(A)
-                t2 = mark()
-                # (the window's assembly is one phase: charge it to the first system)
-                built.append((idx, A, P, label, t0 if j == 0 else ta, t1 if j == 0 else ta, t2,
-                              ta))
+            # (the window's assembly and its build are one phase each: charged
+            # to the window's first system)
+            pres = seq.for_systems(As)
+            t2 = mark()
+            for j, (idx, A, (P, _, label, _)) in enumerate(zip(chunk, As, pres)):
+                if j == 0:
+                    built.append((idx, A, P, label, t0, t1, t2, t1))
+                else:
+                    built.append((idx, A, P, label, None, None, None, None))
             t3 = mark()
             res = block_gcro_solve_batch([(b[1], b[2]) for b in built], Bd,
                                          cfg=solver_cfg, groups=batch)
@@ -301,9 +324,8 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                     rec["X"] = X
                 records.append(rec)
                 state["build_cols"] += A.n if P is not None else 0
-                if timing:
-                    if t0 is not ta:
-                        phases["assemble"].append((t0, t1))
+                if timing and t0 is not None:
+                    phases["assemble"].append((t0, t1))
                     phases["build"].append((ta, t2))
             if timing:
                 phases["solve"].append((t3, t4))

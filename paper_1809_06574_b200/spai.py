@@ -49,7 +49,9 @@ class BuildStats:
     """Per-column diagnostics of a build (spai.py:153-171).  Device results
     are copied to the host lazily, on first access."""
 
-    def __init__(self, resid=None, flags=None, augmented=0, t_events=None, seconds=None):
+    def __init__(self, resid=None, flags=None, augmented=0, t_events=None, seconds=None,
+                 share=1):
+        self._share = share   # builds that shared the timed interval
         self._resid = resid
         self._flags = flags
         self._aug = augmented
@@ -86,7 +88,7 @@ class BuildStats:
         if self._seconds is None and self._events is not None:
             a, b = self._events
             b.synchronize()
-            self._seconds = a.elapsed_time(b) / 1e3
+            self._seconds = a.elapsed_time(b) / 1e3 / self._share
         return float(self._seconds or 0.0)
 
     def summary(self):
@@ -561,6 +563,79 @@ def solve_columns(system, target, pattern, cfg, events=True):
         ev1.record()
     stats = BuildStats(resid, flags, n_aug, (ev0, ev1) if events else None)
     return P, stats, final_pat, final_coef
+
+
+def _seg_tier(t):
+    """Tier the library solves in the segmented register tier (several
+    systems per launch): small dense blocks, warp teams, shared memory."""
+    return t.mode == 0 and t.team == 32 and not t.glob and t.mcap <= 32 and t.ncap <= 15
+
+
+def solve_columns_many(systems, target, pattern, cfg):
+    """solve_columns for several systems that share one structure (the SPAI
+    updates of a parameter sweep), level 0: every least-squares tier is ONE
+    pmp_ls_columns_multi call -- the small-column tier solves every system
+    in one launch -- so a window of updates costs a handful of launches and
+    host calls instead of a few per system.  Bitwise the per-system result.
+    Returns [(factor DeviceCSR, BuildStats)] in order."""
+    systems = list(systems)
+    if (cfg.pattern_level >= 1 or len(systems) < 2 or not USE_LS_PLANS
+            or any(A.structure is not systems[0].structure for A in systems)):
+        out = []
+        for A in systems:
+            P, stats, _, _ = solve_columns(A, target, pattern, cfg)
+            out.append((P, stats))
+        return out
+    import ctypes
+    n = systems[0].n
+    k = len(systems)
+    st = _abi.stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    A0 = systems[0]
+    acolptr, arowidx, _ = A0.csc()
+    tcolptr = trowidx = tvals = None
+    if target is not None:
+        tcolptr, trowidx, tvals = target.csc()
+    tiers = _get_tiers(pattern, A0, target)
+    coefs = [torch.empty(max(pattern.nnz, 1), dtype=torch.float64, device=_dev())
+             for _ in range(k)]
+    resids = [torch.empty(n, dtype=torch.float64, device=_dev()) for _ in range(k)]
+    flags = [torch.zeros(n, dtype=torch.int32, device=_dev()) for _ in range(k)]
+    csc_vals = [A.csc()[2] for A in systems]
+    VP = ctypes.c_void_p * k
+    h_avals = VP(*[v.data_ptr() for v in csc_vals])
+    h_coef = VP(*[c.data_ptr() for c in coefs])
+    h_resid = VP(*[r.data_ptr() for r in resids])
+    h_flags = VP(*[f.data_ptr() for f in flags])
+    for t in tiers:
+        if t.mode != 0 or not _plan_ok(t):
+            for q, A in enumerate(systems):
+                _run_tiers([t], pattern, A.csc(), target.csc() if target is not None else None,
+                           coefs[q], resids[q], flags[q])
+            continue
+        pmode = 5 if t.plan_ready else 4
+        ws = _ws_for(t.glob, t.bytes, t.ncols)
+        _abi.call("pmp_ls_columns_multi", pmode, t.team, t.glob, t.lcap, t.mcap, t.ncap,
+                  t.ncols, _abi.ptr(t.cols), n, _abi.ptr(pattern.iptr), _abi.ptr(pattern.iidx),
+                  _abi.ptr(acolptr), _abi.ptr(arowidx), k, h_avals, _abi.ptr(tcolptr),
+                  _abi.ptr(trowidx), _abi.ptr(tvals), h_coef, h_resid, h_flags,
+                  _abi.ptr(t.plan), _abi.ptr(t.plan_ptr), _abi.ptr(ws),
+                  ws.numel() if ws is not None else 0, st)
+        if _seg_tier(t) and _abi.lib_seg_enabled():
+            first = 1 if pmode == 4 else 0
+            extra = (2 if pmode == 4 else 0) + -(-(k - first) // 64)
+        else:
+            extra = k + (1 if pmode == 4 else 0)
+        _abi.note_launches(extra - 1)
+        t.plan_ready = True
+    out = []
+    for q in range(k):
+        P = _factor_from_columns(pattern, coefs[q])
+        out.append((P, (resids[q], flags[q])))
+    ev1.record()
+    return [(P, BuildStats(r, f, 0, (ev0, ev1), share=k)) for P, (r, f) in out]
 
 
 def _merge(base, bcoef, apat, acoef):
