@@ -53,6 +53,16 @@ static __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+#ifndef PMP_SPMM_RPT
+#define PMP_SPMM_RPT 2
+#endif
+#ifndef PMP_SPMM_CH
+#define PMP_SPMM_CH 8
+#endif
+#ifndef PMP_BAR_ACQREL
+#define PMP_BAR_ACQREL 1
+#endif
+
 // Y[r][c] = sum_e vals[e] X[colidx[e]][c] for this block's rows r0 + [0, nr):
 // NY lanes per row (lane = column), RPT rows per thread, entries gathered CH
 // at a time with every index / value load issued before the X gathers.  X
@@ -63,7 +73,7 @@ template <int NY>
 __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ va, const double* X, int ldx, int sb,
                           double* Y, int ldy, int r0, int nr) {
-  constexpr int PER = kOrthT / NY, RPT = 4, CH = 4;
+  constexpr int PER = kOrthT / NY, RPT = PMP_SPMM_RPT, CH = PMP_SPMM_CH;
   const int c = threadIdx.x % NY, slot = threadIdx.x / NY;
   const bool col_ok = c < sb;
   for (int base = 0; base < nr; base += RPT * PER) {
@@ -410,12 +420,22 @@ struct WBar {
 static __device__ __forceinline__ void wbar(WBar& w) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    const int target = (w.epoch + 1) * w.n;
+#if PMP_BAR_ACQREL
+    // release the block's writes with the arrival, acquire everyone's with
+    // the final observation (no full fences)
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(w.ctr) : "memory");
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(w.ctr) : "memory");
+    } while (v < target);
+#else
     __threadfence();
     atomicAdd(w.ctr, 1);
-    const int target = (w.epoch + 1) * w.n;
     while (*(volatile int*)w.ctr < target) {
     }
     __threadfence();
+#endif
   }
   ++w.epoch;
   __syncthreads();

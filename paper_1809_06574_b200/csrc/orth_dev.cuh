@@ -14,6 +14,12 @@
 
 #include "common.cuh"
 
+#ifndef PMP_UPD_UNROLL
+#define PMP_UPD_UNROLL 8
+#endif
+#ifndef PMP_GRAM_BATCH
+#define PMP_GRAM_BATCH 8
+#endif
 #ifndef PMP_GRAM_INLINE
 #define PMP_GRAM_INLINE __forceinline__
 #endif
@@ -23,6 +29,7 @@ namespace pmp {
 namespace cg = cooperative_groups;
 
 constexpr int kOrthT = 256;
+constexpr int kUpdUnroll = PMP_UPD_UNROLL;
 constexpr double kCholRatio = 1e-5;
 constexpr double kSkipKappa = 4.0;
 
@@ -62,17 +69,18 @@ __device__ PMP_GRAM_INLINE void block_gram(const Rows X, int kx, const double* Y
     if (job < rounds * splits && t < kx) {
       const int per = (nrows + splits - 1) / splits;
       const int ra = sp * per, rb = min(nrows, ra + per);
-      // rows in batches of 4: the X loads of a batch are all in flight
+      // rows in batches of GB: the X loads of a batch are all in flight
       // before its FMAs (row order, hence the sums, unchanged)
       const double* xa = t < X.ka ? X.a + t : X.b + (t - X.ka);
       const int ldxr = t < X.ka ? X.lda : X.ldb;
       int r = ra;
-      for (; r + 4 <= rb; r += 4) {
-        double x[4];
+      constexpr int GB = PMP_GRAM_BATCH;
+      for (; r + GB <= rb; r += GB) {
+        double x[GB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = xa[(size_t)(r + u) * ldxr];
+        for (int u = 0; u < GB; ++u) x[u] = xa[(size_t)(r + u) * ldxr];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < GB; ++u) {
           const double* y = Y + (size_t)(r + u) * ldy;
 #pragma unroll
           for (int c = 0; c < NY; ++c)
@@ -172,7 +180,7 @@ __device__ PMP_GRAM_INLINE void block_update(const Rows X, int kx, double* Y, in
     // the two column segments separately (no per-element branch), unrolled
     // so several row loads are in flight
     const double* xa = X.a + (size_t)r * X.lda;
-#pragma unroll 4
+#pragma unroll kUpdUnroll
     for (int t = 0; t < ka; ++t) {
       const double x = xa[t];
       const double* g = G + t * ny;
@@ -181,7 +189,7 @@ __device__ PMP_GRAM_INLINE void block_update(const Rows X, int kx, double* Y, in
         if (c < ny) acc[c] += x * g[c];
     }
     const double* xb = X.b + (size_t)r * X.ldb - X.ka;
-#pragma unroll 4
+#pragma unroll kUpdUnroll
     for (int t = ka; t < kx; ++t) {
       const double x = xb[t];
       const double* g = G + t * ny;

@@ -102,6 +102,32 @@ __device__ __forceinline__ void sstamp(const SolveArgs& A, int grp, int cyc, int
 #endif
 }
 
+// d[c] = sum_{t < m} a[t] G[(ga + t) na + c] + sum_{t < kb} b[t] G[(gb + t) na + c]
+// for c < na: one row, all outputs (each a / b element loaded once); per
+// output the same summation order as the element-wise loop it replaces
+template <int NY>
+__device__ __forceinline__ void row_combo(const double* a, int m, int ga, const double* b, int kb,
+                                          int gb, const double* G, int na, double* d) {
+#pragma unroll
+  for (int c = 0; c < NY; ++c) d[c] = 0.0;
+#pragma unroll 4
+  for (int t = 0; t < m; ++t) {
+    const double x = a[t];
+    const double* g = G + (size_t)(ga + t) * na;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < na) d[c] += x * g[c];
+  }
+#pragma unroll 4
+  for (int t = 0; t < kb; ++t) {
+    const double x = b[t];
+    const double* g = G + (size_t)(gb + t) * na;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < na) d[c] += x * g[c];
+  }
+}
+
 // one row of [w | z] (columns keep[a], or 0..nk-1 when keep is null) times
 // T^-1 (upper, ld ldt) -> yw / yz; register arrays with static indices
 template <int NY>
@@ -522,21 +548,20 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         G[q] = __ldcg(Yg + (size_t)c * n1 + t);
       }
       __syncthreads();
-      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
-        const int r = q / na, c = q % na;
+      for (int r = threadIdx.x; r < nr; r += kOrthT) {
         const size_t row = (size_t)(r0 + r);
-        double d = 0.0;
         // (V rows from the block's shared-memory copy when cached)
         const double* vr = CACHED ? region + (size_t)r * A.ldx + k : V + row * cap;
-#pragma unroll 4
-        for (int t = 0; t < m; ++t) d += vr[t] * G[(k + t) * na + c];
-        const double* ur = U + row * kc;
-#pragma unroll 4
-        for (int t = 0; t < k; ++t) d += ur[t] * G[t * na + c];
-        DX[row * s + c] = d;
-        const double xt = Xt[row * s + acts[c]] + d;
-        Xt[row * s + acts[c]] = xt;
-        Z[row * s + c] = xt;
+        double d[NY];
+        row_combo<NY>(vr, m, k, U + row * kc, k, 0, G, na, d);
+#pragma unroll
+        for (int c = 0; c < NY; ++c)
+          if (c < na) {
+            DX[row * s + c] = d[c];
+            const double xt = Xt[row * s + acts[c]] + d[c];
+            Xt[row * s + acts[c]] = xt;
+            Z[row * s + c] = xt;
+          }
       }
       // Xa = P Z (factor chain right to left)
       const double* src = Z;
@@ -616,17 +641,15 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       // RB = V[:, :total] img_v + C[:, :k] img_c  (own rows)
       for (int q = threadIdx.x; q < (k + total) * na; q += kOrthT) G[q] = __ldcg(img + (size_t)(q / na) * s + q % na);
       __syncthreads();
-      for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
-        const int r = q / na, c = q % na;
+      for (int r = threadIdx.x; r < nr; r += kOrthT) {
         const size_t row = (size_t)(r0 + r);
-        double d = 0.0;
         const double* vr = CACHED ? region + (size_t)r * A.ldx + k : V + row * cap;
-#pragma unroll 4
-        for (int t = 0; t < total; ++t) d += vr[t] * G[(k + t) * na + c];
         const double* cr = CACHED ? region + (size_t)r * A.ldx : C + row * kc;
-#pragma unroll 4
-        for (int t = 0; t < k; ++t) d += cr[t] * G[t * na + c];
-        RB[row * s + c] = d;
+        double d[NY];
+        row_combo<NY>(vr, total, k, cr, k, 0, G, na, d);
+#pragma unroll
+        for (int c = 0; c < NY; ++c)
+          if (c < na) RB[row * s + c] = d[c];
       }
       __syncthreads();
       double* Wr = RB + (size_t)r0 * s;
