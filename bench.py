@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--workers", type=int, default=1,
                     help="host threads / CUDA streams driving independent systems "
                          "(per-system path, --batch 1)")
-    ap.add_argument("--batch", type=int, default=4,
+    ap.add_argument("--batch", type=int, default=6,
                     help="systems per persistent solve launch (1 = per-system path)")
     return ap.parse_args()
 

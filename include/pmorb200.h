@@ -59,6 +59,19 @@ int pmp_assemble(int nnz, int nterms, const double* const* h_term_vals, const in
                  const int32_t* h_group, const int32_t* h_first, const double* h_coef, int mode,
                  double s, const int32_t* d_rowid, const int32_t* d_colidx, double* d_out,
                  const int32_t* d_perm, double* d_out_perm, int32_t* d_zero_count, void* stream);
+/* Several systems of one recipe shape at once (a parameter sweep: the same
+ * terms, groups and opening terms; system q's coefficients are
+ * h_coef[q * nterms + t] and its shift h_s[q]).  Every term value is read
+ * once for all systems; system q's result goes to h_out[q] (and, with
+ * d_perm, permuted to h_out_perm[q]) -- HOST arrays of device pointers --
+ * and its exact-zero count is added to d_zero_counts[q].  Bit-identical to
+ * nsys pmp_assemble calls. */
+int pmp_assemble_multi(int nnz, int nterms, const double* const* h_term_vals,
+                       const int32_t* h_kind, const int32_t* h_group, const int32_t* h_first,
+                       int nsys, const double* h_coef, const double* h_s, int mode,
+                       const int32_t* d_rowid, const int32_t* d_colidx, double* const* h_out,
+                       const int32_t* d_perm, double* const* h_out_perm,
+                       int32_t* d_zero_counts, void* stream);
 
 /* Drop entries whose value is exactly 0.0 (as_csr eliminate_zeros,
  * sparsecore.py:43).  Output arrays have capacity nnz; d_out_rowptr[n]

@@ -30,6 +30,8 @@ _SIGS = {
     "pmp_version": ([], c_int),
     "pmp_assemble": ([c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_dbl, c_vp, c_vp, c_vp,
                       c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_assemble_multi": ([c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_int,
+                            c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_compact_workspace": ([c_int], c_sz),
     "pmp_compact_zeros": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_transpose_workspace": ([c_int, c_int], c_sz),

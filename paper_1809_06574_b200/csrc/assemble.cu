@@ -84,9 +84,138 @@ __global__ void __launch_bounds__(256) k_assemble(AsmRecipe R, int nnz, const in
   if ((threadIdx.x & 31) == 0 && b && zero_count) atomicAdd(zero_count, __popc(b));
 }
 
+// Several systems of one recipe shape (same terms, groups and opening
+// terms; coefficients and shifts differ -- a parameter sweep): one thread
+// per stored entry loads every term value ONCE and writes the entry of each
+// system.  Per system the arithmetic is k_assemble's exactly (bit-exact).
+constexpr int kAsmMaxSys = 16;
+struct AsmMulti {
+  int nsys;
+  double s[kAsmMaxSys], s2[kAsmMaxSys];
+  double coef[kAsmMaxSys][PMP_MAX_TERMS];
+  double* out[kAsmMaxSys];
+  double* out_perm[kAsmMaxSys];
+};
+
+__global__ void __launch_bounds__(256) k_assemble_multi(AsmRecipe R, AsmMulti S, int nnz,
+                                                        const int* __restrict__ rowid,
+                                                        const int* __restrict__ colidx,
+                                                        const int* __restrict__ perm,
+                                                        int* zero_count) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  double tv[PMP_MAX_TERMS];
+  bool diag = false;
+  int row = 0, pe = 0;
+  if (e < nnz) {
+    if (R.any_diag) {
+      row = __ldg(rowid + e);
+      diag = (__ldg(colidx + e) == row);
+    }
+#pragma unroll
+    for (int t = 0; t < PMP_MAX_TERMS; ++t)
+      tv[t] = t < R.nterms ? term_value(R, t, e, diag, row) : 0.0;
+    if (perm) pe = __ldg(perm + e);
+  }
+  for (int q = 0; q < S.nsys; ++q) {
+    bool zero = false;
+    if (e < nnz) {
+      double gacc[3] = {0.0, 0.0, 0.0};
+      bool gpres[3] = {false, false, false};
+#pragma unroll
+      for (int t = 0; t < PMP_MAX_TERMS; ++t) {
+        if (t >= R.nterms) break;
+        const int g = R.group[t];
+        if (R.first[t]) {
+          gacc[g] = tv[t];
+          gpres[g] = true;
+        } else {
+          gacc[g] = __dadd_rn(gacc[g], __dmul_rn(S.coef[q][t], tv[t]));
+        }
+      }
+      double val;
+      if (R.mode == 0) {
+        bool have = false;
+        val = 0.0;
+        const double gc[3] = {S.s2[q], S.s[q], 1.0};
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+          if (!gpres[g]) continue;
+          const double part = __dmul_rn(gc[g], gacc[g]);
+          val = have ? __dadd_rn(val, part) : part;
+          have = true;
+        }
+        if (val == 0.0) val = 0.0;
+      } else {
+        val = gacc[0];
+        if (fabs(val) < 1e-300) val = 0.0;
+      }
+      zero = (val == 0.0);
+      S.out[q][e] = val;
+      if (perm) S.out_perm[q][pe] = val;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, zero);
+    if (lane == 0 && b && zero_count) atomicAdd(zero_count + q, __popc(b));
+  }
+}
+
 }  // namespace pmp
 
 using namespace pmp;
+
+extern "C" int pmp_assemble_multi(int nnz, int nterms, const double* const* h_term_vals,
+                                  const int32_t* h_kind, const int32_t* h_group,
+                                  const int32_t* h_first, int nsys, const double* h_coef,
+                                  const double* h_s, int mode, const int32_t* d_rowid,
+                                  const int32_t* d_colidx, double* const* h_out,
+                                  const int32_t* d_perm, double* const* h_out_perm,
+                                  int32_t* d_zero_counts, void* stream) {
+  if (nterms < 1 || nterms > PMP_MAX_TERMS || nnz < 0 || (mode != 0 && mode != 1) || nsys < 0 ||
+      (nsys > 0 && (!h_coef || !h_s || !h_out || (d_perm && !h_out_perm)))) {
+    set_error("pmp_assemble_multi: bad arguments (nterms=%d, nnz=%d, mode=%d, nsys=%d)", nterms,
+              nnz, mode, nsys);
+    return PMP_ERR_ARG;
+  }
+  AsmRecipe R;
+  R.nterms = nterms;
+  R.mode = mode;
+  R.s = R.s2 = 0.0;
+  R.any_diag = 0;
+  for (int t = 0; t < nterms; ++t) {
+    R.vals[t] = h_term_vals[t];
+    R.kind[t] = h_kind[t];
+    R.group[t] = h_group[t];
+    R.first[t] = h_first[t];
+    R.coef[t] = 0.0;
+    if (h_group[t] < 0 || h_group[t] > 2 || (mode == 1 && h_group[t] != 0)) {
+      set_error("pmp_assemble_multi: bad group %d for term %d", h_group[t], t);
+      return PMP_ERR_ARG;
+    }
+    if (h_kind[t] == 1) R.any_diag = 1;
+  }
+  if (R.any_diag && !d_rowid) {
+    set_error("pmp_assemble_multi: diagonal terms need d_rowid");
+    return PMP_ERR_ARG;
+  }
+  if (nnz == 0 || nsys == 0) return PMP_OK;
+  for (int q0 = 0; q0 < nsys; q0 += kAsmMaxSys) {
+    AsmMulti S;
+    S.nsys = nsys - q0 < kAsmMaxSys ? nsys - q0 : kAsmMaxSys;
+    for (int q = 0; q < S.nsys; ++q) {
+      const double sv = h_s[q0 + q];
+      S.s[q] = sv;
+      S.s2[q] = sv * sv;  // host double multiply: numpy's s*s
+      for (int t = 0; t < nterms; ++t) S.coef[q][t] = h_coef[(size_t)(q0 + q) * nterms + t];
+      S.out[q] = h_out[q0 + q];
+      S.out_perm[q] = d_perm ? h_out_perm[q0 + q] : nullptr;
+    }
+    k_assemble_multi<<<ceil_div(nnz, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        R, S, nnz, d_rowid, d_colidx, d_perm, d_zero_counts ? d_zero_counts + q0 : nullptr);
+    const int rc = cuda_status("pmp_assemble_multi");
+    if (rc != PMP_OK) return rc;
+  }
+  return PMP_OK;
+}
 
 extern "C" int pmp_assemble(int nnz, int nterms, const double* const* h_term_vals,
                             const int32_t* h_kind, const int32_t* h_group, const int32_t* h_first,

@@ -1289,4 +1289,4 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
 
 
 # systems per persistent solve launch (PMP_BATCH_GROUPS overrides)
-BATCH_GROUPS = int(_os.environ.get("PMP_BATCH_GROUPS", "4"))
+BATCH_GROUPS = int(_os.environ.get("PMP_BATCH_GROUPS", "6"))

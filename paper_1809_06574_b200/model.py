@@ -112,6 +112,39 @@ class _UnionTerms:
             return (out, out_perm)
         return self.finish((out, out_perm), int(zc.item()))
 
+    def run_many(self, recipes, mode, svals, zc):
+        """``run`` for several recipes of one shape (same terms, groups and
+        opening terms) in one pmp_assemble_multi call; exact-zero counts go
+        to zc[q] (device int32, zeroed by the caller).  Returns raw results
+        for ``finish``."""
+        import ctypes
+        st = self.structure
+        r0 = recipes[0]
+        nt = len(r0)
+        k = len(recipes)
+        ptrs = ctypes_array_vp([self.vals[t].data_ptr() for t, _, _, _ in r0])
+        kind = np.array([self.kinds[t] for t, _, _, _ in r0], dtype=np.int32)
+        group = np.array([g for _, g, _, _ in r0], dtype=np.int32)
+        first = np.array([f for _, _, f, _ in r0], dtype=np.int32)
+        coef = np.array([[c for _, _, _, c in r] for r in recipes], dtype=np.float64)
+        sv = np.asarray(svals, dtype=np.float64)
+        outs = [torch.empty(max(st.nnz, 1), dtype=torch.float64, device=_dev())[:st.nnz]
+                for _ in range(k)]
+        perm = None
+        outs_perm = [None] * k
+        if not self.symmetric:
+            perm = st.csc()[2]
+            outs_perm = [torch.empty_like(o) for o in outs]
+        VP = ctypes.c_void_p * k
+        h_out = VP(*[o.data_ptr() for o in outs])
+        h_perm = VP(*[o.data_ptr() for o in outs_perm]) if perm is not None else None
+        _abi.call("pmp_assemble_multi", st.nnz, nt, ptrs, kind.ctypes.data, group.ctypes.data,
+                  first.ctypes.data, k, coef.ctypes.data, sv.ctypes.data, mode,
+                  _abi.ptr(self.rowid), _abi.ptr(st.colidx), h_out, _abi.ptr(perm), h_perm,
+                  _abi.ptr(zc), _abi.stream())
+        _abi.note_launches(-(-k // 16) - 1)
+        return list(zip(outs, outs_perm))
+
     def finish(self, raw, zero_count):
         out, out_perm = raw
         if zero_count:
@@ -215,12 +248,21 @@ class SecondOrderModel:
         if not points:
             return []
         zc = torch.zeros(len(points), dtype=torch.int32, device=_dev())
-        raws = []
-        for i, (s, p) in enumerate(points):
-            u, recipe, sv = self._recipe(s, p)
-            raws.append(u.run(recipe, 0, sv, zc=zc[i:i + 1]))
-        counts = zc.cpu().numpy()
         u = self._union()
+        recs = [self._recipe(s, p) for s, p in points]
+        raws = []
+        i = 0
+        while i < len(recs):
+            # runs of one recipe shape (a term drops out when its parameter
+            # is exactly 0) share one multi-system launch
+            shape = [(t, g, f) for t, g, f, _ in recs[i][1]]
+            j = i + 1
+            while j < len(recs) and [(t, g, f) for t, g, f, _ in recs[j][1]] == shape:
+                j += 1
+            raws += u.run_many([r[1] for r in recs[i:j]], 0, [r[2] for r in recs[i:j]],
+                               zc[i:j])
+            i = j
+        counts = zc.cpu().numpy()
         return [u.finish(r, int(c)) for r, c in zip(raws, counts)]
 
     def _recipe(self, s, pvals):

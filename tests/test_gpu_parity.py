@@ -529,3 +529,22 @@ def test_update_first_many_bitwise(pm):
     for A, (Pm, sm) in list(zip(As, many))[::3]:
         Q, res = orc.update_factor(A1h, A.to_scipy(), pattern_level=0)[:2]
         G.compare_factor(Pm.q.to_scipy(), Q)
+
+
+def test_assemble_many_bit_exact(pm):
+    """A window assembled in multi-system launches == one system at a time,
+    bitwise (symmetric and unsymmetric terms; a zero parameter changes the
+    recipe shape mid-window)."""
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(1, scale=16)
+    rng = np.random.default_rng(5)
+    n = W.mass_terms[0].shape[0]
+    K1 = sp.random(n, n, density=4.0 / n, random_state=rng, format="csr")
+    for stiff in (W.stiffness_terms, [W.stiffness_terms[0], K1]):
+        model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, stiff, rhs=W.rhs)
+        pts = list(W.points()) + [(0.7, np.array([0.0])), (2.0, np.array([0.3]))]
+        many = model.assemble_many(pts)
+        for (s, p), Am in zip(pts, many):
+            A = model.assemble(s, p)
+            assert torch.equal(Am.vals, A.vals)
+            assert np.array_equal(Am.to_scipy().toarray(), A.to_scipy().toarray())
