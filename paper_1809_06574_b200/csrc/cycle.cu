@@ -83,9 +83,10 @@ __global__ void __launch_bounds__(kOrthT, 2) k_cycle(CycleArgs P) {
 
   // ---- workers -----------------------------------------------------------------
   const int ldx = P.ldx;
-  const int ldw = odd_ld(sb);  // W rows live in shared memory in both modes
+  // W rows in shared memory, or (rows beyond shared memory) in global
+  const int ldw = P.wglob ? P.s : odd_ld(sb);
   double* Xs = region;
-  double* Wv = region + (CACHED ? (size_t)nr * ldx : 0);
+  double* Wv = P.wglob ? P.W + (size_t)r0 * P.s : region + (CACHED ? (size_t)nr * ldx : 0);
   double* Q1 = P.Q1g + (size_t)r0 * sb;
   WBar wb{P.ist + 9, (int)gridDim.x - 1, 0, (int)blockIdx.x - 1};
 
@@ -113,7 +114,9 @@ size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int rest
   size_t ctl = nb * 4 * sb * sb + (size_t)sb * sb * nb * (nb + 1) / 2 + (size_t)ldq * na +
                (size_t)sb * ldq + sb * sb + 16 * 96 + 32 + 8 + 16 + 16 +
                (size_t)(2 * sb + 1) * (3 * sb + na) + (size_t)2 * ldq * sb + 8;
-  size_t work = (size_t)rows * ((cached ? ldx : 0) + odd_ld(sb));
+  // cached: 1 = [C | V] rows (and W rows) in shared memory, 0 = W rows
+  // only, 2 = none (W rows in global memory: large n per block)
+  size_t work = (size_t)rows * ((cached == 1 ? ldx : 0) + (cached == 2 ? 0 : odd_ld(sb)));
   return ctl > work ? ctl : work;
 }
 
@@ -172,8 +175,9 @@ int pmp_gcro_cycle_dev(PmpGcroCycle* c) {
   const int ldx = odd_ld(c->kc + c->cap);
   const int NYsel = c->sb <= 8 ? 8 : 16;
   auto pick = [&](int cached) -> void* {
-    if (NYsel == 8) return cached ? (void*)k_cycle<true, 8> : (void*)k_cycle<false, 8>;
-    return cached ? (void*)k_cycle<true, 16> : (void*)k_cycle<false, 16>;
+    const bool c1 = cached == 1;
+    if (NYsel == 8) return c1 ? (void*)k_cycle<true, 8> : (void*)k_cycle<false, 8>;
+    return c1 ? (void*)k_cycle<true, 16> : (void*)k_cycle<false, 16>;
   };
   // geometry: 1 control block + workers; prefer the cached layout with two
   // blocks per SM, then one, then streaming rows from global memory
@@ -181,10 +185,11 @@ int pmp_gcro_cycle_dev(PmpGcroCycle* c) {
   int g = 0, rows = 0;
   size_t smem = 0;
   void* fn = nullptr;
-  const int order2[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
-  const int order1[4][2] = {{1, 1}, {2, 1}, {1, 0}, {2, 0}};
+  const int order2[6][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}, {2, 2}, {1, 2}};
+  const int order1[6][2] = {{1, 1}, {2, 1}, {1, 0}, {2, 0}, {1, 2}, {2, 2}};
   const int(*order)[2] = c->blocks_per_sm == 1 ? order1 : order2;
-  for (int attempt = 0; attempt < 4 && !fn; ++attempt) {
+  int wglob = 0;
+  for (int attempt = 0; attempt < 6 && !fn; ++attempt) {
     const int bps = order[attempt][0], cach = order[attempt][1];
     const int gb = bps * sms;
     int workers = gb - 1;
@@ -201,6 +206,7 @@ int pmp_gcro_cycle_dev(PmpGcroCycle* c) {
     g = workers + 1;
     rows = r;
     smem = sm;
+    wglob = cach == 2;
   }
   if (!fn) {
     set_error("pmp_gcro_cycle_dev: no co-resident geometry (n=%d ldq=%d)", c->n, c->ldq);
@@ -226,6 +232,7 @@ int pmp_gcro_cycle_dev(PmpGcroCycle* c) {
   P.ava = c->a_vals;
   P.V = c->V;
   P.W = c->W;
+  P.wglob = wglob;
   P.T0 = c->T0;
   P.T1 = c->T1;
   P.C = c->C;

@@ -25,6 +25,7 @@ struct CycleArgs {
   int offB, offH1, offH2, offR;
   double *partial, *gout, *Q1g, *sbuf;
   int rows_per_block, ldx, max_iters, inner_restart, hist_cap, nblk;
+  int wglob;  // W rows in global memory (P.W) instead of shared memory
   double tol;
   double* proj;
   int oBmat, oHb, oQR, oTau, oCq, oY, oRes, oBn, oHist;

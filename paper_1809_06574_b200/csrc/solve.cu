@@ -44,6 +44,7 @@ struct SysDesc {
 struct SolveArgs {
   int n, s, cap, kc, outer_dim, inner_restart, max_iters;
   int gsz, rows_per_block, ldx, hist_cap, log_cap, isz;
+  int wglob;  // W rows in global memory (rows beyond shared memory)
   double tol;
   const SysDesc* sys;
   double* ws;
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   L.oHist = A.pHist;
   L.ist = ist;
   L.dbg = nullptr;
+  L.wglob = A.wglob;
   }
   __syncthreads();
 
@@ -520,8 +522,9 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       __syncthreads();
     } else {
       int m = 0, total = na, ncols = 0, status = 0;
-      const int ldw = odd_ld(na);  // W rows in shared memory in both modes
-      double* Wv = region + (CACHED ? (size_t)nr * A.ldx : 0);
+      // W rows in shared memory, or (rows beyond shared memory) in global
+      const int ldw = A.wglob ? s : odd_ld(na);
+      double* Wv = A.wglob ? W + (size_t)r0 * s : region + (CACHED ? (size_t)nr * A.ldx : 0);
       WSmem wsm{G, R1, R2, red, piv, piv2, flag, region, Wv, L.Q1g + (size_t)r0 * na, ldw};
       worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
       sstamp(A, grp, cyc, 3);
@@ -816,8 +819,9 @@ static size_t solve_smem_bytes(int rows, int ldx, int kc, int cap, int s, int re
 }
 
 static void* solve_kernel(int s, int cached) {
-  if (s <= 8) return cached ? (void*)k_solve<true, 8> : (void*)k_solve<false, 8>;
-  return cached ? (void*)k_solve<true, 16> : (void*)k_solve<false, 16>;
+  const bool c1 = cached == 1;
+  if (s <= 8) return c1 ? (void*)k_solve<true, 8> : (void*)k_solve<false, 8>;
+  return c1 ? (void*)k_solve<true, 16> : (void*)k_solve<false, 16>;
 }
 
 extern "C" {
@@ -827,8 +831,9 @@ int pmp_solve_geometry(int n, int s, int cap, int kc, int restart, int groups, i
   const int sms = orth_max_grid() / 2;
   const int ldx = odd_ld(kc + cap);
   if (groups < 1 || s < 1 || s > 16) return PMP_ERR_ARG;
-  const int order[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
-  for (int a = 0; a < 4; ++a) {
+  // cached 1: [C | V] and W rows in shared memory; 0: W rows only; 2: none
+  const int order[6][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}, {2, 2}, {1, 2}};
+  for (int a = 0; a < 6; ++a) {
     const int bps = order[a][0], cach = order[a][1];
     const int g = bps * sms / groups;
     if (g < 2) continue;
@@ -889,6 +894,7 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   A.log_cap = b->log_cap;
   A.isz = b->isz;
   A.tol = b->tol;
+  A.wglob = cached == 2;
   A.sys = reinterpret_cast<const SysDesc*>(b->d_sys);
   A.ws = b->d_ws;
   A.wsz = b->wsz;

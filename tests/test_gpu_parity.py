@@ -548,3 +548,23 @@ def test_assemble_many_bit_exact(pm):
             A = model.assemble(s, p)
             assert torch.equal(Am.vals, A.vals)
             assert np.array_equal(Am.to_scipy().toarray(), A.to_scipy().toarray())
+
+
+def test_large_n_rows_beyond_shared_memory(pm):
+    """n large enough that a block's W rows no longer fit in shared memory
+    (c3 at full size, n = 262,144, s = 16): the persistent solve switches to
+    W rows in global memory; every solution reaches the 1e-8 true residual."""
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(3)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pol = pm.PrecondPolicy("spai-update-first", spai=pm.SpaiConfig(pattern_level=0),
+                           update=pm.UpdateConfig(pattern_level=0))
+    recs, _ = pm.run_sequence(model, W.s_grid[:1], W.p_grid[:2], pol,
+                              pm.SolverConfig(tol=1e-8), keep_solutions=True)
+    pts = [(W.s_grid[0], np.atleast_1d(p)) for p in W.p_grid[:2]]
+    for r in recs:
+        A = model.assemble(*pts[r["index"]]).to_scipy()
+        X = r["X"].cpu().numpy()
+        rel = np.linalg.norm(W.rhs - A @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
+        assert r["converged"] and rel.max() <= 1e-8, (r["index"], rel.max())
