@@ -40,7 +40,7 @@
 
 namespace pmp {
 
-template <bool CACHED, int NY>
+template <bool CACHED, int NY, bool WG>
 __global__ void __launch_bounds__(kOrthT, 2) k_cycle(CycleArgs P) {
   extern __shared__ __align__(16) double sh[];
   const bool ctl = blockIdx.x == 0;
@@ -84,9 +84,9 @@ __global__ void __launch_bounds__(kOrthT, 2) k_cycle(CycleArgs P) {
   // ---- workers -----------------------------------------------------------------
   const int ldx = P.ldx;
   // W rows in shared memory, or (rows beyond shared memory) in global
-  const int ldw = P.wglob ? P.s : odd_ld(sb);
+  const int ldw = WG ? P.s : odd_ld(sb);
   double* Xs = region;
-  double* Wv = P.wglob ? P.W + (size_t)r0 * P.s : region + (CACHED ? (size_t)nr * ldx : 0);
+  double* Wv = WG ? P.W + (size_t)r0 * P.s : region + (CACHED ? (size_t)nr * ldx : 0);
   double* Q1 = P.Q1g + (size_t)r0 * sb;
   WBar wb{P.ist + 9, (int)gridDim.x - 1, 0, (int)blockIdx.x - 1};
 
@@ -175,9 +175,11 @@ int pmp_gcro_cycle_dev(PmpGcroCycle* c) {
   const int ldx = odd_ld(c->kc + c->cap);
   const int NYsel = c->sb <= 8 ? 8 : 16;
   auto pick = [&](int cached) -> void* {
-    const bool c1 = cached == 1;
-    if (NYsel == 8) return c1 ? (void*)k_cycle<true, 8> : (void*)k_cycle<false, 8>;
-    return c1 ? (void*)k_cycle<true, 16> : (void*)k_cycle<false, 16>;
+    if (NYsel == 8)
+      return cached == 1 ? (void*)k_cycle<true, 8, false>
+                         : (cached == 2 ? (void*)k_cycle<false, 8, true> : (void*)k_cycle<false, 8, false>);
+    return cached == 1 ? (void*)k_cycle<true, 16, false>
+                       : (cached == 2 ? (void*)k_cycle<false, 16, true> : (void*)k_cycle<false, 16, false>);
   };
   // geometry: 1 control block + workers; prefer the cached layout with two
   // blocks per SM, then one, then streaming rows from global memory

@@ -161,7 +161,7 @@ __device__ __forceinline__ void fold_rowsolve(const double* w, const double* z, 
     }
 }
 
-template <bool CACHED, int NY>
+template <bool CACHED, int NY, bool WG>
 #ifndef PMP_MINB
 #define PMP_MINB 2
 #endif
@@ -523,8 +523,9 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
     } else {
       int m = 0, total = na, ncols = 0, status = 0;
       // W rows in shared memory, or (rows beyond shared memory) in global
-      const int ldw = A.wglob ? s : odd_ld(na);
-      double* Wv = A.wglob ? W + (size_t)r0 * s : region + (CACHED ? (size_t)nr * A.ldx : 0);
+      // (a compile-time choice: the shared-memory instances keep LDS / STS)
+      const int ldw = WG ? s : odd_ld(na);
+      double* Wv = WG ? W + (size_t)r0 * s : region + (CACHED ? (size_t)nr * A.ldx : 0);
       WSmem wsm{G, R1, R2, red, piv, piv2, flag, region, Wv, L.Q1g + (size_t)r0 * na, ldw};
       worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
       sstamp(A, grp, cyc, 3);
@@ -819,9 +820,11 @@ static size_t solve_smem_bytes(int rows, int ldx, int kc, int cap, int s, int re
 }
 
 static void* solve_kernel(int s, int cached) {
-  const bool c1 = cached == 1;
-  if (s <= 8) return c1 ? (void*)k_solve<true, 8> : (void*)k_solve<false, 8>;
-  return c1 ? (void*)k_solve<true, 16> : (void*)k_solve<false, 16>;
+  if (s <= 8)
+    return cached == 1 ? (void*)k_solve<true, 8, false>
+                       : (cached == 2 ? (void*)k_solve<false, 8, true> : (void*)k_solve<false, 8, false>);
+  return cached == 1 ? (void*)k_solve<true, 16, false>
+                     : (cached == 2 ? (void*)k_solve<false, 16, true> : (void*)k_solve<false, 16, false>);
 }
 
 extern "C" {
