@@ -14,6 +14,8 @@ and torch.distributed.  There is no CPU fallback.
 from .device import DeviceCSR, DevicePattern, Structure
 from .krylov import (SolveReport, SolverBreakdown, SolverConfig, apply_preconditioner,
                      block_gcro_solve, block_gcro_solve_batch, gcro_solve)
+from .mmio import (read_dense_matrix_market, read_matrix_market, write_dense_matrix_market,
+                   write_matrix_market)
 from .model import AffineFamily, SecondOrderModel, evaluate, pmor_l_sequence
 from .sequence import PrecondPolicy, SequencePreconditioner, run_sequence
 from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, spai_build,

@@ -15,14 +15,16 @@ build over the same structure -- the SPAI-update sequence -- is a fixed
 list of kernel launches with no host synchronisation.
 """
 
+import json
 import time
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import scipy.sparse as sp
 import torch
 
-from . import _abi
+from . import _abi, mmio
 from .device import (DeviceCSR, DevicePattern, Structure, _dev, i32, level0_pattern, scratch)
 
 # ---------------------------------------------------------------------------
@@ -176,6 +178,37 @@ class Preconditioner:
         tmp = [torch.empty_like(Vd), torch.empty_like(Vd)] if self.depth > 1 else None
         self.apply_dev(_abi.ptr(Vd), s, s, _abi.ptr(Y), s, tmp)
         return Y.cpu().numpy() if host else Y
+
+    def save(self, directory, stats_summary=None):
+        """Persist the chain as ordered ``factor_NN.mtx`` files plus the
+        ``preconditioner.json`` sidecar, in the reference's layout
+        (spai.py:103-117) so either side can load the other's files."""
+        directory = Path(directory)
+        directory.mkdir(parents=True, exist_ok=True)
+        files = []
+        for i, F in enumerate(self.factors()):
+            name = "factor_%02d.mtx" % i
+            mmio.write_matrix_market(F.to_scipy(), directory / name)
+            files.append(name)
+        sidecar = {"kind": self.kind, "factors": files}
+        if stats_summary:
+            sidecar["stats"] = stats_summary
+        with open(directory / "preconditioner.json", "w") as fh:
+            json.dump(sidecar, fh, indent=2, sort_keys=True)
+            fh.write("\n")
+
+    @classmethod
+    def load(cls, directory):
+        """Rebuild the chain saved by ``save`` (here or by the reference,
+        spai.py:119-128); factors go straight to the device."""
+        directory = Path(directory)
+        with open(directory / "preconditioner.json") as fh:
+            sidecar = json.load(fh)
+        mats = [mmio.read_matrix_market(directory / name) for name in sidecar["factors"]]
+        pre = cls(matrix=mats[-1])
+        for Q in reversed(mats[:-1]):
+            pre = cls(q=Q, base=pre)
+        return pre
 
     def materialize(self):
         """Explicit sparse matrix of the chain, on the host (diagnostics

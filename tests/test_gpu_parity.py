@@ -568,3 +568,50 @@ def test_large_n_rows_beyond_shared_memory(pm):
         X = r["X"].cpu().numpy()
         rel = np.linalg.norm(W.rhs - A @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
         assert r["converged"] and rel.max() <= 1e-8, (r["index"], rel.max())
+
+
+# ---------------------------------------------------------------------------
+# persistence: load the chain the reference saved, apply
+# it on the device; save ours and load it back
+# ---------------------------------------------------------------------------
+
+def test_load_reference_saved_chain(pm, tmp_path):
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "precond_ref")
+    P = pm.Preconditioner.load(d)
+    assert P.kind == "factored" and P.depth == 2
+    g = np.load(os.path.join(d, "apply.npz"))
+    Y = P.apply(g["V"])
+    err = np.linalg.norm(Y - g["Y"]) / np.linalg.norm(g["Y"])
+    assert err <= 1e-13, err
+    # ours -> files -> ours: same factors bit for bit, same apply bit for bit
+    P.save(tmp_path / "p", stats_summary={"columns": int(g["n"])})
+    P2 = pm.Preconditioner.load(tmp_path / "p")
+    for F1, F2 in zip(P.factors(), P2.factors()):
+        a, b = F1.to_scipy(), F2.to_scipy()
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        assert np.array_equal(a.data, b.data)
+    assert np.array_equal(P2.apply(g["V"]), Y)
+
+
+def test_save_load_built_preconditioner(pm, tmp_path):
+    from paper_1809_06574_b200.workloads import make_config
+    W = make_config(1, scale=16)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pts = W.points()
+    A1, A2 = model.assemble(*pts[0]), model.assemble(*pts[1])
+    P1, st = pm.spai_build(A1, pm.SpaiConfig(pattern_level=0))
+    P2, _ = pm.update_first(A1, A2, P1, pm.UpdateConfig(pattern_level=0))
+    P2.save(tmp_path / "chain", stats_summary=st.summary())
+    import json
+    side = json.load(open(tmp_path / "chain" / "preconditioner.json"))
+    assert side["kind"] == "factored" and len(side["factors"]) == 2
+    assert side["stats"]["columns"] == W.n
+    Q = pm.Preconditioner.load(tmp_path / "chain")
+    V = np.random.default_rng(5).standard_normal((W.n, 4))
+    assert np.array_equal(Q.apply(V), P2.apply(V))
+    # the reference's reader sees the same values (scipy.io.mmread + as_csr)
+    import scipy.io
+    R = scipy.io.mmread(str(tmp_path / "chain" / "factor_01.mtx")).tocsr()
+    M = P1.matrix.to_scipy()
+    assert np.array_equal(R.real.toarray(), M.toarray())

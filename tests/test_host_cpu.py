@@ -192,3 +192,62 @@ def test_solve_layout_disjoint():
     assert starts[0] == 0 and all(b > a for a, b in zip(starts, starts[1:]))
     assert total > max(starts)
     assert all(v % 32 == 0 for v in off.values())
+
+
+# ---------------------------------------------------------------------------
+# persistence: Matrix Market interchange with the files the
+# reference's own Preconditioner.save wrote (tests/golden/precond_ref)
+# ---------------------------------------------------------------------------
+
+GOLD_PRE = os.path.join(ROOT, "tests", "golden", "precond_ref")
+
+
+def test_read_reference_matrix_market_files():
+    import json
+    import scipy.io
+    from paper_1809_06574_b200 import mmio
+    side = json.load(open(os.path.join(GOLD_PRE, "preconditioner.json")))
+    assert side["kind"] == "factored" and side["factors"] == ["factor_00.mtx", "factor_01.mtx"]
+    for name in side["factors"]:
+        path = os.path.join(GOLD_PRE, name)
+        M = mmio.read_matrix_market(path)
+        R = scipy.io.mmread(path).tocsr()
+        assert M.dtype == np.float64 and M.has_sorted_indices
+        assert np.abs(R.data.imag).max() == 0.0
+        R = R.real.tocsr()
+        R.eliminate_zeros()
+        R.sort_indices()
+        assert np.array_equal(M.indptr, R.indptr) and np.array_equal(M.indices, R.indices)
+        assert np.array_equal(M.data, R.data)  # 17 digits: bit-exact
+
+
+def test_matrix_market_round_trip_is_bit_exact(tmp_path):
+    import scipy.io
+    from paper_1809_06574_b200 import mmio
+    M = mmio.read_matrix_market(os.path.join(GOLD_PRE, "factor_01.mtx"))
+    out = tmp_path / "f.mtx"
+    mmio.write_matrix_market(M, out)
+    head = open(out).readline()
+    assert head.startswith("%%MatrixMarket matrix coordinate complex general")
+    # what the reference's reader (scipy.io.mmread + as_csr) sees
+    R = scipy.io.mmread(str(out)).tocsr()
+    assert np.array_equal(R.data.real, M.data) and np.abs(R.data.imag).max() == 0.0
+    M2 = mmio.read_matrix_market(out)
+    assert (M2 != M).nnz == 0 and np.array_equal(M2.data, M.data)
+    # dense blocks
+    X = np.random.default_rng(3).standard_normal((7, 3))
+    mmio.write_dense_matrix_market(X, tmp_path / "x.mtx")
+    assert np.array_equal(mmio.read_dense_matrix_market(tmp_path / "x.mtx"), X)
+
+
+def test_matrix_market_rejects_complex_values(tmp_path):
+    import scipy.io
+    import scipy.sparse as sp
+    from paper_1809_06574_b200 import mmio
+    A = sp.csr_matrix(np.array([[1.0 + 1j, 0], [0, 2.0]]))
+    scipy.io.mmwrite(str(tmp_path / "c.mtx"), A, field="complex")
+    with pytest.raises(NotImplementedError):
+        mmio.read_matrix_market(tmp_path / "c.mtx")
+    (tmp_path / "bad.mtx").write_text("%%MatrixMarket matrix nonsense\n1 1 1\n")
+    with pytest.raises(ValueError):
+        mmio.read_matrix_market(tmp_path / "bad.mtx")

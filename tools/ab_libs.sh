@@ -1,0 +1,13 @@
+#!/bin/bash
+# A/B of library variants on the bench (c2 sequence): LIBS="name=path ..."
+# ("main" = the in-tree library).  Two repetitions each, interleaved.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for rep in 1 2; do
+  for kv in ${LIBS:-main=}; do
+    name=${kv%%=*}; path=${kv#*=}
+    if [ -n "$path" ]; then L="PMP_LIB=$path"; else L=""; fi
+    env $L python bench.py --no-cpu-baseline --no-e2e --steps 5 ${BENCH_ARGS} > gpurun_out/ab_${name}_$rep.log 2>&1
+    echo $name rep$rep $(tail -1 gpurun_out/ab_${name}_$rep.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('ms', round(d['ms_per_step'],2), 'solve', round(d['phases_s']['solve']*1e3,2), 'iters', d['iterations']['mean'])" 2>&1 | tail -1)
+  done
+done
