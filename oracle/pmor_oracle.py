@@ -467,3 +467,65 @@ def run_sequence(workload, kind="spai-update-first", level=0, tol=1e-8, systems=
             X, info = block_gcro(A, workload.rhs, P, tol=tol)
             out.append((idx, X, info, st))
     return out
+
+
+# ---------------------------------------------------------------------------
+# moment pipeline (rpmor.py:271-362, sparsecore.py:176-204)
+# ---------------------------------------------------------------------------
+
+def extend_orthonormal_basis(Q, X, tol_drop=1e-10):
+    """Modified Gram-Schmidt, two passes, relative drop test
+    (sparsecore.py:176-204)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    kept = [] if Q is None else [np.ascontiguousarray(Q[:, j]) for j in range(Q.shape[1])]
+    for j in range(X.shape[1]):
+        v = X[:, j].copy()
+        norm0 = np.linalg.norm(v)
+        if norm0 == 0.0:
+            continue
+        for _ in range(2):
+            for q in kept:
+                v -= q * np.dot(q, v)
+        nrm = np.linalg.norm(v)
+        if nrm <= tol_drop * norm0:
+            continue
+        kept.append(v / nrm)
+    return np.column_stack(kept) if kept else np.zeros((n, 0))
+
+
+def rpmor_reduce(terms, B, C, points, levels=1, tol=1e-10, kind="spai-update-first",
+                 pattern_level=0, drop_tol=1e-10):
+    """rpmor.py:307-362 with the SequencePreconditioner of rpmor.py:189-218
+    (kind "none", "spai" or "spai-update-first").  Returns (reduced terms,
+    reduced rhs, reduced output, basis, per-call iteration counts)."""
+    terms = [canon(T) for T in terms]
+    V, iters = None, []
+    A1 = P1 = None
+    for pt in points:
+        A = affine_evaluate(terms, list(pt))
+        if kind == "none":
+            P = None
+        elif kind == "spai" or P1 is None:
+            P, _ = spai_build(A, pattern_level=pattern_level)
+            P = Chain([P])
+            if A1 is None:
+                A1, P1 = A, P
+        else:
+            Q, _ = update_factor(A1, A, pattern_level=pattern_level)
+            P = Chain([Q] + P1.factors)
+        X0, info = block_gcro(A, B, P, tol=tol)
+        iters.append(info["iterations"])
+        V = extend_orthonormal_basis(V, X0, drop_tol)
+        parents = X0
+        for _ in range(levels):
+            blocks = []
+            for c in range(parents.shape[1]):
+                rhs = np.hstack([T @ parents[:, [c]] for T in terms[1:]])
+                Xh, info = block_gcro(A, rhs, P, tol=tol)
+                iters.append(info["iterations"])
+                V = extend_orthonormal_basis(V, Xh, drop_tol)
+                blocks.append(Xh)
+            parents = np.hstack(blocks)
+    red = [V.T @ (T @ V) for T in terms]
+    return red, V.T @ B, C.T @ V, V, iters

@@ -17,6 +17,9 @@ from .krylov import (SolveReport, SolverBreakdown, SolverConfig, apply_precondit
 from .mmio import (read_dense_matrix_market, read_matrix_market, write_dense_matrix_market,
                    write_matrix_market)
 from .model import AffineFamily, SecondOrderModel, evaluate, pmor_l_sequence
+from .rpmor import (ConvergenceError, ExpansionPoint, PipelineReport, ReducedModel,
+                    extend_orthonormal_basis, first_moment_rhs, first_moments,
+                    mgs_orthonormalize, rpmor_reduce, zeroth_moment)
 from .sequence import PrecondPolicy, SequencePreconditioner, run_sequence
 from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, spai_build,
                    spai_column, spai_pattern)

@@ -48,7 +48,7 @@ def write_matrix_market(A, path):
 def read_matrix_market(path):
     """sparsecore.py:262-272: symmetric / skew / hermitian files expanded to
     general storage; malformed files raise ValueError (from the parser)."""
-    M = scipy.io.mmread(str(path))
+    M = scipy.io.mmread(str(path), spmatrix=False)
     if not sp.issparse(M):
         M = sp.csr_matrix(np.atleast_2d(M))
     return canonical_csr(M)
@@ -65,7 +65,7 @@ def write_dense_matrix_market(X, path):
 
 def read_dense_matrix_market(path):
     """sparsecore.py:281-285, returned as a real float64 block."""
-    M = scipy.io.mmread(str(path))
+    M = scipy.io.mmread(str(path), spmatrix=False)
     if sp.issparse(M):
         M = M.toarray()
     M = np.atleast_2d(np.asarray(M))

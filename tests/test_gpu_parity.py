@@ -612,6 +612,85 @@ def test_save_load_built_preconditioner(pm, tmp_path):
     assert np.array_equal(Q.apply(V), P2.apply(V))
     # the reference's reader sees the same values (scipy.io.mmread + as_csr)
     import scipy.io
-    R = scipy.io.mmread(str(tmp_path / "chain" / "factor_01.mtx")).tocsr()
+    R = sp.csr_matrix(scipy.io.mmread(str(tmp_path / "chain" / "factor_01.mtx"), spmatrix=False))
     M = P1.matrix.to_scipy()
     assert np.array_equal(R.real.toarray(), M.toarray())
+
+
+# ---------------------------------------------------------------------------
+# moment pipeline vs the reference's rpmor_reduce
+# (tests/golden/rpmor_small.npz, written by the real reference)
+# ---------------------------------------------------------------------------
+
+def _rpmor_golden(pm):
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "rpmor_small.npz"))
+    terms = [sp.csr_matrix((g["t%d_data" % j], g["t%d_indices" % j], g["t%d_indptr" % j]))
+             for j in range(3)]
+    return g, pm.AffineFamily(terms, rhs=g["B"], output=g["C"])
+
+
+def test_rpmor_reduce_vs_reference(pm, tmp_path):
+    g, fam = _rpmor_golden(pm)
+    pol = pm.PrecondPolicy(kind="spai-update-first", spai=pm.SpaiConfig(pattern_level=0),
+                           update=pm.UpdateConfig(pattern_level=0))
+    pts = [pm.ExpansionPoint(p, label="p%d" % i) for i, p in enumerate(g["points"])]
+    red, rep = pm.rpmor_reduce(fam, pts, levels=1, solver_cfg=pm.SolverConfig(tol=1e-10),
+                               policy=pol)
+    assert rep.basis_size == g["basis"].shape[1]
+    assert [r.n_rhs for r in rep.records] == list(g["n_rhs"])
+    assert [r.level for r in rep.records] == list(g["levels"])
+    it = np.array([r.iterations for r in rep.records])
+    assert np.abs(it - g["iters"]).max() <= 2, (it, g["iters"])
+    V = red.basis.cpu().numpy()
+    assert np.linalg.norm(V - g["basis"]) <= 1e-8 * np.linalg.norm(g["basis"])
+    assert np.abs(V.T @ V - np.eye(V.shape[1])).max() <= 1e-12
+    for j in range(3):
+        ref = g["red_t%d" % j]
+        assert np.linalg.norm(red.terms[j] - ref) <= 1e-8 * np.linalg.norm(ref)
+    for q, H in zip(g["queries"], g["transfer"]):
+        Hq = red.transfer(q)
+        assert np.linalg.norm(Hq - H) <= 1e-8 * np.linalg.norm(H)
+    red.save(tmp_path / "rom")
+    back = pm.ReducedModel.load(tmp_path / "rom")
+    for a, b in zip(back.terms, red.terms):
+        assert np.array_equal(a, b)
+    assert np.array_equal(back.basis, V)
+
+
+def test_moments_known_answers(pm):
+    n = 12
+    I = sp.identity(n, format="csr")
+    Z = sp.csr_matrix((n, n))
+    fam = pm.AffineFamily([I, Z], rhs=np.arange(1.0, n + 1.0)[:, None])
+    X0, _ = pm.zeroth_moment(fam, [0.0])
+    assert np.linalg.norm(X0[:, 0] - np.arange(1.0, n + 1.0)) <= 1e-12
+    X1, _ = pm.first_moments(fam, [0.0], X0)
+    assert np.all(X1 == 0)
+    d = np.array([2.0, 4.0, 8.0])
+    fam = pm.AffineFamily([sp.diags(d).tocsr(), sp.csr_matrix((3, 3))], rhs=np.ones((3, 1)))
+    X0, _ = pm.zeroth_moment(fam, [0.0])
+    assert np.allclose(X0[:, 0], 1.0 / d, rtol=0, atol=1e-12)
+    # first-moment right-hand sides: one SpMM per parameter term
+    g, fam = _rpmor_golden(pm)
+    x0 = np.random.default_rng(1).standard_normal((fam.dim, 1))
+    rhs = pm.first_moment_rhs(fam, x0)
+    ref = np.hstack([T @ x0 for T in fam.terms[1:]])
+    assert np.linalg.norm(rhs - ref) <= 1e-14 * np.linalg.norm(ref)
+    with pytest.raises(ValueError):
+        pm.rpmor_reduce(fam, [])
+
+
+def test_extend_orthonormal_basis_matches_oracle(pm):
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((500, 6))
+    X[:, 3] = X[:, 0] + 2 * X[:, 1]          # dependent: dropped
+    X[:, 5] = 0.0                            # zero: skipped
+    Q = pm.extend_orthonormal_basis(None, X)
+    Qr = orc.extend_orthonormal_basis(None, X)
+    assert Q.shape == Qr.shape == (500, 4)
+    assert np.abs(Q - Qr).max() <= 1e-12
+    Y = rng.standard_normal((500, 3))
+    Q2 = pm.extend_orthonormal_basis(Q, Y)
+    Q2r = orc.extend_orthonormal_basis(Qr, Y)
+    assert np.abs(Q2 - Q2r).max() <= 1e-12

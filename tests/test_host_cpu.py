@@ -7,6 +7,7 @@ import re
 import socket
 
 import numpy as np
+import scipy.sparse as sp
 import pytest
 import torch
 import torch.distributed as dist
@@ -211,7 +212,7 @@ def test_read_reference_matrix_market_files():
     for name in side["factors"]:
         path = os.path.join(GOLD_PRE, name)
         M = mmio.read_matrix_market(path)
-        R = scipy.io.mmread(path).tocsr()
+        R = sp.csr_matrix(scipy.io.mmread(path, spmatrix=False))
         assert M.dtype == np.float64 and M.has_sorted_indices
         assert np.abs(R.data.imag).max() == 0.0
         R = R.real.tocsr()
@@ -230,7 +231,7 @@ def test_matrix_market_round_trip_is_bit_exact(tmp_path):
     head = open(out).readline()
     assert head.startswith("%%MatrixMarket matrix coordinate complex general")
     # what the reference's reader (scipy.io.mmread + as_csr) sees
-    R = scipy.io.mmread(str(out)).tocsr()
+    R = sp.csr_matrix(scipy.io.mmread(str(out), spmatrix=False))
     assert np.array_equal(R.data.real, M.data) and np.abs(R.data.imag).max() == 0.0
     M2 = mmio.read_matrix_market(out)
     assert (M2 != M).nnz == 0 and np.array_equal(M2.data, M.data)
