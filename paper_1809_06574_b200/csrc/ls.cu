@@ -638,6 +638,10 @@ __device__ __forceinline__ double sqrt_nr(double x) {
   return fma(fma(-s, s, x), 0.5 * r, s);
 }
 
+#ifndef PMP_LSSEG_ILP
+#define PMP_LSSEG_ILP 1
+#endif
+
 template <int MR, int SEG>
 struct SegLayout {
   static constexpr int kTile = MR * SEG + 8;  // original block [MR][SEG] (+pad: bank spread)
@@ -705,12 +709,38 @@ __global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMul
     if (fast)
       for (int i = 0; i < mm; ++i) A[i * SEG + sl] = 0.0;
     __syncwarp();
+#if PMP_LSSEG_ILP
+    // batches of 8 entries per lane: every plan load of a batch, then every
+    // value gather, then the smem stores (two dependent round trips per
+    // batch instead of two per entry)
+    if (fast)
+      for (int q0 = sl; q0 < tot + tl; q0 += 8 * SEG) {
+        int ee[8], pp[8];
+        double vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u * SEG;
+          const bool ok = q < tot + tl;
+          ee[u] = ok ? ent[2 * q] : 0;
+          pp[u] = ok ? ent[2 * q + 1] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u * SEG;
+          vv[u] = pp[u] < 0 ? 0.0 : (q < tot ? avals[ee[u]] : (ee[u] < 0 ? 1.0 : P.tvals[ee[u]]));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (pp[u] >= 0) A[(pp[u] & 0xffff) * SEG + (pp[u] >> 16)] = vv[u];
+      }
+#else
     if (fast)
       for (int q = sl; q < tot + tl; q += SEG) {
         const int e = ent[2 * q], pc = ent[2 * q + 1];
         A[(pc & 0xffff) * SEG + (pc >> 16)] =
             q < tot ? avals[e] : (e < 0 ? 1.0 : P.tvals[e]);
       }
+#endif
     __syncwarp();
     double a[MR];
 #pragma unroll
@@ -726,9 +756,18 @@ __global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMul
       const bool act = fast && k < K;
       // trailing norms over rows k.. (rows > k summed first: the pivot's
       // dlarfg needs that part alone)
+#if PMP_LSSEG_ILP
+      // four interleaved partial sums: the 31-long dependent FMA chain was
+      // the step's critical path
+      double sq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = k + 1; i < MR; ++i) sq[(i - k - 1) & 3] += a[i] * a[i];
+      const double sgt = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+#else
       double sgt = 0.0;
 #pragma unroll
       for (int i = k + 1; i < MR; ++i) sgt += a[i] * a[i];
+#endif
       const bool cand = act && iscol && mypos >= k;
       double bv = cand ? a[k] * a[k] + sgt : -1.0;
       int bp = cand ? mypos : 0x7fffffff;
@@ -778,9 +817,16 @@ __global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMul
       // w = a[k] + sum_{i > k} v_i a[i];  a -= tau w v  (columns right of the
       // pivot and the right-hand side)
       if (act && tau != 0.0 && ((iscol && mypos > k) || isrhs)) {
+#if PMP_LSSEG_ILP
+        double wq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = k + 1; i < MR; ++i) wq[(i - k - 1) & 3] += RY[i] * a[i];
+        double w = (wq[0] + wq[1]) + (wq[2] + wq[3]);
+#else
         double w = 0.0;
 #pragma unroll
         for (int i = k + 1; i < MR; ++i) w += RY[i] * a[i];
+#endif
         w += a[k];
         a[k] -= tau * w;
         // re-read v (volatile) instead of holding all of it in registers:
