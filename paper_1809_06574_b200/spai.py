@@ -768,3 +768,35 @@ def spai_build(A, cfg=None, pattern=None, threads=1):
         eff = SpaiConfig(ep=cfg.ep, pattern_level=0, max_fill_per_column=cfg.max_fill_per_column)
     P, stats, _, _ = solve_columns(A, None, pat, eff)
     return Preconditioner(matrix=P), stats
+
+
+def quality(A, P):
+    """||I - A P||_F (spai.py:367-373) on the device: the identity goes
+    through the chain and A in 32-column slabs (SpMMs, never materialising
+    P), each slab's squared norm is the trace of its Gram matrix (pmp_gram);
+    one host read at the end.  Diagnostic only."""
+    A = _as_dev_csr(A)
+    Pc = P if isinstance(P, Preconditioner) else Preconditioner(matrix=P)
+    if Pc.dim != A.n:
+        raise ValueError("preconditioner does not conform with the matrix")
+    n, w = A.n, 32
+    dev = _dev()
+    E = torch.zeros((n, w), dtype=torch.float64, device=dev)
+    Z = torch.empty_like(E)
+    Y = torch.empty_like(E)
+    tmp = [torch.empty_like(E), torch.empty_like(E)] if Pc.depth > 1 else None
+    G = torch.empty((w, w), dtype=torch.float64, device=dev)
+    L = _abi.lib()
+    ws = scratch().get("quality_gram_ws", L.pmp_gram_workspace(n, w, w), zero=True)
+    acc = torch.zeros(1, dtype=torch.float64, device=dev)
+    ar = torch.arange(w, device=dev)
+    for c0 in range(0, n, w):
+        cw = min(w, n - c0)
+        E.zero_()
+        E[c0 + ar[:cw], ar[:cw]] = 1.0
+        Pc.apply_dev(_abi.ptr(E), w, cw, _abi.ptr(Z), w, tmp)
+        A.spmm(_abi.ptr(Z), w, cw, _abi.ptr(Y), w, alpha=-1.0, beta=1.0, Y0=_abi.ptr(E), ldy0=w)
+        _abi.call("pmp_gram", n, cw, _abi.ptr(Y), w, cw, _abi.ptr(Y), w, _abi.ptr(G),
+                  _abi.ptr(ws), ws.numel(), _abi.stream())
+        acc += torch.diagonal(G.view(-1)[:cw * cw].view(cw, cw)).sum()
+    return float(np.sqrt(max(float(acc.item()), 0.0)))

@@ -694,3 +694,40 @@ def test_extend_orthonormal_basis_matches_oracle(pm):
     Q2 = pm.extend_orthonormal_basis(Q, Y)
     Q2r = orc.extend_orthonormal_basis(Qr, Y)
     assert np.abs(Q2 - Q2r).max() <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# experiment CLI vs the reference's run_experiment
+# ---------------------------------------------------------------------------
+
+def test_cli_run_matches_reference_report(pm, tmp_path, monkeypatch):
+    import json
+    from paper_1809_06574_b200 import cli
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    monkeypatch.chdir(root)   # the config names the family by its relative path
+    ref = json.load(open(os.path.join(root, "tests", "golden", "cli_report.json")))
+    code = cli.main(["run", "--config", "tests/golden/cli_config.json",
+                     "--out", str(tmp_path / "run")])
+    assert code == cli.EXIT_OK
+    got = json.load(open(tmp_path / "run" / "report.json"))
+    assert got["config_hash"] == ref["config_hash"]
+    assert got["family_fingerprint"] == ref["family_fingerprint"]
+    assert len(got["records"]) == len(ref["records"])
+    for a, b in zip(got["records"], ref["records"]):
+        for key in ("step", "point_label", "level", "call_index", "n_rhs", "converged"):
+            assert a[key] == b[key], key
+        assert abs(a["iterations"] - b["iterations"]) <= 2
+        assert max(a["final_residuals"]) <= 1e-10
+    for a, b in zip(got["steps"], ref["steps"]):
+        assert a["precond_kind"] == b["precond_kind"]
+        for key in ("norm_identity_minus", "norm_first_minus"):
+            assert abs(a[key] - b[key]) <= 1e-12 * max(1.0, abs(b[key]))
+        assert abs(a["quality_norm"] - b["quality_norm"]) <= 1e-10 * b["quality_norm"]
+        assert a["build_stats"]["columns"] == b["build_stats"]["columns"]
+        assert abs(a["build_stats"]["max_residual"] - b["build_stats"]["max_residual"]) <= 1e-12
+    # the reference's compare accepts the pair
+    d = cli.compare_reports(ref, got)
+    assert len(d["steps"]) == 3
+    # the family written next to the report loads back identically
+    fam2, pts2 = cli.load_family(tmp_path / "run" / "family")
+    assert [p.values.tolist() for p in pts2] == [[0.5, 0.2], [0.8, 0.3], [1.5, 0.7]]

@@ -3,6 +3,7 @@ header declares, the host-side planning / sharding logic, and the
 multi-rank (gloo, world_size 2) broadcast / gather path."""
 
 import os
+import json
 import re
 import socket
 
@@ -252,3 +253,49 @@ def test_matrix_market_rejects_complex_values(tmp_path):
     (tmp_path / "bad.mtx").write_text("%%MatrixMarket matrix nonsense\n1 1 1\n")
     with pytest.raises(ValueError):
         mmio.read_matrix_market(tmp_path / "bad.mtx")
+
+
+# ---------------------------------------------------------------------------
+# experiment CLI: host-side pieces against the report the
+# reference's own run_experiment wrote (tests/golden/cli_report.json)
+# ---------------------------------------------------------------------------
+
+def _golden_report():
+    import json
+    return json.load(open(os.path.join(ROOT, "tests", "golden", "cli_report.json")))
+
+
+def test_cli_family_directory_loads_reference_files():
+    from paper_1809_06574_b200 import cli
+    man = os.path.join(ROOT, "tests", "golden", "cli_family")
+    import json
+    m = json.load(open(os.path.join(man, "manifest.json")))
+    terms = [cli.mmio.read_matrix_market(os.path.join(man, t)) for t in m["terms"]]
+    assert len(terms) == 3 and terms[0].shape == (144, 144)
+    pts = [cli._values_from_json(p["values"]) for p in m["points"]]
+    assert [p.real.tolist() for p in pts] == [[0.5, 0.2], [0.8, 0.3], [1.5, 0.7]]
+    # the fingerprint the reference computed, recomputed here
+    rep = _golden_report()
+    fp = cli._config_hash({"model": rep["config"]["model"],
+                           "points": [[[float(v.real), 0.0] for v in p] for p in pts]})
+    assert fp == rep["family_fingerprint"]
+    assert cli._config_hash(rep["config"]) == rep["config_hash"]
+
+
+def test_cli_report_writer_round_trip(tmp_path):
+    from paper_1809_06574_b200 import cli
+    rep = _golden_report()
+    cli.write_report(rep, tmp_path / "run")
+    recs = cli.load_records_csv(tmp_path / "run" / "report.csv")
+    assert recs == rep["records"]
+    assert (tmp_path / "run" / "summary.txt").read_text().startswith("solver=block-gcro")
+    b = json.loads(json.dumps(rep))
+    for s in b["summary"]["per_step"].values():
+        s["iterations"] -= 1
+    b["summary"]["total_iterations"] -= 3
+    d = cli.compare_reports(rep, b)
+    assert len(d["steps"]) == 3 and d["totals"]["iterations_saving_pct"] > 0
+    b["family_fingerprint"] = "x"
+    with pytest.raises(ValueError):
+        cli.compare_reports(rep, b)
+    assert cli.main(["run"]) == cli.EXIT_USAGE
