@@ -21,7 +21,7 @@ from .rpmor import (ConvergenceError, ExpansionPoint, PipelineReport, ReducedMod
                     extend_orthonormal_basis, first_moment_rhs, first_moments,
                     mgs_orthonormalize, rpmor_reduce, zeroth_moment)
 from .sequence import PrecondPolicy, SequencePreconditioner, run_sequence
-from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, spai_build,
+from .spai import (BuildStats, Preconditioner, SparsityPattern, SpaiConfig, quality, spai_build,
                    spai_column, spai_pattern)
 from .update import (UpdateConfig, SequenceStep, sequence_precondition, update_first,
                      update_first_many, update_second)

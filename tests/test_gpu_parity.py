@@ -731,3 +731,75 @@ def test_cli_run_matches_reference_report(pm, tmp_path, monkeypatch):
     # the family written next to the report loads back identically
     fam2, pts2 = cli.load_family(tmp_path / "run" / "family")
     assert [p.values.tolist() for p in pts2] == [[0.5, 0.2], [0.8, 0.3], [1.5, 0.7]]
+
+
+# ---------------------------------------------------------------------------
+# update_second chains and sequence_precondition (test_update.py:98-184 of the
+# reference, real inputs)
+# ---------------------------------------------------------------------------
+
+def _rand_sparse(n, density, seed):
+    rng = np.random.default_rng(seed)
+    M = sp.random(n, n, density=density, random_state=rng, format="csr")
+    M.data = rng.standard_normal(M.nnz)
+    return M
+
+
+def _well_conditioned(n, seed):
+    M = _rand_sparse(n, 0.1, seed)
+    d = np.asarray(abs(M).sum(axis=1)).ravel() + 1.0
+    return (M + sp.diags(d)).tocsr()
+
+
+def _seq_family(pm, n=30, seed=20):
+    return pm.AffineFamily([_well_conditioned(n, seed), _rand_sparse(n, 0.05, seed + 1),
+                            _rand_sparse(n, 0.05, seed + 2)])
+
+
+def test_update_second_chains(pm):
+    A = _well_conditioned(20, 10)
+    P1, _ = pm.spai_build(A)
+    P2, _ = pm.update_second(A, A, P1)
+    assert np.linalg.norm(P2.q.to_scipy().toarray() - np.eye(20)) <= 1e-10
+    P3, _ = pm.update_second(A, A, P2)
+    assert P3.depth == 3
+    M1 = P1.matrix.to_scipy()
+    assert np.linalg.norm((P3.materialize() - M1).toarray()) <= 1e-12 * np.linalg.norm(M1.toarray())
+    # three systems off one affine family: both strategies within 2x of a fresh build
+    fam = pm.AffineFamily([_well_conditioned(40, 12), _rand_sparse(40, 0.05, 60),
+                           _rand_sparse(40, 0.05, 61)])
+    A1, A2, A3 = (fam.evaluate(p) for p in ([1e-3, 1e-3], [2e-3, 1e-3], [2e-3, 2e-3]))
+    P1, _ = pm.spai_build(A1)
+    fresh, _ = pm.spai_build(A3)
+    first, _ = pm.update_first(A1, A3, P1)
+    prev2, _ = pm.update_second(A1, A2, P1)
+    second, _ = pm.update_second(A2, A3, prev2)
+    qf, q1, q2 = pm.quality(A3, fresh), pm.quality(A3, first), pm.quality(A3, second)
+    ref = np.linalg.norm((sp.identity(40) - A3.to_scipy() @ fresh.matrix.to_scipy()).toarray())
+    assert abs(qf - ref) <= 1e-12 * ref
+    assert q1 <= 2.0 * qf and q2 <= 2.0 * qf and q1 <= q2 + 0.1 * qf
+
+
+def test_sequence_precondition_semantics(pm):
+    fam = _seq_family(pm)
+    precs, steps = pm.sequence_precondition(fam, [pm.ExpansionPoint([1e-3, 1e-3])])
+    assert len(precs) == 1 and precs[0].kind == "explicit" and steps[0].kind == "initial"
+    fam = _seq_family(pm, seed=22)
+    pt = pm.ExpansionPoint([1e-3, -1e-3])
+    precs, steps = pm.sequence_precondition(fam, [pt, pt])
+    assert precs[1].kind == "factored" and steps[1].kind == "update"
+    assert np.linalg.norm(precs[1].q.to_scipy().toarray() - np.eye(30)) <= 1e-10
+    fam = _seq_family(pm, seed=24)
+    pts = [pm.ExpansionPoint([k * 1e-3, -k * 1e-3]) for k in range(4)]
+    precs, _ = pm.sequence_precondition(fam, pts, pm.UpdateConfig(approach="second"))
+    assert [p.depth for p in precs] == [1, 2, 3, 4]
+    precs, _ = pm.sequence_precondition(fam, pts, pm.UpdateConfig(approach="first"))
+    assert [p.depth for p in precs] == [1, 2, 2, 2]
+    fam = _seq_family(pm, seed=28)
+    pts = [pm.ExpansionPoint([0.0, 0.0]), pm.ExpansionPoint([1e-3, 2e-3])]
+    pf, _ = pm.sequence_precondition(fam, pts, pm.UpdateConfig(approach="first"))
+    ps, _ = pm.sequence_precondition(fam, pts, pm.UpdateConfig(approach="second"))
+    a, b = pf[1].q.to_scipy(), ps[1].q.to_scipy()
+    assert np.array_equal(a.data, b.data) and np.array_equal(a.indices, b.indices)
+    with pytest.raises(ValueError):
+        pm.sequence_precondition(fam, [])
