@@ -1436,7 +1436,11 @@ static int launch_seg(const LsParams& P, const LsMulti& S, cudaStream_t st) {
 
 static int launch_ls_seg(const LsParams& P, const LsMulti& S, int mcap, int ncap,
                          cudaStream_t st) {
-  if (ncap <= 7) return mcap <= 16 ? launch_seg<16, 8>(P, S, st) : launch_seg<32, 8>(P, S, st);
+  // (MR = 28 covers the 25-row interior subproblems of the 7-point
+  // stencils without 7 rows of zero padding in every unrolled row loop)
+  if (ncap <= 7)
+    return mcap <= 16 ? launch_seg<16, 8>(P, S, st)
+                      : (mcap <= 28 ? launch_seg<28, 8>(P, S, st) : launch_seg<32, 8>(P, S, st));
   return mcap <= 16 ? launch_seg<16, 16>(P, S, st) : launch_seg<32, 16>(P, S, st);
 }
 
