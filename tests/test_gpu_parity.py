@@ -803,3 +803,51 @@ def test_sequence_precondition_semantics(pm):
     assert np.array_equal(a.data, b.data) and np.array_equal(a.indices, b.indices)
     with pytest.raises(ValueError):
         pm.sequence_precondition(fam, [])
+
+
+# ---------------------------------------------------------------------------
+# affine family semantics (test_affine.py:30-90) and the quality diagnostic
+# (test_spai.py:149-164) on the device path
+# ---------------------------------------------------------------------------
+
+def test_affine_family_semantics(pm):
+    n = 25
+    A0 = _well_conditioned(n, 40)
+    T1, T2 = _rand_sparse(n, 0.1, 41), _rand_sparse(n, 0.1, 42)
+    fam = pm.AffineFamily([A0, T1, T2])
+    assert np.array_equal(fam.evaluate([0.0, 0.0]).to_scipy().toarray(), A0.toarray())
+    got = fam.evaluate([1.0, 0.0]).to_scipy().toarray()
+    assert np.abs(got - (A0 + T1).toarray()).max() <= 1e-15
+    p = np.array([0.3, -1.2])
+    dense = A0.toarray() + p[0] * T1.toarray() + p[1] * T2.toarray()
+    assert np.abs(fam.evaluate(p).to_scipy().toarray() - dense).max() <= 1e-14
+    # additivity in the point: A(p+q) - A(q) = A(p) - A(0)
+    q = np.array([-0.7, 0.4])
+    lhs = fam.evaluate(p + q).to_scipy() - fam.evaluate(q).to_scipy()
+    rhs = fam.evaluate(p).to_scipy() - fam.evaluate([0.0, 0.0]).to_scipy()
+    assert np.abs((lhs - rhs).toarray()).max() <= 1e-13
+    a, b = fam.evaluate(p).to_scipy(), fam.evaluate(p).to_scipy()
+    assert np.array_equal(a.data, b.data) and np.array_equal(a.indices, b.indices)
+    with pytest.raises(ValueError):
+        fam.evaluate([1.0])
+    with pytest.raises(ValueError):
+        pm.AffineFamily([A0, _rand_sparse(n + 1, 0.1, 1)])
+    with pytest.raises(ValueError):
+        pm.AffineFamily([A0])
+    with pytest.raises(NotImplementedError):
+        fam.evaluate([1.0 + 1.0j, 0.0])
+
+
+def test_quality_diagnostic(pm):
+    n = 30
+    A = _well_conditioned(n, 50)
+    inv = sp.csr_matrix(np.linalg.inv(A.toarray()))
+    assert pm.quality(A, pm.Preconditioner(matrix=inv)) <= 1e-12
+    tiny = sp.csr_matrix((np.full(n, 1e-300), (np.arange(n), np.arange(n))), shape=(n, n))
+    assert abs(pm.quality(A, pm.Preconditioner(matrix=tiny)) - np.sqrt(n)) <= 1e-12
+    P, _ = pm.spai_build(A)
+    q = pm.quality(A, P)
+    ref = np.linalg.norm(np.eye(n) - A.toarray() @ P.matrix.to_scipy().toarray())
+    assert abs(q - ref) <= 1e-12 * max(ref, 1.0) and q <= np.sqrt(n)
+    with pytest.raises(ValueError):
+        pm.quality(A, pm.Preconditioner.identity(n + 1))
