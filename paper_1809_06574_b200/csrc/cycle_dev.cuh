@@ -444,8 +444,13 @@ static __device__ __forceinline__ void wbar(WBar& w) {
 
 // grid_reduce (orth_dev.cuh) over the worker blocks of a group: block
 // partials in slots 1 .. n (slot 0 belongs to the control block)
-static __device__ __noinline__ void wreduce(WBar& wb, double* partial, double* gout, int K, double* G,
-                                     double* out, int split, double* out2) {
+// (out of line with the barrier state by value: a WBar& parameter of an
+// out-of-line function forced the callers' barrier state into local memory,
+// so every barrier of the step loop paid local loads / stores)
+static __device__ __noinline__ int wreduce_impl(int* ctr, int nw, int epoch, int wi, double* partial,
+                                                double* gout, int K, double* G, double* out,
+                                                int split, double* out2) {
+  WBar wb{ctr, nw, epoch, wi};
   wbar(wb);
   const int nb = wb.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int o = wb.wi + nb * wid; o < K; o += nb * (kOrthT / 32)) {
@@ -487,6 +492,12 @@ static __device__ __noinline__ void wreduce(WBar& wb, double* partial, double* g
   wbar(wb);
   for (int o = threadIdx.x; o < K; o += kOrthT) G[o] = __ldcg(gout + o);
   __syncthreads();
+  return wb.epoch;
+}
+
+static __device__ __forceinline__ void wreduce(WBar& wb, double* partial, double* gout, int K,
+                                               double* G, double* out, int split, double* out2) {
+  wb.epoch = wreduce_impl(wb.ctr, wb.n, wb.epoch, wb.wi, partial, gout, K, G, out, split, out2);
 }
 
 // step outputs, double-buffered by step parity: B (k x sb), H1, H2 (cap x
