@@ -851,6 +851,35 @@ __global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMul
         if (i < n) Z[i] = a[i];
     }
     __syncwarp();
+#if PMP_LSSEG_ILP
+    // rank (leading |R_ii| > eps |R_00|, hostls.cpp) by a segment ballot and
+    // the back substitution across the segment's lanes: lane i keeps z_i,
+    // each step broadcasts z_k / R_kk (reciprocal of lane k's diagonal) and
+    // the lanes above subtract; the fixed SEG - 1 steps keep every shuffle
+    // warp-uniform (segments have different n)
+    {
+      const double r00 = (fast && K > 0) ? fabs(RY[0]) : 0.0;
+      const bool okd = fast && sl < K && r00 > 0.0 &&
+                       (sl == 0 || fabs(RY[sl * SEG + sl]) > DBL_EPSILON * r00);
+      const unsigned bal = __ballot_sync(FULL, okd);
+      const unsigned sbits = (bal >> (seg * SEG)) & ((SEG == 32) ? 0xffffffffu : ((1u << SEG) - 1u));
+      const int r = __ffs(~sbits) - 1;
+      const bool full = fast && r == n;
+      double z = (full && sl < n) ? Z[sl] : 0.0;
+      const double rd = (full && sl < n) ? 1.0 / RY[sl * SEG + sl] : 0.0;
+#pragma unroll
+      for (int k = SEG - 2; k >= 0; --k) {
+        const double zk = __shfl_sync(FULL, z * rd, seg * SEG + k);
+        if (full && k < n) {
+          if (sl == k) z = zk;
+          else if (sl < k) z -= RY[sl * SEG + k] * zk;
+        }
+      }
+      if (full && sl < n) Z[sl] = z;
+      __syncwarp();
+      if (valid && !degen) fast = full;
+    }
+#else
     if (fast && sl == 0) {
       int r = 0;
       const double r00 = K > 0 ? fabs(RY[0]) : 0.0;
@@ -871,6 +900,7 @@ __global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMul
     }
     __syncwarp();
     if (valid && !degen) fast = wflag[seg] == 0;
+#endif
 
     // ---- coefficients (original support order) and the explicit residual
     //      t - A(J, I) z over the original block, columns in support order --
