@@ -916,11 +916,34 @@ __global__ void __launch_bounds__(256, 2) k_ls_seg(const LsParams P, const LsMul
     __syncwarp();
     double part = 0.0;
     if (fast) {
+#if PMP_LSSEG_ILP
+      // the lane's rows together (independent chains interleave); per row
+      // and for the sum over rows the same order as the row loop
+      constexpr int RU = (MR + SEG - 1) / SEG;
+      double res[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const int i = sl + u * SEG;
+        res[u] = i < mm ? A[i * SEG + n] : 0.0;
+      }
+      for (int cc = 0; cc < n; ++cc) {
+        const double zc = RY[cc];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int i = sl + u * SEG;
+          if (i < mm) res[u] -= A[i * SEG + cc] * zc;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u)
+        if (sl + u * SEG < mm) part += res[u] * res[u];
+#else
       for (int i = sl; i < mm; i += SEG) {
         double res = A[i * SEG + n];
         for (int cc = 0; cc < n; ++cc) res -= A[i * SEG + cc] * RY[cc];
         part += res * res;
       }
+#endif
     } else if (degen) {
       for (int q = sl; q < tl; q += SEG) {
         const double v = (t0 < 0) ? 1.0 : P.tvals[t0 + q];
