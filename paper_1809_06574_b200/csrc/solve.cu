@@ -161,6 +161,56 @@ __device__ __forceinline__ void fold_rowsolve(const double* w, const double* z, 
     }
 }
 
+#ifndef PMP_FOLD_EXACT
+#define PMP_FOLD_EXACT 1
+#endif
+
+#if PMP_FOLD_EXACT
+// The fold of a block whose Gram-based drop test falls inside the
+// cancellation band, column by column as the reference does it
+// (krylov.py:249-265): each image column (already projected against C twice,
+// as a block) is orthogonalised twice against the columns kept so far in
+// this fold, its norm is recomputed from the vector and the 1e-10 drop test
+// applied; kept columns go straight to C / U.  Grid reductions per column:
+// a rare path (it replaced a host re-solve of the whole system).  Out of
+// line, barrier state by value; returns the group barrier epoch, the number
+// of kept columns in *nk_out.
+template <int NY>
+__device__ __noinline__ int fold_exact(int* ctr, int nwk, int epoch, int wi, double* Cr, double* Ur,
+                                       int kc, int k, double* Wr, double* Zr, int s,
+                                       const double* w0, int na, int nr, double* red,
+                                       double* partial, double* gout, double* G, int slot,
+                                       int* nk_out) {
+  WBar wb{ctr, nwk, epoch, wi};
+  int nk = 0;
+  for (int j = 0; j < na; ++j) {
+    if (w0[j] == 0.0) continue;
+    for (int pass = 0; pass < 2 && nk > 0; ++pass) {
+      const Rows Qc{Cr + k, kc, nk, Cr + k, kc};
+      const Rows Qu{Ur + k, kc, nk, Ur + k, kc};
+      block_gram<1>(Qc, nk, Wr + j, s, 1, nr, red, partial, slot);
+      wreduce(wb, partial, gout, nk, G, nullptr, 0, nullptr);
+      block_update<1>(Qc, nk, Wr + j, s, 1, nr, G);
+      block_update<1>(Qu, nk, Zr + j, s, 1, nr, G);
+    }
+    const Rows Wj{Wr + j, s, 1, Wr + j, s};
+    block_gram<1>(Wj, 1, Wr + j, s, 1, nr, red, partial, slot);
+    wreduce(wb, partial, gout, 1, G, nullptr, 0, nullptr);
+    const double nw = sqrt(fmax(G[0], 0.0));
+    if (!(nw > 1e-10 * w0[j])) continue;
+    for (int r = threadIdx.x; r < nr; r += kOrthT) {
+      Cr[(size_t)r * kc + k + nk] = Wr[(size_t)r * s + j] / nw;
+      Ur[(size_t)r * kc + k + nk] = Zr[(size_t)r * s + j] / nw;
+    }
+    __syncthreads();
+    ++nk;
+  }
+  if (threadIdx.x == 0) *nk_out = nk;
+  __syncthreads();
+  return wb.epoch;
+}
+#endif
+
 template <bool CACHED, int NY, bool WG>
 #ifndef PMP_MINB
 #define PMP_MINB 2
@@ -721,9 +771,18 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         s_amb = amb;
       }
       __syncthreads();
-      const int nk = s_nk;
+      int nk = s_nk;
       if (s_amb) {
+#if PMP_FOLD_EXACT
+        wb.epoch = fold_exact<NY>(wb.ctr, wb.n, wb.epoch, wb.wi, C + (size_t)r0 * kc,
+                                  U + (size_t)r0 * kc, kc, k, Wr, Zr, s, w0, na, nr, red,
+                                  partial, gout, G, slot, &s_nk);
+        nk = s_nk;
+        if (threadIdx.x == 0) s_amb = 0;
+        __syncthreads();
+#else
         if (lead && threadIdx.x == 0) { ist[kStatus] = PMP_SOLVE_FALLBACK; ist[kReason] = 4; }
+#endif
       } else if (nk > 0) {
         // Q = W2[:, keep] T^-1 and the directions alike (own rows), in place
         // into the next C / U columns
