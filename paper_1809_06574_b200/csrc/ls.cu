@@ -564,15 +564,18 @@ __device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid
       for (int c = tid; c < n - k; c += T) m.w[k + 1 + c] += M[k + (size_t)(k + 1 + c) * mm];
       tm.sync();
       const int rows = mm - k, ncol = n - k;
-      for (int q = tid; q < rows * ncol; q += T) {
-        int i = k + q % rows;
-        int jj = k + 1 + q / rows;
-        double wj = m.w[jj];
-        if (i == k)
-          M[k + (size_t)jj * mm] -= tau * wj;
-        else
-          M[i + (size_t)jj * mm] -= tau * wj * M[i + (size_t)k * mm];
-      }
+      // threads over the window's rows (v_k = 1 implicitly), column groups
+      // when the window is shorter than the team: one division per step
+      // instead of a division and a modulo per element; same arithmetic
+      const int tpc = rows < T ? rows : T, ngr = T / tpc;
+      const int r = tid % tpc, g = tid / tpc;
+      if (g < ngr)
+        for (int i0 = r; i0 < rows; i0 += tpc) {
+          const int i = k + i0;
+          const double vi = (i0 == 0) ? 1.0 : M[i + (size_t)k * mm];
+          for (int jj = k + 1 + g; jj <= k + ncol; jj += ngr)
+            M[i + (size_t)jj * mm] -= tau * m.w[jj] * vi;
+        }
       tm.sync();
     }
   }
