@@ -239,14 +239,21 @@ class SecondOrderModel:
         u, recipe, s = self._recipe(s, pvals)
         return u.run(recipe, 0, s)
 
-    def assemble_many(self, points):
+    def assemble_many(self, points, defer_zero_check=False):
         """assemble(s, p) for every (s, p) in ``points`` with ONE host
         synchronisation (the exact-zero counts of all systems are read
         together), so a window of systems is enqueued without stalling the
-        device between them."""
+        device between them.
+
+        ``defer_zero_check``: no synchronisation at all -- every system is
+        returned on the union structure and the device tensor of exact-zero
+        counts comes back too: ``(systems, counts)``.  The caller must check
+        the counts before trusting the systems (a non-zero count means the
+        reference's ``as_csr`` would drop entries: re-assemble without
+        deferral)."""
         points = list(points)
         if not points:
-            return []
+            return ([], None) if defer_zero_check else []
         zc = torch.zeros(len(points), dtype=torch.int32, device=_dev())
         u = self._union()
         recs = [self._recipe(s, p) for s, p in points]
@@ -262,6 +269,8 @@ class SecondOrderModel:
             raws += u.run_many([r[1] for r in recs[i:j]], 0, [r[2] for r in recs[i:j]],
                                zc[i:j])
             i = j
+        if defer_zero_check:
+            return [u.finish(r, 0) for r in raws], zc
         counts = zc.cpu().numpy()
         return [u.finish(r, int(c)) for r, c in zip(raws, counts)]
 

@@ -293,23 +293,43 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
         window = max(batch, int(window))
         for c0 in range(0, len(todo), window):
             chunk = todo[c0:c0 + window]
-            built = []
-            t0 = mark()
-            As = model.assemble_many([points[idx] for idx in chunk])
-            t1 = mark()
-            # (the window's assembly and its build are one phase each: charged
-            # to the window's first system)
-            pres = seq.for_systems(As)
-            t2 = mark()
-            for j, (idx, A, (P, _, label, _)) in enumerate(zip(chunk, As, pres)):
-                if j == 0:
-                    built.append((idx, A, P, label, t0, t1, t2, t1))
+
+            def run_window(defer):
+                built = []
+                t0 = mark()
+                pts_ = [points[idx] for idx in chunk]
+                if defer:
+                    As, zc = model.assemble_many(pts_, defer_zero_check=True)
                 else:
-                    built.append((idx, A, P, label, None, None, None, None))
-            t3 = mark()
-            res = block_gcro_solve_batch([(b[1], b[2]) for b in built], Bd,
-                                         cfg=solver_cfg, groups=batch)
-            t4 = mark()
+                    As, zc = model.assemble_many(pts_), None
+                t1 = mark()
+                # (the window's assembly and its build are one phase each:
+                # charged to the window's first system)
+                pres = seq.for_systems(As)
+                t2 = mark()
+                for j, (idx, A, (P, _, label, _)) in enumerate(zip(chunk, As, pres)):
+                    if j == 0:
+                        built.append((idx, A, P, label, t0, t1, t2, t1))
+                    else:
+                        built.append((idx, A, P, label, None, None, None, None))
+                t3 = mark()
+                res = block_gcro_solve_batch([(b[1], b[2]) for b in built], Bd,
+                                             cfg=solver_cfg, groups=batch)
+                t4 = mark()
+                return built, res, t3, t4, zc
+
+            # the window is enqueued without a host synchronisation: its
+            # systems are assembled on the union structure and the exact-zero
+            # counts are checked once the solves are back; a window with an
+            # exact zero (the reference's as_csr drops it: compacted
+            # structures) is redone from the same preconditioner state
+            seq_state = (seq._initial_system, seq._initial_pre, seq._prev_system,
+                         seq._prev_pre)
+            built, res, t3, t4, zc = run_window(True)
+            if int(zc.max().item()) > 0:
+                (seq._initial_system, seq._initial_pre, seq._prev_system,
+                 seq._prev_pre) = seq_state
+                built, res, t3, t4, _ = run_window(False)
             for (idx, A, P, label, t0, t1, t2, ta), (X, rep) in zip(built, res):
                 s, p = points[idx]
                 rec = {"index": idx, "sigma": float(s), "p": [float(v) for v in p],

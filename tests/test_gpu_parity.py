@@ -884,3 +884,30 @@ def test_fold_cancellation_band_stays_on_device(pm):
         X = r["X"].cpu().numpy() if torch.is_tensor(r["X"]) else r["X"]
         rel = np.linalg.norm(W.rhs - A @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
         assert rel.max() <= 1e-8, rel.max()
+
+
+def test_window_with_exact_zeros_matches_per_system_path(pm):
+    """The batched window is enqueued without a host synchronisation and its
+    exact-zero counts are checked after the solves; systems whose assembled
+    values cancel exactly (the reference's as_csr drops them) must come out
+    as on the per-system path, also when the cancelling system is the
+    sequence's first (the SPAI base)."""
+    n = 64
+    K0 = sp.diags([np.ones(n - 1), 4 * np.ones(n), np.ones(n - 1)], (-1, 0, 1)).tocsr()
+    K1 = sp.diags([np.ones(n - 1), np.ones(n - 1)], (-1, 1)).tocsr()
+    M = sp.identity(n, format="csr")
+    B = np.random.default_rng(9).standard_normal((n, 3))
+    model = pm.SecondOrderModel.from_mdk([M], None, [K0, K1], rhs=B)
+    pol = pm.PrecondPolicy("spai-update-first", spai=pm.SpaiConfig(pattern_level=0),
+                           update=pm.UpdateConfig(pattern_level=0))
+    cfg = pm.SolverConfig(tol=1e-10)
+    for p_grid in ([0.5, -1.0, 0.25], [-1.0, 0.5]):
+        got, _ = pm.run_sequence(model, [0.5, 1.0], p_grid, pol, cfg, batch=6, timing=False,
+                                 keep_solutions=True)
+        ref, _ = pm.run_sequence(model, [0.5, 1.0], p_grid, pol, cfg, batch=1, timing=False,
+                                 keep_solutions=True)
+        for a, b in zip(got, ref):
+            assert a["iterations"] == b["iterations"], (p_grid, a["index"])
+            Xa = a["X"].cpu().numpy() if hasattr(a["X"], "cpu") else a["X"]
+            Xb = b["X"].cpu().numpy() if hasattr(b["X"], "cpu") else b["X"]
+            assert np.linalg.norm(Xa - Xb) <= 1e-12 * np.linalg.norm(Xb)
