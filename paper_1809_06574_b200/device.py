@@ -27,9 +27,17 @@ from . import _abi
 _ids = itertools.count(1)
 
 
+_CUDA_OK = False
+
+
 def _dev():
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_1809_06574_b200 needs a CUDA device (B200); no CPU fallback")
+    # (the availability probe goes through NVML on every call -- ~5 us, a
+    # few hundred times per sequence step -- so it is done once)
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1809_06574_b200 needs a CUDA device (B200); no CPU fallback")
+        _CUDA_OK = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
