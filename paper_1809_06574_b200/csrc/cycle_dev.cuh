@@ -535,8 +535,20 @@ static __device__ __forceinline__ int wait_flag(const int* f, int cmp_ge) {
 
 // The control block: absorb each published step while the workers run the
 // next one; post its decision (0 continue, 1 converged, 4 G deficient).
+#ifndef PMP_CTL_NOINLINE
+#define PMP_CTL_NOINLINE 1
+#endif
+#if PMP_CTL_NOINLINE
+// (out of line, the state block by value: the control block's code no
+// longer shares a register allocation with the workers' step loop)
+#define PMP_CTL_RUN_ATTR __noinline__
+#define PMP_CTL_REF
+#else
+#define PMP_CTL_RUN_ATTR
+#define PMP_CTL_REF &
+#endif
 template <int NY>
-__device__ void ctl_run(const CycleArgs& P, const Ctl& S) {
+__device__ PMP_CTL_RUN_ATTR void ctl_run(const CycleArgs& P, const Ctl PMP_CTL_REF S) {
   const int sb = P.sb;
   int hrow = 0, j = 0, total = P.ist[1];
   __shared__ int s_go;
