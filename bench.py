@@ -201,7 +201,8 @@ def run_ours(args):
     # inside each native block step (events recorded in the C driver)
     dominant = ("pmp_solve_batch", "k_orth", "pmp_ls_columns", "pmp_ls_columns_planned", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
                 "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm", "pmp_copy_cols",
-                "pmp_axpby_cols", "pmp_assemble", "pmp_permute", "pmp_ls_columns_multi",
+                "pmp_axpby_cols", "pmp_assemble", "pmp_permute", "pmp_permute_batch",
+                "pmp_ls_columns_multi",
                 "pmp_assemble_multi")
     _abi.count_launches(True)
     recs_all = None

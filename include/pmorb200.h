@@ -94,6 +94,11 @@ int pmp_transpose(int n, int nnz, const int32_t* d_ptr, const int32_t* d_idx,
                   void* stream);
 /* d_dst[d_perm[e]] = d_src[e] for d_perm[e] >= 0 */
 int pmp_permute(int nnz, const int32_t* d_perm, const double* d_src, double* d_dst, void* stream);
+/* pmp_permute over k value arrays in one launch (the factors of a window of
+ * SPAI updates sharing one pattern, spai.py:307 per factor):
+ * d_dst[q*dst_stride + d_perm[e]] = d_src[q*src_stride + e], 0 <= q < k <= 65535 */
+int pmp_permute_batch(int nnz, const int32_t* d_perm, int k, const double* d_src,
+                      long long src_stride, double* d_dst, long long dst_stride, void* stream);
 
 /* ---- kernel 2: SPAI pattern gather (spai_pattern level 0, spai.py:182-207)
  * I_j = rows(A(:, j)) U {j} for an n x n matrix in CSC. */

@@ -38,6 +38,7 @@ _SIGS = {
     "pmp_transpose": ([c_int, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
                        c_vp], c_int),
     "pmp_permute": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_permute_batch": ([c_int, c_vp, c_int, c_vp, ctypes.c_longlong, c_vp, ctypes.c_longlong, c_vp], c_int),
     "pmp_pattern_l0_workspace": ([c_int], c_sz),
     "pmp_pattern_l0": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),
     "pmp_pattern_l0_ptr": ([c_int, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], c_int),

@@ -123,6 +123,16 @@ __global__ void k_permute(int nnz, const int* perm, const double* src, double* d
   if (p >= 0) dst[p] = src[e];
 }
 
+// k value arrays through one permutation (a window of factors sharing one
+// pattern): blockIdx.y selects the array; perm stays L2-resident across y.
+__global__ void k_permute_batch(int nnz, const int* perm, const double* src, long long sstride,
+                                double* dst, long long dstride) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  int p = perm[e];
+  if (p >= 0) dst[blockIdx.y * dstride + p] = src[blockIdx.y * sstride + e];
+}
+
 // ---------------------------------------------------------------------------
 // level-0 pattern: I_j = rows(A(:, j)) U {j}
 // ---------------------------------------------------------------------------
@@ -317,6 +327,18 @@ int pmp_permute(int nnz, const int32_t* perm, const double* src, double* dst, vo
   if (nnz <= 0) return PMP_OK;
   k_permute<<<ceil_div(nnz, 256), 256, 0, S(st)>>>(nnz, perm, src, dst);
   return cuda_status("pmp_permute");
+}
+
+int pmp_permute_batch(int nnz, const int32_t* perm, int k, const double* src, long long sstride,
+                      double* dst, long long dstride, void* st) {
+  if (nnz < 0 || k < 0 || k > 65535) {
+    set_error("pmp_permute_batch: bad nnz / k");
+    return PMP_ERR_ARG;
+  }
+  if (nnz == 0 || k == 0) return PMP_OK;
+  dim3 grid(ceil_div(nnz, 256), k);
+  k_permute_batch<<<grid, 256, 0, S(st)>>>(nnz, perm, src, sstride, dst, dstride);
+  return cuda_status("pmp_permute_batch");
 }
 
 size_t pmp_pattern_l0_workspace(int n) {

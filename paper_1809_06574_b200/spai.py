@@ -632,10 +632,14 @@ def solve_columns_many(systems, target, pattern, cfg):
     if target is not None:
         tcolptr, trowidx, tvals = target.csc()
     tiers = _get_tiers(pattern, A0, target)
-    coefs = [torch.empty(max(pattern.nnz, 1), dtype=torch.float64, device=_dev())
-             for _ in range(k)]
-    resids = [torch.empty(n, dtype=torch.float64, device=_dev()) for _ in range(k)]
-    flags = [torch.zeros(n, dtype=torch.int32, device=_dev()) for _ in range(k)]
+    # one [k, nnz] block: the factors leave it through one batched permute
+    nz = max(pattern.nnz, 1)
+    coef_block = torch.empty((k, nz), dtype=torch.float64, device=_dev())
+    coefs = [coef_block[q] for q in range(k)]
+    resid_block = torch.empty((k, n), dtype=torch.float64, device=_dev())
+    flag_block = torch.zeros((k, n), dtype=torch.int32, device=_dev())  # one fill, not k
+    resids = [resid_block[q] for q in range(k)]
+    flags = [flag_block[q] for q in range(k)]
     csc_vals = [A.csc()[2] for A in systems]
     VP = ctypes.c_void_p * k
     h_avals = VP(*[v.data_ptr() for v in csc_vals])
@@ -664,8 +668,13 @@ def solve_columns_many(systems, target, pattern, cfg):
         _abi.note_launches(extra - 1)
         t.plan_ready = True
     out = []
+    csr, perm = _csr_plan(pattern)
+    val_block = torch.empty((k, nz), dtype=torch.float64, device=_dev())
+    if pattern.nnz:
+        _abi.call("pmp_permute_batch", pattern.nnz, _abi.ptr(perm), k, _abi.ptr(coef_block), nz,
+                  _abi.ptr(val_block), nz, st)
     for q in range(k):
-        P = _factor_from_columns(pattern, coefs[q])
+        P = DeviceCSR(csr, val_block[q, :pattern.nnz], symmetric=False)
         out.append((P, (resids[q], flags[q])))
     ev1.record()
     return [(P, BuildStats(r, f, 0, (ev0, ev1), share=k)) for P, (r, f) in out]

@@ -531,6 +531,30 @@ def test_update_first_many_bitwise(pm):
         G.compare_factor(Pm.q.to_scipy(), Q)
 
 
+def test_permute_batch_matches_single(pm):
+    """pmp_permute_batch (a window's factors in one launch) == pmp_permute
+    per array, bitwise, with strided rows; k = 0 / nnz = 0 are no-ops."""
+    from paper_1809_06574_b200 import _abi
+    g = torch.Generator().manual_seed(7)
+    nnz, k, stride = 1237, 5, 1300
+    perm = torch.randperm(nnz, generator=g).to(torch.int32).cuda()
+    src = torch.randn(k, stride, generator=g, dtype=torch.float64).cuda()
+    dst = torch.full((k, stride), -1.0, dtype=torch.float64, device="cuda")
+    _abi.call("pmp_permute_batch", nnz, _abi.ptr(perm), k, _abi.ptr(src), stride,
+              _abi.ptr(dst), stride, _abi.stream())
+    for q in range(k):
+        ref = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        _abi.call("pmp_permute", nnz, _abi.ptr(perm), _abi.ptr(src[q]), _abi.ptr(ref),
+                  _abi.stream())
+        assert torch.equal(dst[q, :nnz], ref)
+        assert torch.all(dst[q, nnz:] == -1.0)
+    _abi.call("pmp_permute_batch", nnz, _abi.ptr(perm), 0, _abi.ptr(src), stride,
+              _abi.ptr(dst), stride, _abi.stream())
+    _abi.call("pmp_permute_batch", 0, _abi.ptr(perm), k, _abi.ptr(src), stride,
+              _abi.ptr(dst), stride, _abi.stream())
+    torch.cuda.synchronize()
+
+
 def test_assemble_many_bit_exact(pm):
     """A window assembled in multi-system launches == one system at a time,
     bitwise (symmetric and unsymmetric terms; a zero parameter changes the
