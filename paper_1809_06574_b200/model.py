@@ -128,13 +128,17 @@ class _UnionTerms:
         first = np.array([f for _, _, f, _ in r0], dtype=np.int32)
         coef = np.array([[c for _, _, _, c in r] for r in recipes], dtype=np.float64)
         sv = np.asarray(svals, dtype=np.float64)
-        outs = [torch.empty(max(st.nnz, 1), dtype=torch.float64, device=_dev())[:st.nnz]
-                for _ in range(k)]
+        # one [k, nnz] block per output (one allocation, not k): the window's
+        # systems live and die together
+        nz = -(-max(st.nnz, 1) // 32) * 32   # rows 256-byte aligned
+        block = torch.empty((k, nz), dtype=torch.float64, device=_dev())
+        outs = [block[q, :st.nnz] for q in range(k)]
         perm = None
         outs_perm = [None] * k
         if not self.symmetric:
             perm = st.csc()[2]
-            outs_perm = [torch.empty_like(o) for o in outs]
+            pblock = torch.empty((k, nz), dtype=torch.float64, device=_dev())
+            outs_perm = [pblock[q, :st.nnz] for q in range(k)]
         VP = ctypes.c_void_p * k
         h_out = VP(*[o.data_ptr() for o in outs])
         h_perm = VP(*[o.data_ptr() for o in outs_perm]) if perm is not None else None

@@ -633,13 +633,14 @@ def solve_columns_many(systems, target, pattern, cfg):
         tcolptr, trowidx, tvals = target.csc()
     tiers = _get_tiers(pattern, A0, target)
     # one [k, nnz] block: the factors leave it through one batched permute
-    nz = max(pattern.nnz, 1)
+    nz = -(-max(pattern.nnz, 1) // 32) * 32   # rows 256-byte aligned
     coef_block = torch.empty((k, nz), dtype=torch.float64, device=_dev())
     coefs = [coef_block[q] for q in range(k)]
-    resid_block = torch.empty((k, n), dtype=torch.float64, device=_dev())
-    flag_block = torch.zeros((k, n), dtype=torch.int32, device=_dev())  # one fill, not k
-    resids = [resid_block[q] for q in range(k)]
-    flags = [flag_block[q] for q in range(k)]
+    nr = -(-max(n, 1) // 64) * 64
+    resid_block = torch.empty((k, nr), dtype=torch.float64, device=_dev())
+    flag_block = torch.zeros((k, nr), dtype=torch.int32, device=_dev())  # one fill, not k
+    resids = [resid_block[q, :n] for q in range(k)]
+    flags = [flag_block[q, :n] for q in range(k)]
     csc_vals = [A.csc()[2] for A in systems]
     VP = ctypes.c_void_p * k
     h_avals = VP(*[v.data_ptr() for v in csc_vals])
