@@ -1217,6 +1217,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     args.d_result_log = rdbl.data_ptr()
     args.stream = _abi.stream()
     stream = torch.cuda.current_stream()
+    X_block = torch.empty(nsys, n, s, dtype=torch.float64, device=dev)   # one allocation
     Xs = []
     keep = []   # device operands must outlive the launch
     for i, (A, P) in enumerate(systems):
@@ -1232,7 +1233,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
             d.fac_vals[j] = F.vals.data_ptr()
         d.a_rowptr, d.a_colidx, d.a_vals = (st.rowptr.data_ptr(), st.colidx.data_ptr(),
                                             A.vals.data_ptr())
-        X = torch.empty(n, s, dtype=torch.float64, device=dev)
+        X = X_block[i]
         Xs.append(X)
         d.B, d.X = Bd.data_ptr(), X.data_ptr()
     ctypes.memmove(h_sys.data_ptr(), ctypes.addressof(sysd), ctypes.sizeof(sysd))
@@ -1273,8 +1274,8 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
             seg = flat[o:o + 1 + rows_ * s]
             o += seg.size
             rep = SolveReport()
-            hist = seg[1:].reshape(rows_, s)
-            rep.residual_history = [row.copy() for row in hist]
+            # one copy per system; the history rows are views of it
+            rep.residual_history = list(seg[1:].reshape(rows_, s).copy())
             rep.iterations = int(recs[i, 2])
             rep.converged = int(recs[i, 3]) == 0
             rep.matvec_count = int(recs[i, 5])
