@@ -1,26 +1,41 @@
 """Benchmark: the parametric SPAI / SPAI-update / block-GCRO sequence on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
-One step = one full pass of BASELINE config c2 (configs[1]):
-for each of its 40 (sigma, p) systems in pmor_l_sequence order, assemble
-A(sigma, p) = s^2 M(p) + s D(p) + K(p) on the device, build the SPAI
-(system 1) or the SPAI update (systems 2..40, update_first), and solve the
-n x 8 block to 1e-8 with block GCRO.  Inputs (the model's terms and B) are
-resident in HBM when the timed region starts; the L2 (126 MB > the c2
-working set) is flushed before every step by writing a 256 MB buffer.
+Workload (default): BASELINE config c4 (configs[3], the largest one that
+fits one GPU): 3D 128^3 grid, n = 2,097,152, 512 (sigma, p)
+systems in pmor_l_sequence order, B n x 8.  One step = one COLD pass of
+the whole sequence: the model's symbolic caches (level-0 pattern, its
+transpose plan, the least-squares size plans and recorded symbolic plans)
+are dropped first, so every step pays them again, as a new sequence does;
+then every system is assembled on the device, system 1 gets the SPAI and
+systems 2..512 the SPAI update (update_first), and every n x 8 block is
+solved to 1e-8 by block GCRO.  Inputs (the model's term values and B) are
+resident in HBM when the timed region starts; the working set (tens of GB)
+is far larger than the 126 MB L2, and the L2 is also flushed before every
+step by writing a 256 MB buffer.
 
-metric "SPAI(+update) columns/s": value = (n * systems) / sequence seconds,
-i.e. SPAI + update columns delivered per second of the WHOLE sequence
-(assembly + builds + solves); ms_per_step is the sequence time itself, the
-other half of BASELINE.json's metric.  Build-only columns/s is reported as
-"spai_update_columns_per_s".
+metric "SPAI(+update) columns/s": value = (n * systems) / sequence seconds
+-- SPAI + update columns delivered per second of the WHOLE sequence
+(assembly + builds + solves); ms_per_step is the cold sequence time, the
+other half of BASELINE.json's metric.  Also reported:
+``spai_columns_per_s`` = n / spai_build time (device A -> device P, cold:
+pattern, plan and transpose included), ``update_columns_per_s`` = n /
+update_first time (one system), ``update_window_columns_per_s`` (the
+sequence's batched update_first_many), ``warm_ms_per_step`` (symbolic
+caches kept).
 
---impl reference times the CPU oracle (oracle/pmor_oracle.py, a restatement
-of the reference's numpy/scipy path, "port") on this host's cores: each
-step is a bounded sample -- one update_first system (all n columns, column
-chunks over a process pool) plus its block solve -- reported in the same
-columns/s unit.
+Multi-GPU: ``--gpus N`` without a torchrun environment re-executes itself
+under ``torch.distributed.run`` with N ranks.  Systems are dealt
+round-robin over the ranks (fixed total work: "scaling": "strong"), the base
+SPAI is built column-sharded and all-gathered over NCCL (pmp_nccl_*), the
+per-system records are summed over ranks; the step time is the max over
+ranks of CUDA-event time.
+
+--impl reference: the CPU oracle (oracle/pmor_oracle.py, a restatement of
+the reference's numpy/scipy path: "port") on this host's cores, on the same
+config / metric, each step a bounded sample (see ``cpu_sample``):
+extrapolated to the whole sequence and labelled so.
 """
 
 import argparse
@@ -38,23 +53,28 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SPAI(+update) columns/s"
 UNIT = "columns/s"
+CPU_SAMPLE_COLUMNS = 20000
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2,
+                    help="timed end-to-end steps (after one warm-up step)")
+    ap.add_argument("--warm", action="store_true", default=True,
+                    help="also time one step with the symbolic caches kept")
+    ap.add_argument("--no-warm", dest="warm", action="store_false")
     ap.add_argument("--systems", type=int, default=0, help="limit #systems (debug)")
-    ap.add_argument("--workers", type=int, default=1,
-                    help="host threads / CUDA streams driving independent systems "
-                         "(per-system path, --batch 1)")
     ap.add_argument("--batch", type=int, default=6,
-                    help="systems per persistent solve launch (1 = per-system path)")
+                    help="block groups (systems in flight) per persistent solve launch")
+    ap.add_argument("--cpu-solve-iters", type=int, default=5,
+                    help="block steps of the truncated CPU solve sample")
     return ap.parse_args()
 
 
@@ -63,6 +83,21 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -83,7 +118,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -128,29 +163,59 @@ class ClockSampler:
 def workload(cfg, systems=0):
     from paper_1809_06574_b200.workloads import make_config
     W = make_config(cfg)
-    pts = W.points()
+    s_grid, p_grid = list(W.s_grid), list(W.p_grid)
     if systems:
-        pts = pts[:systems]
-    return W, pts
+        s_grid, p_grid = s_grid[:1], p_grid[:systems]
+    pts = [(s, np.atleast_1d(np.asarray(p, dtype=np.float64))) for s in s_grid for p in p_grid]
+    return W, s_grid, p_grid, pts
 
 
-def peaks():
+def config_dict(args, W, nsys, world):
+    """The workload description both arms print (identical keys/values)."""
+    return {"workload": "c%d" % args.config, "n": int(W.n), "systems": int(nsys),
+            "rhs_block": int(W.rhs.shape[1]), "pattern_level": int(W.pattern_level),
+            "precond": "spai-update-first", "tol": 1e-8,
+            "step": "cold sequence (symbolic caches rebuilt every step)",
+            "l2": "working set >> 126 MB L2; L2 also flushed before every step (256 MB write)",
+            "parallelism": "systems round-robin over %d GPU(s), base SPAI column-sharded" % world}
+
+
+def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# algorithmic bytes per launch of the dominant kernel families
 def ls_flops(m, n):
+    """Householder QR + Q^T b + back substitution of an m x n LS problem."""
     return 2.0 * m * n * n - (2.0 / 3.0) * n ** 3 + 4.0 * m * n - n * n
+
+
+def fp64_peaks():
+    """Live DFMA / DMMA peaks of this GPU (pmp_fp64_peak)."""
+    import ctypes
+    from paper_1809_06574_b200 import _abi
+    out = {}
+    for kind, name in ((0, "dfma_tflops"), (1, "dmma_tflops")):
+        v = ctypes.c_double()
+        _abi.check(_abi.lib().pmp_fp64_peak(kind, 2000, ctypes.byref(v), _abi.stream()),
+                   "pmp_fp64_peak")
+        out[name] = v.value
+    return out
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+
+TIMED_KERNELS = ("pmp_solve_batch", "pmp_ls_columns_multi", "pmp_ls_columns_planned",
+                 "pmp_ls_columns", "pmp_assemble_multi", "pmp_assemble", "pmp_permute",
+                 "pmp_permute_batch", "pmp_transpose", "pmp_pattern_l0", "pmp_pattern_l0_ptr",
+                 "pmp_ls_bound")
+
 
 def run_ours(args):
     import torch
@@ -161,14 +226,10 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    W, pts = workload(args.config, args.systems)
-    s_grid, p_grid = W.s_grid, W.p_grid
-    if args.systems:
-        s_grid, p_grid = W.s_grid[:1], W.p_grid[:args.systems]
-    nsys = len(s_grid) * len(p_grid)
+    W, s_grid, p_grid, pts = workload(args.config, args.systems)
+    nsys = len(pts)
     n = W.n
     model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
                                          rhs=W.rhs)
@@ -179,10 +240,11 @@ def run_ours(args):
     Bd = torch.as_tensor(np.ascontiguousarray(W.rhs), device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    def step():
+    def step(cold=True):
+        if cold:
+            model.reset_symbolic()
         return pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
-                               group=group, timing=True, workers=args.workers,
-                               batch=args.batch)
+                               timing=True, batch=args.batch)
 
     def barrier():
         if world > 1:
@@ -195,16 +257,10 @@ def run_ours(args):
     barrier()
     clk = ClockSampler(local)
     clk.start()
-    step_ms = []
-    infos = []
-    # per-kernel device time: "k_orth" = the fused orthogonalisation kernel
-    # inside each native block step (events recorded in the C driver)
-    dominant = ("pmp_solve_batch", "k_orth", "pmp_ls_columns", "pmp_ls_columns_planned", "pmp_fold", "pmp_gcro_cycle_end", "pmp_orth_step",
-                "pmp_tsqr_r", "pmp_gram", "pmp_spmm", "pmp_tsmm", "pmp_copy_cols",
-                "pmp_axpby_cols", "pmp_assemble", "pmp_permute", "pmp_permute_batch",
-                "pmp_ls_columns_multi",
-                "pmp_assemble_multi")
-    _abi.count_launches(True)
+    step_ms, infos = [], []
+    # every ABI call of the timed steps counted; the candidate kernels are
+    # bracketed by CUDA events on the launching (current) stream
+    _abi.count_launches(True, timed=TIMED_KERNELS)
     recs_all = None
     for k in range(args.steps):
         flush.zero_()
@@ -220,73 +276,74 @@ def run_ours(args):
         recs_all = recs
     launches = _abi.launches()
     counters = dict(_abi.COUNTERS)
-    _abi.count_launches(False)
-    clocks = clk.stop()
-    # one extra, untimed step with CUDA events around every launch of the
-    # candidate kernels (per-kernel device time and share of the step)
-    flush.zero_()
-    barrier()
-    _abi.count_launches(True, timed=dominant)
-    i0 = torch.cuda.Event(enable_timing=True)
-    i1 = torch.cuda.Event(enable_timing=True)
-    i0.record()
-    # single stream, so each event pair brackets one kernel and nothing else
-    recs_i, _ = pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
-                                group=group, timing=True, workers=1, batch=args.batch)
-    i1.record()
-    barrier()
-    instr_ms = i0.elapsed_time(i1)
     timed = dict(_abi.timed_events())
     _abi.count_launches(False)
-    t_local = float(np.sum(step_ms))
-    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    clocks = clk.stop()
+    t = torch.tensor([float(np.sum(step_ms))], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = n * nsys * args.steps / (total_ms / 1e3)
+    step_local = float(np.sum(step_ms))
 
-    # per-kernel device time over the timed region (events around each call)
     kern = {}
     for name, lst in timed.items():
         ms = [a.elapsed_time(b) for a, b, _ in lst]
-        kern[name] = {"launches": len(ms), "total_ms": float(np.sum(ms)),
-                      "avg_us": float(np.mean(ms) * 1e3) if ms else 0.0,
-                      "share_of_step": float(np.sum(ms)) / instr_ms}
-    build_s = float(np.mean([i["build_s"] for i in infos]))
-    solve_s = float(np.mean([i["solve_s"] for i in infos]))
-    asm_s = float(np.mean([i["assemble_s"] for i in infos]))
-    cols = infos[-1]["build_columns"]
+        kern[name] = {"launches": len(ms), "launches_per_step": len(ms) / args.steps,
+                      "total_ms": float(np.sum(ms)), "avg_us": float(np.mean(ms) * 1e3),
+                      "share_of_step": float(np.sum(ms)) / step_local}
+    phase = {k: float(np.mean([i[k + "_s"] for i in infos])) for k in ("assemble", "build",
+                                                                       "solve")}
     iters = [r["iterations"] for r in recs_all]
     conv = all(r["converged"] for r in recs_all)
+    if world > 1:
+        allrec = infos[-1].get("records_all") or []
+        iters = [r["iterations"] for r in allrec] or iters
+        conv = all(r["converged"] for r in allrec) if allrec else conv
 
-    roof = roofline(kern, timed, n, W, model, recs_i)
-    roof_ls = roofline_ls(kern, model, nsys)
+    warm = None
+    if args.warm:
+        flush.zero_()
+        barrier()
+        w0 = torch.cuda.Event(enable_timing=True)
+        w1 = torch.cuda.Event(enable_timing=True)
+        w0.record()
+        step(cold=False)
+        w1.record()
+        barrier()
+        warm = w0.elapsed_time(w1)
+        tw = torch.tensor([warm], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        warm = float(tw.item())
+
+    rates = build_rates(pm, model, pts, pol, barrier, torch)
+    peaks = fp64_peaks()
+    roof = roofline(kern, timed, recs_all, args.steps)
+    roof_ls = roofline_ls(kern, model, nsys / world, args.steps, peaks)
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, group, barrier)
+        e2e = run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, barrier)
 
     line = None
     if rank == 0:
-        hbm, _ = peaks()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded generator, SURVEY.md 8.1)",
-            "config": {"workload": "c%d" % args.config, "n": n, "systems": nsys,
-                       "rhs_block": int(W.rhs.shape[1]), "pattern_level": level,
-                       "precond": "spai-update-first", "tol": 1e-8,
-                       "l2": "flushed before every step (256 MB write)",
-                       "parallelism": "systems round-robin over %d GPU(s); %s" % (
-                           world, ("%d systems per persistent solve launch" % args.batch)
-                           if args.batch > 1 else "%d concurrent streams" % args.workers)},
+            "config": config_dict(args, W, nsys, world),
             "sequence_s": ms_per_step / 1e3,
-            "phases_s": {"assemble": asm_s, "build": build_s, "solve": solve_s},
-            "spai_update_columns_per_s": cols / build_s if build_s > 0 else None,
+            "warm_ms_per_step": warm,
+            "phases_s": phase,
+            "spai_columns_per_s": rates["spai_columns_per_s"],
+            "update_columns_per_s": rates["update_columns_per_s"],
+            "update_window_columns_per_s": rates["update_window_columns_per_s"],
+            "build_rates_detail": rates,
             "iterations": {"min": int(min(iters)), "max": int(max(iters)),
-                           "mean": float(np.mean(iters))},
+                           "mean": float(np.mean(iters)), "systems": len(iters)},
             "converged": conv,
             "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches) // args.steps,
@@ -294,79 +351,96 @@ def run_ours(args):
             "kernels": kern,
             "roofline": roof,
             "roofline_ls": roof_ls,
+            "fp64_peaks_measured": peaks,
             "clocks": clocks,
         }
         if e2e is not None:
             line["e2e"] = e2e
-        if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args, W, pts)
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args, W, pts, model, pol, iters)
     if world > 1:
         dist.destroy_process_group()
     return line
 
 
-def roofline(kern, timed, n, W, model, recs=None):
-    """Dominant kernel vs its roofline.  Candidates: the persistent solve
-    kernel and the n-sized Krylov kernels (HBM; algorithmic bytes) and the
-    batched LS kernel (FP64 pipe)."""
-    hbm, which = peaks()
-    if not kern:
+def build_rates(pm, model, pts, pol, barrier, torch, reps=3):
+    """SPAI columns/s = n / spai_build (device A -> device P,
+    cold symbolic state: pattern, plans and transpose included); update
+    columns/s = n / update_first of one system; the window rate of the
+    sequence's batched update_first_many.  Median of `reps` (untimed by the
+    step clock)."""
+    from paper_1809_06574_b200.update import update_first_many
+    n = model.dim
+    sp_t, up_t, win_t = [], [], []
+    k = max(1, min(len(pts) - 1, 16))
+    for _ in range(reps):
+        model.reset_symbolic()
+        A1 = model.assemble(*pts[0])
+        A2 = model.assemble(*pts[min(1, len(pts) - 1)])
+        barrier()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record()
+        P1, _ = pm.spai_build(A1, pol.spai)
+        e[1].record()
+        pm.update_first(A1, A2, P1, pol.update)
+        e[2].record()
+        barrier()
+        sp_t.append(e[0].elapsed_time(e[1]) / 1e3)
+        up_t.append(e[1].elapsed_time(e[2]) / 1e3)
+        As = model.assemble_many(pts[1:1 + k])
+        barrier()
+        e[0].record()
+        update_first_many(A1, As, P1, pol.update)
+        e[3].record()
+        barrier()
+        win_t.append(e[0].elapsed_time(e[3]) / 1e3)
+        del As, A1, A2, P1
+    ts, tu, tw = float(np.median(sp_t)), float(np.median(up_t)), float(np.median(win_t))
+    return {"spai_columns_per_s": n / ts, "update_columns_per_s": n / tu,
+            "update_window_columns_per_s": n * k / tw, "spai_build_s": ts,
+            "update_first_s": tu, "update_window_systems": k, "update_window_s": tw,
+            "reps": reps, "note": "device-resident A in, device-resident factor + stats out; "
+                                  "spai_build on a cold structure"}
+
+
+def roofline(kern, timed, recs, steps):
+    """The dominant kernel (pmp_solve_batch: the persistent block-GCRO
+    solve, ~90 % of the step) against the measured HBM peak.  Algorithmic
+    bytes per launch: the kernel itself accumulates, per system, the bytes
+    of its algorithm's compulsory traffic (the operator chain's
+    matrices and n x s blocks once per block step, [C | V] once per block
+    step, cycle boundaries' blocks) -- the sum over the step's systems,
+    divided by the step's launches."""
+    hbm, which = hbm_peak()
+    name = "pmp_solve_batch"
+    if name not in kern:
         return None
-    name = max(kern, key=lambda k: kern[k]["total_ms"])
     lst = timed[name]
-    st = model.structure
-    nnz = st.nnz
-    if name == "pmp_solve_batch":
-        # the kernel accumulates its algorithmic bytes per system (solve.cu:
-        # operator matrices once per application, [C | V] once per block
-        # step, the n x s blocks it gathers / writes)
-        tot = sum(r.get("algorithmic_bytes") or 0.0 for r in (recs or []))
-        byts = [tot / max(len(lst), 1)] * len(lst)
-    elif name == "k_orth":
-        # [C | V] rows read once, W read, Q written: 8 n (k + total + 2 sb)
-        byts = [8.0 * a[0] * (a[1] + a[2] + 2 * a[3]) for _, _, a in lst]
-    elif name == "pmp_spmm":
-        # 12 B per nnz + 4 (n+1) + 16 n s_b (X gathered once + Y written)
-        byts = [12.0 * nnz + 4.0 * (n + 1) + 16.0 * n * a[4] for _, _, a in lst]
-    elif name == "pmp_gram":
-        byts = [8.0 * n * (a[1] + a[4]) for _, _, a in lst]
-    elif name == "pmp_tsmm":
-        byts = [8.0 * n * (a[1] + a[4] * (2 if a[7] != 0.0 else 1)) for _, _, a in lst]
-    elif name == "pmp_tsqr_r":
-        byts = [8.0 * n * a[1] for _, _, a in lst]
-    else:
-        byts = None
+    per_step_bytes = sum(r.get("algorithmic_bytes") or 0.0 for r in (recs or []))
+    launches_per_step = len(lst) / steps
     ms = np.array([a.elapsed_time(b) for a, b, _ in lst])
+    ach = per_step_bytes * steps / (np.sum(ms) / 1e3) / 1e9
     traffic = None
     try:
-        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                         "ncu_traffic.json")))
-        if name in tj:
-            # DRAM bytes of one launch from the committed ncu --set full capture
-            traffic = tj[name]["dram_bytes_per_launch"]
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        ent = tj.get(name + "_c%s" % os.environ.get("PMP_BENCH_CONFIG", "4")) or tj.get(name)
+        if ent:
+            traffic = ent["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
-    if byts is not None:
-        ach = float(np.sum(byts) / (np.sum(ms) / 1e3) / 1e9)
-        return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm,
-                "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
-                "algorithmic_bytes_per_launch": float(np.mean(byts)),
-                "peak_source": which + " (MEASURED_PEAKS.json hbm_gbs)",
-                "launches": len(lst), "avg_us": kern[name]["avg_us"],
-                "share_of_step": kern[name]["share_of_step"]}
-    # LS kernel: FP64 flops of the Householder solves (DESIGN.md)
-    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
-    return {"kernel": name, "bound": "fp64", "achieved": None, "peak": fp64_peak,
-            "unit": "TFLOP/s", "frac": None, "traffic": None,
-            "peak_source": "nominal FP64 (148 SM x 64 DFMA/clk x 1.965 GHz)"}
+    return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "frac": ach / hbm, "traffic": traffic,
+            "algorithmic_bytes_per_launch": per_step_bytes / max(launches_per_step, 1e-9),
+            "peak_source": which, "launches": len(lst),
+            "avg_us": kern[name]["avg_us"], "share_of_step": kern[name]["share_of_step"]}
 
 
-def roofline_ls(kern, model, nsys):
-    """Secondary roofline: the batched least-squares kernels (SPAI base build
-    + all update builds of the step) against the FP64 pipe.  Algorithmic
-    flops per column F_j = 2 m n^2 - 2/3 n^3 + 4 m n - n^2 (m = |J_j|,
-    n = |I_j|, level-0 patterns: I_j = rows(A(:, j)), J_j = rows(A(:, I_j)),
-    the same for the SPAI and every update of the sequence); nsys builds."""
+def roofline_ls(kern, model, nsys, steps, peaks):
+    """Batched least-squares kernels (SPAI + every update of the step)
+    against the MEASURED FP64 peaks.  Algorithmic flops per column
+    F_j = 2 m n^2 - 2/3 n^3 + 4 m n - n^2 (m = |J_j|, n = |I_j|, level-0
+    supports: I_j = rows(A(:, j)), J_j = rows(A(:, I_j)); the same for the
+    SPAI and every update), `nsys` builds per step on this rank."""
     import scipy.sparse as sp
     names = [k for k in ("pmp_ls_columns_multi", "pmp_ls_columns_planned", "pmp_ls_columns")
              if k in kern]
@@ -378,34 +452,43 @@ def roofline_ls(kern, model, nsys):
     ni = Ab.getnnz(axis=0).astype(np.float64)
     mj = (Ab @ Ab).getnnz(axis=0).astype(np.float64)
     f_sys = float(np.sum(ls_flops(mj, ni)))
-    t = sum(kern[k]["total_ms"] for k in names) / 1e3
+    t = sum(kern[k]["total_ms"] for k in names) / 1e3 / steps
     ach = nsys * f_sys / t / 1e12
-    peak = 148 * 64 * 2 * 1.965e9 / 1e12
-    return {"kernels": names, "bound": "fp64", "achieved": ach, "peak": peak,
-            "unit": "TFLOP/s", "frac": ach / peak, "flops_per_build": f_sys, "builds": nsys,
-            "seconds": t,
-            "peak_source": "nominal FP64 (148 SM x 64 DFMA/clk x 2 x 1.965 GHz; "
-                           "no measured FP64 peak in MEASURED_PEAKS.json)"}
+    dfma = peaks["dfma_tflops"]
+    return {"kernels": names, "bound": "fp64", "achieved": ach, "peak": dfma,
+            "unit": "TFLOP/s", "frac": ach / dfma, "frac_vs_dmma": ach / peaks["dmma_tflops"],
+            "flops_per_build": f_sys, "builds_per_step": nsys, "seconds_per_step": t,
+            "peak_source": "measured live (pmp_fp64_peak: DFMA chains; DMMA m8n8k4 also "
+                           "reported)"}
 
 
-def run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, group, barrier):
-    """Same metric through the public API with host buffers: every step
-    copies the model's term values and B host->device (pinned) and reads
-    every solution back device->host."""
+def run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, barrier):
+    """Same metric through the public API (run_sequence) from HOST buffers:
+    every step copies the model's term values and B host->device from
+    pinned memory and reads every solution block back device->host (each
+    window's X as soon as its solve launch is done, into a pinned ring:
+    every byte of every system's X crosses the link).  Cold steps like the
+    device-resident ones."""
     import torch
 
     u = model._union()
     host_terms = [v.cpu().pin_memory() for v in u.vals]
     Bh = torch.as_tensor(np.ascontiguousarray(W.rhs)).pin_memory()
     Bd = torch.empty_like(Bh, device="cuda")
-    nsys = len(s_grid) * len(p_grid)
+    n, s = W.rhs.shape
+    ring = torch.empty((4, n, s), dtype=torch.float64).pin_memory()
     from paper_1809_06574_b200.sequence import owned_systems
+    nsys = len(s_grid) * len(p_grid)
     mine = owned_systems(nsys, rank, world, pol.kind)
-    Xh = torch.empty((len(mine),) + tuple(W.rhs.shape), dtype=torch.float64).pin_memory()
     h2d = sum(t.numel() * 8 for t in host_terms) + Bh.numel() * 8
-    d2h = Xh.numel() * 8
+    d2h = len(mine) * n * s * 8
+
+    def sink(idx, X):
+        ring[idx % ring.shape[0]].copy_(X, non_blocking=True)
+
     times = []
-    for k in range(args.warmup + args.steps):
+    nsteps = max(1, min(args.e2e_steps, args.steps))
+    for k in range(1 + nsteps):
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -413,107 +496,218 @@ def run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, group, ba
         for hv, dv in zip(host_terms, u.vals):
             dv.copy_(hv, non_blocking=True)
         Bd.copy_(Bh, non_blocking=True)
-        recs, _ = pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
-                                  group=group, keep_solutions=True, timing=False,
-                                  workers=args.workers, batch=args.batch)
-        for i, r in enumerate(recs):
-            Xh[i].copy_(r["X"], non_blocking=True)
+        model.reset_symbolic()
+        pm.run_sequence(model, s_grid, p_grid, pol, cfg, B=Bd, rank=rank, world=world,
+                        timing=False, batch=args.batch, on_solution=sink)
         e1.record()
         barrier()
-        if k >= args.warmup:
+        if k >= 1:
             times.append(e0.elapsed_time(e1))
     t = torch.tensor([float(np.sum(times))], dtype=torch.float64, device="cuda")
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_s = float(t.item()) / 1e3
-    return {"value": W.n * nsys * args.steps / total_s, "unit": UNIT,
-            "ms_per_step": total_s * 1e3 / args.steps,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    return {"value": W.n * nsys * nsteps / total_s, "unit": UNIT,
+            "ms_per_step": total_s * 1e3 / nsteps, "steps": nsteps, "warmup": 1,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "run_sequence(..., on_solution=D2H into pinned host ring)"}
 
 
 # ---------------------------------------------------------------------------
-# CPU side (oracle port)
+# CPU side (oracle port): bounded samples, extrapolated to the sequence
 # ---------------------------------------------------------------------------
 
-def _cpu_chunk(payload):
-    import pmor_oracle as orc
-    A1, A2, cols = payload
-    return orc.update_factor(A1, A2, pattern_level=0, columns=cols)
+_CPU = {}
 
 
-def cpu_sample(W, pts, cores):
-    """One update_first system (all columns, process pool over column
-    chunks) + its block solve; returns seconds and the column count."""
+def _cpu_init(A1, A2):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pmor_oracle as orc
-    from concurrent.futures import ProcessPoolExecutor
-    A1 = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[0])
-    A2 = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[1])
-    P1, _ = orc.spai_build(A1, pattern_level=0) if not hasattr(cpu_sample, "_P1") else \
-        (cpu_sample._P1, None)
-    cpu_sample._P1 = P1
-    n = W.n
-    t0 = time.perf_counter()
-    chunks = np.array_split(np.arange(n), cores)
-    if cores > 1:
-        with ProcessPoolExecutor(cores) as ex:
-            parts = list(ex.map(_cpu_chunk, [(A1, A2, c) for c in chunks]))
-    else:
-        parts = [_cpu_chunk((A1, A2, chunks[0]))]
-    res = [r for p in parts for r in p]
-    Q, _ = orc.assemble_columns(n, res)
-    t1 = time.perf_counter()
-    X, info = orc.block_gcro(A2, W.rhs, orc.Chain([Q, P1]), tol=1e-8)
-    t2 = time.perf_counter()
-    return t2 - t0, t1 - t0, t2 - t1, n, info["iterations"]
+    _CPU["orc"] = orc
+    _CPU["sys"] = orc.canon(A2).tocsc()
+    _CPU["tgt"] = orc.canon(A1).tocsc()
 
 
-def cpu_baseline(args, W, pts):
+def _cpu_cols(cols):
+    orc = _CPU["orc"]
+    S, T = _CPU["sys"], _CPU["tgt"]
+    pat = {int(j): orc.level0_support(S, int(j)) for j in cols}
+    return orc.solve_columns(S, T, pat, 1e-4, 0, 80, [int(j) for j in cols])
+
+
+class CpuSampler:
+    """The reference's algorithm (oracle port) on this host's cores.
+
+    Per sample: (a) the update_first least squares (update.py:78-87,
+    spai.py:273-292) of the first CPU_SAMPLE_COLUMNS columns of
+    default_rng(7).permutation(n), chunked over a process
+    pool created beforehand (not timed); (b) block GCRO (krylov.py:105-275)
+    on the same system, truncated after `solve_iters` block steps (its
+    cycle end included).  Extrapolation to the whole sequence:
+    t_seq = systems * n / rate_cols + systems * t_solve_iters * (iters /
+    solve_iters) -- a per-step cost taken from the FIRST block steps, whose
+    Gram work is below the average step's, so the CPU estimate errs fast."""
+
+    def __init__(self, W, pts, cores, P1, Q):
+        import multiprocessing as mp
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pmor_oracle as orc
+        self.orc = orc
+        self.W = W
+        self.cores = cores
+        self.A1 = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[0])
+        self.A2 = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                   *pts[min(1, len(pts) - 1)])
+        n = W.n
+        self.cols = np.random.default_rng(7).permutation(n)[:min(CPU_SAMPLE_COLUMNS, n)]
+        self.pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init,
+                                                initargs=(self.A1, self.A2))
+        self.chain = orc.Chain([Q, P1])
+        self.pool.map(_cpu_cols, [self.cols[:cores]] * cores)   # warm the workers
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def sample(self, solve_iters):
+        chunks = np.array_split(self.cols, self.cores * 4)
+        t0 = time.perf_counter()
+        parts = self.pool.map(_cpu_cols, chunks)
+        t1 = time.perf_counter()
+        _, info = self.orc.block_gcro(self.A2, self.W.rhs, self.chain, tol=1e-8,
+                                      max_iters=solve_iters)
+        t2 = time.perf_counter()
+        ncols = sum(len(p) for p in parts)
+        return {"cols_s": t1 - t0, "cols": ncols, "solve_s": t2 - t1,
+                "solve_iters": int(info["iterations"])}
+
+
+def extrapolate(smp, n, nsys, iters_mean):
+    rate = smp["cols"] / smp["cols_s"]
+    t_solve = smp["solve_s"] * iters_mean / max(smp["solve_iters"], 1)
+    t_seq = nsys * n / rate + nsys * t_solve
+    return t_seq, rate, t_solve
+
+
+def _cpu_factors_from_device(pm, model, pts, pol):
+    """P1 and Q of system 2 as host CSR (for the CPU solve sample only: the
+    truncated solve's cost depends on their sizes, not their values; the
+    values are the reference's to ~1e-16 -- pinned by the parity tests)."""
+    A1 = model.assemble(*pts[0])
+    A2 = model.assemble(*pts[min(1, len(pts) - 1)])
+    P1, _ = pm.spai_build(A1, pol.spai)
+    P2, _ = pm.update_first(A1, A2, P1, pol.update)
+    return P1.matrix.to_scipy(), P2.q.to_scipy()
+
+
+def cpu_baseline(args, W, pts, model, pol, iters):
+    import paper_1809_06574_b200 as pm
     cores = max(1, len(os.sched_getaffinity(0)))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    tot, tb, ts, n, it = cpu_sample(W, pts, cores)
-    return {"value": n / tot, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": ("one update_first system of c%d (all %d columns over %d processes) + "
-                       "its block GCRO solve to 1e-8 (%d iterations); build %.2f s, solve %.2f s"
-                       % (args.config, n, cores, it, tb, ts))}
+    os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
+    P1, Q = _cpu_factors_from_device(pm, model, pts, pol)
+    cs = CpuSampler(W, pts, cores, P1, Q)
+    try:
+        smp = cs.sample(args.cpu_solve_iters)
+    finally:
+        cs.close()
+    it = float(np.mean(iters))
+    t_seq, rate, t_solve = extrapolate(smp, W.n, len(pts), it)
+    return {"value": W.n * len(pts) / t_seq, "unit": UNIT, "cores": cores, "kind": "port",
+            "extrapolated": True, "sequence_s": t_seq,
+            "sample": ("c%d: update_first least squares of %d columns (default_rng(7) "
+                       "permutation) over %d processes (%.0f columns/s) + block GCRO truncated "
+                       "at %d block steps (%.2f s), extrapolated to %d systems x %d columns and "
+                       "%.2f iterations per solve (this run's mean)"
+                       % (args.config, smp["cols"], cores, rate, smp["solve_iters"],
+                          smp["solve_s"], len(pts), W.n, it))}
 
 
 def run_reference(args):
+    """--impl reference: the reference's algorithm (oracle port) on the host
+    cores, on our arm's config / metric.  Setup (untimed): host assembly,
+    the full base SPAI and one full update (process pool), and ONE full
+    block GCRO solve of system 2 (its iteration count drives the
+    extrapolation).  Each step: a fresh bounded sample (CpuSampler)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return None
-    W, pts = workload(args.config, args.systems)
+    W, s_grid, p_grid, pts = workload(args.config, args.systems)
+    nsys = len(pts)
     cores = max(1, len(os.sched_getaffinity(0)))
-    times = []
-    last = None
-    for k in range(args.warmup + args.steps):
-        tot, tb, ts, n, it = cpu_sample(W, pts, cores)
-        last = (tb, ts, it)
-        if k >= args.warmup:
-            times.append(tot)
-    value = n * args.steps / float(np.sum(times))
+    os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pmor_oracle as orc
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    A1 = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[0])
+    A2 = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                          *pts[min(1, len(pts) - 1)])
+    n = W.n
+    chunks = np.array_split(np.arange(n), cores * 8)
+    with mp.get_context("fork").Pool(cores, initializer=_cpu_init, initargs=(A1, A1)) as pool:
+        resP = [r for part in pool.map(_cpu_cols_spai, chunks) for r in part]
+    P1, _ = orc.assemble_columns(n, resP)
+    with mp.get_context("fork").Pool(cores, initializer=_cpu_init, initargs=(A1, A2)) as pool:
+        resQ = [r for part in pool.map(_cpu_cols, chunks) for r in part]
+    Q, _ = orc.assemble_columns(n, resQ)
+    t_build_full = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    _, info = orc.block_gcro(A2, W.rhs, orc.Chain([Q, P1]), tol=1e-8)
+    t_solve_full = time.perf_counter() - t1
+    it_ref = int(info["iterations"])
+    cs = CpuSampler(W, pts, cores, P1, Q)
+    times, last = [], None
+    try:
+        for k in range(args.warmup + args.steps):
+            smp = cs.sample(args.cpu_solve_iters)
+            t_seq, rate, t_solve = extrapolate(smp, n, nsys, it_ref)
+            last = (smp, rate, t_solve)
+            if k >= args.warmup:
+                times.append(t_seq)
+    finally:
+        cs.close()
     ms = float(np.mean(times)) * 1e3
+    value = n * nsys * args.steps / float(np.sum(times))
+    smp, rate, t_solve = last
+    sample = ("per step: update_first least squares of %d columns of c%d (default_rng(7) "
+              "permutation, %d processes; %.0f columns/s) + block GCRO on system 2 truncated at "
+              "%d block steps, extrapolated to %d systems x %d columns at %d iterations per "
+              "solve (the oracle's full solve of system 2 in setup: %d iterations, %.1f s; "
+              "full base + update builds in setup %.1f s)"
+              % (smp["cols"], args.config, cores, rate, smp["solve_iters"], nsys, n, it_ref,
+                 it_ref, t_solve_full, t_build_full))
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, SURVEY.md 8.1)", "impl": "reference",
-            "config": {"workload": "c%d" % args.config, "n": W.n, "systems": len(pts),
-                       "pattern_level": 0, "precond": "spai-update-first", "tol": 1e-8},
+            "config": config_dict(args, W, nsys, world),
+            "extrapolated": True, "sample": sample,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": "per step: one update_first system (all %d columns, "
-                                       "%d processes) + its block GCRO solve (%d iterations)"
-                                       % (W.n, cores, last[2])},
+                             "extrapolated": True, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
+def _cpu_cols_spai(cols):
+    """SPAI columns (target = identity) on the worker's system."""
+    orc = _CPU["orc"]
+    S = _CPU["tgt"]
+    import scipy.sparse as sp
+    if "eye" not in _CPU:
+        _CPU["eye"] = sp.identity(S.shape[0], format="csc")
+    pat = {int(j): orc.level0_support(S, int(j)) for j in cols}
+    return orc.solve_columns(S, _CPU["eye"], pat, 1e-4, 0, 80, [int(j) for j in cols])
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
-        line = run_reference(args)
-    else:
+    if args.impl == "ours":
+        maybe_spawn(args)
+        os.environ["PMP_BENCH_CONFIG"] = str(args.config)
         line = run_ours(args)
+    else:
+        line = run_reference(args)
     if line is not None:
         print(json.dumps(line), flush=True)
 

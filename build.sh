@@ -9,13 +9,15 @@ SRC=paper_1809_06574_b200/csrc
 mkdir -p build
 objs=()
 pids=()
-for f in structure assemble ls blockops orth cycle solve gcro_host; do
+for f in structure assemble ls blockops orth cycle solve gcro_host peak; do
   $NVCC $FLAGS -c $SRC/$f.cu -o build/$f.o &
   pids+=($!)
   objs+=(build/$f.o)
 done
-$NVCC $FLAGS -c $SRC/hostls.cpp -o build/hostls.o &
-pids+=($!)
-objs+=(build/hostls.o)
+for f in hostls comm; do
+  $NVCC $FLAGS -c $SRC/$f.cpp -o build/$f.o &
+  pids+=($!)
+  objs+=(build/$f.o)
+done
 for p in "${pids[@]}"; do wait $p; done
-$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o paper_1809_06574_b200/libpmorb200.so "${objs[@]}"
+$NVCC -gencode arch=compute_100a,code=sm_100a -shared -o paper_1809_06574_b200/libpmorb200.so "${objs[@]}" -ldl

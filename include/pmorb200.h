@@ -487,6 +487,37 @@ int pmp_host_hls_append(int ldq, int nrhs, int ncols_old, int nnew, int nrows,
                         const double* h_newcols, double* h_QR, double* h_tau, int* h_ext,
                         double* h_C, double* h_Y, double* h_resnorm);
 
+/* ---- measurement --------------------------------------------------------- */
+/* Live FP64 pipe peak of this device (kind 0: DFMA, 8 independent fma
+ * chains per thread; kind 1: DMMA, mma.sync m8n8k4 f64): 4 x #SMs blocks of
+ * 256 threads, `iters` x 128 (DFMA) / 32 (DMMA) instructions per thread,
+ * timed with CUDA events on `stream` after one warm-up launch (this call
+ * synchronises).  *tflops = achieved TFLOP/s.  The denominator of the
+ * least-squares roofline (bench.py roofline_ls). */
+int pmp_fp64_peak(int kind, int iters, double* tflops, void* stream);
+
+/* ---- multi-GPU collectives (NCCL over NVLink / NVSwitch) ------------------
+ * The sequence driver's two exchanges: replicate the base
+ * SPAI P1 (rpmor.py:205-210: every first-approach system depends only on
+ * (A1, P1)) and gather the per-system scalars.  libnccl.so.2 is opened at run
+ * time (no link dependency); pmp_nccl_available() reports whether it loads.
+ * The 128-byte unique id from rank 0 reaches the other ranks out of band
+ * (the Python driver sends it through the torch.distributed store). */
+int pmp_nccl_available(void);
+int pmp_nccl_unique_id(unsigned char* h_out128);
+int pmp_nccl_init(int rank, int world, const unsigned char* h_id128, void** comm);
+int pmp_nccl_destroy(void* comm);
+/* d_buf[0, bytes) from `root` to every rank (P1's CSR arrays). */
+int pmp_nccl_bcast(void* d_buf, size_t bytes, int root, void* comm, void* stream);
+/* In-place variable all-gather: rank r's bytes [h_displs[r], h_displs[r] +
+ * h_counts[r]) of d_buf are replicated on every rank (one grouped broadcast
+ * per rank; the column-sharded base build, spai.py:328-336). */
+int pmp_nccl_allgatherv(void* d_buf, const size_t* h_counts, const size_t* h_displs, int world,
+                        void* comm, void* stream);
+/* Element-wise sum over ranks of `count` doubles, in place (per-system
+ * scalar records, each system owned by exactly one rank). */
+int pmp_nccl_allreduce_f64(double* d_buf, size_t count, void* comm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -108,6 +108,14 @@ _SIGS = {
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp, c_vp], c_int),
+    "pmp_fp64_peak": ([c_int, c_int, c_vp, c_vp], c_int),
+    "pmp_nccl_available": ([], c_int),
+    "pmp_nccl_unique_id": ([c_vp], c_int),
+    "pmp_nccl_init": ([c_int, c_int, c_vp, c_vp], c_int),
+    "pmp_nccl_destroy": ([c_vp], c_int),
+    "pmp_nccl_bcast": ([c_vp, c_sz, c_int, c_vp, c_vp], c_int),
+    "pmp_nccl_allgatherv": ([c_vp, c_vp, c_vp, c_int, c_vp, c_vp], c_int),
+    "pmp_nccl_allreduce_f64": ([c_vp, c_sz, c_vp, c_vp], c_int),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -164,7 +172,8 @@ _NO_LAUNCH = {"pmp_last_error", "pmp_version", "pmp_host_deflate", "pmp_host_hls
               "pmp_host_alloc_mapped", "pmp_host_free_mapped", "pmp_host_device_ptr",
               "pmp_host_wait_flag", "pmp_gcro_absorb", "pmp_orth_debug_stamps",
               "pmp_cycle_debug_stamps", "pmp_solve_geometry",
-              "pmp_cycle_workspace"}
+              "pmp_cycle_workspace", "pmp_nccl_available", "pmp_nccl_unique_id",
+              "pmp_nccl_init", "pmp_nccl_destroy"}
 # pmp_gcro_step launches the SpMM chain (1 + depth) and the orthogonalisation
 _LAUNCHES_PER_CALL["pmp_gcro_step"] = 4
 

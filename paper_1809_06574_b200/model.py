@@ -237,6 +237,18 @@ class SecondOrderModel:
     def structure(self):
         return self._union().structure
 
+    def reset_symbolic(self):
+        """Drop every symbolic result derived from the model's sparsity
+        structure -- the level-0 SPAI pattern, its CSR transpose plan, the
+        least-squares size tiers and recorded symbolic plans, the CSC
+        transpose -- so the next sequence recomputes them, exactly as a
+        freshly constructed model would (the device term values are kept).
+        Matrices assembled before the call keep the old structure."""
+        u = self._union()
+        st = u.structure
+        u.structure = Structure(st.n, st.rowptr, st.colidx,
+                                symmetric_pattern=st.symmetric_pattern)
+
     def assemble(self, s, pvals):
         """(s^2 M(p) + s D(p)) + K(p) as a device CSR, bit-identical to the
         reference's canonical CSR (rpmor.py:92-107)."""

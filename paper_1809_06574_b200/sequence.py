@@ -6,16 +6,19 @@ Mirrors the reference's ``PrecondPolicy`` / ``SequencePreconditioner``
 order, zoo.py:268-284: sigma outermost, p inner; first system gets a fresh
 SPAI, the others the configured update).
 
-Multi-GPU (one process per GPU, torch.distributed over NCCL): with the
-"first" approach every system depends only on (A1, P1) (rpmor.py:208-210),
-so systems are dealt round-robin over ranks by their global sequence index.
-Every rank assembles A1 and its own systems locally from the replicated
-terms; the level-0 pattern -- hence the CSR structure of P1 -- is
-deterministic, so rank 0 builds P1 and one broadcast of its values
-(nnz(P1) float64) replicates it.  Per-system scalars are all-gathered at
-the end; solutions stay on their owner GPU.  "spai" runs independently per
-rank; "spai-update-second" has a true chain dependency and therefore runs
-as replicas (every rank walks the whole chain).
+Multi-GPU (one process per GPU; collectives through NCCL behind the C-ABI,
+comm.py): with the "first" approach every system depends only on (A1, P1)
+(rpmor.py:208-210), so systems are dealt round-robin over ranks by their
+global sequence index.  Every rank assembles A1 and its own systems locally
+from the replicated terms.  P1 is built column-sharded at pattern level 0
+(rank r solves its contiguous column range, one grouped all-gather
+replicates the coefficients: spai.spai_build_sharded); at level >= 1 rank 0
+builds it and broadcasts structure and values.  Per-system scalar records
+are summed over ranks at the end (one allreduce of a zero-padded table:
+every system has exactly one owner) into ``info["records_all"]``;
+solutions stay on their owner GPU.  "spai" runs independently per rank;
+"spai-update-second" has a true chain dependency and therefore runs as
+replicas (every rank walks the whole chain).
 """
 
 import time
@@ -24,10 +27,9 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .device import DeviceCSR, level0_pattern
 from . import krylov as _krylov
 from .krylov import SolverConfig, block_gcro_solve, block_gcro_solve_batch
-from .spai import Preconditioner, SpaiConfig, _factor_from_columns, spai_build
+from .spai import Preconditioner, SpaiConfig, spai_build, spai_build_sharded
 from .update import UpdateConfig, update_first, update_first_many, update_second
 
 PRECOND_KINDS = ("none", "spai", "spai-update-first", "spai-update-second")
@@ -115,39 +117,23 @@ def owned_systems(n_systems, rank, world, kind="spai-update-first"):
     return [i for i in range(n_systems) if i % world == rank]
 
 
-def broadcast_values(t, src=0, group=None):
-    """Broadcast a tensor's values from `src` (NCCL for CUDA tensors; the
-    gloo path used by the CPU tests broadcasts a host copy)."""
-    import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
-        return t
-    backend = dist.get_backend(group)
-    if t.is_cuda and backend == "nccl":
-        dist.broadcast(t, src, group=group)
-        return t
-    h = t.detach().cpu().contiguous()
-    dist.broadcast(h, src, group=group)
-    t.copy_(h)
-    return t
-
-
 RECORD_FIELDS = ("index", "iterations", "converged", "matvec_count", "precond_apply_count",
                  "max_final_residual")
 
 
 def gather_records(records, n_systems, group=None):
-    """All-gather the per-system scalar records (sum over ranks of a
-    zero-padded table; each system is owned by exactly one rank)."""
-    import torch.distributed as dist
-    table = np.zeros((n_systems, len(RECORD_FIELDS)), dtype=np.float64)
-    for r in records:
-        table[r["index"]] = [r[f] if f != "index" else r["index"] + 1 for f in RECORD_FIELDS]
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        backend = dist.get_backend(group)
+    """Every system's scalar record on every rank: the zero-padded
+    (n_systems x fields) table of this rank's systems, summed over ranks
+    (each system has exactly one owner) -- pmp_nccl_allreduce_f64 on the
+    device under NCCL, a host allreduce under gloo."""
+    from .comm import get_comm, record_table
+    table = record_table(records, n_systems, RECORD_FIELDS)
+    comm = get_comm(group)
+    if comm.world > 1:
         t = torch.as_tensor(table)
-        if backend == "nccl":
+        if comm.uses_nccl:
             t = t.cuda()
-        dist.all_reduce(t, group=group)
+        comm.allreduce_sum_f64(t)
         table = t.cpu().numpy()
     out = []
     for row in table:
@@ -157,6 +143,8 @@ def gather_records(records, n_systems, group=None):
         d["index"] = int(d["index"]) - 1
         d["iterations"] = int(d["iterations"])
         d["converged"] = bool(d["converged"])
+        d["matvec_count"] = int(d["matvec_count"])
+        d["precond_apply_count"] = int(d["precond_apply_count"])
         out.append(d)
     return out
 
@@ -166,22 +154,29 @@ def gather_records(records, n_systems, group=None):
 # ---------------------------------------------------------------------------
 
 # HBM budget for one solve window (operators + preconditioner factors + X)
-WINDOW_BYTES = int(__import__("os").environ.get("PMP_WINDOW_BYTES", str(24 << 30)))
+WINDOW_BYTES = int(__import__("os").environ.get("PMP_WINDOW_BYTES", str(64 << 30)))
 
 
 def _window_systems(model, B):
     """Systems per solve window: every system's A (values), its update factor
     (indices + values) and X stay resident until the window's launch ends."""
     n, s = B.shape
-    nnz = getattr(model, "union_nnz", None)
-    if nnz is None:
-        nnz = 27 * n
-    per = 8 * nnz + 12 * nnz + 8 * n * s + 64 * n
-    return max(1, WINDOW_BYTES // per)
+    st = model.structure
+    nnz = st.nnz
+    nonsym = not model._union().symmetric
+    # per system: assembled values (+ their CSC copy when unsymmetric), the
+    # update factor's coefficient and CSR value rows (pattern nnz <= nnz of
+    # the structure at level 0), residual / flag rows, X
+    per = 8 * nnz * (2 if nonsym else 1) + 16 * nnz + 12 * n + 8 * n * s
+    # the persistent solve's per-group workspace (V n x cap, C / U n x kc,
+    # nine n x s blocks) comes out of the same budget
+    cap = 50 + 2 * s + 2
+    ws = 8 * n * (cap + 2 * (10 + s) + 9 * s) * 6
+    return max(1, (WINDOW_BYTES - ws) // per)
 
 def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, rank=0, world=1,
                  group=None, keep_solutions=False, timing=True, workers=1, batch=None,
-                 window=None):
+                 window=None, on_solution=None):
     """Run the whole parametric sequence; returns (records, info).
 
     records: one dict per system this rank owns (index, sigma, p, label,
@@ -205,6 +200,10 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     stream, so the latency-bound block solves of independent systems overlap
     on the device; grid-barrier kernels are serialised through one shared
     stream (pmp_set_coop_stream).
+
+    on_solution(index, X): called with every solution block (device tensor,
+    on the current stream) as soon as its solve is done -- e.g. to copy it to
+    the host -- without keeping every X alive (keep_solutions).
     """
     import threading
     from . import _abi
@@ -233,21 +232,24 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     sharded = world > 1 and policy.kind == "spai-update-first"
     A1 = P1 = None
     if sharded:
-        # every rank: A1 locally; rank 0 builds P1; broadcast the values
+        # every rank: A1 locally; P1 column-sharded over the ranks (level 0)
+        # or built by rank 0 and broadcast with its structure (level >= 1)
+        from .comm import get_comm
+        comm = get_comm(group)
+        if comm.world != world or comm.rank != rank:
+            raise ValueError("rank/world (%d/%d) do not match the process group (%d/%d)"
+                             % (rank, world, comm.rank, comm.world))
         t0 = mark()
         A1 = model.assemble(*points[0])
         t1 = mark()
         phases["assemble"].append((t0, t1))
-        if rank == 0:
-            P1, _ = spai_build(A1, policy.spai, threads=policy.threads)
+        P1, _ = spai_build_sharded(A1, policy.spai, comm)
+        if policy.spai.pattern_level == 0:   # this rank's share of P1's columns
+            state["build_cols"] += A1.n * (rank + 1) // world - A1.n * rank // world
+        elif rank == 0:
             state["build_cols"] += A1.n
-        else:
-            pat = level0_pattern(A1)
-            vals = torch.empty(pat.nnz, dtype=torch.float64, device=A1.vals.device)
-            P1 = Preconditioner(matrix=_factor_from_columns(pat, vals))
         t2 = mark()
         phases["build"].append((t1, t2))
-        broadcast_values(P1.matrix.vals, 0, group)
         seq.seed(A1, P1)
 
     def do_system(idx):
@@ -271,6 +273,8 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                "launches": getattr(rep, "device_launches", 0)}
         if keep_solutions:
             rec["X"] = X
+        if on_solution is not None:
+            on_solution(idx, X)
         with lock:
             records.append(rec)
             state["build_cols"] += cols
@@ -285,9 +289,7 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     if batched:
         # assemble + precondition a chunk of systems, then solve the chunk in
         # one persistent launch (one block group per system)
-        todo = [i for i in mine if not (sharded and i == 0)]
-        if sharded and 0 in mine:
-            do_system(0)
+        todo = list(mine)
         if window is None:
             window = _window_systems(model, Bd)
         window = max(batch, int(window))
@@ -297,7 +299,9 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
             def run_window(defer):
                 built = []
                 t0 = mark()
-                pts_ = [points[idx] for idx in chunk]
+                # sharded: system 0 is (A1, P1), already assembled and built
+                head = sharded and chunk[0] == 0
+                pts_ = [points[idx] for idx in (chunk[1:] if head else chunk)]
                 if defer:
                     As, zc = model.assemble_many(pts_, defer_zero_check=True)
                 else:
@@ -305,7 +309,10 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                 t1 = mark()
                 # (the window's assembly and its build are one phase each:
                 # charged to the window's first system)
-                pres = seq.for_systems(As)
+                pres = seq.for_systems(As) if As else []
+                if head:
+                    As = [A1] + As
+                    pres = [(P1, 0.0, "spai", None)] + pres
                 t2 = mark()
                 for j, (idx, A, (P, _, label, _)) in enumerate(zip(chunk, As, pres)):
                     if j == 0:
@@ -326,7 +333,7 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
             seq_state = (seq._initial_system, seq._initial_pre, seq._prev_system,
                          seq._prev_pre)
             built, res, t3, t4, zc = run_window(True)
-            if int(zc.max().item()) > 0:
+            if zc is not None and int(zc.max().item()) > 0:
                 (seq._initial_system, seq._initial_pre, seq._prev_system,
                  seq._prev_pre) = seq_state
                 built, res, t3, t4, _ = run_window(False)
@@ -342,8 +349,11 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                        "algorithmic_bytes": getattr(rep, "algorithmic_bytes", None)}
                 if keep_solutions:
                     rec["X"] = X
+                if on_solution is not None:
+                    on_solution(idx, X)
                 records.append(rec)
-                state["build_cols"] += A.n if P is not None else 0
+                if P is not None and not (sharded and idx == 0):  # (P1: counted above)
+                    state["build_cols"] += A.n
                 if timing and t0 is not None:
                     phases["assemble"].append((t0, t1))
                     phases["build"].append((ta, t2))
@@ -388,6 +398,8 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
             raise errors[0]
     records.sort(key=lambda r: r["index"])
     info = {"build_columns": state["build_cols"]}
+    if world > 1:
+        info["records_all"] = gather_records(records, nsys, group)
     if timing:
         torch.cuda.synchronize()
         for k, lst in phases.items():

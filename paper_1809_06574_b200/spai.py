@@ -780,6 +780,75 @@ def spai_build(A, cfg=None, pattern=None, threads=1):
     return Preconditioner(matrix=P), stats
 
 
+def spai_build_sharded(A, cfg=None, comm=None):
+    """Base SPAI built across the ranks of ``comm``: every
+    column is an independent least-squares problem (spai.py:273-292,
+    SPEC "columns are independent"), so rank r solves the contiguous columns
+    [b_r, b_{r+1}) of the level-0 pattern -- deterministic on every rank --
+    and one grouped all-gather (pmp_nccl_allgatherv) replicates the
+    coefficients (pattern order), residuals and flags; every rank then
+    permutes its full copy to CSR.  Bitwise the single-rank build.
+
+    Level >= 1 (augmented supports are only known after the first pass and
+    differ per column): rank 0 builds, then its CSR structure -- nnz first --
+    and values are broadcast, so every rank holds rank 0's exact factor.
+    Returns (Preconditioner, BuildStats) on every rank."""
+    from .comm import column_bounds, get_comm
+    A = _as_dev_csr(A)
+    cfg = cfg or SpaiConfig()
+    comm = comm or get_comm()
+    if comm.world <= 1:
+        return spai_build(A, cfg)
+    n = A.n
+    dev = _dev()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    if cfg.pattern_level >= 1:
+        meta = torch.zeros(2, dtype=torch.float64, device=dev)
+        if comm.rank == 0:
+            P0, st0 = spai_build(A, cfg)
+            M = P0.matrix
+            meta[0] = float(M.nnz)
+            meta[1] = float(st0.augmented_columns)
+        comm.bcast(meta, 0)
+        nnz, n_aug = int(meta[0].item()), int(meta[1].item())
+        if comm.rank == 0:
+            rowptr, colidx, vals = M.structure.rowptr, M.structure.colidx, M.vals
+            resid, flags = st0._resid, st0._flags
+        else:
+            rowptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            colidx = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz]
+            vals = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)[:nnz]
+            resid = torch.empty(n, dtype=torch.float64, device=dev)
+            flags = torch.empty(n, dtype=torch.int32, device=dev)
+        for t in (rowptr, colidx, vals, resid, flags):
+            comm.bcast(t, 0)
+        ev1.record()
+        if comm.rank == 0:
+            P = P0
+        else:
+            P = Preconditioner(matrix=DeviceCSR(Structure(n, rowptr, colidx), vals,
+                                                symmetric=False))
+        return P, BuildStats(resid, flags, n_aug, (ev0, ev1))
+    pat = level0_pattern(A)
+    b = column_bounds(n, comm.world)
+    c0, c1 = b[comm.rank], b[comm.rank + 1]
+    coef = torch.zeros(max(pat.nnz, 1), dtype=torch.float64, device=dev)
+    resid = torch.zeros(n, dtype=torch.float64, device=dev)
+    flags = torch.zeros(n, dtype=torch.int32, device=dev)
+    if c1 > c0:
+        tiers = _get_tiers(pat, A, None, np.arange(c0, c1, dtype=np.int64))
+        _run_tiers(tiers, pat, A.csc(), None, coef, resid, flags)
+    iptr = pat.iptr.cpu().numpy().astype(np.int64)
+    comm.allgatherv(coef, [int(iptr[x]) for x in b])
+    comm.allgatherv(resid, b)
+    comm.allgatherv(flags, b)
+    P = _factor_from_columns(pat, coef[:pat.nnz])
+    ev1.record()
+    return Preconditioner(matrix=P), BuildStats(resid, flags, 0, (ev0, ev1))
+
+
 def quality(A, P):
     """||I - A P||_F (spai.py:367-373) on the device: the identity goes
     through the chain and A in 32-column slabs (SpMMs, never materialising

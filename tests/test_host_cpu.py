@@ -101,20 +101,34 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1809_06574_b200.sequence import (broadcast_values, gather_records,
-                                                owned_systems)
+    from paper_1809_06574_b200.comm import column_bounds, get_comm
+    from paper_1809_06574_b200.sequence import gather_records, owned_systems
+    comm = get_comm()
+    assert (comm.rank, comm.world, comm.uses_nccl) == (rank, world, False)
     vals = torch.arange(10, dtype=torch.float64) if rank == 0 else torch.zeros(10,
                                                                                dtype=torch.float64)
-    broadcast_values(vals, 0)
+    comm.bcast(vals, 0)
+    # column-sharded build exchange: rank r fills only its own range
+    b = column_bounds(11, world)
+    coef = torch.zeros(11, dtype=torch.float64)
+    coef[b[rank]:b[rank + 1]] = 100.0 * (rank + 1) + torch.arange(b[rank], b[rank + 1])
+    comm.allgatherv(coef, b)
+    flags = torch.zeros(11, dtype=torch.int32)
+    flags[b[rank]:b[rank + 1]] = rank + 1
+    comm.allgatherv(flags, b)
     recs = [{"index": i, "iterations": 10 + i, "converged": True, "matvec_count": 3 * i,
              "precond_apply_count": 2 * i, "max_final_residual": 1e-9}
             for i in owned_systems(7, rank, world)]
     table = gather_records(recs, 7)
-    q.put((rank, vals.tolist(), [(r["index"], r["iterations"]) for r in table]))
+    q.put((rank, vals.tolist(), coef.tolist(), flags.tolist(),
+           [(r["index"], r["iterations"], r["matvec_count"]) for r in table]))
     dist.destroy_process_group()
 
 
-def test_gloo_two_ranks_broadcast_and_gather():
+def test_gloo_two_ranks_broadcast_allgather_and_gather():
+    """Host logic of the multi-GPU driver (comm.py, sequence.gather_records)
+    over 2 gloo ranks: broadcast of P1, the column-sharded all-gather with
+    uneven ranges, the per-system record table."""
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
@@ -126,9 +140,15 @@ def test_gloo_two_ranks_broadcast_and_gather():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, vals, table in out:
+    from paper_1809_06574_b200.comm import column_bounds
+    b = column_bounds(11, world)
+    want = [100.0 * (r + 1) + i for r in range(world) for i in range(b[r], b[r + 1])]
+    wflags = [r + 1 for r in range(world) for i in range(b[r], b[r + 1])]
+    for rank, vals, coef, flags, table in out:
         assert vals == list(range(10))
-        assert table == [(i, 10 + i) for i in range(7)]
+        assert coef == want
+        assert flags == wflags
+        assert table == [(i, 10 + i, 3 * i) for i in range(7)]
 
 
 def test_inner_state_layout_matches_header(tmp_path):
