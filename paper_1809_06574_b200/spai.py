@@ -316,9 +316,19 @@ def _bucket_merge(sel, cols, lcap, m, nI, bytes_fn, limit, team, glob, mode):
     O(n log n) and a handful of launches even for power-law sizes."""
     if sel.size == 0:
         return []
-    key = np.stack([lcap[sel], _coarse(nI[sel]), _coarse(m[sel])], axis=1)
-    ukeys, inv = np.unique(key, axis=0, return_inverse=True)
-    inv = inv.ravel()
+    # one int64 key per column (21 bits per coarsened dimension): a 1-D
+    # unique is a plain sort, np.unique(axis=0) a lexicographic one that
+    # took seconds at n = 2^21
+    k0, k1, k2 = lcap[sel], _coarse(nI[sel]), _coarse(m[sel])
+    if max(int(k0.max()), int(k1.max()), int(k2.max())) >= (1 << 21):
+        key = np.stack([k0, k1, k2], axis=1)
+        ukeys, inv = np.unique(key, axis=0, return_inverse=True)
+        inv = inv.ravel()
+    else:
+        key1 = (k0 << 42) | (k1 << 21) | k2
+        uk, inv = np.unique(key1, return_inverse=True)
+        inv = inv.ravel()
+        ukeys = np.stack([uk >> 42, (uk >> 21) & ((1 << 21) - 1), uk & ((1 << 21) - 1)], axis=1)
     gbytes = bytes_fn(ukeys[:, 0], ukeys[:, 2], ukeys[:, 1])
     order = np.argsort(gbytes, kind="stable")
     by_group = np.argsort(inv, kind="stable")

@@ -11,14 +11,16 @@ OUT=build/variants/$NAME
 mkdir -p $OUT
 objs=()
 pids=()
-for f in structure assemble ls blockops orth cycle solve gcro_host; do
+for f in structure assemble ls blockops orth cycle solve gcro_host peak; do
   nvcc $FLAGS -c $SRC/$f.cu -o $OUT/$f.o &
   pids+=($!)
   objs+=($OUT/$f.o)
 done
-nvcc $FLAGS -c $SRC/hostls.cpp -o $OUT/hostls.o &
-pids+=($!)
-objs+=($OUT/hostls.o)
+for f in hostls comm; do
+  nvcc $FLAGS -c $SRC/$f.cpp -o $OUT/$f.o &
+  pids+=($!)
+  objs+=($OUT/$f.o)
+done
 for p in "${pids[@]}"; do wait $p; done
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/libpmorb200_$NAME.so "${objs[@]}"
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/libpmorb200_$NAME.so "${objs[@]}" -ldl
 echo build/variants/libpmorb200_$NAME.so
