@@ -9,7 +9,7 @@ SRC=paper_1809_06574_b200/csrc
 mkdir -p build
 objs=()
 pids=()
-for f in structure assemble ls blockops orth cycle solve gcro_host peak; do
+for f in structure assemble ls blockops orth cycle solve gcro_host peak cplx; do
   $NVCC $FLAGS -c $SRC/$f.cu -o build/$f.o &
   pids+=($!)
   objs+=(build/$f.o)

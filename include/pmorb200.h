@@ -496,6 +496,34 @@ int pmp_host_hls_append(int ldq, int nrhs, int ncols_old, int nnew, int nrows,
  * least-squares roofline (bench.py roofline_ls). */
 int pmp_fp64_peak(int kind, int iters, double* tflops, void* stream);
 
+/* ---- complex128 through the real form ---------------------------------------
+ * The reference computes in complex128 (sparsecore.py:8-10).  Complex
+ * matrices run on the real kernels as R(A) (2n x 2n, entry (r, c) -> block
+ * [[Re, -Im], [Im, Re]], every block stored in full, every row holding its
+ * diagonal block); complex vectors as R(x) = (re_0, im_0, re_1, im_1, ...).
+ * Complex least squares over a support I is exactly real least squares over
+ * R(A)'s columns {2k, 2k+1 : k in I}; the complex block Krylov space of B is
+ * the real one of [R(b_0), R(i b_0), R(b_1), ...] (see csrc/cplx.cu). */
+/* Real form of an n x n complex CSR (rows sorted, diagonal present): writes
+ * d_rowptr2[2n+1], d_colidx2[4 nnz] (may be NULL: values only), d_vals2[4 nnz].
+ * d_im may be NULL (zero imaginary part). */
+int pmp_realify(int n, const int32_t* d_rowptr, const int32_t* d_colidx, const double* d_re,
+                const double* d_im, int32_t* d_rowptr2, int32_t* d_colidx2, double* d_vals2,
+                void* stream);
+/* n x s complex block (row-major re / im, ld ldx) -> 2n x 2s real block
+ * (ld ldy >= 2s): column 2c = R(x_c), column 2c+1 = R(i x_c). */
+int pmp_realify_block(int n, int s, const double* d_re, const double* d_im, int ldx, double* d_y,
+                      int ldy, void* stream);
+/* inverse: x_c = column stride*c of the 2n-row real block. */
+int pmp_derealify_block(int n, int s, const double* d_y, int ldy, int stride, double* d_re,
+                        double* d_im, int ldx, void* stream);
+/* d_out[e] = |re[e] + i im[e]| (level-1 weights use |A|, spai.py:212). */
+int pmp_modulus(int nnz, const double* d_re, const double* d_im, double* d_out, void* stream);
+/* complex supports (iptr[n+1], iidx) -> real-form supports of columns 2j and
+ * 2j+1: {2k, 2k+1 : k in I_j} (optr[2n+1], oidx[4 nnz]). */
+int pmp_pattern_realify(int n, const int32_t* d_iptr, const int32_t* d_iidx, int32_t* d_optr,
+                        int32_t* d_oidx, void* stream);
+
 /* ---- multi-GPU collectives (NCCL over NVLink / NVSwitch) ------------------
  * The sequence driver's two exchanges: replicate the base
  * SPAI P1 (rpmor.py:205-210: every first-approach system depends only on

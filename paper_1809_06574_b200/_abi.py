@@ -109,6 +109,11 @@ _SIGS = {
     "pmp_host_hls_append": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp, c_vp], c_int),
     "pmp_fp64_peak": ([c_int, c_int, c_vp, c_vp], c_int),
+    "pmp_realify": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_realify_block": ([c_int, c_int, c_vp, c_vp, c_int, c_vp, c_int, c_vp], c_int),
+    "pmp_derealify_block": ([c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_int, c_vp], c_int),
+    "pmp_modulus": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_pattern_realify": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_nccl_available": ([], c_int),
     "pmp_nccl_unique_id": ([c_vp], c_int),
     "pmp_nccl_init": ([c_int, c_int, c_vp, c_vp], c_int),

@@ -607,6 +607,22 @@ struct WSmem {
   int ldw;
 };
 
+// The block step's tall-skinny products for the shared-memory geometries:
+// the scalar thread-per-row / lane-per-column forms (default), or FP64
+// tensor-core fragments loaded straight from global memory (PMP_MMA=1;
+// measured slower there -- c2 161 -> 176 us per block step -- the
+// global-row geometry stages its operands instead, stage_dev.cuh).
+#ifndef PMP_MMA
+#define PMP_MMA 0
+#endif
+#if PMP_MMA
+#define PMP_STEP_GRAM block_gram_mma<NY>
+#define PMP_STEP_UPDATE block_update_mma<NY>
+#else
+#define PMP_STEP_GRAM block_gram<NY>
+#define PMP_STEP_UPDATE block_update<NY>
+#endif
+
 template <bool CACHED, int NY>
 __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int r0, int nr,
                              bool lead, int& m, int& total, int& ncols, int& it, int& status) {
@@ -660,17 +676,17 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const double* Vrows = CACHED ? Xs + k : P.V + (size_t)r0 * cap;
     const int ldvr = CACHED ? ldx : cap;
     const Rows Vonly{Vrows, ldvr, total, Vrows, ldvr};
-    block_gram<NY>(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
+    PMP_STEP_GRAM(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
     cstamp(P, stp, 2);
     wreduce(wb, P.partial, P.gout, kx * sb, G, sbf.B, k * sb, sbf.H1);
     cstamp(P, stp, 3);
-    block_update<NY>(CV, kx, Wv, ldw, sb, nr, G);
+    PMP_STEP_UPDATE(CV, kx, Wv, ldw, sb, nr, G);
     cstamp(P, stp, 4);
     // ---- R2: [V | W1]^T W1 ------------------------------------------------------
     const int kx2 = total + sb;
     {
       const Rows VW{Vrows, ldvr, total, Wv, ldw};
-      block_gram<NY>(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
+      PMP_STEP_GRAM(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
       cstamp(P, stp, 5);
       wreduce(wb, P.partial, P.gout, kx2 * sb, G, sbf.H2, total * sb, nullptr);
       cstamp(P, stp, 6);
@@ -692,7 +708,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
 #ifdef PMP_STAMPS
     cstamp(P, stp, 12);
 #endif
-    block_update<NY>(Vonly, total, Wv, ldw, sb, nr, G);
+    PMP_STEP_UPDATE(Vonly, total, Wv, ldw, sb, nr, G);
 #ifdef PMP_STAMPS
     cstamp(P, stp, 13);
 #endif

@@ -12,6 +12,7 @@
 //   pmp_gcro_absorb : spin on the step's flag in that memory, then update
 //                     Bmat / Hb (krylov.py:190-202) and append the new block
 //                     columns to the incremental QR of G (pmp_host_hls_append).
+#include <atomic>
 #include <chrono>
 
 #include "common.cuh"
@@ -74,6 +75,9 @@ int pmp_host_wait_flag(const double* flag, double sentinel, long long timeout_us
       }
     }
   }
+  // the flag is written last: order every later read of the mirror after
+  // the flag observation (weakly ordered hosts, compiler reordering)
+  std::atomic_thread_fence(std::memory_order_acquire);
   return PMP_OK;
 }
 

@@ -205,6 +205,152 @@ __device__ PMP_GRAM_INLINE void block_update(const Rows X, int kx, double* Y, in
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core (DMMA m8n8k4) forms of the two tall-skinny products of the
+// block step.  The point is the memory access, not the flops: a fragment load
+// of the A operand touches 8 rows x 32 B (update) or 4 rows x 64 B (Gram) --
+// whole sectors, every byte used -- where the thread-per-row update had each
+// warp-wide load hit 32 different rows, 8 of 32 bytes used per sector and
+// the rest left to an L1 that the kernel's shared memory squeezes to a few
+// tens of KB (ncu: 35 % excess sectors).  Fragment layout (PTX ISA, .f64
+// m8n8k4): g = lane >> 2, t = lane & 3; A[g][t], B[t][g], C/D[g][2t + i].
+// Fixed summation order (4-term chunks in row / column order): bitwise
+// reproducible run to run.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Y[r][c] -= sum_t X(r, t) G[t][c] (G row-major ld ny, shared memory): one
+// warp per 8-row block, ALL kx columns of the block's rows streamed as
+// 8 x 4 A fragments (four in flight), G as B fragments.
+template <int NY>
+__device__ __noinline__ void block_update_mma(const Rows X, int kx, double* Y, int ldy, int ny,
+                                              int nrows, const double* G) {
+  constexpr int NH = (NY + 7) / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nch = (kx + 3) >> 2;
+  for (int rb = wid * 8; rb < nrows; rb += (kOrthT / 32) * 8) {
+    const int r = rb + g;
+    const bool rok = r < nrows;
+    const double* xa = X.a + (size_t)(rok ? r : 0) * X.lda;
+    const double* xb = X.b + (size_t)(rok ? r : 0) * X.ldb - X.ka;
+    double acc[NH][2];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) acc[h][0] = acc[h][1] = 0.0;
+    for (int ch = 0; ch < nch; ch += 4) {
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = (ch + u) * 4 + t4;
+        a[u] = (rok && t < kx) ? (t < X.ka ? xa[t] : xb[t]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (ch + u >= nch) break;  // warp-uniform
+        const int t = (ch + u) * 4 + t4;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int c = h * 8 + g;
+          const double b = (t < kx && c < ny) ? G[t * ny + c] : 0.0;
+          dmma884(acc[h], a[u], b);
+        }
+      }
+    }
+    if (rok) {
+      double* y = Y + (size_t)r * ldy;
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int c = h * 8 + 2 * t4 + i;
+          if (c < ny) y[c] -= acc[h][i];
+        }
+    }
+  }
+  __syncthreads();
+}
+
+// partial[slot][t * ny + c] = sum over this block's rows of X(r, t) Y[r][c]:
+// jobs = (8-column tile of X, row split); one warp per job, 4 x 4 rows per
+// round of fragments; splits summed in a fixed order through `red`
+// (>= 512 * NH doubles).
+template <int NY>
+__device__ __noinline__ void block_gram_mma(const Rows X, int kx, const double* Y, int ldy, int ny,
+                                            int nrows, double* red, double* partial, int slot) {
+  constexpr int NH = (NY + 7) / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int K = kx * ny;
+  double* part = partial + (size_t)slot * K;
+  const int ntile = (kx + 7) >> 3;
+  int splits = (kOrthT / 32) / ntile;
+  if (splits < 1) splits = 1;
+  const int njobs = ntile * splits;
+  const int per = ((nrows + splits - 1) / splits + 3) & ~3;
+  for (int j0 = 0; j0 < njobs; j0 += kOrthT / 32) {
+    const int job = j0 + wid;
+    double acc[NH][2];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) acc[h][0] = acc[h][1] = 0.0;
+    if (job < njobs) {  // warp-uniform
+      const int tile = job / splits, sp = job % splits;
+      const int ra = sp * per, rb = min(nrows, ra + per);
+      const int t = tile * 8 + g;
+      const bool tok = t < kx;
+      const double* xcol = tok ? (t < X.ka ? X.a + t : X.b + (t - X.ka)) : X.a;
+      const int ldxc = (tok && t >= X.ka) ? X.ldb : X.lda;
+      for (int r0 = ra; r0 < rb; r0 += 16) {
+        double a[4], b[NH][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = r0 + 4 * u + t4;
+          const bool ok = r < rb;
+          a[u] = (ok && tok) ? xcol[(size_t)r * ldxc] : 0.0;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const int c = h * 8 + g;
+            b[h][u] = (ok && c < ny) ? Y[(size_t)r * ldy + c] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int h = 0; h < NH; ++h) dmma884(acc[h], a[u], b[h][u]);
+      }
+    }
+    if (job < njobs) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        red[((size_t)(job - j0) * NH + h) * 64 + g * 8 + 2 * t4] = acc[h][0];
+        red[((size_t)(job - j0) * NH + h) * 64 + g * 8 + 2 * t4 + 1] = acc[h][1];
+      }
+    }
+    __syncthreads();
+    // fixed-order sum over the splits of the tiles finished in this round
+    const int tile_lo = j0 / splits, tile_hi = min(ntile, (j0 + kOrthT / 32) / splits);
+    const int nout = (tile_hi - tile_lo) * 8 * ny;
+    for (int o = threadIdx.x; o < nout; o += kOrthT) {
+      const int tl = o / (8 * ny), rem = o % (8 * ny);
+      const int tt = rem / ny, c = rem % ny;
+      const int tile = tile_lo + tl, t = tile * 8 + tt;
+      if (t < kx) {
+        double s = 0.0;
+        for (int q = 0; q < splits; ++q) {
+          const int jj = tile * splits + q - j0;
+          s += red[((size_t)jj * NH + c / 8) * 64 + tt * 8 + (c % 8)];
+        }
+        part[t * ny + c] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Pivoted Cholesky of the m x m SPD matrix A (row-major, shared memory,
 // destroyed) by one warp with rolled loops: lane i owns row i.  R (row-major,
 // upper) is the factor of P^T A P, piv the permutation.  Small code on

@@ -25,7 +25,7 @@
 // projected problem, a drop test inside the cancellation band) ends the
 // group with status PMP_SOLVE_FALLBACK and the host re-solves that system
 // on the host-driven path.
-#include "cycle_dev.cuh"
+#include "stage_dev.cuh"
 
 namespace pmp {
 
@@ -45,6 +45,7 @@ struct SolveArgs {
   int n, s, cap, kc, outer_dim, inner_restart, max_iters;
   int gsz, rows_per_block, ldx, hist_cap, log_cap, isz;
   int wglob;  // W rows in global memory (rows beyond shared memory)
+  int stage_rows, stage_n;  // global-row geometry: staged ring (rows per stage, stages)
   double tol;
   const SysDesc* sys;
   double* ws;
@@ -269,6 +270,18 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   // became an L2 round trip
   __shared__ CycleArgs L;
   __shared__ int acts[16];
+  __shared__ uint64_t ring_bar[4];
+  __shared__ unsigned ring_seq;
+  if constexpr (WG) {
+    if (A.stage_rows > 0) {
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < A.stage_n; ++i) mbar_init(&ring_bar[i], 1);
+        mbar_fence_init();
+        ring_seq = 0;
+      }
+      __syncthreads();
+    }
+  }
   WBar wb{ist + 9, nw, 0, wi};
   WBar gb{ist + kGbar, A.gsz, 0, lb};
   const int slot = lb;  // partial slot of a worker (1 .. nw)
@@ -577,7 +590,18 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       const int ldw = WG ? s : odd_ld(na);
       double* Wv = WG ? W + (size_t)r0 * s : region + (CACHED ? (size_t)nr * A.ldx : 0);
       WSmem wsm{G, R1, R2, red, piv, piv2, flag, region, Wv, L.Q1g + (size_t)r0 * na, ldw};
-      worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
+      bool staged = false;
+      if constexpr (WG) {
+        if (A.stage_rows > 0) {
+          // (the control block's state lives in `region` of block 0 only:
+          // the workers' region is free for the staging ring)
+          const Ring ring{ring_bar, region, A.stage_n, A.stage_rows, kc, cap, s, 0u};
+          worker_inner_staged<NY>(L, wb, wsm, ring, &ring_seq, r0, nr, lead, m, total, ncols,
+                                  it, status);
+          staged = true;
+        }
+      }
+      if (!staged) worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
       sstamp(A, grp, cyc, 3);
     }
     gbar(gb);
@@ -957,6 +981,24 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   A.isz = b->isz;
   A.tol = b->tol;
   A.wglob = cached == 2;
+  A.stage_rows = 0;
+  A.stage_n = 0;
+#ifndef PMP_STAGE
+#define PMP_STAGE 1
+#endif
+  if (PMP_STAGE && cached == 2 && (b->s % 2) == 0 && (b->kc % 2) == 0 && (b->cap % 2) == 0) {
+    // ring of S stages x R rows of [C | V | W] in the workers' region
+    const size_t region = cycle_region_doubles(rows, A.ldx, b->s, b->kc + b->cap, b->s,
+                                               b->inner_restart, cached);
+    const size_t row = (size_t)b->kc + b->cap + b->s;
+    for (int S = 3; S >= 2 && A.stage_rows == 0; --S) {
+      const int R = (int)(region / (S * row)) & ~7;
+      if (R >= 8) {
+        A.stage_rows = R > 64 ? 64 : R;
+        A.stage_n = S;
+      }
+    }
+  }
   A.sys = reinterpret_cast<const SysDesc*>(b->d_sys);
   A.ws = b->d_ws;
   A.wsz = b->wsz;

@@ -1,0 +1,528 @@
+// Block step of the persistent solve for the GLOBAL-ROW geometry (large n:
+// c3 / c4 / c5 -- W rows in HBM), with the tall-skinny products fed by
+// bulk asynchronous copies (cp.async.bulk, the TMA engine's 1-D form) into a
+// shared-memory ring, and computed by FP64 tensor-core fragments (DMMA
+// m8n8k4) from shared memory.
+//
+// Why: at these sizes every phase of the block step streams the block's rows
+// of [C | V] and W from HBM.  The thread-per-row / lane-per-column loops keep
+// only a few loads in flight per warp at 16 warps per SM (the kernel's
+// register and shared-memory footprint), so the Gram / update phases ran at
+// 2-3 TB/s (ncu: 0.29 eligible warps per scheduler, L1 hit 55 %, 35 %
+// excess sectors).  Here one thread posts the copies of tile i + S - 1 while
+// the block computes tile i: S x R rows (tens of KB) in flight per block, no
+// register cost, whole 16-byte-aligned rows.
+//
+// The CGS2 step (krylov.py:186-196) becomes three streaming passes over the
+// block's rows instead of four:
+//   pass 1   [C | V]^T W                                 -> reduce -> B, H1
+//   pass 2   W1 = W - [C | V] [B; H1], then [V | W1]^T W1  -> reduce -> H2, W1^T W1
+//            (the Pythagorean G_W = W1^T W1 - H2^T H2 is factored before pass 3)
+//   pass 3   W2 = W1 - V H2 and, when the Cholesky-QR needs one pass
+//            (kappa <= 4), the new block Q = W2 P R^-1 straight into V
+// Same operations as the scalar path (cycle_dev.cuh worker_inner), different
+// (fixed) summation order.
+#pragma once
+
+#include "cycle_dev.cuh"
+
+namespace pmp {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra "
+      "WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy writes (this block's stores of W / V / C rows) before
+// async-proxy reads of the same global memory (the bulk copies)
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// One ring of S stages, R rows each: [C rows (ld kc) | V rows (ld cap) | W rows (ld s)].
+struct Ring {
+  uint64_t* bar;   // S mbarriers
+  double* base;    // S x stage doubles
+  int S, R;
+  int kc, cap, s;  // leading dimensions of the staged row blocks
+  unsigned seq;    // tiles consumed so far (all passes): stage / parity of the next
+  __device__ __forceinline__ size_t stage_doubles() const {
+    return (size_t)R * (kc + cap + s);
+  }
+  __device__ __forceinline__ double* Cs(int st) const { return base + st * stage_doubles(); }
+  __device__ __forceinline__ double* Vs(int st) const { return Cs(st) + (size_t)R * kc; }
+  __device__ __forceinline__ double* Ws(int st) const { return Vs(st) + (size_t)R * cap; }
+};
+
+// which parts a pass stages
+struct StageSpec {
+  const double* C;  // this block's C rows (ld kc), or null
+  const double* V;  // this block's V rows (ld cap), or null
+  int vcols;        // leading V columns needed (rounded up to even: 16-byte copies)
+  const double* W;  // this block's W rows (ld s), or null
+};
+
+// lanes of warp 0: post tile `tile` (rows [tile R, min(nr, ...))) into stage st
+__device__ __forceinline__ void ring_issue(const Ring& g, const StageSpec& sp, int tile, int nr,
+                                           int st) {
+  const int lane = threadIdx.x & 31;
+  const int ra = tile * g.R, nt = min(g.R, nr - ra);
+  uint64_t* bar = g.bar + st;
+  const uint32_t vb = (uint32_t)sp.vcols * 8;
+  uint32_t bytes = 0;
+  if (sp.C) bytes += (uint32_t)nt * g.kc * 8;
+  if (sp.V) bytes += (uint32_t)nt * vb;
+  if (sp.W) bytes += (uint32_t)nt * g.s * 8;
+  if (lane == 0) mbar_expect_tx(bar, bytes);
+  __syncwarp();
+  if (lane == 0 && sp.C) bulk_g2s(g.Cs(st), sp.C + (size_t)ra * g.kc, (uint32_t)nt * g.kc * 8, bar);
+  if (lane == 1 && sp.W) bulk_g2s(g.Ws(st), sp.W + (size_t)ra * g.s, (uint32_t)nt * g.s * 8, bar);
+  if (sp.V)
+    for (int r = lane; r < nt; r += 32)
+      bulk_g2s(g.Vs(st) + (size_t)r * g.cap, sp.V + (size_t)(ra + r) * g.cap, vb, bar);
+}
+
+// run `body(tile, stage, rows)` over the block's nr rows, S - 1 tiles ahead
+template <class F>
+__device__ __forceinline__ void ring_pass(Ring& g, const StageSpec& sp, int nr, F body) {
+  const int ntiles = (nr + g.R - 1) / g.R;
+  __syncthreads();  // every generic write of the rows to be staged is done
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) fence_proxy_async();
+    __syncwarp();
+    for (int i = 0; i < min(g.S - 1, ntiles); ++i) ring_issue(g, sp, i, nr, (g.seq + i) % g.S);
+  }
+  for (int i = 0; i < ntiles; ++i) {
+    const unsigned q = g.seq + i;
+    const int st = q % g.S;
+    if (threadIdx.x < 32 && i + g.S - 1 < ntiles)
+      ring_issue(g, sp, i + g.S - 1, nr, (q + g.S - 1) % g.S);
+    mbar_wait(g.bar + st, (q / g.S) & 1);
+    body(i, st, min(g.R, nr - i * g.R));
+    __syncthreads();  // stage st is free again
+  }
+  g.seq += ntiles;
+}
+
+// acc[j][e] (t-tile w + 8 j of the warp, chain e = 4-row chunk parity) +=
+// sum over the tile's rows of X(r, t) Y[r][c]; X = [a (ka cols, ld lda) |
+// b (ld ldb)], Y ld ldy, rows nt (a multiple of 8 except for the last tile)
+template <int NY, int NT>
+__device__ __forceinline__ void tile_gram(double (&acc)[NT][2][(NY + 7) / 8][2], const double* xa,
+                                          int lda, int ka, const double* xb, int ldb, int kx,
+                                          const double* Y, int ldy, int ny, int nt) {
+  constexpr int NH = (NY + 7) / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int t = (wid + 8 * j) * 8 + g;
+    if ((wid + 8 * j) * 8 >= kx) break;  // warp-uniform
+    const bool tok = t < kx;
+    const double* xc = tok ? (t < ka ? xa + t : xb + (t - ka)) : xa;
+    const int ldc = (tok && t >= ka) ? ldb : lda;
+    for (int r0 = 0; r0 < nt; r0 += 8) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = r0 + 4 * e + t4;
+        const bool ok = r < nt;
+        const double a = (ok && tok) ? xc[(size_t)r * ldc] : 0.0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int c = h * 8 + g;
+          const double b = (ok && c < ny) ? Y[(size_t)r * ldy + c] : 0.0;
+          dmma884(acc[j][e][h], a, b);
+        }
+      }
+    }
+  }
+}
+
+template <int NY, int NT>
+__device__ __forceinline__ void acc_zero(double (&acc)[NT][2][(NY + 7) / 8][2]) {
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int h = 0; h < (NY + 7) / 8; ++h) acc[j][e][h][0] = acc[j][e][h][1] = 0.0;
+}
+
+// partial[t * ny + c] <- acc (the warp's t-tiles; chains summed 0 + 1)
+template <int NY, int NT>
+__device__ __forceinline__ void tile_gram_store(const double (&acc)[NT][2][(NY + 7) / 8][2],
+                                                int kx, int ny, double* part) {
+  constexpr int NH = (NY + 7) / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int t = (wid + 8 * j) * 8 + g;
+    if (t >= kx) continue;
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = h * 8 + 2 * t4 + i;
+        if (c < ny) part[t * ny + c] = acc[j][0][h][i] + acc[j][1][h][i];
+      }
+  }
+}
+
+// Y[r][c] -= sum_t X(r, t) G[t][c] for the tile's rows (8-row blocks over the
+// warps); X = [a (ka, lda) | b (ldb)], kx columns; G row-major ld ny (smem)
+template <int NY>
+__device__ __forceinline__ void tile_update(const double* xa, int lda, int ka, const double* xb,
+                                            int ldb, int kx, const double* G, double* Y, int ldy,
+                                            int ny, int nt) {
+  constexpr int NH = (NY + 7) / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nch = (kx + 3) >> 2;
+  for (int rb = wid * 8; rb < nt; rb += (kOrthT / 32) * 8) {
+    const int r = rb + g;
+    const bool rok = r < nt;
+    const double* ra = xa + (size_t)(rok ? r : 0) * lda;
+    const double* rbp = xb + (size_t)(rok ? r : 0) * ldb - ka;
+    // four independent accumulator chains (chunk mod 4), summed in a fixed
+    // order: the DMMA latency is not serialised over kx / 4 chunks
+    double acc4[4][NH][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < NH; ++h) acc4[u][h][0] = acc4[u][h][1] = 0.0;
+    for (int ch0 = 0; ch0 < nch; ch0 += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = (ch0 + u) * 4 + t4;
+        const double a = (rok && t < kx) ? (t < ka ? ra[t] : rbp[t]) : 0.0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int c = h * 8 + g;
+          const double b = (t < kx && c < ny) ? G[t * ny + c] : 0.0;
+          dmma884(acc4[u][h], a, b);
+        }
+      }
+    }
+    double acc[NH][2];
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        acc[h][i] = (acc4[0][h][i] + acc4[1][h][i]) + (acc4[2][h][i] + acc4[3][h][i]);
+    if (rok) {
+      double* y = Y + (size_t)r * ldy;
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int c = h * 8 + 2 * t4 + i;
+          if (c < ny) y[c] -= acc[h][i];
+        }
+    }
+  }
+}
+
+// y = x[piv] R^-1 for the tile's rows (thread per row): the new V block
+template <int NY>
+__device__ __forceinline__ void tile_trsm(const double* X, int ldx, double* Y, int ldy, int nt,
+                                          int m, const double* R, const int* piv,
+                                          const double* rinv) {
+  for (int r = threadIdx.x; r < nt; r += kOrthT) {
+    double x[NY], y[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) x[c] = (c < m) ? X[(size_t)r * ldx + (piv ? piv[c] : c)] : 0.0;
+#pragma unroll
+    for (int c = 0; c < NY; ++c) {
+      if (c < m) {
+        double s = x[c];
+#pragma unroll
+        for (int a = 0; a < NY; ++a)
+          if (a < c) s -= y[a] * R[a * m + c];
+        y[c] = s * rinv[c];
+      } else {
+        y[c] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < m) Y[(size_t)r * ldy + c] = y[c];
+  }
+}
+
+// pass 1: part[t * sb + c] = sum over the block's rows of [C | V](r, t) W[r][c]
+template <int NY>
+__device__ __noinline__ void staged_gram1(Ring g, const double* C, int k, const double* V,
+                                          int total, const double* W, int sb, int nr,
+                                          double* part, unsigned* seq) {
+  constexpr int NH = (NY + 7) / 8, NT = 2;
+  const int kx = k + total;
+  double acc[NT][2][NH][2];
+  acc_zero<NY, NT>(acc);
+  const StageSpec sp{k > 0 ? C : nullptr, V, (total + 1) & ~1, W};
+  g.seq = *seq;
+  ring_pass(g, sp, nr, [&](int, int st, int nt) {
+    tile_gram<NY, NT>(acc, g.Cs(st), g.kc, k, g.Vs(st), g.cap, kx, g.Ws(st), g.s, sb, nt);
+  });
+  tile_gram_store<NY, NT>(acc, kx, sb, part);
+  *seq = g.seq;
+  __syncthreads();
+}
+
+// pass 2: W1 = W - [C | V] G (G = [B; H1], kx x sb, smem), written back to
+// W; part2[t * sb + c] = sum of [V | W1](r, t) W1[r][c] (t < total + sb)
+template <int NY>
+__device__ __noinline__ void staged_upd1_gram2(Ring g, const double* C, int k, const double* V,
+                                               int total, double* W, int sb, int nr,
+                                               const double* G, double* part, unsigned* seq) {
+  constexpr int NH = (NY + 7) / 8, NT = 2;
+  const int kx = k + total, kx2 = total + sb;
+  double acc[NT][2][NH][2];
+  acc_zero<NY, NT>(acc);
+  const StageSpec sp{k > 0 ? C : nullptr, V, (total + 1) & ~1, W};
+  g.seq = *seq;
+  ring_pass(g, sp, nr, [&](int tile, int st, int nt) {
+    double* Wt = g.Ws(st);
+    tile_update<NY>(g.Cs(st), g.kc, k, g.Vs(st), g.cap, kx, G, Wt, g.s, sb, nt);
+    __syncthreads();
+    // W1 rows back to HBM (pass 3 and the cycle end read them)
+    double* Wg = W + (size_t)tile * g.R * g.s;
+    for (int q = threadIdx.x; q < nt * g.s; q += kOrthT) Wg[q] = Wt[q];
+    tile_gram<NY, NT>(acc, g.Vs(st), g.cap, total, Wt, g.s, kx2, Wt, g.s, sb, nt);
+  });
+  tile_gram_store<NY, NT>(acc, kx2, sb, part);
+  *seq = g.seq;
+  __syncthreads();
+}
+
+// pass 3: W2 = W1 - V H2 (H2: total x sb, smem); with `Rq` (one Cholesky-QR
+// pass suffices) the new block Q = W2[:, piv] R^-1 goes straight to Vq (ld
+// cap); otherwise W2 is written back to W for the second pass
+template <int NY>
+__device__ __noinline__ void staged_upd2(Ring g, const double* V, int total, double* W, int sb,
+                                         int nr, const double* H2, const double* Rq,
+                                         const int* piv, double* Vq, unsigned* seq) {
+  __shared__ double rinv[16];
+  if (Rq && threadIdx.x < sb) rinv[threadIdx.x] = 1.0 / Rq[threadIdx.x * sb + threadIdx.x];
+  const StageSpec sp{nullptr, V, (total + 1) & ~1, W};
+  g.seq = *seq;
+  ring_pass(g, sp, nr, [&](int tile, int st, int nt) {
+    double* Wt = g.Ws(st);
+    tile_update<NY>(g.Vs(st), g.cap, total, g.Vs(st), g.cap, total, H2, Wt, g.s, sb, nt);
+    __syncthreads();
+    if (Rq) {
+      tile_trsm<NY>(Wt, g.s, Vq + (size_t)tile * g.R * g.cap, g.cap, nt, sb, Rq, piv, rinv);
+    } else {
+      double* Wg = W + (size_t)tile * g.R * g.s;
+      for (int q = threadIdx.x; q < nt * g.s; q += kOrthT) Wg[q] = Wt[q];
+    }
+  });
+  *seq = g.seq;
+  __syncthreads();
+}
+
+}  // namespace pmp
+
+namespace pmp {
+
+// The worker side of one cycle's inner loop for the global-row geometry
+// (worker_inner in cycle_dev.cuh with the Gram / update phases replaced by
+// the three staged passes above).  Same contract: steps until restart
+// length, max_iters, a stop decision of the control block, or a Cholesky
+// flag; the lead worker writes the final state and the done flag.
+template <int NY>
+__device__ void worker_inner_staged(const CycleArgs& P, WBar& wb, const WSmem& S_, Ring ring,
+                                    unsigned* seq, int r0, int nr, bool lead, int& m, int& total,
+                                    int& ncols, int& it, int& status) {
+  double* G = S_.G;
+  double* R1 = S_.R1;
+  double* R2 = S_.R2;
+  double* red = S_.red;
+  int* piv = S_.piv;
+  int* piv2 = S_.piv2;
+  int* flag = S_.flag;
+  double* Wv = S_.Wv;  // this block's W rows in HBM (ld P.s)
+  double* Q1 = S_.Q1;
+  const int ldw = S_.ldw;
+  const int sb = P.sb, k = P.k, cap = P.cap, kc = P.kc;
+  double* Cr = const_cast<double*>(P.C) + (size_t)r0 * kc;
+  double* Vr = P.V + (size_t)r0 * cap;
+  int q = 0;
+  const int it_start = it;
+  while (true) {
+    if (it >= P.max_iters || m >= P.inner_restart) {
+      status = it >= P.max_iters ? 3 : 2;
+      if (q > 0) {
+        const int d = wait_flag(P.ist + 16 + q - 1, 0);
+        if (d == 1) status = 0;
+        if (d == 4) status = 4;
+      }
+      break;
+    }
+    const int q0 = m;
+    const int stp = it - it_start;
+    const StepBuf sbf = step_buf(P, q);
+    cstamp(P, stp, 0);
+    // ---- W = A F_0 .. F_{nfac-1} V[:, q0 : q0 + sb] ---------------------------
+    const double* src = P.V + q0;
+    int lds = cap;
+    for (int f = P.nfac - 1; f >= 0; --f) {
+      double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
+      spmm_rows<NY>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst + (size_t)r0 * P.s, P.s,
+                    r0, nr);
+      wbar(wb);
+      src = dst;
+      lds = P.s;
+    }
+    spmm_rows<NY>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr);
+    cstamp(P, stp, 1);
+
+    // ---- pass 1: [C | V]^T W ---------------------------------------------------
+    const int kx = k + total;
+    staged_gram1<NY>(ring, Cr, k, Vr, total, Wv, sb, nr,
+                     P.partial + (size_t)(wb.wi + 1) * kx * sb, seq);
+    cstamp(P, stp, 2);
+    wreduce(wb, P.partial, P.gout, kx * sb, G, sbf.B, k * sb, sbf.H1);
+    cstamp(P, stp, 3);
+    // ---- pass 2: W1 = W - [C | V] G, then [V | W1]^T W1 -------------------------
+    const int kx2 = total + sb;
+    staged_upd1_gram2<NY>(ring, Cr, k, Vr, total, Wv, sb, nr, G,
+                          P.partial + (size_t)(wb.wi + 1) * kx2 * sb, seq);
+    cstamp(P, stp, 4);
+    cstamp(P, stp, 5);
+    wreduce(wb, P.partial, P.gout, kx2 * sb, G, sbf.H2, total * sb, nullptr);
+    cstamp(P, stp, 6);
+    // G_W = W1^T W1 - H2^T H2 (R2), symmetrised into red, factored before
+    // pass 3 (it does not depend on W2)
+    const int n4 = 4 * sb * sb, lim4 = (n4 + 31) & ~31;
+    for (int q4 = threadIdx.x; q4 < lim4; q4 += kOrthT) {
+      const bool act = q4 < n4;
+      const int qq = q4 >> 2, part = q4 & 3;
+      const int i = act ? qq / sb : 0, j = act ? qq % sb : 0;
+      double s = 0.0;
+      if (act)
+        for (int t = part; t < total; t += 4) s += G[t * sb + i] * G[t * sb + j];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (act && part == 0) R2[qq] = G[(size_t)(total + i) * sb + j] - s;
+    }
+    __syncthreads();
+    for (int qq = threadIdx.x; qq < sb * sb; qq += kOrthT) {
+      const int i = qq / sb, j = qq % sb;
+      red[qq] = 0.5 * (R2[i * sb + j] + R2[j * sb + i]);
+    }
+    __syncthreads();
+    cstamp(P, stp, 12);
+    if (threadIdx.x < 32) {
+      bool ok = warp_cholesky_smem(red, sb, R1, piv, true, kCholRatio);
+      if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
+    }
+    __syncthreads();
+    bool single = false;
+    if (flag[0] == 0) single = fabs(R1[0]) / fabs(R1[(sb - 1) * sb + (sb - 1)]) <= kSkipKappa;
+    cstamp(P, stp, 13);
+    // ---- pass 3: W2 = W1 - V H2 (and Q = W2 P R^-1 -> V when single) -------------
+    staged_upd2<NY>(ring, Vr, total, Wv, sb, nr, G, (flag[0] == 0 && single) ? R1 : nullptr,
+                    piv, Vr + total, seq);
+    cstamp(P, stp, 14);
+    cstamp(P, stp, 7);
+    if (flag[0] == 0 && !single) {
+      block_trsm_rows<NY>(Wv, ldw, Q1, sb, nr, sb, R1, piv);
+      const Rows Qv{Q1, sb, sb, Q1, sb};
+      block_gram<NY>(Qv, sb, Q1, sb, sb, nr, red, P.partial, wb.wi + 1);
+      wreduce(wb, P.partial, P.gout, sb * sb, G, nullptr, 0, nullptr);
+      if (threadIdx.x < 32) {
+        bool ok = warp_cholesky_smem(G, sb, R2, piv2, false, 0.0);
+        if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
+      }
+      __syncthreads();
+    }
+    cstamp(P, stp, 8);
+    if (flag[0]) {
+      // W2 is in P.W (this block's rows): the host Householder fallback
+      status = 5;
+      if (q > 0) {
+        const int d = wait_flag(P.ist + 16 + q - 1, 0);
+        if (d == 1) status = 0;
+        if (d == 4) status = 4;
+      }
+      if (status == 5 && lead) {
+        const int lens[3] = {k * sb, total * sb, total * sb};
+        const int offs[3] = {P.offB, P.offH1, P.offH2};
+        const double* srcs[3] = {sbf.B, sbf.H1, sbf.H2};
+        for (int a = 0; a < 3; ++a)
+          for (int qq = threadIdx.x; qq < lens[a]; qq += kOrthT)
+            P.mirror[offs[a] + qq] = __ldcg(srcs[a] + qq);
+      }
+      break;
+    }
+    if (!single) block_trsm_rows<NY>(Q1, sb, Vr + total, cap, nr, sb, R2, nullptr);
+    if (lead) {
+      // R = R2 R1 (pivoted order), un-pivoted: R[i, piv[c]] = R'[i, c]
+      for (int qq = threadIdx.x; qq < sb * sb; qq += kOrthT) {
+        const int i = qq / sb, c = qq % sb;
+        double s = 0.0;
+        if (single) {
+          s = R1[i * sb + c];
+        } else {
+          for (int a = i; a <= c; ++a) s += R2[i * sb + a] * R1[a * sb + c];
+        }
+        sbf.R[i * sb + piv[c]] = (c >= i) ? s : 0.0;
+      }
+    }
+    cstamp(P, stp, 9);
+    wbar(wb);  // new V block (and the step outputs) visible
+    cstamp(P, stp, 10);
+    if (q > 0) {
+      const int d = wait_flag(P.ist + 16 + q - 1, 0);
+      if (d == 1 || d == 4) {
+        status = d == 1 ? 0 : 4;
+        break;
+      }
+    }
+    cstamp(P, stp, 11);
+    if (lead && threadIdx.x == 0) {
+      __threadfence();
+      *(volatile int*)(P.ist + 7) = q + 1;  // publish step q to the control block
+    }
+    ++q;
+    ncols += (ncols == 0) ? k + sb : sb;
+    ++it;
+    m = total;
+    total += sb;
+  }
+  if (lead && threadIdx.x == 0) {
+    P.ist[0] = m;
+    P.ist[1] = total;
+    P.ist[2] = ncols;
+    P.ist[3] = it;
+    P.ist[4] = status;
+    __threadfence();
+    *(volatile int*)(P.ist + 8) = 1;  // done: the control block finishes up
+  }
+}
+
+}  // namespace pmp

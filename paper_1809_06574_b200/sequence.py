@@ -204,6 +204,11 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     on_solution(index, X): called with every solution block (device tensor,
     on the current stream) as soon as its solve is done -- e.g. to copy it to
     the host -- without keeping every X alive (keep_solutions).
+
+    Memory: a window's solutions live in one [k, n, s] allocation (as do its
+    assembled values and factor coefficients); keep_solutions therefore
+    stores a private copy of each X, so holding one system's solution never
+    pins the whole window's block.
     """
     import threading
     from . import _abi
@@ -348,7 +353,7 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                        "launches": getattr(rep, "device_launches", 0),
                        "algorithmic_bytes": getattr(rep, "algorithmic_bytes", None)}
                 if keep_solutions:
-                    rec["X"] = X
+                    rec["X"] = X.clone()   # (X is a view of the window's block)
                 if on_solution is not None:
                     on_solution(idx, X)
                 records.append(rec)

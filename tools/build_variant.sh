@@ -11,7 +11,7 @@ OUT=build/variants/$NAME
 mkdir -p $OUT
 objs=()
 pids=()
-for f in structure assemble ls blockops orth cycle solve gcro_host peak; do
+for f in structure assemble ls blockops orth cycle solve gcro_host peak cplx; do
   nvcc $FLAGS -c $SRC/$f.cu -o $OUT/$f.o &
   pids+=($!)
   objs+=($OUT/$f.o)
