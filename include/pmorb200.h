@@ -524,6 +524,18 @@ int pmp_modulus(int nnz, const double* d_re, const double* d_im, double* d_out, 
 int pmp_pattern_realify(int n, const int32_t* d_iptr, const int32_t* d_iidx, int32_t* d_optr,
                         int32_t* d_oidx, void* stream);
 
+/* Complex assembly (rpmor.py:92-107 mode 0 / affine.py:118-134 mode 1) over
+ * a union pattern: as pmp_assemble, with complex coefficients (h_cr + i h_ci),
+ * complex shift s and s^2 (computed by the caller as the reference does,
+ * Python complex s * s), term values h_re[t] (+ i h_im[t]; h_im or an entry
+ * NULL: real term).  Writes the complex result (d_re, d_im) per union
+ * entry, counts exact 0 + 0i entries; mode 1 prunes |v| < 1e-300. */
+int pmp_assemble_cplx(int nnz, int nterms, const double* const* h_re, const double* const* h_im,
+                      const int32_t* h_kind, const int32_t* h_group, const int32_t* h_first,
+                      const double* h_cr, const double* h_ci, int mode, double sr, double si,
+                      double s2r, double s2i, const int32_t* d_rowid, const int32_t* d_colidx,
+                      double* d_re, double* d_im, int32_t* d_zero_count, void* stream);
+
 /* ---- multi-GPU collectives (NCCL over NVLink / NVSwitch) ------------------
  * The sequence driver's two exchanges: replicate the base
  * SPAI P1 (rpmor.py:205-210: every first-approach system depends only on

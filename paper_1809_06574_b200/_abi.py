@@ -114,6 +114,8 @@ _SIGS = {
     "pmp_derealify_block": ([c_int, c_int, c_vp, c_int, c_int, c_vp, c_vp, c_int, c_vp], c_int),
     "pmp_modulus": ([c_int, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_pattern_realify": ([c_int, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pmp_assemble_cplx": ([c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
+                           c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "pmp_nccl_available": ([], c_int),
     "pmp_nccl_unique_id": ([c_vp], c_int),
     "pmp_nccl_init": ([c_int, c_int, c_vp, c_vp], c_int),

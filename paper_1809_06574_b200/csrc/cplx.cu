@@ -109,6 +109,110 @@ __global__ void k_pattern_realify(int n, const int* __restrict__ iptr, const int
   }
 }
 
+// ---------------------------------------------------------------------------
+// complex assembly: A = (s^2 M(p) + s D(p)) + K(p) (rpmor.py:92-107, complex
+// s / p / terms) or A0 + sum c_j A_j (affine.py:118-134), per union entry in
+// the reference's operation order (scipy / numpy complex arithmetic: each
+// product (ar br - ai bi) + i (ar bi + ai br) and each sum rounded
+// separately -- __dmul_rn / __dadd_rn / __dsub_rn, no FMA).  With real term
+// values every product is a real x real product, so the result does not
+// depend on how numpy contracts its complex multiply (bit-exact); complex
+// term values follow the unfused formula.
+// ---------------------------------------------------------------------------
+
+struct CAsm {
+  int nterms, mode, any_diag;
+  double sr, si, s2r, s2i;
+  const double* re[PMP_MAX_TERMS];
+  const double* im[PMP_MAX_TERMS];  // null: real term
+  int kind[PMP_MAX_TERMS];          // 0 union-expanded, 1 diagonal n-vector
+  int group[PMP_MAX_TERMS];
+  int first[PMP_MAX_TERMS];
+  double cr[PMP_MAX_TERMS], ci[PMP_MAX_TERMS];
+};
+
+__device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double& r,
+                                     double& i) {
+  r = __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, bi));
+  i = __dadd_rn(__dmul_rn(ar, bi), __dmul_rn(ai, br));
+}
+
+__global__ void __launch_bounds__(256) k_assemble_cplx(CAsm R, int nnz, const int* __restrict__ rowid,
+                                                       const int* __restrict__ colidx,
+                                                       double* __restrict__ ore,
+                                                       double* __restrict__ oim,
+                                                       int* zero_count) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  bool zero = false;
+  if (e < nnz) {
+    bool diag = false;
+    int row = 0;
+    if (R.any_diag) {
+      row = __ldg(rowid + e);
+      diag = (__ldg(colidx + e) == row);
+    }
+    double gr[3] = {0.0, 0.0, 0.0}, gi[3] = {0.0, 0.0, 0.0};
+    bool gp[3] = {false, false, false};
+#pragma unroll 1
+    for (int t = 0; t < R.nterms; ++t) {
+      const int g = R.group[t];
+      double vr, vi;
+      if (R.kind[t] == 0) {
+        vr = __ldg(R.re[t] + e);
+        vi = R.im[t] ? __ldg(R.im[t] + e) : 0.0;
+      } else {
+        vr = diag ? __ldg(R.re[t] + row) : 0.0;
+        vi = (diag && R.im[t]) ? __ldg(R.im[t] + row) : 0.0;
+      }
+      if (R.first[t]) {
+        gr[g] = vr;
+        gi[g] = vi;
+        gp[g] = true;
+      } else {
+        double pr, pi;
+        cmul(R.cr[t], R.ci[t], vr, vi, pr, pi);
+        gr[g] = __dadd_rn(gr[g], pr);
+        gi[g] = __dadd_rn(gi[g], pi);
+      }
+    }
+    double vr = 0.0, vi = 0.0;
+    if (R.mode == 0) {
+      bool have = false;
+      const double cr[3] = {R.s2r, R.sr, 1.0}, ci[3] = {R.s2i, R.si, 0.0};
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        if (!gp[g]) continue;
+        double pr, pi;
+        if (g == 2) {
+          pr = gr[g];  // 1.0 * part: exact
+          pi = gi[g];
+        } else {
+          cmul(cr[g], ci[g], gr[g], gi[g], pr, pi);
+        }
+        if (have) {
+          vr = __dadd_rn(vr, pr);
+          vi = __dadd_rn(vi, pi);
+        } else {
+          vr = pr;
+          vi = pi;
+        }
+        have = true;
+      }
+    } else {
+      vr = gr[0];
+      vi = gi[0];
+      if (hypot(vr, vi) < 1e-300) vr = vi = 0.0;  // affine.py:36, :132-133
+    }
+    if (vr == 0.0) vr = 0.0;
+    if (vi == 0.0) vi = 0.0;
+    zero = (vr == 0.0 && vi == 0.0);
+    ore[e] = vr;
+    oim[e] = vi;
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, zero);
+  if ((threadIdx.x & 31) == 0 && b && zero_count) atomicAdd(zero_count, __popc(b));
+}
+
 }  // namespace pmp
 
 using namespace pmp;
@@ -175,6 +279,43 @@ int pmp_pattern_realify(int n, const int32_t* d_iptr, const int32_t* d_iidx, int
   k_pattern_realify<<<(n + 1 + 255) / 256, 256, 0, S(stream)>>>(n, d_iptr, d_iidx, d_optr,
                                                                 d_oidx);
   return cuda_status("pmp_pattern_realify");
+}
+
+int pmp_assemble_cplx(int nnz, int nterms, const double* const* h_re, const double* const* h_im,
+                      const int32_t* h_kind, const int32_t* h_group, const int32_t* h_first,
+                      const double* h_cr, const double* h_ci, int mode, double sr, double si,
+                      double s2r, double s2i, const int32_t* d_rowid, const int32_t* d_colidx,
+                      double* d_re, double* d_im, int32_t* d_zero_count, void* stream) {
+  if (nnz < 0 || nterms < 1 || nterms > PMP_MAX_TERMS || !h_re || !d_re || !d_im) {
+    set_error("pmp_assemble_cplx: bad arguments");
+    return PMP_ERR_ARG;
+  }
+  CAsm R;
+  R.nterms = nterms;
+  R.mode = mode;
+  R.any_diag = 0;
+  R.sr = sr;
+  R.si = si;
+  R.s2r = s2r;
+  R.s2i = s2i;
+  for (int t = 0; t < nterms; ++t) {
+    R.re[t] = h_re[t];
+    R.im[t] = h_im ? h_im[t] : nullptr;
+    R.kind[t] = h_kind[t];
+    R.group[t] = h_group[t];
+    R.first[t] = h_first[t];
+    R.cr[t] = h_cr[t];
+    R.ci[t] = h_ci[t];
+    if (h_kind[t] == 1) R.any_diag = 1;
+  }
+  if (R.any_diag && (!d_rowid || !d_colidx)) {
+    set_error("pmp_assemble_cplx: diagonal terms need row ids");
+    return PMP_ERR_ARG;
+  }
+  if (!nnz) return PMP_OK;
+  k_assemble_cplx<<<(nnz + 255) / 256, 256, 0, S(stream)>>>(R, nnz, d_rowid, d_colidx, d_re, d_im,
+                                                           d_zero_count);
+  return cuda_status("pmp_assemble_cplx");
 }
 
 }  // extern "C"

@@ -45,7 +45,7 @@ struct SolveArgs {
   int n, s, cap, kc, outer_dim, inner_restart, max_iters;
   int gsz, rows_per_block, ldx, hist_cap, log_cap, isz;
   int wglob;  // W rows in global memory (rows beyond shared memory)
-  int stage_rows, stage_n;  // global-row geometry: staged ring (rows per stage, stages)
+  int stage_rows, stage_n;  // global-row geometry: staged ring (doubles per stage, stages)
   double tol;
   const SysDesc* sys;
   double* ws;
@@ -270,18 +270,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   // became an L2 round trip
   __shared__ CycleArgs L;
   __shared__ int acts[16];
-  __shared__ uint64_t ring_bar[4];
-  __shared__ unsigned ring_seq;
-  if constexpr (WG) {
-    if (A.stage_rows > 0) {
-      if (threadIdx.x == 0) {
-        for (int i = 0; i < A.stage_n; ++i) mbar_init(&ring_bar[i], 1);
-        mbar_fence_init();
-        ring_seq = 0;
-      }
-      __syncthreads();
-    }
-  }
+
   WBar wb{ist + 9, nw, 0, wi};
   WBar gb{ist + kGbar, A.gsz, 0, lb};
   const int slot = lb;  // partial slot of a worker (1 .. nw)
@@ -595,9 +584,8 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         if (A.stage_rows > 0) {
           // (the control block's state lives in `region` of block 0 only:
           // the workers' region is free for the staging ring)
-          const Ring ring{ring_bar, region, A.stage_n, A.stage_rows, kc, cap, s, 0u};
-          worker_inner_staged<NY>(L, wb, wsm, ring, &ring_seq, r0, nr, lead, m, total, ncols,
-                                  it, status);
+          const Ring ring{region, A.stage_n, A.stage_rows, kc, cap, s};
+          worker_inner_staged<NY>(L, wb, wsm, ring, r0, nr, lead, m, total, ncols, it, status);
           staged = true;
         }
       }
@@ -990,11 +978,13 @@ int pmp_solve_batch(PmpSolveBatch* b) {
     // ring of S stages x R rows of [C | V | W] in the workers' region
     const size_t region = cycle_region_doubles(rows, A.ldx, b->s, b->kc + b->cap, b->s,
                                                b->inner_restart, cached);
-    const size_t row = (size_t)b->kc + b->cap + b->s;
-    for (int S = 3; S >= 2 && A.stage_rows == 0; --S) {
-      const int R = (int)(region / (S * row)) & ~7;
-      if (R >= 8) {
-        A.stage_rows = R > 64 ? 64 : R;
+    // (stage_rows carries the stage size in doubles: a pass packs as many
+    // rows as its columns allow, >= 8 even at full width)
+    const size_t row = (size_t)bank_pad(b->kc) + bank_pad(b->cap) + bank_pad(b->s);
+    for (int S = 4; S >= 2 && A.stage_rows == 0; --S) {
+      const size_t stage = (region / S) & ~(size_t)1;
+      if (stage >= 8 * row) {
+        A.stage_rows = (int)stage;
         A.stage_n = S;
       }
     }

@@ -62,69 +62,112 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// One ring of S stages, R rows each: [C rows (ld kc) | V rows (ld cap) | W rows (ld s)].
+// One ring of S stages of `stage` doubles each in the workers' shared
+// memory.  A pass lays its tile out per stage as [C rows | V rows | W rows]
+// with padded strides (8 m + 4 doubles: the 4 rows of a DMMA half-warp
+// fragment land 8 banks apart) and as many rows as fit the columns it
+// actually needs (more rows per tile early in a cycle, when V is narrow).
 struct Ring {
-  uint64_t* bar;   // S mbarriers
-  double* base;    // S x stage doubles
-  int S, R;
-  int kc, cap, s;  // leading dimensions of the staged row blocks
-  unsigned seq;    // tiles consumed so far (all passes): stage / parity of the next
-  __device__ __forceinline__ size_t stage_doubles() const {
-    return (size_t)R * (kc + cap + s);
-  }
-  __device__ __forceinline__ double* Cs(int st) const { return base + st * stage_doubles(); }
-  __device__ __forceinline__ double* Vs(int st) const { return Cs(st) + (size_t)R * kc; }
-  __device__ __forceinline__ double* Ws(int st) const { return Vs(st) + (size_t)R * cap; }
+  double* base;
+  int S, stage;       // stages, doubles per stage
+  int kc, cap, s;     // global leading dimensions of C, V, W rows
 };
 
-// which parts a pass stages
+__host__ __device__ __forceinline__ int bank_pad(int w) { return ((w + 3) & ~7) + 4; }
+
+struct Tile {
+  int R;               // rows per tile
+  int cst, vst, wst;   // strides of the C / V / W parts (0: part absent)
+  int ccols, vcols, wcols;  // columns copied (even)
+  __device__ __forceinline__ double* Cs(const Ring& g, int st) const {
+    return g.base + (size_t)st * g.stage;
+  }
+  __device__ __forceinline__ double* Vs(const Ring& g, int st) const {
+    return Cs(g, st) + (size_t)R * cst;
+  }
+  __device__ __forceinline__ double* Ws(const Ring& g, int st) const {
+    return Vs(g, st) + (size_t)R * vst;
+  }
+};
+
+__device__ __forceinline__ Tile make_tile(const Ring& g, bool c, int vcols, bool w) {
+  Tile t;
+  t.ccols = c ? g.kc : 0;
+  t.vcols = (vcols + 1) & ~1;
+  t.wcols = w ? g.s : 0;
+  t.cst = c ? bank_pad(g.kc) : 0;
+  t.vst = bank_pad(t.vcols);
+  t.wst = w ? bank_pad(g.s) : 0;
+  int R = (g.stage / (t.cst + t.vst + t.wst)) & ~7;
+  t.R = R > 64 ? 64 : R;
+  return t;
+}
+
+// which global rows a pass stages
 struct StageSpec {
   const double* C;  // this block's C rows (ld kc), or null
-  const double* V;  // this block's V rows (ld cap), or null
-  int vcols;        // leading V columns needed (rounded up to even: 16-byte copies)
+  const double* V;  // this block's V rows (ld cap)
   const double* W;  // this block's W rows (ld s), or null
 };
 
-// lanes of warp 0: post tile `tile` (rows [tile R, min(nr, ...))) into stage st
-__device__ __forceinline__ void ring_issue(const Ring& g, const StageSpec& sp, int tile, int nr,
-                                           int st) {
-  const int lane = threadIdx.x & 31;
-  const int ra = tile * g.R, nt = min(g.R, nr - ra);
-  uint64_t* bar = g.bar + st;
-  const uint32_t vb = (uint32_t)sp.vcols * 8;
-  uint32_t bytes = 0;
-  if (sp.C) bytes += (uint32_t)nt * g.kc * 8;
-  if (sp.V) bytes += (uint32_t)nt * vb;
-  if (sp.W) bytes += (uint32_t)nt * g.s * 8;
-  if (lane == 0) mbar_expect_tx(bar, bytes);
-  __syncwarp();
-  if (lane == 0 && sp.C) bulk_g2s(g.Cs(st), sp.C + (size_t)ra * g.kc, (uint32_t)nt * g.kc * 8, bar);
-  if (lane == 1 && sp.W) bulk_g2s(g.Ws(st), sp.W + (size_t)ra * g.s, (uint32_t)nt * g.s * 8, bar);
-  if (sp.V)
-    for (int r = lane; r < nt; r += 32)
-      bulk_g2s(g.Vs(st) + (size_t)r * g.cap, sp.V + (size_t)(ra + r) * g.cap, vb, bar);
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait(int pending) {
+  switch (pending) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+  }
+}
+
+// every thread: its share of the 16-byte copies of tile `tile` into stage st
+__device__ __forceinline__ void ring_issue(const Ring& g, const Tile& T, const StageSpec& sp,
+                                           int tile, int nr, int st) {
+  const int ra = tile * T.R, nt = min(T.R, nr - ra);
+  const int cc = T.ccols >> 1, vc = T.vcols >> 1, wc = T.wcols >> 1;
+  const int nc = nt * cc, nv = nt * vc, nw = nt * wc;
+  double* Cd = T.Cs(g, st);
+  double* Vd = T.Vs(g, st);
+  double* Wd = T.Ws(g, st);
+  for (int q = threadIdx.x; q < nc + nv + nw; q += kOrthT) {
+    if (q < nc) {
+      const int r = q / cc, c = q - r * cc;
+      cp_async16(Cd + (size_t)r * T.cst + 2 * c, sp.C + (size_t)(ra + r) * g.kc + 2 * c);
+    } else if (q < nc + nv) {
+      const int x = q - nc, r = x / vc, c = x - r * vc;
+      cp_async16(Vd + (size_t)r * T.vst + 2 * c, sp.V + (size_t)(ra + r) * g.cap + 2 * c);
+    } else {
+      const int x = q - nc - nv, r = x / wc, c = x - r * wc;
+      cp_async16(Wd + (size_t)r * T.wst + 2 * c, sp.W + (size_t)(ra + r) * g.s + 2 * c);
+    }
+  }
 }
 
 // run `body(tile, stage, rows)` over the block's nr rows, S - 1 tiles ahead
 template <class F>
-__device__ __forceinline__ void ring_pass(Ring& g, const StageSpec& sp, int nr, F body) {
-  const int ntiles = (nr + g.R - 1) / g.R;
-  __syncthreads();  // every generic write of the rows to be staged is done
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) fence_proxy_async();
-    __syncwarp();
-    for (int i = 0; i < min(g.S - 1, ntiles); ++i) ring_issue(g, sp, i, nr, (g.seq + i) % g.S);
+__device__ __forceinline__ void ring_pass(const Ring& g, const Tile& T, const StageSpec& sp,
+                                          int nr, F body) {
+  const int ntiles = (nr + T.R - 1) / T.R;
+  __syncthreads();  // this block's earlier writes of the rows are done
+  for (int i = 0; i < g.S - 1; ++i) {
+    if (i < ntiles) ring_issue(g, T, sp, i, nr, i % g.S);
+    cp_async_commit();
   }
   for (int i = 0; i < ntiles; ++i) {
-    const unsigned q = g.seq + i;
-    const int st = q % g.S;
-    if (threadIdx.x < 32 && i + g.S - 1 < ntiles)
-      ring_issue(g, sp, i + g.S - 1, nr, (q + g.S - 1) % g.S);
-    mbar_wait(g.bar + st, (q / g.S) & 1);
-    body(i, st, min(g.R, nr - i * g.R));
-    __syncthreads();  // stage st is free again
+    const int st = i % g.S;
+    if (i + g.S - 1 < ntiles) ring_issue(g, T, sp, i + g.S - 1, nr, (i + g.S - 1) % g.S);
+    cp_async_commit();          // (possibly empty: the group count stays in step)
+    cp_async_wait(g.S - 1);     // tile i's group is complete
+    __syncthreads();
+    body(i, st, min(T.R, nr - i * T.R));
+    __syncthreads();            // stage st is free again
   }
-  g.seq += ntiles;
 }
 
 // acc[j][e] (t-tile w + 8 j of the warp, chain e = 4-row chunk parity) +=
@@ -277,18 +320,18 @@ __device__ __forceinline__ void tile_trsm(const double* X, int ldx, double* Y, i
 template <int NY>
 __device__ __noinline__ void staged_gram1(Ring g, const double* C, int k, const double* V,
                                           int total, const double* W, int sb, int nr,
-                                          double* part, unsigned* seq) {
-  constexpr int NH = (NY + 7) / 8, NT = 2;
+                                          double* part) {
+  constexpr int NT = 2;
   const int kx = k + total;
-  double acc[NT][2][NH][2];
+  double acc[NT][2][(NY + 7) / 8][2];
   acc_zero<NY, NT>(acc);
-  const StageSpec sp{k > 0 ? C : nullptr, V, (total + 1) & ~1, W};
-  g.seq = *seq;
-  ring_pass(g, sp, nr, [&](int, int st, int nt) {
-    tile_gram<NY, NT>(acc, g.Cs(st), g.kc, k, g.Vs(st), g.cap, kx, g.Ws(st), g.s, sb, nt);
+  const Tile T = make_tile(g, k > 0, total, true);
+  const StageSpec sp{C, V, W};
+  ring_pass(g, T, sp, nr, [&](int, int st, int nt) {
+    tile_gram<NY, NT>(acc, T.Cs(g, st), T.cst, k, T.Vs(g, st), T.vst, kx, T.Ws(g, st), T.wst,
+                      sb, nt);
   });
   tile_gram_store<NY, NT>(acc, kx, sb, part);
-  *seq = g.seq;
   __syncthreads();
 }
 
@@ -297,24 +340,26 @@ __device__ __noinline__ void staged_gram1(Ring g, const double* C, int k, const 
 template <int NY>
 __device__ __noinline__ void staged_upd1_gram2(Ring g, const double* C, int k, const double* V,
                                                int total, double* W, int sb, int nr,
-                                               const double* G, double* part, unsigned* seq) {
-  constexpr int NH = (NY + 7) / 8, NT = 2;
+                                               const double* G, double* part) {
+  constexpr int NT = 2;
   const int kx = k + total, kx2 = total + sb;
-  double acc[NT][2][NH][2];
+  double acc[NT][2][(NY + 7) / 8][2];
   acc_zero<NY, NT>(acc);
-  const StageSpec sp{k > 0 ? C : nullptr, V, (total + 1) & ~1, W};
-  g.seq = *seq;
-  ring_pass(g, sp, nr, [&](int tile, int st, int nt) {
-    double* Wt = g.Ws(st);
-    tile_update<NY>(g.Cs(st), g.kc, k, g.Vs(st), g.cap, kx, G, Wt, g.s, sb, nt);
+  const Tile T = make_tile(g, k > 0, total, true);
+  const StageSpec sp{C, V, W};
+  ring_pass(g, T, sp, nr, [&](int tile, int st, int nt) {
+    double* Wt = T.Ws(g, st);
+    tile_update<NY>(T.Cs(g, st), T.cst, k, T.Vs(g, st), T.vst, kx, G, Wt, T.wst, sb, nt);
     __syncthreads();
     // W1 rows back to HBM (pass 3 and the cycle end read them)
-    double* Wg = W + (size_t)tile * g.R * g.s;
-    for (int q = threadIdx.x; q < nt * g.s; q += kOrthT) Wg[q] = Wt[q];
-    tile_gram<NY, NT>(acc, g.Vs(st), g.cap, total, Wt, g.s, kx2, Wt, g.s, sb, nt);
+    double* Wg = W + (size_t)tile * T.R * g.s;
+    for (int q = threadIdx.x; q < nt * sb; q += kOrthT) {
+      const int r = q / sb, c = q - r * sb;
+      Wg[(size_t)r * g.s + c] = Wt[(size_t)r * T.wst + c];
+    }
+    tile_gram<NY, NT>(acc, T.Vs(g, st), T.vst, total, Wt, T.wst, kx2, Wt, T.wst, sb, nt);
   });
   tile_gram_store<NY, NT>(acc, kx2, sb, part);
-  *seq = g.seq;
   __syncthreads();
 }
 
@@ -324,23 +369,26 @@ __device__ __noinline__ void staged_upd1_gram2(Ring g, const double* C, int k, c
 template <int NY>
 __device__ __noinline__ void staged_upd2(Ring g, const double* V, int total, double* W, int sb,
                                          int nr, const double* H2, const double* Rq,
-                                         const int* piv, double* Vq, unsigned* seq) {
+                                         const int* piv, double* Vq) {
   __shared__ double rinv[16];
   if (Rq && threadIdx.x < sb) rinv[threadIdx.x] = 1.0 / Rq[threadIdx.x * sb + threadIdx.x];
-  const StageSpec sp{nullptr, V, (total + 1) & ~1, W};
-  g.seq = *seq;
-  ring_pass(g, sp, nr, [&](int tile, int st, int nt) {
-    double* Wt = g.Ws(st);
-    tile_update<NY>(g.Vs(st), g.cap, total, g.Vs(st), g.cap, total, H2, Wt, g.s, sb, nt);
+  const Tile T = make_tile(g, false, total, true);
+  const StageSpec sp{nullptr, V, W};
+  ring_pass(g, T, sp, nr, [&](int tile, int st, int nt) {
+    double* Wt = T.Ws(g, st);
+    tile_update<NY>(T.Vs(g, st), T.vst, total, T.Vs(g, st), T.vst, total, H2, Wt, T.wst, sb,
+                    nt);
     __syncthreads();
     if (Rq) {
-      tile_trsm<NY>(Wt, g.s, Vq + (size_t)tile * g.R * g.cap, g.cap, nt, sb, Rq, piv, rinv);
+      tile_trsm<NY>(Wt, T.wst, Vq + (size_t)tile * T.R * g.cap, g.cap, nt, sb, Rq, piv, rinv);
     } else {
-      double* Wg = W + (size_t)tile * g.R * g.s;
-      for (int q = threadIdx.x; q < nt * g.s; q += kOrthT) Wg[q] = Wt[q];
+      double* Wg = W + (size_t)tile * T.R * g.s;
+      for (int q = threadIdx.x; q < nt * sb; q += kOrthT) {
+        const int r = q / sb, c = q - r * sb;
+        Wg[(size_t)r * g.s + c] = Wt[(size_t)r * T.wst + c];
+      }
     }
   });
-  *seq = g.seq;
   __syncthreads();
 }
 
@@ -355,8 +403,8 @@ namespace pmp {
 // flag; the lead worker writes the final state and the done flag.
 template <int NY>
 __device__ void worker_inner_staged(const CycleArgs& P, WBar& wb, const WSmem& S_, Ring ring,
-                                    unsigned* seq, int r0, int nr, bool lead, int& m, int& total,
-                                    int& ncols, int& it, int& status) {
+                                    int r0, int nr, bool lead, int& m, int& total, int& ncols,
+                                    int& it, int& status) {
   double* G = S_.G;
   double* R1 = S_.R1;
   double* R2 = S_.R2;
@@ -403,14 +451,14 @@ __device__ void worker_inner_staged(const CycleArgs& P, WBar& wb, const WSmem& S
     // ---- pass 1: [C | V]^T W ---------------------------------------------------
     const int kx = k + total;
     staged_gram1<NY>(ring, Cr, k, Vr, total, Wv, sb, nr,
-                     P.partial + (size_t)(wb.wi + 1) * kx * sb, seq);
+                     P.partial + (size_t)(wb.wi + 1) * kx * sb);
     cstamp(P, stp, 2);
     wreduce(wb, P.partial, P.gout, kx * sb, G, sbf.B, k * sb, sbf.H1);
     cstamp(P, stp, 3);
     // ---- pass 2: W1 = W - [C | V] G, then [V | W1]^T W1 -------------------------
     const int kx2 = total + sb;
     staged_upd1_gram2<NY>(ring, Cr, k, Vr, total, Wv, sb, nr, G,
-                          P.partial + (size_t)(wb.wi + 1) * kx2 * sb, seq);
+                          P.partial + (size_t)(wb.wi + 1) * kx2 * sb);
     cstamp(P, stp, 4);
     cstamp(P, stp, 5);
     wreduce(wb, P.partial, P.gout, kx2 * sb, G, sbf.H2, total * sb, nullptr);
@@ -446,7 +494,7 @@ __device__ void worker_inner_staged(const CycleArgs& P, WBar& wb, const WSmem& S
     cstamp(P, stp, 13);
     // ---- pass 3: W2 = W1 - V H2 (and Q = W2 P R^-1 -> V when single) -------------
     staged_upd2<NY>(ring, Vr, total, Wv, sb, nr, G, (flag[0] == 0 && single) ? R1 : nullptr,
-                    piv, Vr + total, seq);
+                    piv, Vr + total);
     cstamp(P, stp, 14);
     cstamp(P, stp, 7);
     if (flag[0] == 0 && !single) {

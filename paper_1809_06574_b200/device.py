@@ -130,6 +130,9 @@ class DeviceCSR:
         self.vals = vals
         self.symmetric = bool(symmetric)
         self._csc_vals = None
+        # complex matrices are stored as their real form R(A) (cplx.py):
+        # shape / n are then the REAL dimensions (2n), complex_n the complex
+        self.cplx = False
 
     # -- construction / export --------------------------------------------
     @classmethod
@@ -157,7 +160,18 @@ class DeviceCSR:
                                   symmetric_pattern=sym or None)
         return cls(structure, f64(A.data), symmetric=sym)
 
+    @property
+    def complex_n(self):
+        return self.structure.n // 2 if self.cplx else self.structure.n
+
     def to_scipy(self, drop_zeros=True):
+        """Host CSR (complex128 for a complex matrix's real form)."""
+        if self.cplx:
+            from .cplx import to_complex_scipy
+            return to_complex_scipy(self, drop_zeros)
+        return self.to_scipy_real(drop_zeros)
+
+    def to_scipy_real(self, drop_zeros=True):
         s = self.structure
         M = sp.csr_matrix((self.vals.cpu().numpy(), s.colidx.cpu().numpy(), s.rowptr.cpu().numpy()),
                           shape=(s.n, s.n))

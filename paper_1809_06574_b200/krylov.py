@@ -467,6 +467,11 @@ def block_gcro_solve(A, B, P=None, cfg=None):
     solution comes back as numpy) or a CUDA tensor (solution stays on the
     device)."""
     cfg = cfg or SolverConfig()
+    if P is not None and not isinstance(P, Preconditioner):
+        raise TypeError("P must be a Preconditioner or None")
+    from .spai import _any_complex
+    if _any_complex(A, B, P) or (torch.is_tensor(B) and torch.is_complex(B)):
+        return _solve_complex(A, B, P, cfg)
     A = _as_dev_csr(A)
     n = A.n
     host_out = not torch.is_tensor(B)
@@ -483,6 +488,37 @@ def block_gcro_solve(A, B, P=None, cfg=None):
         raise ValueError("preconditioner dimension %d does not match system %d" % (P.dim, n))
     X, report = _solve(A, Bd, P, cfg)
     return (X.cpu().numpy() if host_out else X), report
+
+
+def _solve_complex(A, B, P, cfg):
+    """Complex block GCRO (krylov.py:105-275) on the real form (cplx.py):
+    the 2s-column block [R(b_0), R(i b_0), ...] with the restart length and
+    the outer-space dimension doubled (both count real columns), X from the
+    even columns; counts and residual rows reported per complex column."""
+    from . import cplx as _cx
+    R = _as_dev_csr(A, cplx=True)
+    n = R.complex_n
+    host_out = not torch.is_tensor(B)
+    Bh = np.asarray(B) if host_out else B
+    vec = Bh.ndim == 1
+    if Bh.shape[0] != n:
+        raise ValueError("right-hand side has %d rows, matrix is %dx%d" % (Bh.shape[0], n, n))
+    if P is not None:
+        P = P.as_complex()
+        if P.dim != n:
+            raise ValueError("preconditioner dimension %d does not match system %d" % (P.dim, n))
+    Br = _cx.block_to_real(Bh, pairs=True)
+    cfg2 = SolverConfig(tol=cfg.tol, max_iters=cfg.max_iters,
+                        outer_space_dim=2 * cfg.outer_space_dim,
+                        inner_restart=2 * cfg.inner_restart, deflation_tol=cfg.deflation_tol)
+    X2, rep = _solve(R, Br, P, cfg2)
+    X = _cx.block_from_real(X2, 2)
+    rep.matvec_count //= 2
+    rep.precond_apply_count //= 2
+    rep.residual_history = [np.asarray(h)[0::2].copy() for h in rep.residual_history]
+    if vec:
+        X = X[:, 0]
+    return (X.cpu().numpy() if host_out else X), rep
 
 
 class _Projected:
@@ -1168,10 +1204,13 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     kc = cfg.outer_space_dim + s
     ok = (s <= 16 and cfg.inner_restart + s <= 96 and cfg.outer_space_dim + s <= kc)
     chains = []
+    from .spai import _any_complex
     for A, P in systems:
         if P is not None and not isinstance(P, Preconditioner):
             raise TypeError("P must be a Preconditioner or None")
         chains.append(P.factors() if P is not None else [])
+    if any(_any_complex(A, P) for A, P in systems):
+        return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
     if not ok or max(len(c) for c in chains) > 3:
         return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
     gsz = ctypes.c_int()

@@ -22,35 +22,47 @@ from .device import DeviceCSR, Structure, _dev, f64, i32, scratch
 
 
 def _canon(T):
+    """as_csr (sparsecore.py:26-44): float64 when the imaginary part is zero,
+    complex128 otherwise (complex terms run through the real form, cplx.py)."""
     T = sp.csr_matrix(T)
-    if np.iscomplexobj(T.data):
-        if T.nnz and np.any(T.data.imag != 0):
-            raise NotImplementedError("complex-valued terms are not supported by the B200 path")
+    cx = np.iscomplexobj(T.data) and T.nnz and np.any(T.data.imag != 0)
+    if np.iscomplexobj(T.data) and not cx:
         T = sp.csr_matrix((T.data.real, T.indices, T.indptr), shape=T.shape)
-    T = sp.csr_matrix(T, dtype=np.float64, copy=True)
+    T = sp.csr_matrix(T, dtype=np.complex128 if cx else np.float64, copy=True)
     T.sum_duplicates()
     T.sort_indices()
     T.eliminate_zeros()
     return T
 
 
-def _real_scalar(c, what):
-    c = complex(c)
-    if c.imag != 0:
-        raise NotImplementedError("complex %s is not supported by the B200 path yet" % what)
-    return c.real
+def _is_cx(c):
+    return complex(c).imag != 0
+
+
+def _block(a):
+    """float64 unless the imaginary part is non-zero (then complex128)."""
+    a = np.asarray(a)
+    if np.iscomplexobj(a) and np.any(a.imag != 0):
+        return a.astype(np.complex128)
+    return np.asarray(a.real if np.iscomplexobj(a) else a, dtype=np.float64)
 
 
 class _UnionTerms:
-    """Union pattern of a list of terms and their device layout."""
+    """Union pattern of a list of terms and their device layout.  With
+    ``with_diag`` (the complex path) the diagonal joins the union: the real
+    form needs every diagonal block (cplx.py)."""
 
-    def __init__(self, terms):
+    def __init__(self, terms, with_diag=False):
         n = terms[0].shape[0]
         S = None
         for T in terms:
             ones = sp.csr_matrix((np.ones(T.nnz), T.indices, T.indptr), shape=T.shape)
             S = ones if S is None else S + ones
         S = sp.csr_matrix(S)
+        self.n_added_diag = 0
+        if with_diag:
+            self.n_added_diag = int(n - np.count_nonzero(S.diagonal()))
+            S = sp.csr_matrix(S + sp.identity(n, format="csr"))
         S.sort_indices()
         self.n = n
         self.symmetric = all(((T - T.T).nnz == 0) or not np.any((T - T.T).data) for T in terms)
@@ -59,13 +71,14 @@ class _UnionTerms:
                                    symmetric_pattern=sym_pattern or None)
         rows = np.repeat(np.arange(n), np.diff(S.indptr))
         self.vals = []
+        self.ivals = []     # imaginary parts (None: real term)
         self.kinds = []
         for T in terms:
             Tc = T.tocoo()
+            cx = np.iscomplexobj(T.data)
             if Tc.nnz and np.all(Tc.row == Tc.col):
-                d = np.zeros(n)
+                d = np.zeros(n, dtype=T.dtype)
                 d[Tc.row] = Tc.data
-                self.vals.append(f64(d))
                 self.kinds.append(1)
             else:
                 # slot of every term entry inside the union pattern: both
@@ -75,10 +88,11 @@ class _UnionTerms:
                 tkeys = (np.repeat(np.arange(n, dtype=np.int64), np.diff(T.indptr)) * n
                          + T.indices)
                 pos = np.searchsorted(skeys, tkeys)
-                full = np.zeros(S.nnz)
-                full[pos] = T.data
-                self.vals.append(f64(full))
+                d = np.zeros(S.nnz, dtype=T.dtype)
+                d[pos] = T.data
                 self.kinds.append(0)
+            self.vals.append(f64(d.real if cx else d))
+            self.ivals.append(f64(d.imag) if cx else None)
         self.rowid = i32(rows) if 1 in self.kinds else None
         if not self.symmetric:
             self.structure.csc()
@@ -149,6 +163,61 @@ class _UnionTerms:
         _abi.note_launches(-(-k // 16) - 1)
         return list(zip(outs, outs_perm))
 
+    def run_complex(self, recipe, mode, s):
+        """Complex assembly (pmp_assemble_cplx): recipe entries (term, group,
+        first, complex coef); s complex (mode 0).  Returns the real form."""
+        st = self.structure
+        nt = len(recipe)
+        re_p = ctypes_array_vp([self.vals[t].data_ptr() for t, _, _, _ in recipe])
+        im_p = ctypes_array_vp([self.ivals[t].data_ptr() if self.ivals[t] is not None else 0
+                                for t, _, _, _ in recipe])
+        kind = np.array([self.kinds[t] for t, _, _, _ in recipe], dtype=np.int32)
+        group = np.array([g for _, g, _, _ in recipe], dtype=np.int32)
+        first = np.array([f for _, _, f, _ in recipe], dtype=np.int32)
+        cr = np.array([complex(c).real for _, _, _, c in recipe], dtype=np.float64)
+        ci = np.array([complex(c).imag for _, _, _, c in recipe], dtype=np.float64)
+        s = complex(s)
+        s2 = s * s          # Python complex product, as the reference (rpmor.py:100)
+        re = torch.empty(max(st.nnz, 1), dtype=torch.float64, device=_dev())[:st.nnz]
+        im = torch.empty_like(re)
+        zc = torch.zeros(1, dtype=torch.int32, device=_dev())
+        rowid = self.rowid if self.rowid is not None else st.rowid()
+        _abi.call("pmp_assemble_cplx", st.nnz, nt, re_p, im_p, kind.ctypes.data,
+                  group.ctypes.data, first.ctypes.data, cr.ctypes.data, ci.ctypes.data, mode,
+                  s.real, s.imag, s2.real, s2.imag, _abi.ptr(rowid), _abi.ptr(st.colidx),
+                  _abi.ptr(re), _abi.ptr(im), _abi.ptr(zc), _abi.stream())
+        return self.finish_complex(re, im, int(zc.item()))
+
+    def finish_complex(self, re, im, zero_count):
+        """Complex values on the union (+ diagonal) structure -> the real form
+        (cplx.py).  Entries that came out exactly 0 + 0i beyond the diagonal
+        positions the union added are dropped, as as_csr does: that rare
+        case goes through the canonicalising host path."""
+        from .cplx import realify_csr
+        st = self.structure
+        n = st.n
+        if zero_count > self.n_added_diag:
+            M = sp.csr_matrix((re.cpu().numpy() + 1j * im.cpu().numpy(), st.colidx.cpu().numpy(),
+                               st.rowptr.cpu().numpy()), shape=(n, n))
+            return realify_csr(M)
+        if getattr(self, "real_struct", None) is None:
+            rp2 = torch.empty(2 * n + 1, dtype=torch.int32, device=_dev())
+            ci2 = torch.empty(max(4 * st.nnz, 1), dtype=torch.int32, device=_dev())
+            v0 = torch.empty(max(4 * st.nnz, 1), dtype=torch.float64, device=_dev())
+            _abi.call("pmp_realify", n, _abi.ptr(st.rowptr), _abi.ptr(st.colidx), None, None,
+                      _abi.ptr(rp2), _abi.ptr(ci2), _abi.ptr(v0), _abi.stream())
+            self.real_struct = Structure(2 * n, rp2, ci2[:4 * st.nnz],
+                                         symmetric_pattern=st.symmetric_pattern)
+        v2 = torch.empty(max(4 * st.nnz, 1), dtype=torch.float64, device=_dev())[:4 * st.nnz]
+        _abi.call("pmp_realify", n, _abi.ptr(st.rowptr), _abi.ptr(st.colidx), _abi.ptr(re),
+                  _abi.ptr(im), _abi.ptr(self.real_struct.rowptr), None, _abi.ptr(v2),
+                  _abi.stream())
+        A = DeviceCSR(self.real_struct, v2, symmetric=False)
+        A.cplx = True
+        A.cplx_struct = st
+        A.cplx_re, A.cplx_im = re, im
+        return A
+
     def finish(self, raw, zero_count):
         out, out_perm = raw
         if zero_count:
@@ -205,8 +274,8 @@ class SecondOrderModel:
             return None if ts is None else [_canon(T) for T in ts]
         m = cls(mass_terms=clean(mass_terms), damping_terms=clean(damping_terms),
                 stiffness_terms=clean(stiffness_terms),
-                rhs=None if rhs is None else np.atleast_2d(np.asarray(rhs, dtype=np.float64).T).T,
-                output=None if output is None else np.asarray(output, dtype=np.float64))
+                rhs=None if rhs is None else np.atleast_2d(_block(rhs).T).T,
+                output=None if output is None else _block(output))
         if m.mass_terms is None and m.damping_terms is None and m.stiffness_terms is None:
             raise ValueError("need at least one of mass/damping/stiffness terms")
         return m
@@ -237,6 +306,47 @@ class SecondOrderModel:
     def structure(self):
         return self._union().structure
 
+    @property
+    def has_complex_terms(self):
+        return any(np.iscomplexobj(T.data) for ts in
+                   (self.mass_terms, self.damping_terms, self.stiffness_terms) for T in ts or [])
+
+    def needs_complex(self, s, pvals):
+        """Complex assembly: complex terms, shift or parameters."""
+        return (self.has_complex_terms or _is_cx(s)
+                or any(_is_cx(c) for c in np.atleast_1d(pvals)))
+
+    def _union_c(self):
+        u = getattr(self, "_uc", None)
+        if u is None:
+            terms, groups = [], []
+            for g, ts in enumerate((self.mass_terms, self.damping_terms, self.stiffness_terms)):
+                for T in ts or []:
+                    terms.append(T)
+                    groups.append(g)
+            u = _UnionTerms(terms, with_diag=True)
+            u.groups = groups
+            self._uc = u
+        return u
+
+    def _assemble_complex(self, s, pvals):
+        """(s^2 M(p) + s D(p)) + K(p) for complex s / p / terms, on the device,
+        as its real form (rpmor.py:92-107 with the reference's complex
+        arithmetic; cplx.py)."""
+        u = self._union_c()
+        pv = np.atleast_1d(np.asarray(pvals, dtype=np.complex128))
+        recipe = []
+        t = 0
+        for g, ts in enumerate((self.mass_terms, self.damping_terms, self.stiffness_terms)):
+            if ts is None:
+                continue
+            recipe.append((t, g, 1, 1.0))
+            for i, c in enumerate(pv[:len(ts) - 1]):
+                if c != 0:
+                    recipe.append((t + i + 1, g, 0, complex(c)))
+            t += len(ts)
+        return u.run_complex(recipe, 0, complex(s))
+
     def reset_symbolic(self):
         """Drop every symbolic result derived from the model's sparsity
         structure -- the level-0 SPAI pattern, its CSR transpose plan, the
@@ -252,6 +362,8 @@ class SecondOrderModel:
     def assemble(self, s, pvals):
         """(s^2 M(p) + s D(p)) + K(p) as a device CSR, bit-identical to the
         reference's canonical CSR (rpmor.py:92-107)."""
+        if self.family is None and self.needs_complex(s, pvals):
+            return self._assemble_complex(s, pvals)
         u, recipe, s = self._recipe(s, pvals)
         return u.run(recipe, 0, s)
 
@@ -270,6 +382,9 @@ class SecondOrderModel:
         points = list(points)
         if not points:
             return ([], None) if defer_zero_check else []
+        if any(self.needs_complex(s, p) for s, p in points):
+            out = [self.assemble(s, p) for s, p in points]
+            return (out, None) if defer_zero_check else out
         zc = torch.zeros(len(points), dtype=torch.int32, device=_dev())
         u = self._union()
         recs = [self._recipe(s, p) for s, p in points]
@@ -294,8 +409,8 @@ class SecondOrderModel:
         if self.family is not None:
             raise ValueError("affine-form models are evaluated at expansion points; "
                              "use family.evaluate")
-        s = _real_scalar(s, "shift")
-        pv = [_real_scalar(c, "parameter") for c in np.atleast_1d(pvals)]
+        s = complex(s).real
+        pv = [complex(c).real for c in np.atleast_1d(pvals)]
         u = self._union()
         recipe = []
         t = 0
@@ -323,8 +438,8 @@ class AffineFamily:
                 raise ValueError("all terms must be square with equal dimension; got %s vs %s"
                                  % (T.shape, (n, n)))
         self.terms = terms
-        self.rhs = None if rhs is None else np.asarray(rhs, dtype=np.float64).reshape(n, -1)
-        self.output = None if output is None else np.asarray(output, dtype=np.float64)
+        self.rhs = None if rhs is None else _block(rhs).reshape(n, -1)
+        self.output = None if output is None else _block(output)
         self._u = None
 
     @property
@@ -337,10 +452,19 @@ class AffineFamily:
 
     def evaluate(self, point):
         vals = getattr(point, "values", point)
-        coeffs = [_real_scalar(c, "parameter") for c in np.atleast_1d(vals)]
+        coeffs = [complex(c) for c in np.atleast_1d(vals)]
         if len(coeffs) != self.n_params:
             raise ValueError("point has %d components, family has %d parameters"
                              % (len(coeffs), self.n_params))
+        if any(np.iscomplexobj(T.data) for T in self.terms) or any(c.imag != 0 for c in coeffs):
+            if getattr(self, "_uc", None) is None:
+                self._uc = _UnionTerms(self.terms, with_diag=True)
+            recipe = [(0, 0, 1, 1.0)]
+            for j, c in enumerate(coeffs):
+                if c != 0:
+                    recipe.append((j + 1, 0, 0, c))
+            return self._uc.run_complex(recipe, 1, 0.0)
+        coeffs = [c.real for c in coeffs]
         if self._u is None:
             self._u = _UnionTerms(self.terms)
         recipe = [(0, 0, 1, 1.0)]

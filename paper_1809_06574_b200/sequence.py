@@ -216,8 +216,12 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
     policy = policy or PrecondPolicy("spai-update-first")
     solver_cfg = solver_cfg or SolverConfig(tol=1e-8)
     B = model.rhs if B is None else B
-    Bd = B if torch.is_tensor(B) else torch.as_tensor(np.ascontiguousarray(B, dtype=np.float64),
-                                                       device="cuda")
+    if torch.is_tensor(B):
+        Bd = B
+    elif np.iscomplexobj(B) and np.any(np.asarray(B).imag != 0):
+        Bd = np.asarray(B, dtype=np.complex128)   # complex: realified per solve (cplx.py)
+    else:
+        Bd = torch.as_tensor(np.ascontiguousarray(np.real(B), dtype=np.float64), device="cuda")
     points = [(s, np.atleast_1d(p)) for s in s_grid for p in p_grid]
     nsys = len(points)
     mine = owned_systems(nsys, rank, world, policy.kind)

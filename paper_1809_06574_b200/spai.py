@@ -52,8 +52,13 @@ class BuildStats:
     are copied to the host lazily, on first access."""
 
     def __init__(self, resid=None, flags=None, augmented=0, t_events=None, seconds=None,
-                 share=1):
+                 share=1, stride=1):
         self._share = share   # builds that shared the timed interval
+        # complex builds solve the real form's 2n columns: column 2j is the
+        # complex column j (cplx.py), so every other entry is reported
+        if stride > 1:
+            resid = resid[::stride].contiguous() if resid is not None else None
+            flags = flags[::stride].contiguous() if flags is not None else None
         self._resid = resid
         self._flags = flags
         self._aug = augmented
@@ -110,10 +115,30 @@ class BuildStats:
 # ---------------------------------------------------------------------------
 
 
-def _as_dev_csr(M):
+def _as_dev_csr(M, cplx=False):
+    """Device CSR of M; complex inputs (or ``cplx``) as their real form R(M)
+    (cplx.py)."""
+    from . import cplx as _cx
     if isinstance(M, DeviceCSR):
+        if cplx and not M.cplx:
+            return _cx.realify_csr(M.to_scipy())
         return M
+    if cplx or _cx.is_complex_host(M):
+        return _cx.realify_csr(M)
     return DeviceCSR.from_scipy(M)
+
+
+def _any_complex(*ms):
+    from . import cplx as _cx
+    for M in ms:
+        if M is None:
+            continue
+        if isinstance(M, Preconditioner):
+            if M.cplx:
+                return True
+        elif _cx.is_complex(M):
+            return True
+    return False
 
 
 class Preconditioner:
@@ -130,8 +155,10 @@ class Preconditioner:
         else:
             if q is None or base is None:
                 raise ValueError("factored form needs both q and base")
-            q = _as_dev_csr(q)
-            if q.shape[0] != base.dim:
+            q = _as_dev_csr(q, cplx=base.cplx)
+            if q.cplx and not base.cplx:
+                base = base.as_complex()
+            if q.complex_n != base.dim:
                 raise ValueError("factor dimension does not match base preconditioner")
             self.matrix, self.q, self.base = None, q, base
 
@@ -140,8 +167,21 @@ class Preconditioner:
         return "explicit" if self.matrix is not None else "factored"
 
     @property
+    def cplx(self):
+        """Complex preconditioner (factors held as real forms, cplx.py)."""
+        return (self.matrix if self.matrix is not None else self.q).cplx
+
+    def as_complex(self):
+        """The same operator on complex vectors (real factors realified)."""
+        if self.cplx:
+            return self
+        if self.matrix is not None:
+            return Preconditioner(matrix=_as_dev_csr(self.matrix, cplx=True))
+        return Preconditioner(q=_as_dev_csr(self.q, cplx=True), base=self.base.as_complex())
+
+    @property
     def dim(self):
-        return (self.matrix if self.matrix is not None else self.q).shape[0]
+        return (self.matrix if self.matrix is not None else self.q).complex_n
 
     @property
     def depth(self):
@@ -169,7 +209,25 @@ class Preconditioner:
             src, lds = dst, ldd
 
     def apply(self, V):
+        from . import cplx as _cx
         host = not torch.is_tensor(V)
+        if self.cplx or (host and _cx.is_complex_host(V)) or (
+                torch.is_tensor(V) and torch.is_complex(V)):
+            P = self.as_complex()
+            n = P.dim
+            vec = (np.ndim(V) == 1) if host else V.dim() == 1
+            Vr = _cx.block_to_real(V, pairs=False)
+            if Vr.shape[0] != 2 * n:
+                raise ValueError("preconditioner is %dx%d, block has %d rows"
+                                 % (n, n, Vr.shape[0] // 2))
+            s = Vr.shape[1]
+            Y = torch.empty_like(Vr)
+            tmp = [torch.empty_like(Vr), torch.empty_like(Vr)] if P.depth > 1 else None
+            P.apply_dev(_abi.ptr(Vr), s, s, _abi.ptr(Y), s, tmp)
+            out = _cx.block_from_real(Y, 1)
+            if vec:
+                out = out[:, 0]
+            return out.cpu().numpy() if host else out
         Vd = _block_to_dev(V)
         n, s = Vd.shape
         if n != self.dim:
@@ -584,7 +642,10 @@ def solve_columns(system, target, pattern, cfg, events=True):
     flags = torch.zeros(n, dtype=torch.int32, device=_dev())
     _run_tiers(tiers, pattern, A_csc, T_csc, coef, resid, flags)
     final_pat, final_coef, n_aug = pattern, coef, 0
-    if cfg.pattern_level >= 1 and n > 0:
+    if cfg.pattern_level >= 1 and n > 0 and system.cplx:
+        final_pat, final_coef, n_aug = _augment_complex(system, target, pattern, coef, resid,
+                                                        flags, cfg, A_csc, T_csc)
+    elif cfg.pattern_level >= 1 and n > 0:
         sel = torch.empty(n, dtype=torch.int32, device=_dev())
         cnt = torch.zeros(1, dtype=torch.int32, device=_dev())
         ws = scratch().get("select", _abi.lib().pmp_select_workspace(n))
@@ -604,8 +665,44 @@ def solve_columns(system, target, pattern, cfg, events=True):
         P = _factor_from_columns(final_pat, final_coef)
     if events:
         ev1.record()
-    stats = BuildStats(resid, flags, n_aug, (ev0, ev1) if events else None)
+    if system.cplx:
+        P.cplx = True
+    stats = BuildStats(resid, flags, n_aug, (ev0, ev1) if events else None,
+                       stride=2 if system.cplx else 1)
     return P, stats, final_pat, final_coef
+
+
+def _augment_complex(system, target, pattern, coef, resid, flags, cfg, A_csc, T_csc):
+    """Level-1 pass of a complex build on the real form (spai.py:285-289):
+    complex column j (real columns 2j, 2j+1) is augmented when its residual
+    -- that of real column 2j -- exceeds ep; the extra rows are ranked by the
+    complex moduli |A| |A|[:, j] (spai.py:210-222) on the complex structure,
+    realified, and both real columns re-solved."""
+    from . import cplx as _cx
+    n2 = system.n
+    n = n2 // 2
+    st = _abi.stream()
+    even = torch.arange(0, n2, 2, dtype=torch.int32, device=_dev())
+    sel = torch.empty(n, dtype=torch.int32, device=_dev())
+    cnt = torch.zeros(1, dtype=torch.int32, device=_dev())
+    ws = scratch().get("select", _abi.lib().pmp_select_workspace(n))
+    _abi.call("pmp_select_gt", n, _abi.ptr(even), _abi.ptr(resid), float(cfg.ep), _abi.ptr(sel),
+              _abi.ptr(cnt), _abi.ptr(ws), ws.numel(), st)
+    n_aug = int(cnt.item())
+    if not n_aug:
+        return pattern, coef, 0
+    jsel = (sel[:n_aug] // 2).to(torch.int32)
+    absA = _cx.modulus_csr(system)
+    base_c = level0_pattern(absA)
+    apat_c = _augment(absA, base_c, jsel, n_aug, cfg.max_fill_per_column)
+    apat = _cx.realify_pattern(apat_c)
+    jh = jsel.cpu().numpy().astype(np.int64)
+    cols = np.sort(np.concatenate([2 * jh, 2 * jh + 1]))
+    atiers = _get_tiers(apat, system, target, cols)
+    acoef = torch.empty(max(apat.nnz, 1), dtype=torch.float64, device=_dev())
+    _run_tiers(atiers, apat, A_csc, T_csc, acoef, resid, flags)
+    fp, fc = _merge(pattern, coef, apat, acoef)
+    return fp, fc, n_aug
 
 
 def _seg_tier(t):
@@ -686,9 +783,11 @@ def solve_columns_many(systems, target, pattern, cfg):
                   _abi.ptr(val_block), nz, st)
     for q in range(k):
         P = DeviceCSR(csr, val_block[q, :pattern.nnz], symmetric=False)
+        P.cplx = systems[q].cplx
         out.append((P, (resids[q], flags[q])))
     ev1.record()
-    return [(P, BuildStats(r, f, 0, (ev0, ev1), share=k)) for P, (r, f) in out]
+    stride = 2 if A0.cplx else 1
+    return [(P, BuildStats(r, f, 0, (ev0, ev1), share=k, stride=stride)) for P, (r, f) in out]
 
 
 def _merge(base, bcoef, apat, acoef):
@@ -744,8 +843,12 @@ def _to_device_pattern(pattern, n):
 
 
 def spai_pattern(A, level=0, max_fill_per_column=80):
-    """A-priori pattern (spai.py:182-207), computed on the device."""
+    """A-priori pattern (spai.py:182-207), computed on the device (complex
+    matrices: on the complex structure, ranked by |A|)."""
     A = _as_dev_csr(A)
+    if A.cplx:
+        from .cplx import modulus_csr
+        A = modulus_csr(A)
     base = level0_pattern(A)
     if level == 0:
         return SparsityPattern(A.n, base.columns())
@@ -761,6 +864,20 @@ def spai_column(A, i, pattern_i):
     support = np.unique(np.asarray(pattern_i, dtype=np.int64))
     if support.size == 0:
         raise ValueError("column pattern must be nonempty")
+    if A.cplx:
+        # real form: column 2i over rows {2k, 2k+1 : k in support}
+        n = A.n
+        cols = [np.zeros(0, dtype=np.int64)] * n
+        cols[2 * int(i)] = np.sort(np.concatenate([2 * support, 2 * support + 1]))
+        pat = DevicePattern.from_columns(n, cols)
+        tiers = _get_tiers(pat, A, None, np.array([2 * int(i)]))
+        coef = torch.empty(max(pat.nnz, 1), dtype=torch.float64, device=_dev())
+        resid = torch.empty(n, dtype=torch.float64, device=_dev())
+        flags = torch.zeros(n, dtype=torch.int32, device=_dev())
+        _run_tiers(tiers, pat, A.csc(), None, coef, resid, flags)
+        z = coef[:2 * support.size].cpu().numpy()
+        return (support, z[0::2] + 1j * z[1::2], float(resid[2 * int(i)].item()),
+                bool(flags[2 * int(i)].item()))
     n = A.n
     cols = [np.zeros(0, dtype=np.int64)] * n
     cols[int(i)] = support
@@ -781,10 +898,14 @@ def spai_build(A, cfg=None, pattern=None, threads=1):
     A = _as_dev_csr(A)
     cfg = cfg or SpaiConfig()
     if pattern is None:
-        pat = level0_pattern(A)
+        pat = level0_pattern(A)   # (real form: the complex supports realified)
         eff = cfg
     else:
-        pat = _to_device_pattern(pattern, A.n)
+        if A.cplx:
+            from .cplx import realify_pattern
+            pat = realify_pattern(_to_device_pattern(pattern, A.complex_n))
+        else:
+            pat = _to_device_pattern(pattern, A.n)
         eff = SpaiConfig(ep=cfg.ep, pattern_level=0, max_fill_per_column=cfg.max_fill_per_column)
     P, stats, _, _ = solve_columns(A, None, pat, eff)
     return Preconditioner(matrix=P), stats
@@ -864,10 +985,15 @@ def quality(A, P):
     through the chain and A in 32-column slabs (SpMMs, never materialising
     P), each slab's squared norm is the trace of its Gram matrix (pmp_gram);
     one host read at the end.  Diagnostic only."""
-    A = _as_dev_csr(A)
     Pc = P if isinstance(P, Preconditioner) else Preconditioner(matrix=P)
-    if Pc.dim != A.n:
+    cx = _any_complex(A, Pc)
+    A = _as_dev_csr(A, cplx=cx)
+    if cx:
+        Pc = Pc.as_complex()
+    if Pc.dim != A.complex_n:
         raise ValueError("preconditioner does not conform with the matrix")
+    # (complex: the real form R(I - A P) holds every entry twice -- columns
+    # 2j and 2j+1 have equal norms -- hence the 1/sqrt(2) below)
     n, w = A.n, 32
     dev = _dev()
     E = torch.zeros((n, w), dtype=torch.float64, device=dev)
@@ -888,4 +1014,5 @@ def quality(A, P):
         _abi.call("pmp_gram", n, cw, _abi.ptr(Y), w, cw, _abi.ptr(Y), w, _abi.ptr(G),
                   _abi.ptr(ws), ws.numel(), _abi.stream())
         acc += torch.diagonal(G.view(-1)[:cw * cw].view(cw, cw)).sum()
-    return float(np.sqrt(max(float(acc.item()), 0.0)))
+    q = float(np.sqrt(max(float(acc.item()), 0.0)))
+    return q / np.sqrt(2.0) if cx else q

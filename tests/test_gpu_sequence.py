@@ -119,3 +119,33 @@ def test_c3_sequence_vs_reference(pm):
         ref = [g["iterations"] for g in gold["records"]]
         its = [recs[i]["iterations"] for i in range(128)]
         assert abs(np.mean(its) - np.mean(ref)) <= 0.5
+
+
+@pytest.mark.parametrize("lvl", [0, 1])
+def test_update_second_vs_reference(pm, lvl):
+    """update_second (update.py:90-97): Q of system 3 against system 2 on
+    top of the first update (chain depth 3) -- values vs the real reference,
+    and the depth-3 chain's block solve (tests/golden/update2_c1s24.npz)."""
+    import sys
+    sys.path.insert(0, os.path.join(G.GOLDEN, "..", "..", "oracle"))
+    import pmor_oracle as orc
+    from paper_1809_06574_b200.workloads import make_config
+    g = G.load("update2_c1s24")
+    W = make_config(1, scale=24)
+    model = pm.SecondOrderModel.from_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms,
+                                         rhs=W.rhs)
+    pts = W.points()
+    A = [model.assemble(*pts[i]) for i in range(3)]
+    P1, _ = pm.spai_build(A[0], pm.SpaiConfig(pattern_level=lvl))
+    P2, _ = pm.update_first(A[0], A[1], P1, pm.UpdateConfig(pattern_level=lvl))
+    P3, st = pm.update_second(A[1], A[2], P2, pm.UpdateConfig(approach="second",
+                                                              pattern_level=lvl))
+    assert P3.depth == int(g["depth%d" % lvl]) == 3
+    G.compare_factor(P3.q.to_scipy(), G.csr(g, "Q%d" % lvl))
+    assert np.max(np.abs(st.residuals - g["Q%d_resid" % lvl])) <= 1e-12
+    assert st.augmented_columns == int(g["Q%d_aug" % lvl])
+    X, rep = pm.block_gcro_solve(A[2], W.rhs, P=P3, cfg=pm.SolverConfig(tol=1e-8))
+    Ah = orc.assemble_mdk(W.mass_terms, W.damping_terms, W.stiffness_terms, *pts[2])
+    rel = np.linalg.norm(W.rhs - Ah @ X, axis=0) / np.linalg.norm(W.rhs, axis=0)
+    assert rep.converged and np.all(rel <= 1e-8)
+    assert abs(rep.iterations - int(g["s%d_iters" % lvl])) <= 2
