@@ -112,12 +112,10 @@ __global__ void k_pattern_realify(int n, const int* __restrict__ iptr, const int
 // ---------------------------------------------------------------------------
 // complex assembly: A = (s^2 M(p) + s D(p)) + K(p) (rpmor.py:92-107, complex
 // s / p / terms) or A0 + sum c_j A_j (affine.py:118-134), per union entry in
-// the reference's operation order (scipy / numpy complex arithmetic: each
-// product (ar br - ai bi) + i (ar bi + ai br) and each sum rounded
-// separately -- __dmul_rn / __dadd_rn / __dsub_rn, no FMA).  With real term
-// values every product is a real x real product, so the result does not
-// depend on how numpy contracts its complex multiply (bit-exact); complex
-// term values follow the unfused formula.
+// the reference's operation order and rounding (numpy's complex128 multiply
+// contracts one product of each part into an FMA, see cmul; sums are rounded
+// separately -- __dadd_rn).  With real term values and real coefficients
+// every product is a real x real product and the contraction is invisible.
 // ---------------------------------------------------------------------------
 
 struct CAsm {
@@ -131,10 +129,15 @@ struct CAsm {
   double cr[PMP_MAX_TERMS], ci[PMP_MAX_TERMS];
 };
 
+// numpy's complex128 product a * b (the reference's arithmetic: its SIMD loop
+// is mul + fused muladdsub, tests/golden/make_complex_golden.py pins it):
+// re = fma(a_re, b_re, -(a_im b_im)), im = fma(a_re, b_im, a_im b_re) -- NOT
+// symmetric in (a, b).  scipy's scalar * matrix is data * scalar (a = data,
+// rpmor.py:47, :104); affine.py:129 is scalar * data (a = scalar).
 __device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double& r,
                                      double& i) {
-  r = __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, bi));
-  i = __dadd_rn(__dmul_rn(ar, bi), __dmul_rn(ai, br));
+  r = __fma_rn(ar, br, -__dmul_rn(ai, bi));
+  i = __fma_rn(ar, bi, __dmul_rn(ai, br));
 }
 
 __global__ void __launch_bounds__(256) k_assemble_cplx(CAsm R, int nnz, const int* __restrict__ rowid,
@@ -170,7 +173,10 @@ __global__ void __launch_bounds__(256) k_assemble_cplx(CAsm R, int nnz, const in
         gp[g] = true;
       } else {
         double pr, pi;
-        cmul(R.cr[t], R.ci[t], vr, vi, pr, pi);
+        if (R.mode == 0)
+          cmul(vr, vi, R.cr[t], R.ci[t], pr, pi);  // data * scalar
+        else
+          cmul(R.cr[t], R.ci[t], vr, vi, pr, pi);  // scalar * data
         gr[g] = __dadd_rn(gr[g], pr);
         gi[g] = __dadd_rn(gi[g], pi);
       }
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(256) k_assemble_cplx(CAsm R, int nnz, const in
           pr = gr[g];  // 1.0 * part: exact
           pi = gi[g];
         } else {
-          cmul(cr[g], ci[g], gr[g], gi[g], pr, pi);
+          cmul(gr[g], gi[g], cr[g], ci[g], pr, pi);  // part data * coef
         }
         if (have) {
           vr = __dadd_rn(vr, pr);

@@ -141,7 +141,35 @@ def mdk_case():
     print("wrote cx_mdk")
 
 
+def affine_case():
+    """Genuinely complex terms x complex coefficients: pins the rounding of
+    numpy's complex multiply (scalar * data in affine.py:129, data * scalar
+    through scipy in rpmor.py:47 / :104)."""
+    from pmorprec.affine import AffineFamily
+    out = {}
+    terms = [random_sparse(36, density=0.12, seed=31 + 2 * j, shift=3.0 if j == 0 else 0.0)
+             for j in range(4)]
+    for j, T in enumerate(terms):
+        csr("T%d" % j, T, out)
+    fam = AffineFamily(terms)
+    pts = [np.array([0.5 - 0.25j, 1.5 + 2.0j, -0.3 + 0.7j]),
+           np.array([1.0 / 3.0 + 1j / 7.0, 0.0, 2.5j])]
+    for i, pt in enumerate(pts):
+        out["pt%d" % i] = pt
+        csr("A%d" % i, fam.evaluate(pt), out)
+    # complex terms through the second-order form as well
+    m = SecondOrderModel.from_mdk([terms[1], terms[2]], [terms[3]], [terms[0], terms[2]])
+    mp = [(0.3 + 1.5j, [0.75 - 0.25j]), (1.25, [0.5j])]
+    for i, (s, p) in enumerate(mp):
+        out["ms%d" % i] = np.array(complex(s))
+        out["mp%d" % i] = np.asarray(p, dtype=np.complex128)
+        csr("M%d" % i, m.assemble(s, p), out)
+    np.savez_compressed(os.path.join(HERE, "cx_affine.npz"), **out)
+    print("wrote cx_affine")
+
+
 if __name__ == "__main__":
     rand_case()
     gyro_case()
     mdk_case()
+    affine_case()

@@ -144,6 +144,26 @@ def test_mdk_complex_shift_assembly_bit_exact(pm):
         assert np.array_equal(A.data, Ar.data), i
 
 
+def test_complex_terms_times_complex_coefficients_bit_exact(pm):
+    """numpy's complex multiply is not symmetric in its operands (one product
+    of each part is fused): affine.py:129 is scalar * data, scipy's
+    scalar * matrix (rpmor.py:47, :104) is data * scalar."""
+    g = G.load("cx_affine")
+    terms = [ccsr(g, "T%d" % j) for j in range(4)]
+    fam = pm.AffineFamily(terms)
+    for i in range(2):
+        A = fam.evaluate(g["pt%d" % i]).to_scipy()
+        Ar = ccsr(g, "A%d" % i)
+        assert np.array_equal(A.indptr, Ar.indptr) and np.array_equal(A.indices, Ar.indices)
+        assert np.array_equal(A.data, Ar.data), i
+    m = pm.SecondOrderModel.from_mdk([terms[1], terms[2]], [terms[3]], [terms[0], terms[2]])
+    for i in range(2):
+        A = m.assemble(complex(g["ms%d" % i]), g["mp%d" % i]).to_scipy()
+        Ar = ccsr(g, "M%d" % i)
+        assert np.array_equal(A.indptr, Ar.indptr) and np.array_equal(A.indices, Ar.indices)
+        assert np.array_equal(A.data, Ar.data), i
+
+
 # ---- the reference's unit-test assertions on complex inputs -------------------
 
 def test_spai_column_full_pattern_matches_dense_inverse(pm):
