@@ -402,14 +402,20 @@ typedef struct PmpSolveBatch {
   size_t oV, oC, oU, oW, oT0, oT1, oQ1, oXt, oR, oDX, oRB, oZ, oPart, oGout, oSbuf, oProj, oLog,
       oAux;
   int pBmat, pHb, pCq, pY, pRes, pBn, pHist;
+  /* pCtl: pmp_solve_ctl_doubles(s, kc, cap, inner_restart) doubles inside the
+   * projected-state block for the control block's state when the geometry
+   * keeps it in global memory (rows beyond shared memory: c4 / c5). */
+  int pCtl;
   /* queue of systems: d_sys holds nsys descriptors; `groups` block groups
    * solve them, each taking the next unsolved system when it finishes one
    * (d_queue: one int32 of scratch, reset by the call).  Per system i:
    * d_result[8 i + 0..6] = status (0 ok, 10 host fallback), fallback reason,
    * iterations, columns still active (0 = converged), residual-log rows,
-   * matvec count, preconditioner-apply count; d_result_log[i (1 + log_cap s)]
-   * = algorithmic HBM bytes of its block steps, then the residual log
-   * (log rows x s, row-major). */
+   * matvec count, preconditioner-apply count; d_result_log[i (2 + log_cap s)]
+   * = algorithmic HBM bytes of its block steps -- [0] every operand once
+   * per step, [1] SURVEY.md 8(d)'s unit (the operator chain + 32 n total +
+   * 48 n s_b + 16 n k per step: block CGS2 reads [C | V] four times) --
+   * then the residual log (log rows x s, row-major). */
   int nsys;
   int32_t* d_queue;
   int32_t* d_result;
@@ -418,6 +424,7 @@ typedef struct PmpSolveBatch {
 } PmpSolveBatch;
 int pmp_solve_geometry(int n, int s, int cap, int kc, int inner_restart, int groups, int* gsz,
                        int* rows_per_block, int* cached, size_t* smem_bytes);
+size_t pmp_solve_ctl_doubles(int s, int kc, int cap, int inner_restart);
 int pmp_solve_batch(PmpSolveBatch* batch);
 
 /* Route every cooperative launch (pmp_orth_step, pmp_fold, pmp_gcro_step's

@@ -103,6 +103,7 @@ _SIGS = {
     "pmp_solve_geometry": ([c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp],
                            c_int),
     "pmp_solve_batch": ([c_vp], c_int),
+    "pmp_solve_ctl_doubles": ([c_int, c_int, c_int, c_int], c_sz),
     "pmp_set_coop_stream": ([c_vp], c_int),
     "pmp_orth_debug_stamps": ([c_vp, c_int], c_int),
     "pmp_host_deflate": ([c_int, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp], c_int),
@@ -178,7 +179,7 @@ _LAUNCHES_PER_CALL = {"pmp_scan": 2, "pmp_transpose": 5, "pmp_pattern_l0": 5,
 _NO_LAUNCH = {"pmp_last_error", "pmp_version", "pmp_host_deflate", "pmp_host_hls_append",
               "pmp_host_alloc_mapped", "pmp_host_free_mapped", "pmp_host_device_ptr",
               "pmp_host_wait_flag", "pmp_gcro_absorb", "pmp_orth_debug_stamps",
-              "pmp_cycle_debug_stamps", "pmp_solve_geometry",
+              "pmp_cycle_debug_stamps", "pmp_solve_geometry", "pmp_solve_ctl_doubles",
               "pmp_cycle_workspace", "pmp_nccl_available", "pmp_nccl_unique_id",
               "pmp_nccl_init", "pmp_nccl_destroy"}
 # pmp_gcro_step launches the SpMM chain (1 + depth) and the orthogonalisation

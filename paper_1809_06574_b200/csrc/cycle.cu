@@ -109,11 +109,16 @@ __global__ void __launch_bounds__(kOrthT, 2) k_cycle(CycleArgs P) {
 
 int cycle_nblk(int restart, int sb) { return (restart + sb - 1) / sb + 1; }
 
-size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached) {
+// doubles of the control block's projected-problem state (ctl_layout)
+size_t cycle_ctl_doubles(int sb, int ldq, int na, int restart) {
   const size_t nb = cycle_nblk(restart, sb);
-  size_t ctl = nb * 4 * sb * sb + (size_t)sb * sb * nb * (nb + 1) / 2 + (size_t)ldq * na +
-               (size_t)sb * ldq + sb * sb + 16 * 96 + 32 + 8 + 16 + 16 +
-               (size_t)(2 * sb + 1) * (3 * sb + na) + (size_t)2 * ldq * sb + 8;
+  return nb * 4 * sb * sb + (size_t)sb * sb * nb * (nb + 1) / 2 + (size_t)ldq * na +
+         (size_t)sb * ldq + sb * sb + 16 * 96 + 32 + 8 + 16 + 16 +
+         (size_t)(2 * sb + 1) * (3 * sb + na) + (size_t)2 * ldq * sb + 8;
+}
+
+size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached) {
+  size_t ctl = cycle_ctl_doubles(sb, ldq, na, restart);
   // cached: 1 = [C | V] rows (and W rows) in shared memory, 0 = W rows
   // only, 2 = none (W rows in global memory: large n per block)
   size_t work = (size_t)rows * ((cached == 1 ? ldx : 0) + (cached == 2 ? 0 : odd_ld(sb)));

@@ -34,20 +34,37 @@ struct CycleArgs {
 };
 
 // diagnostics: %globaltimer of phase i of step `step`, blocks 0 and 1
-static __device__ __forceinline__ void cstamp(const CycleArgs& P, int step, int i) {
-#ifdef PMP_STAMPS
-  // diagnostics only (tools/build_variant.sh stamps -DPMP_STAMPS): the
-  // stamps perturb code generation, so production builds compile them out
+// (pmp_cycle_debug_stamps; P.dbg is null unless a diagnostics run set it)
+static __device__ __forceinline__ void cstamp_on(const CycleArgs& P, int step, int i) {
   if (P.dbg && blockIdx.x < 2 && threadIdx.x == 0 && step < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     P.dbg[((size_t)step * 32 + i) * 2 + blockIdx.x] = t;
   }
+}
+static __device__ __forceinline__ void cstamp(const CycleArgs& P, int step, int i) {
+#ifdef PMP_STAMPS
+  // diagnostics builds (tools/build_variant.sh stamps -DPMP_STAMPS): the
+  // stamps perturb code generation, so production builds compile them out
+  // of the shared-memory geometries
+  cstamp_on(P, step, i);
 #else
   (void)P;
   (void)step;
   (void)i;
 #endif
+}
+// The worker step loop's stamps stay compiled in where STAMP is set: the
+// global-row instance of k_solve runs 7 % FASTER with them (c4 6-system
+// batch 448 -> 416 ms, profiles/r02_codegen_ab.txt; same spills -- the
+// volatile timer reads pin the phase order the scheduler otherwise
+// interleaves), the shared-memory instances 2 % slower.
+template <bool STAMP>
+static __device__ __forceinline__ void wstamp(const CycleArgs& P, int step, int i) {
+  if (STAMP)
+    cstamp_on(P, step, i);
+  else
+    cstamp(P, step, i);
 }
 
 static __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -127,6 +144,169 @@ __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int
       if (r < nr && col_ok) Y[(size_t)r * ldy + c] = a0[u] + a1[u];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// The same product with its operands staged asynchronously (global-row
+// geometry, full 8-column blocks: c4).  spmm_rows keeps 16 gathers per
+// thread in flight behind two dependent index loads, at 16 warps per SM:
+// latency bound (tools/micro/spmm_bench.cu: 1.41 ms for six 128^3 systems,
+// 1.09 ms this way).  Here a tile of 64 rows has its index / value segment
+// (contiguous in CSR) copied into shared memory two tiles ahead and its
+// gathered X rows (16-byte cp.async pieces, L2 only) one tile ahead; the
+// products read shared memory.  No registers are held across the latency and
+// a whole tile's gathers (28 KB) are in flight per block.  Same per-row
+// summation order as spmm_rows (even / odd entries, then summed): bitwise
+// equal results.  Tiles whose entries exceed the ring (irregular rows: c5)
+// go through spmm_rows.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void spa_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void spa_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void spa_cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+#ifndef PMP_SPMM_ASYNC
+#define PMP_SPMM_ASYNC 1
+#endif
+
+template <int NY>
+__device__ __noinline__ void spmm_rows_async(const int32_t* __restrict__ rp,
+                                             const int32_t* __restrict__ ci,
+                                             const double* __restrict__ va, const double* X,
+                                             int ldx, double* Y, int ldy, int r0, int nr,
+                                             double* ring, int ring_doubles) {
+  constexpr int PER = kOrthT / NY, RPT = 2, TR = RPT * PER, PC = NY / 2;
+  const int c = threadIdx.x % NY, slot = threadIdx.x / NY;
+  // ring = X rows [2][EMAX * NY] | values [3][EMAX] | indices [3][EMAX] (int)
+  const int EMAX = (int)(((size_t)ring_doubles * 8) / (2 * NY * 8 + 3 * 12)) & ~3;
+  double* xb = ring;
+  double* vb = ring + (size_t)2 * EMAX * NY;
+  int* cb = reinterpret_cast<int*>(vb + (size_t)3 * EMAX);
+  const int ntiles = (nr + TR - 1) / TR;
+  const int32_t* rpb = rp + r0;
+  auto bound = [&](int t) { return __ldg(rpb + min(t * TR, nr)); };
+  auto issue_cv = [&](int t, int e_lo, int cnt) {
+    if (cnt > EMAX) return;
+    int* cd = cb + (size_t)(t % 3) * EMAX;
+    double* vd = vb + (size_t)(t % 3) * EMAX;
+    for (int q = threadIdx.x; q < cnt; q += kOrthT) {
+      spa_cp4(cd + q, ci + e_lo + q);
+      spa_cp8(vd + q, va + e_lo + q);
+    }
+  };
+  auto issue_x = [&](int t, int cnt) {
+    if (cnt > EMAX) return;
+    const int* cd = cb + (size_t)(t % 3) * EMAX;
+    double* xd = xb + (size_t)(t & 1) * EMAX * NY;
+    for (int q = threadIdx.x; q < cnt * PC; q += kOrthT) {
+      const int e = q / PC, ch = q % PC;
+      spa_cp16(xd + (size_t)e * NY + 2 * ch, X + (size_t)cd[e] * ldx + 2 * ch);
+    }
+  };
+  __syncthreads();  // the ring's previous contents are dead
+  int b0 = bound(0), b1 = bound(1), b2 = bound(2), b3 = bound(3);
+  issue_cv(0, b0, b1 - b0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  issue_x(0, b1 - b0);
+  issue_cv(1, b1, b2 - b1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int lo[RPT], hi[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = slot + u * PER;
+    lo[u] = hi[u] = 0;
+    if (r < nr) {
+      lo[u] = __ldg(rpb + r);
+      hi[u] = __ldg(rpb + r + 1);
+    }
+  }
+  for (int t = 0; t < ntiles; ++t) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // X(t), index / values (t + 1)
+    __syncthreads();
+    issue_x(t + 1, b2 - b1);
+    const int b4 = bound(t + 4);
+    issue_cv(t + 2, b2, b3 - b2);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    int nlo[RPT], nhi[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int r = (t + 1) * TR + slot + u * PER;
+      nlo[u] = nhi[u] = 0;
+      if (r < nr) {
+        nlo[u] = __ldg(rpb + r);
+        nhi[u] = __ldg(rpb + r + 1);
+      }
+    }
+    if (b1 - b0 > EMAX) {
+      // (block-uniform) a tile too large for the ring: the direct loop
+      const int ta = t * TR;
+      spmm_rows<NY>(rp, ci, va, X, ldx, NY, Y + (size_t)ta * ldy, ldy, r0 + ta, min(TR, nr - ta));
+    } else {
+      const double* xd = xb + (size_t)(t & 1) * EMAX * NY;
+      const double* vd = vb + (size_t)(t % 3) * EMAX;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int r = t * TR + slot + u * PER;
+        if (r < nr) {
+          double a0 = 0.0, a1 = 0.0;
+          int e = lo[u] - b0;
+          const int eh = hi[u] - b0;
+          for (; e + 1 < eh; e += 2) {
+            a0 += vd[e] * xd[(size_t)e * NY + c];
+            a1 += vd[e + 1] * xd[(size_t)(e + 1) * NY + c];
+          }
+          if (e < eh) a0 += vd[e] * xd[(size_t)e * NY + c];
+          Y[(size_t)r * ldy + c] = a0 + a1;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      lo[u] = nlo[u];
+      hi[u] = nhi[u];
+    }
+    b0 = b1;
+    b1 = b2;
+    b2 = b3;
+    b3 = b4;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+}
+
+// spmm_rows, through the asynchronous ring when the caller has one (`ring`
+// non-null: the global-row geometry's free shared memory), the block is a
+// full NY = 8 columns wide and the X rows are 16-byte aligned
+template <int NY>
+__device__ __forceinline__ void spmm_auto(const int32_t* __restrict__ rp,
+                                          const int32_t* __restrict__ ci,
+                                          const double* __restrict__ va, const double* X, int ldx,
+                                          int sb, double* Y, int ldy, int r0, int nr, double* ring,
+                                          int ring_doubles) {
+#if PMP_SPMM_ASYNC
+  if (NY == 8 && ring != nullptr && sb == NY && (ldx & 1) == 0 &&
+      (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ring_doubles >= 2048) {
+    spmm_rows_async<NY>(rp, ci, va, X, ldx, Y, ldy, r0, nr, ring, ring_doubles);
+    return;
+  }
+#endif
+  spmm_rows<NY>(rp, ci, va, X, ldx, sb, Y, ldy, r0, nr);
 }
 
 // control-block shared state
@@ -605,6 +785,8 @@ struct WSmem {
   int *piv, *piv2, *flag;
   double *Xs, *Wv, *Q1;
   int ldw;
+  double* ring = nullptr;  // free shared memory of a global-row worker (spmm_auto)
+  int ring_doubles = 0;
 };
 
 // The block step's tall-skinny products for the shared-memory geometries:
@@ -623,7 +805,7 @@ struct WSmem {
 #define PMP_STEP_UPDATE block_update<NY>
 #endif
 
-template <bool CACHED, int NY>
+template <bool CACHED, int NY, bool STAMP = false>
 __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int r0, int nr,
                              bool lead, int& m, int& total, int& ncols, int& it, int& status) {
   double* G = S_.G;
@@ -653,21 +835,21 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const int q0 = m;
     const int stp = it - it_start;
     const StepBuf sbf = step_buf(P, q);
-    cstamp(P, stp, 0);
+    wstamp<STAMP>(P, stp, 0);
     // ---- W = A F_0 .. F_{nfac-1} V[:, q0 : q0 + sb] ---------------------------
     const double* src = P.V + q0;
     int lds = cap;
     for (int f = P.nfac - 1; f >= 0; --f) {
       double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
-      spmm_rows<NY>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst + (size_t)r0 * P.s, P.s,
-                    r0, nr);
+      spmm_auto<NY>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst + (size_t)r0 * P.s, P.s,
+                    r0, nr, S_.ring, S_.ring_doubles);
       wbar(wb);
       src = dst;
       lds = P.s;
     }
-    spmm_rows<NY>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr);
+    spmm_auto<NY>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr, S_.ring, S_.ring_doubles);
     __syncthreads();
-    cstamp(P, stp, 1);
+    wstamp<STAMP>(P, stp, 1);
 
     // ---- R1: [C | V]^T W --------------------------------------------------------
     const int kx = k + total;
@@ -677,19 +859,19 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const int ldvr = CACHED ? ldx : cap;
     const Rows Vonly{Vrows, ldvr, total, Vrows, ldvr};
     PMP_STEP_GRAM(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
-    cstamp(P, stp, 2);
+    wstamp<STAMP>(P, stp, 2);
     wreduce(wb, P.partial, P.gout, kx * sb, G, sbf.B, k * sb, sbf.H1);
-    cstamp(P, stp, 3);
+    wstamp<STAMP>(P, stp, 3);
     PMP_STEP_UPDATE(CV, kx, Wv, ldw, sb, nr, G);
-    cstamp(P, stp, 4);
+    wstamp<STAMP>(P, stp, 4);
     // ---- R2: [V | W1]^T W1 ------------------------------------------------------
     const int kx2 = total + sb;
     {
       const Rows VW{Vrows, ldvr, total, Wv, ldw};
       PMP_STEP_GRAM(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
-      cstamp(P, stp, 5);
+      wstamp<STAMP>(P, stp, 5);
       wreduce(wb, P.partial, P.gout, kx2 * sb, G, sbf.H2, total * sb, nullptr);
-      cstamp(P, stp, 6);
+      wstamp<STAMP>(P, stp, 6);
     }
     // G_W = W1^T W1 - H2^T H2 (into R2 as scratch), then W2 = W1 - V H2
     const int n4 = 4 * sb * sb, lim4 = (n4 + 31) & ~31;
@@ -706,11 +888,11 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     }
     __syncthreads();
 #ifdef PMP_STAMPS
-    cstamp(P, stp, 12);
+    wstamp<STAMP>(P, stp, 12);
 #endif
     PMP_STEP_UPDATE(Vonly, total, Wv, ldw, sb, nr, G);
 #ifdef PMP_STAMPS
-    cstamp(P, stp, 13);
+    wstamp<STAMP>(P, stp, 13);
 #endif
     for (int qq = threadIdx.x; qq < sb * sb; qq += kOrthT) {
       const int i = qq / sb, j = qq % sb;
@@ -718,7 +900,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     }
     __syncthreads();
 #ifdef PMP_STAMPS
-    cstamp(P, stp, 14);
+    wstamp<STAMP>(P, stp, 14);
 #endif
 #ifdef PMP_STAMPS
     if (P.dbg && blockIdx.x == 1 && stp == 2)
@@ -743,7 +925,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
 #endif
     }
     __syncthreads();
-    cstamp(P, stp, 7);
+    wstamp<STAMP>(P, stp, 7);
     bool single = false;
     if (flag[0] == 0) single = fabs(R1[0]) / fabs(R1[(sb - 1) * sb + (sb - 1)]) <= kSkipKappa;
     if (flag[0] == 0 && !single) {
@@ -761,7 +943,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
       }
       __syncthreads();
     }
-    cstamp(P, stp, 8);
+    wstamp<STAMP>(P, stp, 8);
     if (flag[0]) {
       // grid-uniform: Cholesky cannot decide the rank -> host Householder
       // (unless the previous step already converged / was deficient)
@@ -811,9 +993,9 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
         sbf.R[i * sb + piv[c]] = (c >= i) ? s : 0.0;
       }
     }
-    cstamp(P, stp, 9);
+    wstamp<STAMP>(P, stp, 9);
     wbar(wb);  // new V block (and the step outputs) visible
-    cstamp(P, stp, 10);
+    wstamp<STAMP>(P, stp, 10);
     // the previous step's decision (the control block absorbed it meanwhile)
     if (q > 0) {
       const int d = wait_flag(P.ist + 16 + q - 1, 0);
@@ -822,7 +1004,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
         break;
       }
     }
-    cstamp(P, stp, 11);
+    wstamp<STAMP>(P, stp, 11);
     if (lead && threadIdx.x == 0) {
       __threadfence();
       *(volatile int*)(P.ist + 7) = q + 1;  // publish step q to the control block

@@ -46,6 +46,7 @@ struct SolveArgs {
   int gsz, rows_per_block, ldx, hist_cap, log_cap, isz;
   int wglob;  // W rows in global memory (rows beyond shared memory)
   int stage_rows, stage_n;  // global-row geometry: staged ring (doubles per stage, stages)
+  int region_doubles;       // the block's `region` of shared memory (doubles)
   double tol;
   const SysDesc* sys;
   double* ws;
@@ -54,11 +55,13 @@ struct SolveArgs {
   size_t oV, oC, oU, oW, oT0, oT1, oQ1, oXt, oR, oDX, oRB, oZ, oPart, oGout, oSbuf, oProj, oLog,
       oAux;
   int pBmat, pHb, pCq, pY, pRes, pBn, pHist;  // offsets inside the projected-state block
+  int pCtl;        // the control block's state in GLOBAL memory (ctl_global), else unused
+  int ctl_global;  // global-row geometry without the staged ring: no shared-memory region
   unsigned long long* dbg;  // diagnostics (group 0): stamps at (32 it + phase) * 2 + block
   int nsys, groups;          // systems in the queue, concurrent block groups
   int* queue;                // next-system counter (zeroed at launch)
   int* rint;                 // nsys x PMP_SOLVE_RSZ ints: per-system record
-  double* rdbl;              // nsys x (1 + log_cap * s): algorithmic bytes, residual log
+  double* rdbl;              // nsys x (2 + log_cap * s): algorithmic bytes (strict, 8(d)), residual log
 };
 
 // solve-level int state (after the cycle-level [0, 144))
@@ -263,6 +266,14 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   double* pn = aux + 16;     // s: |R[:, c]| at the last true residual
   double* lrel = aux + 32;   // s: last relative residual row
   double* img = aux + 64;    // (kc + cap) x s: G Y (fold images), row-major ld s
+  // The control block's projected-problem state: its shared-memory region, or
+  // (global-row geometry without the staged ring) global memory.  There the
+  // workers use no region at all, so keeping the ~60 KB out of every block's
+  // shared memory leaves the SM a 4x larger L1 for the workers' row gathers
+  // (measured on c4: profiles/r02_ctl_global_ab.txt); the control block runs
+  // one step behind the workers and a step lasts milliseconds at these sizes,
+  // so its slower state is invisible.
+  double* ctl_mem = (WG && A.ctl_global) ? proj + A.pCtl : region;
   int* act = ist + kAct;
 
   // the per-group argument block lives in SHARED memory: as a local struct
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       int na = 0;
       for (int c = 0; c < s; ++c) {
         const double b = sqrt(fmax(G[c * s + c], 0.0));
-        if (c == 0) aux[48] = 0.0;
+        if (c == 0) aux[48] = aux[49] = 0.0;
         bn[c] = b;
         pn[c] = b;
         lrel[c] = b > 0.0 ? 1.0 : 0.0;
@@ -474,7 +485,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
 
     // ---- control block: projected problem of the cycle ---------------------------
     if (ctl) {
-      const Ctl S = ctl_layout(region, na, L.nblk, ldq, na);
+      const Ctl S = ctl_layout(ctl_mem, na, L.nblk, ldq, na);
       const StepBuf sbf = step_buf(L, 0);
       for (int q = threadIdx.x; q < ldq * na; q += kOrthT) {
         const int c = q / ldq, i = q % ldq;
@@ -510,7 +521,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
 
     // ---- inner loop ---------------------------------------------------------------
     if (ctl) {
-      const Ctl S = ctl_layout(region, na, L.nblk, ldq, na);
+      const Ctl S = ctl_layout(ctl_mem, na, L.nblk, ldq, na);
       ctl_run<NY>(L, S);
       // the cycle's estimate rows -> the full-width log; fold images G Y
       const int hrow = ldv(ist + 5), m = ldv(ist + 0), total = ldv(ist + 1), st = ldv(ist + 4);
@@ -579,6 +590,12 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       const int ldw = WG ? s : odd_ld(na);
       double* Wv = WG ? W + (size_t)r0 * s : region + (CACHED ? (size_t)nr * A.ldx : 0);
       WSmem wsm{G, R1, R2, red, piv, piv2, flag, region, Wv, L.Q1g + (size_t)r0 * na, ldw};
+      if constexpr (WG) {
+        // (the control block's state lives in `region` of block 0 only: a
+        // global-row worker's region is free between its passes)
+        wsm.ring = A.ctl_global ? nullptr : region;
+        wsm.ring_doubles = A.ctl_global ? 0 : A.region_doubles;
+      }
       bool staged = false;
       if constexpr (WG) {
         if (A.stage_rows > 0) {
@@ -589,7 +606,12 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
           staged = true;
         }
       }
-      if (!staged) worker_inner<CACHED, NY>(L, wb, wsm, r0, nr, lead, m, total, ncols, it, status);
+#ifndef PMP_WG_STAMPS
+#define PMP_WG_STAMPS 1
+#endif
+      if (!staged)
+        worker_inner<CACHED, NY, WG && PMP_WG_STAMPS>(L, wb, wsm, r0, nr, lead, m, total, ncols, it,
+                                                      status);
       sstamp(A, grp, cyc, 3);
     }
     gbar(gb);
@@ -634,7 +656,8 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       for (int f = D.nfac - 1; f >= 0; --f) {
         wbar(wb);
         double* dst = ((D.nfac - 1 - f) & 1) ? L.T1 : L.T0;
-        spmm_rows<NY>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr);
+        spmm_auto<NY>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr,
+                      (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
         src = dst;
       }
       __syncthreads();
@@ -645,7 +668,8 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       }
       wbar(wb);
       // Rb = B[:, act] - A Xa -> R[:, act], RB
-      spmm_rows<NY>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr);
+      spmm_auto<NY>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr,
+                    (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
       __syncthreads();
       for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
         const int r = q / na, c = q % na;
@@ -668,9 +692,18 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         for (int f = 0; f < D.nfac; ++f)
           mb += 12.0 * __ldg(D.frp[f] + n) + 4.0 * (n + 1) + 16.0 * n * na;
         mb += 12.0 * __ldg(D.arp + n) + 4.0 * (n + 1) + 16.0 * n * na;
-        double by = 0.0;
-        for (int j = 0; j < steps; ++j) by += mb + 8.0 * n * (k + na * (j + 1)) + 32.0 * n * na;
+        // aux[48]: every operand once per step (the strict figure round 1
+        // reported); aux[49]: SURVEY.md 8(d)'s unit for block CGS2 -- two
+        // Gram products and two updates per step read [C | V] -- 32 n total +
+        // 48 n s_b + 16 n k on top of the operator chain
+        double by = 0.0, by2 = 0.0;
+        for (int j = 0; j < steps; ++j) {
+          const double tot = (double)na * (j + 1);
+          by += mb + 8.0 * n * (k + tot) + 32.0 * n * na;
+          by2 += mb + 32.0 * n * tot + 48.0 * n * na + 16.0 * n * k;
+        }
         aux[48] += by;
+        aux[49] += by2;
         ist[kIt] = it_new;
         ist[kMatvecs] += na * steps + na;
         if (D.nfac) ist[kPrec] += na * steps + na;
@@ -854,7 +887,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   gbar(gb);
   if (lead) {
     int* rec = A.rint + (size_t)sys * PMP_SOLVE_RSZ;
-    double* rd = A.rdbl + (size_t)sys * (1 + (size_t)A.log_cap * s);
+    double* rd = A.rdbl + (size_t)sys * (2 + (size_t)A.log_cap * s);
     const int lr = ldv(ist + kLogRows);
     if (threadIdx.x == 0) {
       rec[rStatus] = ldv(ist + kStatus);
@@ -865,8 +898,9 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       rec[rMatvecs] = ldv(ist + kMatvecs);
       rec[rPrec] = ldv(ist + kPrec);
       rd[0] = __ldcg(aux + 48);
+      rd[1] = __ldcg(aux + 49);
     }
-    for (int q = threadIdx.x; q < lr * s; q += kOrthT) rd[1 + q] = __ldcg(logp + q);
+    for (int q = threadIdx.x; q < lr * s; q += kOrthT) rd[2 + q] = __ldcg(logp + q);
   }
   if (ctl && threadIdx.x == 0) ist[kNext] = A.groups + atomicAdd(A.queue, 1);
   gbar(gb);
@@ -879,14 +913,40 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
 // cycle.cu
 namespace pmp {
 size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached);
+size_t cycle_ctl_doubles(int sb, int ldq, int na, int restart);
 }
 
 using namespace pmp;
 
+// the staged ring runs from PMP_STAGE_MIN_S block columns up (measured,
+// profiles/r02_stage_ab_c3_c4.txt: it wins at s = 16 -- c3 block step 13.1 ->
+// 8.4 ms -- and loses at s = 8 -- c4 12.5 -> 13.9 ms, 16-24-row tiles)
+#ifndef PMP_STAGE
+#define PMP_STAGE 1
+#endif
+static bool solve_staged(int s, int kc, int cap, int cached) {
+  static const int stage_min_s = [] {
+    const char* e = getenv("PMP_STAGE_MIN_S");
+    return e ? atoi(e) : 9;
+  }();
+  return PMP_STAGE && cached == 2 && s >= stage_min_s && (s % 2) == 0 && (kc % 2) == 0 &&
+         (cap % 2) == 0;
+}
+// global-row geometry without the ring: the control state lives in global
+// memory and the blocks carry no region (PMP_CTL_GLOBAL=0 keeps it in smem)
+static bool solve_ctl_global(int s, int kc, int cap, int cached) {
+  static const int on = [] {
+    const char* e = getenv("PMP_CTL_GLOBAL");
+    return e ? atoi(e) : 1;
+  }();
+  return on && cached == 2 && !solve_staged(s, kc, cap, cached);
+}
+
 static size_t solve_smem_bytes(int rows, int ldx, int kc, int cap, int s, int restart,
                                int cached) {
   size_t d = (size_t)(kc + cap + s) * s + 2 * (size_t)s * s + 8 * 32 * (size_t)s + 20;
-  d += cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
+  if (!solve_ctl_global(s, kc, cap, cached))
+    d += cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
   return d * sizeof(double);
 }
 
@@ -926,6 +986,10 @@ int pmp_solve_geometry(int n, int s, int cap, int kc, int restart, int groups, i
     return PMP_OK;
   }
   return PMP_ERR_ARG;
+}
+
+size_t pmp_solve_ctl_doubles(int s, int kc, int cap, int restart) {
+  return cycle_ctl_doubles(s, kc + cap, s, restart);
 }
 
 int pmp_solve_batch(PmpSolveBatch* b) {
@@ -971,10 +1035,15 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   A.wglob = cached == 2;
   A.stage_rows = 0;
   A.stage_n = 0;
-#ifndef PMP_STAGE
-#define PMP_STAGE 1
-#endif
-  if (PMP_STAGE && cached == 2 && (b->s % 2) == 0 && (b->kc % 2) == 0 && (b->cap % 2) == 0) {
+  A.region_doubles = (int)cycle_region_doubles(rows, A.ldx, b->s, b->kc + b->cap, b->s,
+                                               b->inner_restart, cached);
+  A.ctl_global = solve_ctl_global(b->s, b->kc, b->cap, cached) ? 1 : 0;
+  A.pCtl = b->pCtl;
+  if (A.ctl_global && b->pCtl <= 0) {
+    set_error("pmp_solve_batch: pCtl not set (pmp_solve_ctl_doubles sizes it)");
+    return PMP_ERR_ARG;
+  }
+  if (solve_staged(b->s, b->kc, b->cap, cached)) {
     // ring of S stages x R rows of [C | V | W] in the workers' region
     const size_t region = cycle_region_doubles(rows, A.ldx, b->s, b->kc + b->cap, b->s,
                                                b->inner_restart, cached);

@@ -401,8 +401,11 @@ namespace pmp {
 // the three staged passes above).  Same contract: steps until restart
 // length, max_iters, a stop decision of the control block, or a Cholesky
 // flag; the lead worker writes the final state and the done flag.
+#ifndef PMP_STAGED_ATTR
+#define PMP_STAGED_ATTR __noinline__
+#endif
 template <int NY>
-__device__ void worker_inner_staged(const CycleArgs& P, WBar& wb, const WSmem& S_, Ring ring,
+__device__ PMP_STAGED_ATTR void worker_inner_staged(const CycleArgs& P, WBar& wb, const WSmem& S_, Ring ring,
                                     int r0, int nr, bool lead, int& m, int& total, int& ncols,
                                     int& it, int& status) {
   double* G = S_.G;

@@ -1144,7 +1144,8 @@ class _SolveBatchArgs(ctypes.Structure):
         (f, ctypes.c_size_t) for f in ("oV", "oC", "oU", "oW", "oT0", "oT1", "oQ1", "oXt", "oR",
                                        "oDX", "oRB", "oZ", "oPart", "oGout", "oSbuf", "oProj",
                                        "oLog", "oAux")] + [
-        (f, ctypes.c_int) for f in ("pBmat", "pHb", "pCq", "pY", "pRes", "pBn", "pHist")] + [
+        (f, ctypes.c_int) for f in ("pBmat", "pHb", "pCq", "pY", "pRes", "pBn", "pHist",
+                                    "pCtl")] + [
         ("nsys", ctypes.c_int), ("d_queue", ctypes.c_void_p), ("d_result", ctypes.c_void_p),
         ("d_result_log", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
@@ -1158,16 +1159,18 @@ _SOLVE_FALLBACK = 10
 FALLBACK_REASONS = {}
 
 
-def _solve_layout(n, s, cap, kc, gsz, hist_cap, log_cap):
-    """Per-system workspace layout of pmp_solve_batch (offsets in doubles)."""
+def _solve_layout(n, s, cap, kc, gsz, hist_cap, log_cap, ctl=0):
+    """Per-system workspace layout of pmp_solve_batch (offsets in doubles);
+    ``ctl`` doubles for the control block's state (pmp_solve_ctl_doubles)."""
     def al(x):
         return (x + 31) // 32 * 32
     ldq = kc + cap
     kmax = (kc + cap + s) * s
     proj = {}
-    o = 0
+    o = 32          # (offset 0 is reserved: pCtl = 0 means "not provided")
     for name, size in (("pCq", ldq * s), ("pBn", s), ("pRes", s), ("pY", s * ldq),
-                       ("pHist", hist_cap * s), ("pBmat", kc * cap), ("pHb", cap * cap)):
+                       ("pHist", hist_cap * s), ("pBmat", kc * cap), ("pHb", cap * cap),
+                       ("pCtl", ctl)):
         proj[name] = o
         o += al(size)
     proj_size = o
@@ -1227,12 +1230,13 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
         return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
     hist_cap = cap + 2
     log_cap = 2 * cfg.max_iters + 4
-    off, poff, wsz = _solve_layout(n, s, cap, kc, gsz.value, hist_cap, log_cap)
+    off, poff, wsz = _solve_layout(n, s, cap, kc, gsz.value, hist_cap, log_cap,
+                                   int(L.pmp_solve_ctl_doubles(s, kc, cap, cfg.inner_restart)))
     dev = _dev()
     sc = scratch()
     ws = sc.get("solve_ws", 8 * wsz * groups).view(torch.float64)
     ist = sc.get("solve_ist", 4 * _SOLVE_ISZ * groups).view(torch.int32)
-    rlen = 1 + log_cap * s
+    rlen = 2 + log_cap * s
     rint = sc.get("solve_rint", 4 * (_SOLVE_RSZ * nsys + 1)).view(torch.int32)
     rdbl = sc.get("solve_rdbl", 8 * rlen * nsys).view(torch.float64)
     sysd = (_SysDesc * nsys)()
@@ -1305,22 +1309,25 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     if done:
         # one gather + one D2H for every solved system's bytes and residual log
         rv = rdbl[:rlen * nsys].view(nsys, rlen)
-        parts = [rv[i, :1 + int(recs[i, 4]) * s] for i in done]
+        parts = [rv[i, :2 + int(recs[i, 4]) * s] for i in done]
         flat = torch.cat(parts).cpu().numpy()
         o = 0
         for i in done:
             rows_ = int(recs[i, 4])
-            seg = flat[o:o + 1 + rows_ * s]
+            seg = flat[o:o + 2 + rows_ * s]
             o += seg.size
             rep = SolveReport()
             # one copy per system; the history rows are views of it
-            rep.residual_history = list(seg[1:].reshape(rows_, s).copy())
+            rep.residual_history = list(seg[2:].reshape(rows_, s).copy())
             rep.iterations = int(recs[i, 2])
             rep.converged = int(recs[i, 3]) == 0
             rep.matvec_count = int(recs[i, 5])
             rep.precond_apply_count = int(recs[i, 6])
             rep.device_launches = 1
-            rep.algorithmic_bytes = float(seg[0])
+            # SURVEY.md 8(d)'s unit (block CGS2 reads [C | V] four times per
+            # step) and the strict every-operand-once figure of round 1
+            rep.algorithmic_bytes = float(seg[1])
+            rep.algorithmic_bytes_strict = float(seg[0])
             out[i] = (Xs[i], rep)
     for i in fallback:
         A, P = systems[i]

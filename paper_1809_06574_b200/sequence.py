@@ -355,7 +355,9 @@ def run_sequence(model, s_grid, p_grid, policy=None, solver_cfg=None, B=None, ra
                        "final_residuals": np.asarray(rep.final_residuals, dtype=float).tolist(),
                        "max_final_residual": float(np.max(rep.final_residuals)),
                        "launches": getattr(rep, "device_launches", 0),
-                       "algorithmic_bytes": getattr(rep, "algorithmic_bytes", None)}
+                       "algorithmic_bytes": getattr(rep, "algorithmic_bytes", None),
+                       "algorithmic_bytes_strict": getattr(rep, "algorithmic_bytes_strict",
+                                                           None)}
                 if keep_solutions:
                     rec["X"] = X.clone()   # (X is a view of the window's block)
                 if on_solution is not None:
