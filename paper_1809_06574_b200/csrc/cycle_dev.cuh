@@ -87,7 +87,10 @@ static __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // may have been written earlier in this kernel by other blocks: loads
 // bypass L1 (ld.cg).  Accumulation order matches k_spmm (even / odd
 // entries, then summed).
-template <int NY>
+#ifndef PMP_SPMM_CA
+#define PMP_SPMM_CA 1
+#endif
+template <int NY, bool CA = false>
 __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ va, const double* X, int ldx, int sb,
                           double* Y, int ldy, int r0, int nr) {
@@ -127,7 +130,10 @@ __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int
       for (int u = 0; u < RPT; ++u)
 #pragma unroll
         for (int q = 0; q < CH; ++q)
-          x[u][q] = (j[u][q] >= 0 && col_ok) ? __ldcg(X + (size_t)j[u][q] * ldx + c) : 0.0;
+          x[u][q] = (j[u][q] >= 0 && col_ok)
+                        ? (CA ? __ldca(X + (size_t)j[u][q] * ldx + c)
+                              : __ldcg(X + (size_t)j[u][q] * ldx + c))
+                        : 0.0;
 #pragma unroll
       for (int u = 0; u < RPT; ++u)
 #pragma unroll
@@ -180,7 +186,7 @@ __device__ __forceinline__ void spa_cp4(void* dst, const void* src) {
 }
 
 #ifndef PMP_SPMM_ASYNC
-#define PMP_SPMM_ASYNC 1
+#define PMP_SPMM_ASYNC 0
 #endif
 
 template <int NY>
@@ -293,7 +299,7 @@ __device__ __noinline__ void spmm_rows_async(const int32_t* __restrict__ rp,
 // spmm_rows, through the asynchronous ring when the caller has one (`ring`
 // non-null: the global-row geometry's free shared memory), the block is a
 // full NY = 8 columns wide and the X rows are 16-byte aligned
-template <int NY>
+template <int NY, bool CA = false>
 __device__ __forceinline__ void spmm_auto(const int32_t* __restrict__ rp,
                                           const int32_t* __restrict__ ci,
                                           const double* __restrict__ va, const double* X, int ldx,
@@ -306,7 +312,7 @@ __device__ __forceinline__ void spmm_auto(const int32_t* __restrict__ rp,
     return;
   }
 #endif
-  spmm_rows<NY>(rp, ci, va, X, ldx, sb, Y, ldy, r0, nr);
+  spmm_rows<NY, CA>(rp, ci, va, X, ldx, sb, Y, ldy, r0, nr);
 }
 
 // control-block shared state
@@ -797,6 +803,9 @@ struct WSmem {
 #ifndef PMP_MMA
 #define PMP_MMA 0
 #endif
+#ifndef PMP_GRAM_FLAT
+#define PMP_GRAM_FLAT 1
+#endif
 #if PMP_MMA
 #define PMP_STEP_GRAM block_gram_mma<NY>
 #define PMP_STEP_UPDATE block_update_mma<NY>
@@ -841,13 +850,15 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     int lds = cap;
     for (int f = P.nfac - 1; f >= 0; --f) {
       double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
-      spmm_auto<NY>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst + (size_t)r0 * P.s, P.s,
-                    r0, nr, S_.ring, S_.ring_doubles);
+      spmm_auto<NY, STAMP && PMP_SPMM_CA>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb,
+                                          dst + (size_t)r0 * P.s, P.s, r0, nr, S_.ring,
+                                          S_.ring_doubles);
       wbar(wb);
       src = dst;
       lds = P.s;
     }
-    spmm_auto<NY>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr, S_.ring, S_.ring_doubles);
+    spmm_auto<NY, STAMP && PMP_SPMM_CA>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr, S_.ring,
+                                        S_.ring_doubles);
     __syncthreads();
     wstamp<STAMP>(P, stp, 1);
 
@@ -858,7 +869,10 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const double* Vrows = CACHED ? Xs + k : P.V + (size_t)r0 * cap;
     const int ldvr = CACHED ? ldx : cap;
     const Rows Vonly{Vrows, ldvr, total, Vrows, ldvr};
-    PMP_STEP_GRAM(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
+    if (STAMP && PMP_GRAM_FLAT && kx <= 128)
+      block_gram_flat<NY>(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
+    else
+      PMP_STEP_GRAM(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
     wstamp<STAMP>(P, stp, 2);
     wreduce(wb, P.partial, P.gout, kx * sb, G, sbf.B, k * sb, sbf.H1);
     wstamp<STAMP>(P, stp, 3);
@@ -868,7 +882,10 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const int kx2 = total + sb;
     {
       const Rows VW{Vrows, ldvr, total, Wv, ldw};
-      PMP_STEP_GRAM(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
+      if (STAMP && PMP_GRAM_FLAT && kx2 <= 128)
+        block_gram_flat<NY>(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
+      else
+        PMP_STEP_GRAM(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
       wstamp<STAMP>(P, stp, 5);
       wreduce(wb, P.partial, P.gout, kx2 * sb, G, sbf.H2, total * sb, nullptr);
       wstamp<STAMP>(P, stp, 6);

@@ -115,6 +115,65 @@ __device__ PMP_GRAM_INLINE void block_gram(const Rows X, int kx, const double* Y
   }
 }
 
+// The same product with the block's threads laid out flat over (row split,
+// column): thread id -> column t = id % kx of split id / kx, 256 / kx splits
+// of the rows.  block_gram gives each warp 32 columns of one round, so a
+// last round of kx % 32 columns leaves most of its lanes idle (kx = 42: a
+// third of the block's lanes); here every lane carries a column's row chain
+// and 256 / kx > 8 / rounds splits keep more loads in flight.  Used by the
+// global-row geometry (rows stream from HBM: the loads in flight bound the
+// phase).  Fixed summation order (rows in order within a split, splits in
+// order): deterministic, not bitwise equal to block_gram.  kx <= 128.
+template <int NY>
+__device__ __forceinline__ void block_gram_flat(const Rows X, int kx, const double* Y, int ldy,
+                                                int ny, int nrows, double* red, double* partial,
+                                                int slot) {
+  const int K = kx * ny;
+  double* part = partial + (size_t)slot * K;
+  const int nsplit = kOrthT / kx;
+  const int sp = threadIdx.x / kx, t = threadIdx.x - sp * kx;
+  double acc[NY];
+#pragma unroll
+  for (int c = 0; c < NY; ++c) acc[c] = 0.0;
+  if (sp < nsplit) {
+    const int per = (nrows + nsplit - 1) / nsplit;
+    const int ra = sp * per, rb = min(nrows, ra + per);
+    const double* xa = t < X.ka ? X.a + t : X.b + (t - X.ka);
+    const int ldxr = t < X.ka ? X.lda : X.ldb;
+    int r = ra;
+    constexpr int GB = PMP_GRAM_BATCH;
+    for (; r + GB <= rb; r += GB) {
+      double x[GB];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) x[u] = xa[(size_t)(r + u) * ldxr];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const double* y = Y + (size_t)(r + u) * ldy;
+#pragma unroll
+        for (int c = 0; c < NY; ++c)
+          if (c < ny) acc[c] += x[u] * y[c];
+      }
+    }
+    for (; r < rb; ++r) {
+      const double x = xa[(size_t)r * ldxr];
+      const double* y = Y + (size_t)r * ldy;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c < ny) acc[c] += x * y[c];
+    }
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < ny) red[(size_t)threadIdx.x * ny + c] = acc[c];
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < K; o += kOrthT) {
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += red[(size_t)q * K + o];
+    part[o] = s;
+  }
+  __syncthreads();
+}
+
 // distributed fixed-order reduction of the block partials; every block ends
 // with the full K-vector in smem G.  Entries [0, split) are also copied to
 // out, entries [split, K) to out2 (either may be null).

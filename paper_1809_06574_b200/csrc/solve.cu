@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       for (int f = D.nfac - 1; f >= 0; --f) {
         wbar(wb);
         double* dst = ((D.nfac - 1 - f) & 1) ? L.T1 : L.T0;
-        spmm_auto<NY>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr,
+        spmm_auto<NY, WG && PMP_SPMM_CA>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr,
                       (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
         src = dst;
       }
@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       }
       wbar(wb);
       // Rb = B[:, act] - A Xa -> R[:, act], RB
-      spmm_auto<NY>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr,
+      spmm_auto<NY, WG && PMP_SPMM_CA>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr,
                     (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
       __syncthreads();
       for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
