@@ -33,6 +33,36 @@ __device__ __forceinline__ double term_value(const AsmRecipe& R, int t, int e, b
   return diag ? __ldg(R.vals[t] + row) : 0.0;
 }
 
+// The three group accumulators (mass / damping / stiffness parts) live in
+// registers: indexing a small array with the term's group put it in local
+// memory (ncu on k_assemble_multi at c4: 0.8 of 32 bytes used per local
+// sector, the kernel at 0.87 TB/s instead of HBM speed).  Same operations in
+// the same order as the array form: bit-exact.
+struct Groups {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  bool p0 = false, p1 = false, p2 = false;
+  __device__ __forceinline__ void open(int g, double v) {
+    if (g == 0) { a0 = v; p0 = true; }
+    else if (g == 1) { a1 = v; p1 = true; }
+    else { a2 = v; p2 = true; }
+  }
+  __device__ __forceinline__ void add(int g, double c, double v) {
+    const double t = __dmul_rn(c, v);
+    if (g == 0) a0 = __dadd_rn(a0, t);
+    else if (g == 1) a1 = __dadd_rn(a1, t);
+    else a2 = __dadd_rn(a2, t);
+  }
+  // (s2 * mass + s * damping) + stiffness over the groups present
+  __device__ __forceinline__ double mdk(double s2, double s) const {
+    bool have = false;
+    double val = 0.0;
+    if (p0) { val = __dmul_rn(s2, a0); have = true; }
+    if (p1) { const double part = __dmul_rn(s, a1); val = have ? __dadd_rn(val, part) : part; have = true; }
+    if (p2) { const double part = __dmul_rn(1.0, a2); val = have ? __dadd_rn(val, part) : part; }
+    return val;
+  }
+};
+
 __global__ void __launch_bounds__(256) k_assemble(AsmRecipe R, int nnz, const int* __restrict__ rowid,
                                                   const int* __restrict__ colidx,
                                                   double* __restrict__ out, const int* __restrict__ perm,
@@ -46,34 +76,22 @@ __global__ void __launch_bounds__(256) k_assemble(AsmRecipe R, int nnz, const in
       row = __ldg(rowid + e);
       diag = (__ldg(colidx + e) == row);
     }
-    double gacc[3] = {0.0, 0.0, 0.0};
-    bool gpres[3] = {false, false, false};
+    Groups G;
 #pragma unroll 1
     for (int t = 0; t < R.nterms; ++t) {
       const int g = R.group[t];
       const double v = term_value(R, t, e, diag, row);
-      if (R.first[t]) {
-        gacc[g] = v;
-        gpres[g] = true;
-      } else {
-        gacc[g] = __dadd_rn(gacc[g], __dmul_rn(R.coef[t], v));
-      }
+      if (R.first[t])
+        G.open(g, v);
+      else
+        G.add(g, R.coef[t], v);
     }
     double val;
     if (R.mode == 0) {
-      bool have = false;
-      val = 0.0;
-      const double gc[3] = {R.s2, R.s, 1.0};
-#pragma unroll
-      for (int g = 0; g < 3; ++g) {
-        if (!gpres[g]) continue;
-        double part = __dmul_rn(gc[g], gacc[g]);
-        val = have ? __dadd_rn(val, part) : part;
-        have = true;
-      }
+      val = G.mdk(R.s2, R.s);
       if (val == 0.0) val = 0.0;  // canonical +0 for dropped entries
     } else {
-      val = gacc[0];
+      val = G.a0;
       if (fabs(val) < 1e-300) val = 0.0;
     }
     zero = (val == 0.0);
@@ -97,6 +115,10 @@ struct AsmMulti {
   double* out_perm[kAsmMaxSys];
 };
 
+// NT: the recipe's term count when it is small (the loops over the terms are
+// then exactly NT long: at 16 predicated iterations per system the kernel was
+// issue-bound, ncu: 88 % of issue slots), 16 = any count.
+template <int NT>
 __global__ void __launch_bounds__(256) k_assemble_multi(AsmRecipe R, AsmMulti S, int nnz,
                                                         const int* __restrict__ rowid,
                                                         const int* __restrict__ colidx,
@@ -104,7 +126,7 @@ __global__ void __launch_bounds__(256) k_assemble_multi(AsmRecipe R, AsmMulti S,
                                                         int* zero_count) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  double tv[PMP_MAX_TERMS];
+  double tv[NT];
   bool diag = false;
   int row = 0, pe = 0;
   if (e < nnz) {
@@ -113,41 +135,30 @@ __global__ void __launch_bounds__(256) k_assemble_multi(AsmRecipe R, AsmMulti S,
       diag = (__ldg(colidx + e) == row);
     }
 #pragma unroll
-    for (int t = 0; t < PMP_MAX_TERMS; ++t)
-      tv[t] = t < R.nterms ? term_value(R, t, e, diag, row) : 0.0;
+    for (int t = 0; t < NT; ++t)
+      tv[t] = (NT < PMP_MAX_TERMS || t < R.nterms) ? term_value(R, t, e, diag, row) : 0.0;
     if (perm) pe = __ldg(perm + e);
   }
   for (int q = 0; q < S.nsys; ++q) {
     bool zero = false;
     if (e < nnz) {
-      double gacc[3] = {0.0, 0.0, 0.0};
-      bool gpres[3] = {false, false, false};
+      Groups G;
 #pragma unroll
-      for (int t = 0; t < PMP_MAX_TERMS; ++t) {
-        if (t >= R.nterms) break;
-        const int g = R.group[t];
-        if (R.first[t]) {
-          gacc[g] = tv[t];
-          gpres[g] = true;
-        } else {
-          gacc[g] = __dadd_rn(gacc[g], __dmul_rn(S.coef[q][t], tv[t]));
+      for (int t = 0; t < NT; ++t) {
+        if (NT < PMP_MAX_TERMS || t < R.nterms) {
+          const int g = R.group[t];
+          if (R.first[t])
+            G.open(g, tv[t]);
+          else
+            G.add(g, S.coef[q][t], tv[t]);
         }
       }
       double val;
       if (R.mode == 0) {
-        bool have = false;
-        val = 0.0;
-        const double gc[3] = {S.s2[q], S.s[q], 1.0};
-#pragma unroll
-        for (int g = 0; g < 3; ++g) {
-          if (!gpres[g]) continue;
-          const double part = __dmul_rn(gc[g], gacc[g]);
-          val = have ? __dadd_rn(val, part) : part;
-          have = true;
-        }
+        val = G.mdk(S.s2[q], S.s[q]);
         if (val == 0.0) val = 0.0;
       } else {
-        val = gacc[0];
+        val = G.a0;
         if (fabs(val) < 1e-300) val = 0.0;
       }
       zero = (val == 0.0);
@@ -209,8 +220,20 @@ extern "C" int pmp_assemble_multi(int nnz, int nterms, const double* const* h_te
       S.out[q] = h_out[q0 + q];
       S.out_perm[q] = d_perm ? h_out_perm[q0 + q] : nullptr;
     }
-    k_assemble_multi<<<ceil_div(nnz, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        R, S, nnz, d_rowid, d_colidx, d_perm, d_zero_counts ? d_zero_counts + q0 : nullptr);
+    int* zc = d_zero_counts ? d_zero_counts + q0 : nullptr;
+    const dim3 grid(ceil_div(nnz, 256));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+#define PMP_ASM_CASE(N)                                                                  \
+  case N:                                                                                \
+    k_assemble_multi<N><<<grid, 256, 0, st>>>(R, S, nnz, d_rowid, d_colidx, d_perm, zc); \
+    break;
+    switch (nterms <= 8 ? nterms : 16) {
+      PMP_ASM_CASE(1) PMP_ASM_CASE(2) PMP_ASM_CASE(3) PMP_ASM_CASE(4) PMP_ASM_CASE(5)
+      PMP_ASM_CASE(6) PMP_ASM_CASE(7) PMP_ASM_CASE(8)
+      default:
+        k_assemble_multi<16><<<grid, 256, 0, st>>>(R, S, nnz, d_rowid, d_colidx, d_perm, zc);
+    }
+#undef PMP_ASM_CASE
     const int rc = cuda_status("pmp_assemble_multi");
     if (rc != PMP_OK) return rc;
   }

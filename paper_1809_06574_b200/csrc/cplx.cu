@@ -154,8 +154,10 @@ __global__ void __launch_bounds__(256) k_assemble_cplx(CAsm R, int nnz, const in
       row = __ldg(rowid + e);
       diag = (__ldg(colidx + e) == row);
     }
-    double gr[3] = {0.0, 0.0, 0.0}, gi[3] = {0.0, 0.0, 0.0};
-    bool gp[3] = {false, false, false};
+    // (group accumulators as register selects: a dynamically indexed array
+    // lives in local memory, assemble.cu Groups)
+    double gr0 = 0.0, gr1 = 0.0, gr2 = 0.0, gi0 = 0.0, gi1 = 0.0, gi2 = 0.0;
+    bool gp0 = false, gp1 = false, gp2 = false;
 #pragma unroll 1
     for (int t = 0; t < R.nterms; ++t) {
       const int g = R.group[t];
@@ -168,19 +170,22 @@ __global__ void __launch_bounds__(256) k_assemble_cplx(CAsm R, int nnz, const in
         vi = (diag && R.im[t]) ? __ldg(R.im[t] + row) : 0.0;
       }
       if (R.first[t]) {
-        gr[g] = vr;
-        gi[g] = vi;
-        gp[g] = true;
+        if (g == 0) { gr0 = vr; gi0 = vi; gp0 = true; }
+        else if (g == 1) { gr1 = vr; gi1 = vi; gp1 = true; }
+        else { gr2 = vr; gi2 = vi; gp2 = true; }
       } else {
         double pr, pi;
         if (R.mode == 0)
           cmul(vr, vi, R.cr[t], R.ci[t], pr, pi);  // data * scalar
         else
           cmul(R.cr[t], R.ci[t], vr, vi, pr, pi);  // scalar * data
-        gr[g] = __dadd_rn(gr[g], pr);
-        gi[g] = __dadd_rn(gi[g], pi);
+        if (g == 0) { gr0 = __dadd_rn(gr0, pr); gi0 = __dadd_rn(gi0, pi); }
+        else if (g == 1) { gr1 = __dadd_rn(gr1, pr); gi1 = __dadd_rn(gi1, pi); }
+        else { gr2 = __dadd_rn(gr2, pr); gi2 = __dadd_rn(gi2, pi); }
       }
     }
+    const double gr[3] = {gr0, gr1, gr2}, gi[3] = {gi0, gi1, gi2};
+    const bool gp[3] = {gp0, gp1, gp2};
     double vr = 0.0, vi = 0.0;
     if (R.mode == 0) {
       bool have = false;

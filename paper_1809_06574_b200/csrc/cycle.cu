@@ -117,6 +117,12 @@ size_t cycle_ctl_doubles(int sb, int ldq, int na, int restart) {
          (size_t)(2 * sb + 1) * (3 * sb + na) + (size_t)2 * ldq * sb + 8;
 }
 
+// doubles of a worker's rows kept in shared memory (cached: 1 = [C | V] and W
+// rows, 0 = W rows only, 2 = none)
+size_t cycle_work_doubles(int rows, int ldx, int sb, int cached) {
+  return (size_t)rows * ((cached == 1 ? ldx : 0) + (cached == 2 ? 0 : odd_ld(sb)));
+}
+
 size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached) {
   size_t ctl = cycle_ctl_doubles(sb, ldq, na, restart);
   // cached: 1 = [C | V] rows (and W rows) in shared memory, 0 = W rows

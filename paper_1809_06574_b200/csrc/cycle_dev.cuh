@@ -814,7 +814,12 @@ struct WSmem {
 #define PMP_STEP_UPDATE block_update<NY>
 #endif
 
-template <bool CACHED, int NY, bool STAMP = false>
+// OPT: per-instance code-generation choices of the step loop (measured per
+// geometry, profiles/r02_codegen_ab.txt): kOptStamp keeps the phase stamps
+// compiled in, kOptCA gathers the SpMM's X rows through L1, kOptFlat uses
+// the flat Gram thread layout.
+constexpr int kOptStamp = 1, kOptCA = 2, kOptFlat = 4;
+template <bool CACHED, int NY, int OPT = 0>
 __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int r0, int nr,
                              bool lead, int& m, int& total, int& ncols, int& it, int& status) {
   double* G = S_.G;
@@ -844,23 +849,23 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const int q0 = m;
     const int stp = it - it_start;
     const StepBuf sbf = step_buf(P, q);
-    wstamp<STAMP>(P, stp, 0);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 0);
     // ---- W = A F_0 .. F_{nfac-1} V[:, q0 : q0 + sb] ---------------------------
     const double* src = P.V + q0;
     int lds = cap;
     for (int f = P.nfac - 1; f >= 0; --f) {
       double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
-      spmm_auto<NY, STAMP && PMP_SPMM_CA>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb,
+      spmm_auto<NY, (OPT & kOptCA) != 0>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb,
                                           dst + (size_t)r0 * P.s, P.s, r0, nr, S_.ring,
                                           S_.ring_doubles);
       wbar(wb);
       src = dst;
       lds = P.s;
     }
-    spmm_auto<NY, STAMP && PMP_SPMM_CA>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr, S_.ring,
+    spmm_auto<NY, (OPT & kOptCA) != 0>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr, S_.ring,
                                         S_.ring_doubles);
     __syncthreads();
-    wstamp<STAMP>(P, stp, 1);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 1);
 
     // ---- R1: [C | V]^T W --------------------------------------------------------
     const int kx = k + total;
@@ -869,26 +874,26 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     const double* Vrows = CACHED ? Xs + k : P.V + (size_t)r0 * cap;
     const int ldvr = CACHED ? ldx : cap;
     const Rows Vonly{Vrows, ldvr, total, Vrows, ldvr};
-    if (STAMP && PMP_GRAM_FLAT && kx <= 128)
+    if ((OPT & kOptFlat) && kx <= 128)
       block_gram_flat<NY>(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
     else
       PMP_STEP_GRAM(CV, kx, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
-    wstamp<STAMP>(P, stp, 2);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 2);
     wreduce(wb, P.partial, P.gout, kx * sb, G, sbf.B, k * sb, sbf.H1);
-    wstamp<STAMP>(P, stp, 3);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 3);
     PMP_STEP_UPDATE(CV, kx, Wv, ldw, sb, nr, G);
-    wstamp<STAMP>(P, stp, 4);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 4);
     // ---- R2: [V | W1]^T W1 ------------------------------------------------------
     const int kx2 = total + sb;
     {
       const Rows VW{Vrows, ldvr, total, Wv, ldw};
-      if (STAMP && PMP_GRAM_FLAT && kx2 <= 128)
+      if ((OPT & kOptFlat) && kx2 <= 128)
         block_gram_flat<NY>(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
       else
         PMP_STEP_GRAM(VW, kx2, Wv, ldw, sb, nr, red, P.partial, wb.wi + 1);
-      wstamp<STAMP>(P, stp, 5);
+      wstamp<(OPT & kOptStamp) != 0>(P, stp, 5);
       wreduce(wb, P.partial, P.gout, kx2 * sb, G, sbf.H2, total * sb, nullptr);
-      wstamp<STAMP>(P, stp, 6);
+      wstamp<(OPT & kOptStamp) != 0>(P, stp, 6);
     }
     // G_W = W1^T W1 - H2^T H2 (into R2 as scratch), then W2 = W1 - V H2
     const int n4 = 4 * sb * sb, lim4 = (n4 + 31) & ~31;
@@ -905,11 +910,11 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     }
     __syncthreads();
 #ifdef PMP_STAMPS
-    wstamp<STAMP>(P, stp, 12);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 12);
 #endif
     PMP_STEP_UPDATE(Vonly, total, Wv, ldw, sb, nr, G);
 #ifdef PMP_STAMPS
-    wstamp<STAMP>(P, stp, 13);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 13);
 #endif
     for (int qq = threadIdx.x; qq < sb * sb; qq += kOrthT) {
       const int i = qq / sb, j = qq % sb;
@@ -917,7 +922,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     }
     __syncthreads();
 #ifdef PMP_STAMPS
-    wstamp<STAMP>(P, stp, 14);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 14);
 #endif
 #ifdef PMP_STAMPS
     if (P.dbg && blockIdx.x == 1 && stp == 2)
@@ -942,7 +947,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
 #endif
     }
     __syncthreads();
-    wstamp<STAMP>(P, stp, 7);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 7);
     bool single = false;
     if (flag[0] == 0) single = fabs(R1[0]) / fabs(R1[(sb - 1) * sb + (sb - 1)]) <= kSkipKappa;
     if (flag[0] == 0 && !single) {
@@ -960,7 +965,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
       }
       __syncthreads();
     }
-    wstamp<STAMP>(P, stp, 8);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 8);
     if (flag[0]) {
       // grid-uniform: Cholesky cannot decide the rank -> host Householder
       // (unless the previous step already converged / was deficient)
@@ -1010,9 +1015,9 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
         sbf.R[i * sb + piv[c]] = (c >= i) ? s : 0.0;
       }
     }
-    wstamp<STAMP>(P, stp, 9);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 9);
     wbar(wb);  // new V block (and the step outputs) visible
-    wstamp<STAMP>(P, stp, 10);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 10);
     // the previous step's decision (the control block absorbed it meanwhile)
     if (q > 0) {
       const int d = wait_flag(P.ist + 16 + q - 1, 0);
@@ -1021,7 +1026,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
         break;
       }
     }
-    wstamp<STAMP>(P, stp, 11);
+    wstamp<(OPT & kOptStamp) != 0>(P, stp, 11);
     if (lead && threadIdx.x == 0) {
       __threadfence();
       *(volatile int*)(P.ist + 7) = q + 1;  // publish step q to the control block

@@ -374,6 +374,174 @@ __device__ void ls_residual_store(const LsParams& P, const LsMem& m, const int* 
   tm.sync();
 }
 
+// Column-pivoted Householder QR of the team's dense block M (mm x (n + 1),
+// column-major, the target in column n) for the multi-warp teams (c3: 125 x
+// 27 per column, 128 threads).  Same factorisation as the loop in ls_column
+// (which the warp tier keeps), organised for fewer team barriers per
+// reflector -- 5 instead of 11:
+//  * trailing column norms are computed once and DOWNDATED with the finished
+//    row of R (|a_j|^2 -= r_kj^2, recomputed exactly when the downdate has
+//    cancelled below sqrt(eps) of the last exact value: xGEQP3's safeguard,
+//    the pivoting the reference's gelsy itself uses) instead of being
+//    recomputed from the window every step;
+//  * warp 0 downdates, re-norms and finds the pivot with shuffles (first
+//    maximum wins, like the sequential scan);
+//  * every thread forms the reflector's scalars itself from the team sum, the
+//    reflector is applied unscaled (w_j = a_kj + scal * sum x_i a_ij) so no
+//    scaling pass separates the two sweeps, and the vector below the
+//    diagonal is not stored (only R and Q^T t are used afterwards).
+#ifndef PMP_LS_TEAM_QR
+#define PMP_LS_TEAM_QR 1
+#endif
+template <int T>
+__device__ void ls_qr_team(const LsMem& m, double* M, int mm, int n, const Team<T>& tm) {
+  const int tid = tm.tid, lane = tid & 31, wid = tid >> 5;
+  const unsigned full = 0xffffffffu;
+  const int K = mm < n ? mm : n;
+  tm.colsum(
+      n, 0, mm,
+      [&](int c, int i) {
+        const double v = M[i + (size_t)c * mm];
+        return v * v;
+      },
+      m.nrm);
+  tm.sync();
+  for (int c = tid; c < n; c += T) m.z[c] = m.nrm[c];  // last exactly computed values
+  tm.sync();
+  for (int k = 0; k < K; ++k) {
+    if (wid == 0) {
+      double best = -1.0;
+      int bi = n;
+      for (int c0 = k; c0 < n; c0 += 32) {
+        const int c = c0 + lane;
+        double v = -1.0;
+        bool redo = false;
+        if (c < n) {
+          v = m.nrm[c];
+          if (k > 0) {
+            const double r = M[(k - 1) + (size_t)c * mm];
+            v -= r * r;
+            redo = !(v > 1.4901161193847656e-8 * m.z[c]);
+          }
+        }
+        unsigned todo = __ballot_sync(full, redo);
+        while (todo) {
+          const int b = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int cb = c0 + b;
+          double s2 = 0.0;
+          for (int i = k + lane; i < mm; i += 32) {
+            const double x = M[i + (size_t)cb * mm];
+            s2 += x * x;
+          }
+          s2 = warp_sum(s2);
+          if (lane == b) {
+            v = s2;
+            m.z[c] = s2;
+          }
+        }
+        if (c < n) {
+          m.nrm[c] = v;
+          if (v > best) {
+            best = v;
+            bi = c;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(full, best, o);
+        const int oi = __shfl_xor_sync(full, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int p = bi < n ? bi : k;
+        m.misc[0] = p;
+        if (p != k) {
+          const int t = m.perm[k];
+          m.perm[k] = m.perm[p];
+          m.perm[p] = t;
+          m.nrm[p] = m.nrm[k];
+          m.z[p] = m.z[k];
+        }
+      }
+    }
+    tm.sync();
+    const int p = m.misc[0];
+    double part = 0.0;
+    for (int i = tid; i < mm; i += T) {
+      double a = M[i + (size_t)k * mm];
+      if (p != k) {
+        const double b = M[i + (size_t)p * mm];
+        M[i + (size_t)p * mm] = a;
+        M[i + (size_t)k * mm] = b;
+        a = b;
+      }
+      if (i > k) part += a * a;
+    }
+    part = warp_sum(part);
+    if (lane == 0) m.red[wid] = part;
+    tm.sync();
+    double xn2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < T / 32; ++i) xn2 += m.red[i];
+    const double alpha = M[k + (size_t)k * mm];
+    tm.sync();
+    double tau = 0.0, scal = 0.0;
+    if (xn2 > 0.0) {
+      const double beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+      if (tid == 0) M[k + (size_t)k * mm] = beta;
+    }
+    if (tid == 0) m.tau[k] = tau;
+    if (tau != 0.0) {
+      // w_j = a_kj + scal * sum_{i > k} x_i a_ij, j = k + 1 .. n (target included)
+      {
+        const int ncols = n - k;
+        int g = 32;
+        while (g > 1 && g * ncols > T) g >>= 1;
+        const int groups = T / g;
+        const int gid = tid / g, lig = tid % g;
+        const int rounds = (ncols + groups - 1) / groups;
+        const double* xk = M + (size_t)k * mm;
+        for (int rd = 0; rd < rounds; ++rd) {
+          const int c = rd * groups + gid;
+          double s0 = 0.0, s1 = 0.0;
+          if (c < ncols) {
+            const double* aj = M + (size_t)(k + 1 + c) * mm;
+            int i = k + 1 + lig;
+            for (; i + g < mm; i += 2 * g) {
+              s0 += xk[i] * aj[i];
+              s1 += xk[i + g] * aj[i + g];
+            }
+            if (i < mm) s0 += xk[i] * aj[i];
+          }
+          double sv = s0 + s1;
+          for (int o = g >> 1; o > 0; o >>= 1) sv += __shfl_xor_sync(full, sv, o);
+          if (c < ncols && lig == 0) m.w[k + 1 + c] = M[k + (size_t)(k + 1 + c) * mm] + scal * sv;
+        }
+      }
+      tm.sync();
+      const int rows = mm - k, ncol = n - k;
+      const int tpc = rows < T ? rows : T, ngr = T / tpc;
+      const int r = tid % tpc, g2 = tid / tpc;
+      if (g2 < ngr)
+        for (int i0 = r; i0 < rows; i0 += tpc) {
+          const int i = k + i0;
+          const double vi = (i0 == 0) ? 1.0 : scal * M[i + (size_t)k * mm];
+          const double tv = tau * vi;
+          for (int jj = k + 1 + g2; jj <= k + ncol; jj += ngr) M[i + (size_t)jj * mm] -= tv * m.w[jj];
+        }
+      tm.sync();
+    }
+  }
+}
+
 template <int T>
 __device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid) {
   LsMem m = ls_carve(mem, P.lcap, P.mcap, P.ncap);
@@ -495,6 +663,9 @@ __device__ void ls_column(const LsParams& P, int j, int cpos, char* mem, int tid
 
   // ---- column-pivoted Householder QR ----------------------------------------
   const int K = mm < n ? mm : n;
+  if (T > 32 && PMP_LS_TEAM_QR) {
+    ls_qr_team<T>(m, M, mm, n, tm);
+  } else
   for (int k = 0; k < K; ++k) {
     // squared norms of the trailing columns over rows k..m-1
     tm.colsum(

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
   // (measured on c4: profiles/r02_ctl_global_ab.txt); the control block runs
   // one step behind the workers and a step lasts milliseconds at these sizes,
   // so its slower state is invisible.
-  double* ctl_mem = (WG && A.ctl_global) ? proj + A.pCtl : region;
+  double* ctl_mem = A.ctl_global ? proj + A.pCtl : region;
   int* act = ist + kAct;
 
   // the per-group argument block lives in SHARED memory: as a local struct
@@ -606,12 +606,15 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
           staged = true;
         }
       }
-#ifndef PMP_WG_STAMPS
-#define PMP_WG_STAMPS 1
+#ifndef PMP_WG_OPT
+#define PMP_WG_OPT (kOptStamp | kOptCA | kOptFlat)
+#endif
+#ifndef PMP_SM_OPT
+#define PMP_SM_OPT kOptFlat
 #endif
       if (!staged)
-        worker_inner<CACHED, NY, WG && PMP_WG_STAMPS>(L, wb, wsm, r0, nr, lead, m, total, ncols, it,
-                                                      status);
+        worker_inner<CACHED, NY, WG ? PMP_WG_OPT : PMP_SM_OPT>(L, wb, wsm, r0, nr, lead, m, total,
+                                                               ncols, it, status);
       sstamp(A, grp, cyc, 3);
     }
     gbar(gb);
@@ -656,7 +659,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       for (int f = D.nfac - 1; f >= 0; --f) {
         wbar(wb);
         double* dst = ((D.nfac - 1 - f) & 1) ? L.T1 : L.T0;
-        spmm_auto<NY, WG && PMP_SPMM_CA>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr,
+        spmm_auto<NY, ((WG ? PMP_WG_OPT : PMP_SM_OPT) & kOptCA) != 0>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr,
                       (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
         src = dst;
       }
@@ -668,7 +671,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       }
       wbar(wb);
       // Rb = B[:, act] - A Xa -> R[:, act], RB
-      spmm_auto<NY, WG && PMP_SPMM_CA>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr,
+      spmm_auto<NY, ((WG ? PMP_WG_OPT : PMP_SM_OPT) & kOptCA) != 0>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr,
                     (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
       __syncthreads();
       for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
@@ -914,6 +917,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
 namespace pmp {
 size_t cycle_region_doubles(int rows, int ldx, int sb, int ldq, int na, int restart, int cached);
 size_t cycle_ctl_doubles(int sb, int ldq, int na, int restart);
+size_t cycle_work_doubles(int rows, int ldx, int sb, int cached);
 }
 
 using namespace pmp;
@@ -939,14 +943,16 @@ static bool solve_ctl_global(int s, int kc, int cap, int cached) {
     const char* e = getenv("PMP_CTL_GLOBAL");
     return e ? atoi(e) : 1;
   }();
+  if (on >= 2 && cached == 0) return true;  // (experiment: W rows only in the region)
   return on && cached == 2 && !solve_staged(s, kc, cap, cached);
 }
 
 static size_t solve_smem_bytes(int rows, int ldx, int kc, int cap, int s, int restart,
                                int cached) {
   size_t d = (size_t)(kc + cap + s) * s + 2 * (size_t)s * s + 8 * 32 * (size_t)s + 20;
-  if (!solve_ctl_global(s, kc, cap, cached))
-    d += cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
+  d += solve_ctl_global(s, kc, cap, cached)
+           ? cycle_work_doubles(rows, ldx, s, cached)
+           : cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
   return d * sizeof(double);
 }
 
