@@ -424,16 +424,24 @@ def roofline(kern, timed, recs, steps):
     ms = np.array([a.elapsed_time(b) for a, b, _ in lst])
     ach = per_step_bytes * steps / (np.sum(ms) / 1e3) / 1e9
     ach_strict = strict_bytes * steps / (np.sum(ms) / 1e3) / 1e9
+    # DRAM bytes from the committed ncu --set full capture of this config's
+    # k_solve (a 6-system batch, tools/gpu_ncu_solve.sh), scaled to this
+    # run's launch by the ratio of algorithmic bytes
     traffic = None
+    traffic_note = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        ent = tj.get(name + "_c%s" % os.environ.get("PMP_BENCH_CONFIG", "4")) or tj.get(name)
+        ent = tj.get(name + "_c%s" % os.environ.get("PMP_BENCH_CONFIG", "4"))
         if ent:
-            traffic = ent["dram_bytes_per_launch"]
+            per_launch = per_step_bytes / max(launches_per_step, 1e-9)
+            traffic = ent["dram_bytes"] * per_launch / ent["algorithmic_bytes"]
+            traffic_note = ("%s: %.4g DRAM bytes for %.4g algorithmic (x%.2f), scaled to this "
+                            "launch" % (ent["source"], ent["dram_bytes"], ent["algorithmic_bytes"],
+                                        ent["dram_bytes"] / ent["algorithmic_bytes"]))
     except (OSError, ValueError, KeyError):
         pass
     return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-            "frac": ach / hbm, "traffic": traffic,
+            "frac": ach / hbm, "traffic": traffic, "traffic_source": traffic_note,
             "algorithmic_bytes_per_launch": per_step_bytes / max(launches_per_step, 1e-9),
             "algorithmic_unit": "SURVEY.md 8(d): per block step, operator chain (12 nnz + 4 (n+1) "
                                 "+ 16 n s_b per matrix) + block CGS2 (32 n total + 48 n s_b + "

@@ -90,6 +90,10 @@ static __device__ __forceinline__ void named_bar(int id, int nthreads) {
 #ifndef PMP_SPMM_CA
 #define PMP_SPMM_CA 1
 #endif
+#ifndef PMP_SPMM_RP_AHEAD
+#define PMP_SPMM_RP_AHEAD 1
+#endif
+
 template <int NY, bool CA = false>
 __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const double* __restrict__ va, const double* X, int ldx, int sb,
@@ -97,6 +101,20 @@ __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int
   constexpr int PER = kOrthT / NY, RPT = PMP_SPMM_RPT, CH = PMP_SPMM_CH;
   const int c = threadIdx.x % NY, slot = threadIdx.x / NY;
   const bool col_ok = c < sb;
+#if PMP_SPMM_RP_AHEAD
+  // the next pass's row extents are loaded one pass ahead: the row-pointer
+  // load leaves the dependent chain (pointer -> index -> gather) of a pass
+  int nlo[RPT], nhi[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = slot + u * PER;
+    nlo[u] = nhi[u] = 0;
+    if (r < nr) {
+      nlo[u] = __ldg(rp + r0 + r);
+      nhi[u] = __ldg(rp + r0 + r + 1);
+    }
+  }
+#endif
   for (int base = 0; base < nr; base += RPT * PER) {
     int lo[RPT], hi[RPT];
     double a0[RPT], a1[RPT];
@@ -104,14 +122,25 @@ __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
       const int r = base + slot + u * PER;
-      lo[u] = 0;
-      hi[u] = 0;
       a0[u] = 0.0;
       a1[u] = 0.0;
+#if PMP_SPMM_RP_AHEAD
+      lo[u] = nlo[u];
+      hi[u] = nhi[u];
+      const int rn = r + RPT * PER;
+      nlo[u] = nhi[u] = 0;
+      if (rn < nr) {
+        nlo[u] = __ldg(rp + r0 + rn);
+        nhi[u] = __ldg(rp + r0 + rn + 1);
+      }
+#else
+      lo[u] = 0;
+      hi[u] = 0;
       if (r < nr) {
         lo[u] = __ldg(rp + r0 + r);
         hi[u] = __ldg(rp + r0 + r + 1);
       }
+#endif
       len = max(len, hi[u] - lo[u]);
     }
     for (int e0 = 0; e0 < len; e0 += CH) {

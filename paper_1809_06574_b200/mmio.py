@@ -4,12 +4,11 @@ Files are written the way the reference's ``write_matrix_market`` writes
 them: canonical CSR (``as_csr``: duplicates summed, indices sorted, explicit
 zeros removed) printed by ``scipy.io.mmwrite(field="complex", precision=17,
 symmetry="general")``, so both sides read each other's files bit-exactly.
-The B200 path computes in real FP64 and writes +0 imaginary parts (the
-reference's complex arithmetic sometimes prints -0; the values read back
-are the same).  Reading accepts
-any Matrix Market file the reference accepts; complex data with a non-zero
-imaginary part raises ``NotImplementedError`` (complex128 is the first
-"next" row of SURVEY.md 8(f)).
+Real systems are written with +0 imaginary parts (the reference's complex
+arithmetic sometimes prints -0; the values read back are the same).  Reading
+accepts any Matrix Market file the reference accepts and returns float64
+data when every imaginary part is zero, complex128 otherwise (complex
+systems run through their real form on the device, cplx.py).
 
 Host-side only: persistence is file I/O around the device path.
 """
@@ -22,15 +21,14 @@ MM_PRECISION = 17  # sparsecore.py:247 -- bit-exact text round trips
 
 
 def canonical_csr(A):
-    """The reference's ``as_csr`` (sparsecore.py:26-44) restricted to real
-    data: float64 CSR, duplicates summed, sorted indices, no explicit zeros."""
+    """The reference's ``as_csr`` (sparsecore.py:26-44): CSR, duplicates
+    summed, sorted indices, no explicit zeros; float64 when the data is real
+    (or complex with all-zero imaginary parts), complex128 otherwise."""
     A = sp.csr_matrix(A)
-    if np.iscomplexobj(A.data):
-        if A.nnz and np.abs(A.data.imag).max() != 0:
-            raise NotImplementedError("complex-valued matrices are not supported by the B200 "
-                                      "path yet (real FP64 only)")
+    cx = np.iscomplexobj(A.data) and A.nnz and np.abs(A.data.imag).max() != 0
+    if np.iscomplexobj(A.data) and not cx:
         A = sp.csr_matrix((A.data.real, A.indices, A.indptr), shape=A.shape)
-    A = sp.csr_matrix(A, dtype=np.float64, copy=True)
+    A = sp.csr_matrix(A, dtype=np.complex128 if cx else np.float64, copy=True)
     A.sum_duplicates()
     A.sort_indices()
     A.eliminate_zeros()
@@ -64,14 +62,14 @@ def write_dense_matrix_market(X, path):
 
 
 def read_dense_matrix_market(path):
-    """sparsecore.py:281-285, returned as a real float64 block."""
+    """sparsecore.py:281-285; float64 when every imaginary part is zero,
+    complex128 otherwise."""
     M = scipy.io.mmread(str(path), spmatrix=False)
     if sp.issparse(M):
         M = M.toarray()
     M = np.atleast_2d(np.asarray(M))
     if np.iscomplexobj(M):
         if np.abs(M.imag).max(initial=0.0) != 0:
-            raise NotImplementedError("complex-valued blocks are not supported by the B200 "
-                                      "path yet (real FP64 only)")
+            return np.ascontiguousarray(M, dtype=np.complex128)
         M = M.real
     return np.ascontiguousarray(M, dtype=np.float64)

@@ -262,14 +262,22 @@ def test_matrix_market_round_trip_is_bit_exact(tmp_path):
     assert np.array_equal(mmio.read_dense_matrix_market(tmp_path / "x.mtx"), X)
 
 
-def test_matrix_market_rejects_complex_values(tmp_path):
+def test_matrix_market_complex_round_trip(tmp_path):
+    """Complex files (sparsecore.py:250-285) read back bit-exactly as
+    complex128; all-zero imaginary parts come back as float64."""
     import scipy.io
     import scipy.sparse as sp
     from paper_1809_06574_b200 import mmio
-    A = sp.csr_matrix(np.array([[1.0 + 1j, 0], [0, 2.0]]))
-    scipy.io.mmwrite(str(tmp_path / "c.mtx"), A, field="complex")
-    with pytest.raises(NotImplementedError):
-        mmio.read_matrix_market(tmp_path / "c.mtx")
+    A = sp.csr_matrix(np.array([[1.0 + 1.0 / 3.0j, 0], [0.1 - 2j, 2.0]]))
+    mmio.write_matrix_market(A, tmp_path / "c.mtx")
+    B = mmio.read_matrix_market(tmp_path / "c.mtx")
+    assert B.dtype == np.complex128 and np.array_equal(B.toarray(), A.toarray())
+    scipy.io.mmwrite(str(tmp_path / "r.mtx"), sp.csr_matrix(np.eye(2) * (1 + 0j)), field="complex")
+    assert mmio.read_matrix_market(tmp_path / "r.mtx").dtype == np.float64
+    X = np.array([[1.0 + 0.5j, 2.0], [0.25j, -1.0 / 7.0]])
+    mmio.write_dense_matrix_market(X, tmp_path / "x.mtx")
+    Y = mmio.read_dense_matrix_market(tmp_path / "x.mtx")
+    assert Y.dtype == np.complex128 and np.array_equal(Y, X)
     (tmp_path / "bad.mtx").write_text("%%MatrixMarket matrix nonsense\n1 1 1\n")
     with pytest.raises(ValueError):
         mmio.read_matrix_market(tmp_path / "bad.mtx")

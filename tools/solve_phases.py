@@ -52,6 +52,10 @@ def main():
     _abi.lib().pmp_cycle_debug_stamps(None, 0)
     print("batch of %d: %.3f ms; iterations %s" % (a.groups, e0.elapsed_time(e1),
                                                     [r.iterations for _, r in res]))
+    alg = sum(getattr(r, "algorithmic_bytes", 0.0) for _, r in res)
+    strict = sum(getattr(r, "algorithmic_bytes_strict", 0.0) for _, r in res)
+    print("algorithmic bytes of the batch: %.6e (SURVEY 8(d) unit), %.6e (every operand once)"
+          % (alg, strict))
     st = buf[:4096].view(64, 32, 2).cpu().numpy().astype(np.int64)[:, :, 1]
     rows = []
     for it in range(64):
@@ -82,12 +86,9 @@ def main():
                 continue
             parts = []
             for i, nm in enumerate(names):
-                if v[i] and v[i + 1]:
+                if v[i] and v[i + 1] and 0 <= v[i + 1] - v[i] < 10 ** 12:
                     parts.append("%s %.1f" % (nm, (v[i + 1] - v[i]) / 1e3))
             print("  cycle %d: %s" % (c, ", ".join(parts)))
-        g = buf[40 * 64:40 * 64 + 64].cpu().numpy().view(np.float64)
-        print("  G (step 2):", np.array2string(g.reshape(8, 8), precision=3))
-        np.save(os.path.join(ROOT, "gpurun_out", "gchol.npy"), g)
 
 
 if __name__ == "__main__":
