@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--systems", type=int, default=0, help="limit #systems (debug)")
     ap.add_argument("--batch", type=int, default=6,
                     help="block groups (systems in flight) per persistent solve launch")
+    ap.add_argument("--level1-systems", type=int, default=3,
+                    help="systems of the pattern_level=1 sample (0: skip)")
     ap.add_argument("--cpu-solve-iters", type=int, default=5,
                     help="block steps of the truncated CPU solve sample")
     return ap.parse_args()
@@ -327,6 +329,10 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, pm, model, W, s_grid, p_grid, pol, cfg, rank, world, barrier)
 
+    lvl1 = None
+    if args.level1_systems > 0 and world == 1:
+        lvl1 = level1_sample(args, pm, model, s_grid, p_grid, cfg, Bd, barrier, torch)
+
     line = None
     if rank == 0:
         line = {
@@ -356,11 +362,41 @@ def run_ours(args):
         }
         if e2e is not None:
             line["e2e"] = e2e
+        if lvl1 is not None:
+            line["level1_sample"] = lvl1
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(args, W, pts, model, pol, iters)
     if world > 1:
         dist.destroy_process_group()
     return line
+
+
+def level1_sample(args, pm, model, s_grid, p_grid, cfg, Bd, barrier, torch):
+    """pattern_level = 1 (the reference's default, spai.py:143 / update.py:50)
+    on the first systems of the same sequence: cold spai_build + update_first
+    with residual-driven augmentation (spai.py:285-289) + the solves.  Level 1
+    has no window path (its supports depend on every system's values): the
+    systems run one at a time on the same device kernels.  A bounded sample,
+    outside the timed steps."""
+    k = min(args.level1_systems, len(p_grid))
+    pol1 = pm.PrecondPolicy("spai-update-first", spai=pm.SpaiConfig(pattern_level=1),
+                            update=pm.UpdateConfig(pattern_level=1))
+    model.reset_symbolic()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    recs, info = pm.run_sequence(model, s_grid[:1], p_grid[:k], pol1, cfg, B=Bd, timing=True,
+                                 batch=args.batch)
+    e1.record()
+    barrier()
+    t = e0.elapsed_time(e1) / 1e3
+    model.reset_symbolic()
+    return {"pattern_level": 1, "systems": k, "sequence_s": t,
+            "columns_per_s": model.dim * k / t,
+            "phases_s": {ph: float(info[ph + "_s"]) for ph in ("assemble", "build", "solve")},
+            "iterations": [int(r["iterations"]) for r in recs],
+            "converged": bool(all(r["converged"] for r in recs)),
+            "note": "first %d systems of the sequence, cold, systems one at a time" % k}
 
 
 def build_rates(pm, model, pts, pol, barrier, torch, reps=3):

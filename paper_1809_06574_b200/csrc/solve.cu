@@ -944,15 +944,37 @@ static bool solve_ctl_global(int s, int kc, int cap, int cached) {
     return e ? atoi(e) : 1;
   }();
   if (on >= 2 && cached == 0) return true;  // (experiment: W rows only in the region)
-  return on && cached == 2 && !solve_staged(s, kc, cap, cached);
+  // staged geometry (s >= 9: c3): with the control state in global memory the
+  // blocks need only the ring, and two of them fit an SM instead of one
+  // (PMP_STAGE_CTLG; measured in profiles/r02_codegen_ab.txt)
+  static const int stg = [] {
+    const char* e = getenv("PMP_STAGE_CTLG");
+    return e ? atoi(e) : 1;
+  }();
+  if (cached == 2 && solve_staged(s, kc, cap, cached)) return on && stg != 0;
+  return on && cached == 2;
+}
+
+// doubles of a block's shared-memory region: the control state and / or the
+// workers' rows (cycle_region_doubles), only the workers' rows when the
+// control state is in global memory, or -- staged geometry with the control
+// state in global memory -- a ring that fills a two-blocks-per-SM budget
+static size_t solve_region_doubles(int rows, int ldx, int kc, int cap, int s, int restart,
+                                   int cached) {
+  if (!solve_ctl_global(s, kc, cap, cached))
+    return cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
+  if (solve_staged(s, kc, cap, cached)) {
+    const size_t fixed = (size_t)(kc + cap + s) * s + 2 * (size_t)s * s + 8 * 32 * (size_t)s + 20;
+    const size_t budget = (size_t)108 * 1024 / sizeof(double);
+    return budget > fixed + 2048 ? ((budget - fixed) & ~(size_t)1) : 2048;
+  }
+  return cycle_work_doubles(rows, ldx, s, cached);
 }
 
 static size_t solve_smem_bytes(int rows, int ldx, int kc, int cap, int s, int restart,
                                int cached) {
   size_t d = (size_t)(kc + cap + s) * s + 2 * (size_t)s * s + 8 * 32 * (size_t)s + 20;
-  d += solve_ctl_global(s, kc, cap, cached)
-           ? cycle_work_doubles(rows, ldx, s, cached)
-           : cycle_region_doubles(rows, ldx, s, kc + cap, s, restart, cached);
+  d += solve_region_doubles(rows, ldx, kc, cap, s, restart, cached);
   return d * sizeof(double);
 }
 
@@ -1041,7 +1063,7 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   A.wglob = cached == 2;
   A.stage_rows = 0;
   A.stage_n = 0;
-  A.region_doubles = (int)cycle_region_doubles(rows, A.ldx, b->s, b->kc + b->cap, b->s,
+  A.region_doubles = (int)solve_region_doubles(rows, A.ldx, b->kc, b->cap, b->s,
                                                b->inner_restart, cached);
   A.ctl_global = solve_ctl_global(b->s, b->kc, b->cap, cached) ? 1 : 0;
   A.pCtl = b->pCtl;
@@ -1051,8 +1073,7 @@ int pmp_solve_batch(PmpSolveBatch* b) {
   }
   if (solve_staged(b->s, b->kc, b->cap, cached)) {
     // ring of S stages x R rows of [C | V | W] in the workers' region
-    const size_t region = cycle_region_doubles(rows, A.ldx, b->s, b->kc + b->cap, b->s,
-                                               b->inner_restart, cached);
+    const size_t region = (size_t)A.region_doubles;
     // (stage_rows carries the stage size in doubles: a pass packs as many
     // rows as its columns allow, >= 8 even at full width)
     const size_t row = (size_t)bank_pad(b->kc) + bank_pad(b->cap) + bank_pad(b->s);
