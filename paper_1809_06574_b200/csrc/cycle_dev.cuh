@@ -181,6 +181,102 @@ __device__ __noinline__ void spmm_rows(const int32_t* __restrict__ rp, const int
   }
 }
 
+// spmm_rows over TILES DEALT CYCLICALLY to the group's workers (worker wi of
+// nw takes tiles wi, wi + nw, ... of kCycTile rows of the whole matrix)
+// instead of one contiguous row range per block.  With contiguous ranges
+// the blocks of a group sweep 48 distant fronts at once, so a far neighbour
+// of a grid stencil (row r +- 128^2 at c4) is re-read from HBM every time:
+// ncu put k_solve's DRAM traffic at 2.0x the algorithmic bytes, the SpMM's X
+// read ~3x.  Dealt cyclically the group works on one window of nw tiles that
+// moves through the matrix, and a row gathered as somebody's far neighbour
+// is still in L2 when its own tile comes up.  Inside a tile the near
+// neighbours (+-1, +-128) still hit L1.  The output rows belong to other
+// blocks afterwards: the caller places a group barrier before reading them.
+// Same per-row arithmetic as spmm_rows (bitwise equal).
+constexpr int kCycTile = 512;
+template <int NY, bool CA>
+__device__ __noinline__ void spmm_rows_cyc(const int32_t* __restrict__ rp,
+                                           const int32_t* __restrict__ ci,
+                                           const double* __restrict__ va, const double* X, int ldx,
+                                           int sb, double* Y, int ldy, int n, int wi, int nw) {
+  constexpr int PER = kOrthT / NY, RPT = PMP_SPMM_RPT, CH = PMP_SPMM_CH, STEP = RPT * PER;
+  constexpr int PPT = kCycTile / STEP;  // passes per tile
+  static_assert(kCycTile % STEP == 0, "tile must be whole passes");
+  const int c = threadIdx.x % NY, slot = threadIdx.x / NY;
+  const bool col_ok = c < sb;
+  const int ntile = (n + kCycTile - 1) / kCycTile;
+  const int mine = wi < ntile ? (ntile - wi + nw - 1) / nw : 0;  // this worker's tiles
+  const int npass = mine * PPT;
+  // global row of (pass p, sub-row u) of this thread
+  auto rowof = [&](int p, int u) {
+    return (wi + (p / PPT) * nw) * kCycTile + (p % PPT) * STEP + slot + u * PER;
+  };
+  int nlo[RPT], nhi[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = rowof(0, u);
+    nlo[u] = nhi[u] = 0;
+    if (npass > 0 && r < n) {
+      nlo[u] = __ldg(rp + r);
+      nhi[u] = __ldg(rp + r + 1);
+    }
+  }
+  for (int p = 0; p < npass; ++p) {
+    int lo[RPT], hi[RPT];
+    double a0[RPT], a1[RPT];
+    int len = 0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      a0[u] = 0.0;
+      a1[u] = 0.0;
+      lo[u] = nlo[u];
+      hi[u] = nhi[u];
+      const int rn = rowof(p + 1, u);
+      nlo[u] = nhi[u] = 0;
+      if (p + 1 < npass && rn < n) {
+        nlo[u] = __ldg(rp + rn);
+        nhi[u] = __ldg(rp + rn + 1);
+      }
+      len = max(len, hi[u] - lo[u]);
+    }
+    for (int e0 = 0; e0 < len; e0 += CH) {
+      int j[RPT][CH];
+      double w[RPT][CH], x[RPT][CH];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int e = lo[u] + e0 + q;
+          const bool ok = e < hi[u];
+          j[u][q] = ok ? __ldg(ci + e) : -1;
+          w[u][q] = ok ? __ldg(va + e) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+          x[u][q] = (j[u][q] >= 0 && col_ok)
+                        ? (CA ? __ldca(X + (size_t)j[u][q] * ldx + c)
+                              : __ldcg(X + (size_t)j[u][q] * ldx + c))
+                        : 0.0;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          if (q & 1)
+            a1[u] += w[u][q] * x[u][q];
+          else
+            a0[u] += w[u][q] * x[u][q];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int r = rowof(p, u);
+      if (r < n && col_ok) Y[(size_t)r * ldy + c] = a0[u] + a1[u];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The same product with its operands staged asynchronously (global-row
 // geometry, full 8-column blocks: c4).  spmm_rows keeps 16 gathers per
@@ -847,7 +943,7 @@ struct WSmem {
 // geometry, profiles/r02_codegen_ab.txt): kOptStamp keeps the phase stamps
 // compiled in, kOptCA gathers the SpMM's X rows through L1, kOptFlat uses
 // the flat Gram thread layout.
-constexpr int kOptStamp = 1, kOptCA = 2, kOptFlat = 4;
+constexpr int kOptStamp = 1, kOptCA = 2, kOptFlat = 4, kOptCyc = 8;
 template <bool CACHED, int NY, int OPT = 0>
 __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int r0, int nr,
                              bool lead, int& m, int& total, int& ncols, int& it, int& status) {
@@ -882,6 +978,21 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     // ---- W = A F_0 .. F_{nfac-1} V[:, q0 : q0 + sb] ---------------------------
     const double* src = P.V + q0;
     int lds = cap;
+    if ((OPT & kOptCyc) && P.wglob) {
+      // tiles dealt cyclically over the group's workers; W's rows come from
+      // other blocks, hence the extra group barrier
+      for (int f = P.nfac - 1; f >= 0; --f) {
+        double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
+        spmm_rows_cyc<NY, (OPT & kOptCA) != 0>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst, P.s,
+                                                P.n, wb.wi, wb.n);
+        wbar(wb);
+        src = dst;
+        lds = P.s;
+      }
+      spmm_rows_cyc<NY, (OPT & kOptCA) != 0>(P.arp, P.aci, P.ava, src, lds, sb, P.W, P.s, P.n, wb.wi,
+                                              wb.n);
+      wbar(wb);
+    } else {
     for (int f = P.nfac - 1; f >= 0; --f) {
       double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
       spmm_auto<NY, (OPT & kOptCA) != 0>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb,
@@ -893,6 +1004,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     }
     spmm_auto<NY, (OPT & kOptCA) != 0>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr, S_.ring,
                                         S_.ring_doubles);
+    }
     __syncthreads();
     wstamp<(OPT & kOptStamp) != 0>(P, stp, 1);
 

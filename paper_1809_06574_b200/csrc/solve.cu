@@ -165,6 +165,21 @@ __device__ __forceinline__ void fold_rowsolve(const double* w, const double* z, 
     }
 }
 
+// The cycle boundaries' Gram products: the flat thread layout in the
+// global-row instance (few columns -- k + na <= 18 -- leave half of
+// block_gram's lanes idle), block_gram elsewhere.
+#ifndef PMP_BOUNDARY_FLAT
+#define PMP_BOUNDARY_FLAT 1
+#endif
+template <int NY, bool FLAT>
+__device__ __forceinline__ void gram_b(const Rows X, int kx, const double* Y, int ldy, int ny,
+                                       int nrows, double* red, double* partial, int slot) {
+  if (FLAT && NY <= 8 && PMP_BOUNDARY_FLAT && kx <= 128)  // (s = 16: 1168 -> 1186 ms, off)
+    block_gram_flat<NY>(X, kx, Y, ldy, ny, nrows, red, partial, slot);
+  else
+    block_gram<NY>(X, kx, Y, ldy, ny, nrows, red, partial, slot);
+}
+
 #ifndef PMP_FOLD_EXACT
 #define PMP_FOLD_EXACT 1
 #endif
@@ -349,7 +364,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
     }
     const double* Bv = D.B + (size_t)r0 * s;
     const Rows BB{Bv, s, s, Bv, s};
-    block_gram<NY>(BB, s, Bv, s, s, nr, red, partial, slot);
+    gram_b<NY, WG>(BB, s, Bv, s, s, nr, red, partial, slot);
     wreduce(wb, partial, gout, s * s, G, nullptr, 0, nullptr);
     if (lead && threadIdx.x == 0) {
       int na = 0;
@@ -405,13 +420,13 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       const StepBuf sbf = step_buf(L, 0);
       if (k > 0) {
         const Rows CV{C + (size_t)r0 * kc, kc, k, C + (size_t)r0 * kc, kc};
-        block_gram<NY>(CV, k, Zw, s, na, nr, red, partial, slot);
+        gram_b<NY, WG>(CV, k, Zw, s, na, nr, red, partial, slot);
         wreduce(wb, partial, gout, k * na, G, sbf.B, k * na, nullptr);
         block_update<NY>(CV, k, Zw, s, na, nr, G);
       }
       {
         const Rows ZZ{Zw, s, na, Zw, s};
-        block_gram<NY>(ZZ, na, Zw, s, na, nr, red, partial, slot);
+        gram_b<NY, WG>(ZZ, na, Zw, s, na, nr, red, partial, slot);
         wreduce(wb, partial, gout, na * na, G, nullptr, 0, nullptr);
       }
       for (int q = threadIdx.x; q < na * na; q += kOrthT) {
@@ -430,7 +445,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       if (flag[0] == 0 && !single) {
         block_trsm_rows<NY>(Zw, s, Q1, na, nr, na, R1, piv);
         const Rows Qv{Q1, na, na, Q1, na};
-        block_gram<NY>(Qv, na, Q1, na, na, nr, red, partial, slot);
+        gram_b<NY, WG>(Qv, na, Q1, na, na, nr, red, partial, slot);
         wreduce(wb, partial, gout, na * na, G, nullptr, 0, nullptr);
         if (threadIdx.x < 32) {
           const bool ok = warp_cholesky_smem(G, na, R2, piv2, false, 0.0);
@@ -607,7 +622,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         }
       }
 #ifndef PMP_WG_OPT
-#define PMP_WG_OPT (kOptStamp | kOptCA | kOptFlat)
+#define PMP_WG_OPT (kOptStamp | kOptCA | kOptFlat | kOptCyc)
 #endif
 #ifndef PMP_SM_OPT
 #define PMP_SM_OPT kOptFlat
@@ -656,13 +671,23 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       }
       // Xa = P Z (factor chain right to left)
       const double* src = Z;
+      constexpr int kOpt = WG ? PMP_WG_OPT : PMP_SM_OPT;
+      // tiles dealt cyclically (spmm_rows_cyc); 8-column blocks only (s = 16: 1168 -> 1179 ms)
+      constexpr bool kCyc = WG && NY <= 8 && (kOpt & kOptCyc) != 0;
       for (int f = D.nfac - 1; f >= 0; --f) {
         wbar(wb);
         double* dst = ((D.nfac - 1 - f) & 1) ? L.T1 : L.T0;
-        spmm_auto<NY, ((WG ? PMP_WG_OPT : PMP_SM_OPT) & kOptCA) != 0>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst + (size_t)r0 * s, s, r0, nr,
-                      (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
+        if (kCyc)
+          spmm_rows_cyc<NY, (kOpt & kOptCA) != 0>(D.frp[f], D.fci[f], D.fva[f], src, s, na, dst, s, n,
+                                                  wb.wi, wb.n);
+        else
+          spmm_auto<NY, (kOpt & kOptCA) != 0>(D.frp[f], D.fci[f], D.fva[f], src, s, na,
+                                              dst + (size_t)r0 * s, s, r0, nr,
+                                              (WG && !A.ctl_global) ? region : nullptr,
+                                              A.region_doubles);
         src = dst;
       }
+      if (kCyc && D.nfac > 0) wbar(wb);  // this block's rows of P Z came from other blocks
       __syncthreads();
       for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
         const int r = q / na, c = q % na;
@@ -671,8 +696,15 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       }
       wbar(wb);
       // Rb = B[:, act] - A Xa -> R[:, act], RB
-      spmm_auto<NY, ((WG ? PMP_WG_OPT : PMP_SM_OPT) & kOptCA) != 0>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s, r0, nr,
-                    (WG && !A.ctl_global) ? region : nullptr, A.region_doubles);
+      if (kCyc) {
+        spmm_rows_cyc<NY, (kOpt & kOptCA) != 0>(D.arp, D.aci, D.ava, src, s, na, RB, s, n, wb.wi,
+                                                wb.n);
+        wbar(wb);
+      } else {
+        spmm_auto<NY, (kOpt & kOptCA) != 0>(D.arp, D.aci, D.ava, src, s, na, RB + (size_t)r0 * s, s,
+                                            r0, nr, (WG && !A.ctl_global) ? region : nullptr,
+                                            A.region_doubles);
+      }
       __syncthreads();
       for (int q = threadIdx.x; q < nr * na; q += kOrthT) {
         const int r = q / na, c = q % na;
@@ -684,7 +716,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       __syncthreads();
       const double* RBr = RB + (size_t)r0 * s;
       const Rows RR{RBr, s, na, RBr, s};
-      block_gram<NY>(RR, na, RBr, s, na, nr, red, partial, slot);
+      gram_b<NY, WG>(RR, na, RBr, s, na, nr, red, partial, slot);
       wreduce(wb, partial, gout, na * na, G, nullptr, 0, nullptr);
       if (lead && threadIdx.x == 0) {
         const int steps = it_new - it0;
@@ -760,7 +792,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
       const Rows Conly{C + (size_t)r0 * kc, kc, k, C + (size_t)r0 * kc, kc};
       const Rows Uonly{U + (size_t)r0 * kc, kc, k, U + (size_t)r0 * kc, kc};
       // pass 1: [C | W]^T W -> H1, M0 = W^T W
-      block_gram<NY>(Cr, k + na, Wr, s, na, nr, red, partial, slot);
+      gram_b<NY, WG>(Cr, k + na, Wr, s, na, nr, red, partial, slot);
       wreduce(wb, partial, gout, (k + na) * na, G, nullptr, 0, nullptr);
       double* w0 = R1;  // |w_c| (before any projection)
       for (int c = threadIdx.x; c < na; c += kOrthT) w0[c] = sqrt(fmax(G[(k + c) * na + c], 0.0));
@@ -769,7 +801,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         block_update<NY>(Conly, k, Wr, s, na, nr, G);
         block_update<NY>(Uonly, k, Zr, s, na, nr, G);
         // pass 2: [C | W1]^T W1 -> H2, M1; M = M1 - H2^T H2
-        block_gram<NY>(Cr, k + na, Wr, s, na, nr, red, partial, slot);
+        gram_b<NY, WG>(Cr, k + na, Wr, s, na, nr, red, partial, slot);
         wreduce(wb, partial, gout, (k + na) * na, G, nullptr, 0, nullptr);
         for (int q = threadIdx.x; q < na * na; q += kOrthT) {
           const int i = q / na, j = q % na;
@@ -848,7 +880,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         if (!(tmax <= kSkipKappa * tmin)) {
           // second Cholesky-QR pass over the new columns
           const Rows Qn{C + (size_t)r0 * kc + k, kc, nk, C + (size_t)r0 * kc + k, kc};
-          block_gram<NY>(Qn, nk, C + (size_t)r0 * kc + k, kc, nk, nr, red, partial, slot);
+          gram_b<NY, WG>(Qn, nk, C + (size_t)r0 * kc + k, kc, nk, nr, red, partial, slot);
           wreduce(wb, partial, gout, nk * nk, G, nullptr, 0, nullptr);
           if (threadIdx.x < 32) {
             const bool ok = warp_cholesky_smem(G, nk, R1, piv2, false, 0.0);

@@ -440,6 +440,22 @@ __device__ PMP_STAGED_ATTR void worker_inner_staged(const CycleArgs& P, WBar& wb
     // ---- W = A F_0 .. F_{nfac-1} V[:, q0 : q0 + sb] ---------------------------
     const double* src = P.V + q0;
     int lds = cap;
+#ifndef PMP_STAGED_CYC
+#define PMP_STAGED_CYC 0
+#endif
+    if (PMP_STAGED_CYC) {
+      // tiles dealt cyclically over the group's workers (spmm_rows_cyc)
+      for (int f = P.nfac - 1; f >= 0; --f) {
+        double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
+        spmm_rows_cyc<NY, false>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst, P.s, P.n, wb.wi,
+                                 wb.n);
+        wbar(wb);
+        src = dst;
+        lds = P.s;
+      }
+      spmm_rows_cyc<NY, false>(P.arp, P.aci, P.ava, src, lds, sb, P.W, P.s, P.n, wb.wi, wb.n);
+      wbar(wb);
+    } else {
     for (int f = P.nfac - 1; f >= 0; --f) {
       double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
       spmm_rows<NY>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst + (size_t)r0 * P.s, P.s,
@@ -449,6 +465,7 @@ __device__ PMP_STAGED_ATTR void worker_inner_staged(const CycleArgs& P, WBar& wb
       lds = P.s;
     }
     spmm_rows<NY>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr);
+    }
     cstamp(P, stp, 1);
 
     // ---- pass 1: [C | V]^T W ---------------------------------------------------

@@ -21,6 +21,7 @@ small matrices the host needs; n-sized data never leaves HBM.
 """
 
 import ctypes
+import os as _os
 import time
 from dataclasses import dataclass, field
 
@@ -460,7 +461,15 @@ def _colnorms(D, Wp, ldw, nw):
     return np.sqrt(np.maximum(g, 0.0))
 
 
-def block_gcro_solve(A, B, P=None, cfg=None):
+# A single solve goes through the same persistent kernel as the sequence
+# windows (pmp_solve_batch, one block group); the host-driven path (k_cycle
+# per cycle, host between cycles) serves what that kernel hands back
+# (status 10: deflation, rank-deficient projected problem), chains longer
+# than 3 factors and PMP_SINGLE_HOST=1.
+SINGLE_VIA_BATCH = _os.environ.get("PMP_SINGLE_HOST", "0")[:1] == "0"
+
+
+def block_gcro_solve(A, B, P=None, cfg=None, _host=False):
     """Solve A X = B for all columns of B simultaneously (krylov.py:105-275).
 
     ``A`` may be a scipy matrix or a DeviceCSR; ``B`` a numpy array (the
@@ -486,7 +495,13 @@ def block_gcro_solve(A, B, P=None, cfg=None):
         raise TypeError("P must be a Preconditioner or None")
     if P is not None and P.dim != n:
         raise ValueError("preconditioner dimension %d does not match system %d" % (P.dim, n))
-    X, report = _solve(A, Bd, P, cfg)
+    if SINGLE_VIA_BATCH and not _host and Bd.shape[1] >= 1 and n > 0:
+        t0 = time.perf_counter()
+        X, report = block_gcro_solve_batch([(A, P)], Bd, cfg=cfg, groups=1)[0]
+        if not report.wall_time:   # (the record's D2H synchronised the launch)
+            report.wall_time = time.perf_counter() - t0
+    else:
+        X, report = _solve(A, Bd, P, cfg)
     return (X.cpu().numpy() if host_out else X), report
 
 
@@ -1213,9 +1228,9 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
             raise TypeError("P must be a Preconditioner or None")
         chains.append(P.factors() if P is not None else [])
     if any(_any_complex(A, P) for A, P in systems):
-        return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
+        return [block_gcro_solve(A, Bd, P=P, cfg=cfg, _host=True) for A, P in systems]
     if not ok or max(len(c) for c in chains) > 3:
-        return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
+        return [block_gcro_solve(A, Bd, P=P, cfg=cfg, _host=True) for A, P in systems]
     gsz = ctypes.c_int()
     rows = ctypes.c_int()
     cached = ctypes.c_int()
@@ -1227,7 +1242,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
     rc = L.pmp_solve_geometry(n, s, cap, kc, cfg.inner_restart, groups, ctypes.byref(gsz),
                               ctypes.byref(rows), ctypes.byref(cached), ctypes.byref(smem))
     if rc:
-        return [block_gcro_solve(A, Bd, P=P, cfg=cfg) for A, P in systems]
+        return [block_gcro_solve(A, Bd, P=P, cfg=cfg, _host=True) for A, P in systems]
     hist_cap = cap + 2
     log_cap = 2 * cfg.max_iters + 4
     off, poff, wsz = _solve_layout(n, s, cap, kc, gsz.value, hist_cap, log_cap,
@@ -1331,7 +1346,7 @@ def block_gcro_solve_batch(systems, B, cfg=None, groups=None):
             out[i] = (Xs[i], rep)
     for i in fallback:
         A, P = systems[i]
-        out[i] = block_gcro_solve(A, Bd, P=P, cfg=cfg)
+        out[i] = block_gcro_solve(A, Bd, P=P, cfg=cfg, _host=True)
     return out
 
 
