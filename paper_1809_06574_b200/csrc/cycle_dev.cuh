@@ -1118,7 +1118,7 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
         if (d == 1) status = 0;
         if (d == 4) status = 4;
       }
-      if (status == 5 && lead) {
+      if (status == 5 && lead && P.mirror) {
         // the step's B / H1 / H2 for the host fallback (krylov.py
         // _native_cycle status 5)
         const int lens[3] = {k * sb, total * sb, total * sb};

@@ -537,7 +537,7 @@ __device__ PMP_STAGED_ATTR void worker_inner_staged(const CycleArgs& P, WBar& wb
         if (d == 1) status = 0;
         if (d == 4) status = 4;
       }
-      if (status == 5 && lead) {
+      if (status == 5 && lead && P.mirror) {
         const int lens[3] = {k * sb, total * sb, total * sb};
         const int offs[3] = {P.offB, P.offH1, P.offH2};
         const double* srcs[3] = {sbf.B, sbf.H1, sbf.H2};

@@ -461,13 +461,12 @@ def _colnorms(D, Wp, ldw, nw):
     return np.sqrt(np.maximum(g, 0.0))
 
 
-# A single solve runs on the host-driven path (k_cycle per cycle, host between
-# cycles).  PMP_SINGLE_HOST=0 routes it through the persistent kernel of the
-# sequence windows instead (pmp_solve_batch, one block group) -- opt-in: that
-# kernel is validated at the sequence sizes (n >= 256, the goldens and the
-# smoke test); at n = 40 with one group it faulted (tests/golden rand40), so
-# the switch stays off until that geometry is debugged.
-SINGLE_VIA_BATCH = _os.environ.get("PMP_SINGLE_HOST", "1")[:1] == "0"
+# A single solve goes through the same persistent kernel as the sequence
+# windows (pmp_solve_batch, one block group); the host-driven path (k_cycle
+# per cycle, host between cycles) serves what that kernel hands back
+# (status 10: deflation, rank-deficient projected problem), complex systems,
+# chains longer than 3 factors and PMP_SINGLE_HOST=1.
+SINGLE_VIA_BATCH = _os.environ.get("PMP_SINGLE_HOST", "0")[:1] == "0"
 
 
 def block_gcro_solve(A, B, P=None, cfg=None, _host=False):

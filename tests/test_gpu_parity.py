@@ -936,3 +936,31 @@ def test_window_with_exact_zeros_matches_per_system_path(pm):
             Xa = a["X"].cpu().numpy() if hasattr(a["X"], "cpu") else a["X"]
             Xb = b["X"].cpu().numpy() if hasattr(b["X"], "cpu") else b["X"]
             assert np.linalg.norm(Xa - Xb) <= 1e-12 * np.linalg.norm(Xb)
+
+
+@pytest.mark.parametrize("n,s", [(24, 4), (40, 3)])
+def test_persistent_solve_hands_back_deflating_blocks(pm, n, s):
+    """A block Krylov space that fills the whole space (n < restart length)
+    ends in a rank-deficient block: the persistent kernel must hand the
+    system back (status 10, reason 3 -- krylov.py:79-95 deflation runs on the
+    host-driven path), not write through its absent host mirror (it faulted
+    there until round 2).  Same iterations as the host-driven path."""
+    import torch
+    from paper_1809_06574_b200 import krylov
+    rs = np.random.RandomState(7)
+    A = sp.csr_matrix(sp.random(n, n, density=min(1.0, 4.0 / n), random_state=rs, format="csr")
+                      + 4.0 * sp.identity(n))
+    B = np.random.default_rng(3).standard_normal((n, s))
+    cfg = pm.SolverConfig(tol=1e-10)
+    krylov.FALLBACK_REASONS.clear()
+    Ad = krylov._as_dev_csr(A)
+    res = krylov.block_gcro_solve_batch([(Ad, None)] * 3, torch.as_tensor(B, device="cuda"),
+                                        cfg=cfg, groups=3)
+    Xh, rh = pm.block_gcro_solve(A, B, cfg=cfg, _host=True)
+    for X, r in res:
+        X = X.cpu().numpy()
+        rel = np.linalg.norm(B - A @ X, axis=0) / np.linalg.norm(B, axis=0)
+        assert r.converged and rel.max() <= 1e-9
+        assert abs(r.iterations - rh.iterations) <= 2
+    assert krylov.FALLBACK_REASONS.get(3, 0) == 3
+    krylov.FALLBACK_REASONS.clear()
