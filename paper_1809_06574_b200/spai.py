@@ -457,9 +457,15 @@ def _plan(pattern, sys_colptr, sys_rowidx, t_colptr, t_rowidx, t_key, sys_key, c
     m = msize.cpu().numpy().astype(np.int64)[cols]
     tiers = _split_tiers(cols, lcap, m, nI)
     # per-column sizes of a symbolic plan record (pmp_ls_columns_planned)
-    pos = {int(c): i for i, c in enumerate(cols)} if cols_host is not None else None
+    # (position of every tier column in `cols`, vectorised: a Python dict over
+    # the 2 M augmented columns of a level-1 build at c4 cost 0.6 s per system)
+    order = scols = None
+    if cols_host is not None:
+        order = np.argsort(cols, kind="stable")
+        scols = cols[order]
     for t in tiers:
-        idx = t.cols_host if pos is None else np.array([pos[int(c)] for c in t.cols_host])
+        idx = (t.cols_host if order is None
+               else order[np.searchsorted(scols, np.asarray(t.cols_host, dtype=np.int64))])
         t.plan_sizes = 4 + nI[idx] + 2 * L[idx]
     if key is not None:
         pattern.cache[key] = tiers
