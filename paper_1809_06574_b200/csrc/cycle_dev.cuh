@@ -277,166 +277,21 @@ __device__ __noinline__ void spmm_rows_cyc(const int32_t* __restrict__ rp,
   }
 }
 
-// ---------------------------------------------------------------------------
-// The same product with its operands staged asynchronously (global-row
-// geometry, full 8-column blocks: c4).  spmm_rows keeps 16 gathers per
-// thread in flight behind two dependent index loads, at 16 warps per SM:
-// latency bound (tools/micro/spmm_bench.cu: 1.41 ms for six 128^3 systems,
-// 1.09 ms this way).  Here a tile of 64 rows has its index / value segment
-// (contiguous in CSR) copied into shared memory two tiles ahead and its
-// gathered X rows (16-byte cp.async pieces, L2 only) one tile ahead; the
-// products read shared memory.  No registers are held across the latency and
-// a whole tile's gathers (28 KB) are in flight per block.  Same per-row
-// summation order as spmm_rows (even / odd entries, then summed): bitwise
-// equal results.  Tiles whose entries exceed the ring (irregular rows: c5)
-// go through spmm_rows.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void spa_cp16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void spa_cp8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void spa_cp4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-
-#ifndef PMP_SPMM_ASYNC
-#define PMP_SPMM_ASYNC 0
-#endif
-
-template <int NY>
-__device__ __noinline__ void spmm_rows_async(const int32_t* __restrict__ rp,
-                                             const int32_t* __restrict__ ci,
-                                             const double* __restrict__ va, const double* X,
-                                             int ldx, double* Y, int ldy, int r0, int nr,
-                                             double* ring, int ring_doubles) {
-  constexpr int PER = kOrthT / NY, RPT = 2, TR = RPT * PER, PC = NY / 2;
-  const int c = threadIdx.x % NY, slot = threadIdx.x / NY;
-  // ring = X rows [2][EMAX * NY] | values [3][EMAX] | indices [3][EMAX] (int)
-  const int EMAX = (int)(((size_t)ring_doubles * 8) / (2 * NY * 8 + 3 * 12)) & ~3;
-  double* xb = ring;
-  double* vb = ring + (size_t)2 * EMAX * NY;
-  int* cb = reinterpret_cast<int*>(vb + (size_t)3 * EMAX);
-  const int ntiles = (nr + TR - 1) / TR;
-  const int32_t* rpb = rp + r0;
-  auto bound = [&](int t) { return __ldg(rpb + min(t * TR, nr)); };
-  auto issue_cv = [&](int t, int e_lo, int cnt) {
-    if (cnt > EMAX) return;
-    int* cd = cb + (size_t)(t % 3) * EMAX;
-    double* vd = vb + (size_t)(t % 3) * EMAX;
-    for (int q = threadIdx.x; q < cnt; q += kOrthT) {
-      spa_cp4(cd + q, ci + e_lo + q);
-      spa_cp8(vd + q, va + e_lo + q);
-    }
-  };
-  auto issue_x = [&](int t, int cnt) {
-    if (cnt > EMAX) return;
-    const int* cd = cb + (size_t)(t % 3) * EMAX;
-    double* xd = xb + (size_t)(t & 1) * EMAX * NY;
-    for (int q = threadIdx.x; q < cnt * PC; q += kOrthT) {
-      const int e = q / PC, ch = q % PC;
-      spa_cp16(xd + (size_t)e * NY + 2 * ch, X + (size_t)cd[e] * ldx + 2 * ch);
-    }
-  };
-  __syncthreads();  // the ring's previous contents are dead
-  int b0 = bound(0), b1 = bound(1), b2 = bound(2), b3 = bound(3);
-  issue_cv(0, b0, b1 - b0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  issue_x(0, b1 - b0);
-  issue_cv(1, b1, b2 - b1);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  int lo[RPT], hi[RPT];
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    const int r = slot + u * PER;
-    lo[u] = hi[u] = 0;
-    if (r < nr) {
-      lo[u] = __ldg(rpb + r);
-      hi[u] = __ldg(rpb + r + 1);
-    }
-  }
-  for (int t = 0; t < ntiles; ++t) {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");  // X(t), index / values (t + 1)
-    __syncthreads();
-    issue_x(t + 1, b2 - b1);
-    const int b4 = bound(t + 4);
-    issue_cv(t + 2, b2, b3 - b2);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    int nlo[RPT], nhi[RPT];
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      const int r = (t + 1) * TR + slot + u * PER;
-      nlo[u] = nhi[u] = 0;
-      if (r < nr) {
-        nlo[u] = __ldg(rpb + r);
-        nhi[u] = __ldg(rpb + r + 1);
-      }
-    }
-    if (b1 - b0 > EMAX) {
-      // (block-uniform) a tile too large for the ring: the direct loop
-      const int ta = t * TR;
-      spmm_rows<NY>(rp, ci, va, X, ldx, NY, Y + (size_t)ta * ldy, ldy, r0 + ta, min(TR, nr - ta));
-    } else {
-      const double* xd = xb + (size_t)(t & 1) * EMAX * NY;
-      const double* vd = vb + (size_t)(t % 3) * EMAX;
-#pragma unroll
-      for (int u = 0; u < RPT; ++u) {
-        const int r = t * TR + slot + u * PER;
-        if (r < nr) {
-          double a0 = 0.0, a1 = 0.0;
-          int e = lo[u] - b0;
-          const int eh = hi[u] - b0;
-          for (; e + 1 < eh; e += 2) {
-            a0 += vd[e] * xd[(size_t)e * NY + c];
-            a1 += vd[e + 1] * xd[(size_t)(e + 1) * NY + c];
-          }
-          if (e < eh) a0 += vd[e] * xd[(size_t)e * NY + c];
-          Y[(size_t)r * ldy + c] = a0 + a1;
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      lo[u] = nlo[u];
-      hi[u] = nhi[u];
-    }
-    b0 = b1;
-    b1 = b2;
-    b2 = b3;
-    b3 = b4;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-}
-
-// spmm_rows, through the asynchronous ring when the caller has one (`ring`
-// non-null: the global-row geometry's free shared memory), the block is a
-// full NY = 8 columns wide and the X rows are 16-byte aligned
+// spmm_rows for the step loop and the cycle boundaries; `ring` is unused
+// since the asynchronous-ring variant was measured and dropped: cp.async
+// index / value segments two tiles ahead, gathered X rows one tile ahead,
+// products from shared memory -- 1.09 vs 1.41 ms alone
+// (tools/micro/spmm_bench.cu keeps it), but its 74 KB of shared memory per
+// block shrink L1 to 28 KB and every other gather phase of k_solve slows
+// (c4 batch 634 vs 491 ms, profiles/r02_codegen_ab.txt).
 template <int NY, bool CA = false>
 __device__ __forceinline__ void spmm_auto(const int32_t* __restrict__ rp,
                                           const int32_t* __restrict__ ci,
                                           const double* __restrict__ va, const double* X, int ldx,
                                           int sb, double* Y, int ldy, int r0, int nr, double* ring,
                                           int ring_doubles) {
-#if PMP_SPMM_ASYNC
-  if (NY == 8 && ring != nullptr && sb == NY && (ldx & 1) == 0 &&
-      (reinterpret_cast<uintptr_t>(X) & 15) == 0 && ring_doubles >= 2048) {
-    spmm_rows_async<NY>(rp, ci, va, X, ldx, Y, ldy, r0, nr, ring, ring_doubles);
-    return;
-  }
-#endif
+  (void)ring;
+  (void)ring_doubles;
   spmm_rows<NY, CA>(rp, ci, va, X, ldx, sb, Y, ldy, r0, nr);
 }
 

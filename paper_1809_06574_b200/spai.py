@@ -408,8 +408,17 @@ def _bucket_merge(sel, cols, lcap, m, nI, bytes_fn, limit, team, glob, mode):
 def _coarse(v):
     """Round up to {1, 1.25, 1.5, 1.75} x 2^k (at least 8)."""
     v = np.maximum(np.asarray(v, dtype=np.int64), 8)
-    p = 1 << (np.floor(np.log2(v)).astype(np.int64) - 2)
-    return ((v + p - 1) // p) * p
+
+    def rnd(x):
+        p = 1 << (np.floor(np.log2(x)).astype(np.int64) - 2)
+        return ((x + p - 1) // p) * p
+    vmax = int(v.max()) if v.size else 8
+    if v.size > 4096 and vmax <= (1 << 22):
+        # sizes are small integers: one table, one gather (log2 over millions
+        # of columns was the largest item of the cold planning profile)
+        lut = rnd(np.maximum(np.arange(vmax + 1, dtype=np.int64), 8))
+        return lut[v]
+    return rnd(v)
 
 
 def _tier_from(team, glob, cols, lcap, m, nI, idx, mode=0):
