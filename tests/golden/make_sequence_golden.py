@@ -100,9 +100,12 @@ def main():
     ap.add_argument("--procs", type=int, default=6)
     ap.add_argument("--systems", default="all",
                     help="comma list of sequence indices, 'all', or 'stride:K'")
+    ap.add_argument("--scale", type=int, default=0,
+                    help="make_config's scale (a shrunken generator: grid side, or n for c5); "
+                         "the golden is then seq_<cfg>s<scale>.json")
     args = ap.parse_args()
     cfgno = int(args.config[1])
-    W = make_config(cfgno)
+    W = make_config(cfgno, scale=args.scale or None)
     pts = W.points()
     if args.systems == "all":
         idx = list(range(len(pts)))
@@ -144,7 +147,7 @@ def main():
         r["sigma"] = float(pts[r["index"]][0])
         r["p"] = [float(v) for v in pts[r["index"]][1]]
     r1 = np.asarray(st1.residuals)
-    out = {"config": args.config, "n": int(W.n), "n_systems": len(pts),
+    out = {"config": args.config, "scale": int(args.scale), "n": int(W.n), "n_systems": len(pts),
            "systems": idx, "records": recs,
            "p1": {"nnz": int(P1m.nnz), "resid_sum": float(r1.sum()),
                   "resid_max": float(r1.max()), "fro": float(sp.linalg.norm(P1m))},
@@ -152,7 +155,8 @@ def main():
            "numpy": np.__version__, "scipy": __import__("scipy").__version__,
            "solver": "SolverConfig(tol=1e-8)", "policy": "spai-update-first, pattern_level=0",
            "seconds": time.perf_counter() - t0}
-    path = os.path.join(HERE, "seq_%s.json" % args.config)
+    path = os.path.join(HERE, "seq_%s%s.json" % (args.config,
+                                                 ("s%d" % args.scale) if args.scale else ""))
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)
     its = [r["iterations"] for r in recs]

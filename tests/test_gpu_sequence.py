@@ -41,13 +41,13 @@ def pm():
     return pm
 
 
-def _run(pm, cfgno, n_p=None, batch=6):
+def _run(pm, cfgno, n_p=None, batch=6, scale=None):
     import sys
     sys.path.insert(0, os.path.join(G.GOLDEN, "..", "..", "oracle"))
     import pmor_oracle as orc
     from paper_1809_06574_b200 import krylov
     from paper_1809_06574_b200.workloads import make_config
-    W = make_config(cfgno)
+    W = make_config(cfgno, scale=scale)
     s_grid, p_grid = list(W.s_grid), list(W.p_grid)
     if n_p is not None:
         s_grid, p_grid = s_grid[:1], p_grid[:n_p]
@@ -119,6 +119,17 @@ def test_c3_sequence_vs_reference(pm):
         ref = [g["iterations"] for g in gold["records"]]
         its = [recs[i]["iterations"] for i in range(128)]
         assert abs(np.mean(its) - np.mean(ref)) <= 0.5
+
+
+def test_c5_scaled_sequence_vs_reference(pm):
+    """c5's generator (power-law row lengths 4..200, random columns) at
+    n = 6000: the whole 64-system sequence on the device, the reference's
+    records for systems 0, 1, 2, 17, 40 compared system by system.  (At full
+    size one reference build of c5 is ~4 h of CPU.)"""
+    gold = _golden("c5s6000")
+    recs, resid = _run(pm, 5, scale=6000)
+    assert len(recs) == 64
+    _compare(gold, recs, resid)
 
 
 @pytest.mark.parametrize("lvl", [0, 1])
