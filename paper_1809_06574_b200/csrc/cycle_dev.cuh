@@ -798,7 +798,7 @@ struct WSmem {
 // geometry, profiles/r02_codegen_ab.txt): kOptStamp keeps the phase stamps
 // compiled in, kOptCA gathers the SpMM's X rows through L1, kOptFlat uses
 // the flat Gram thread layout.
-constexpr int kOptStamp = 1, kOptCA = 2, kOptFlat = 4, kOptCyc = 8;
+constexpr int kOptStamp = 1, kOptCA = 2, kOptFlat = 4, kOptCyc = 8, kOptFuse = 16;
 template <bool CACHED, int NY, int OPT = 0>
 __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int r0, int nr,
                              bool lead, int& m, int& total, int& ncols, int& it, int& status) {
@@ -908,13 +908,21 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
 #ifdef PMP_STAMPS
     wstamp<(OPT & kOptStamp) != 0>(P, stp, 12);
 #endif
-    PMP_STEP_UPDATE(Vonly, total, Wv, ldw, sb, nr, G);
+    // kOptFuse (global-row instance): the Cholesky factor of G_W does not
+    // depend on W2, so it is taken first (G_W symmetrised into `red`: G still
+    // holds H2) and, when one Cholesky-QR pass suffices, W2 = W1 - V H2 goes
+    // straight into the new V block (block_update_trsm); otherwise the
+    // original order below.
+    constexpr bool kFuse = (OPT & kOptFuse) != 0 && !CACHED;
+    bool fused_done = false;
+    if (!kFuse) PMP_STEP_UPDATE(Vonly, total, Wv, ldw, sb, nr, G);
 #ifdef PMP_STAMPS
     wstamp<(OPT & kOptStamp) != 0>(P, stp, 13);
 #endif
+    double* Gs = kFuse ? red : G;  // the symmetrised G_W
     for (int qq = threadIdx.x; qq < sb * sb; qq += kOrthT) {
       const int i = qq / sb, j = qq % sb;
-      G[qq] = 0.5 * (R2[i * sb + j] + R2[j * sb + i]);
+      Gs[qq] = 0.5 * (R2[i * sb + j] + R2[j * sb + i]);
     }
     __syncthreads();
 #ifdef PMP_STAMPS
@@ -931,9 +939,9 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
       const long long c0 = clock64();
 #endif
 #ifdef PMP_CHOL_REG
-      bool ok = warp_cholesky_reg<NY>(G, sb, R1, piv, true, kCholRatio);
+      bool ok = warp_cholesky_reg<NY>(Gs, sb, R1, piv, true, kCholRatio);
 #else
-      bool ok = warp_cholesky_smem(G, sb, R1, piv, true, kCholRatio);
+      bool ok = warp_cholesky_smem(Gs, sb, R1, piv, true, kCholRatio);
 #endif
       if (threadIdx.x == 0) flag[0] = ok ? 0 : 1;
 #ifdef PMP_STAMPS
@@ -946,6 +954,15 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     wstamp<(OPT & kOptStamp) != 0>(P, stp, 7);
     bool single = false;
     if (flag[0] == 0) single = fabs(R1[0]) / fabs(R1[(sb - 1) * sb + (sb - 1)]) <= kSkipKappa;
+    if (kFuse) {
+      if (flag[0] == 0 && single) {
+        block_update_trsm<NY>(Vonly, total, Wv, ldw, sb, nr, G, R1, piv,
+                              P.V + (size_t)r0 * cap + total, cap);
+        fused_done = true;
+      } else {
+        PMP_STEP_UPDATE(Vonly, total, Wv, ldw, sb, nr, G);
+      }
+    }
     if (flag[0] == 0 && !single) {
 #ifdef PMP_STAMPS
       if (P.dbg && lead && threadIdx.x == 0 && stp < 64)
@@ -989,7 +1006,9 @@ __device__ void worker_inner(const CycleArgs& P, WBar& wb, const WSmem& S_, int 
     {
       double* qd = CACHED ? Xs + k + total : P.V + (size_t)r0 * cap + total;
       const int ldqd = CACHED ? ldx : cap;
-      if (single)
+      if (fused_done) {
+        // (the new block is in V already)
+      } else if (single)
         block_trsm_rows<NY>(Wv, ldw, qd, ldqd, nr, sb, R1, piv);
       else
         block_trsm_rows<NY>(Q1, sb, qd, ldqd, nr, sb, R2, nullptr);

@@ -615,6 +615,84 @@ __device__ __noinline__ void block_trsm_rows(const double* X, int ldx, double* Y
   __syncthreads();
 }
 
+// block_update and block_trsm_rows in one pass over the rows (thread per
+// row): y = Y[r] - X(r, :) G, then Q[r] = y[piv] R^-1 written to Qd; Y is not
+// written back.  For the block step whose Cholesky-QR needs a single pass:
+// W2 = W1 - V H2 is consumed where it is produced, so W2 is neither stored
+// nor read again (one pass over the block's W rows and one barrier-free
+// sweep less per step).  Same arithmetic as the two functions in sequence.
+template <int NY>
+__device__ __forceinline__ void block_update_trsm(const Rows X, int kx, const double* Y, int ldy,
+                                                  int ny, int nrows, const double* G,
+                                                  const double* R, const int* piv, double* Qd,
+                                                  int ldq) {
+  __shared__ double rinv_f[16];
+  __shared__ int piv_f[16];
+  if (threadIdx.x < ny) {
+    rinv_f[threadIdx.x] = 1.0 / R[threadIdx.x * ny + threadIdx.x];
+    piv_f[threadIdx.x] = piv[threadIdx.x];
+  }
+  __syncthreads();
+  const int ka = min(kx, X.ka);
+  for (int r = threadIdx.x; r < nrows; r += kOrthT) {
+    double acc[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) acc[c] = 0.0;
+    const double* xa = X.a + (size_t)r * X.lda;
+#pragma unroll kUpdUnroll
+    for (int t = 0; t < ka; ++t) {
+      const double x = xa[t];
+      const double* g = G + t * ny;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c < ny) acc[c] += x * g[c];
+    }
+    const double* xb = X.b + (size_t)r * X.ldb - X.ka;
+#pragma unroll kUpdUnroll
+    for (int t = ka; t < kx; ++t) {
+      const double x = xb[t];
+      const double* g = G + t * ny;
+#pragma unroll
+      for (int c = 0; c < NY; ++c)
+        if (c < ny) acc[c] += x * g[c];
+    }
+    const double* y = Y + (size_t)r * ldy;
+    double w2[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) w2[c] = (c < ny) ? y[c] - acc[c] : 0.0;
+    // q = w2[piv] R^-1 (row-vector triangular solve, as block_trsm_rows)
+    double xq[NY], q[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) {
+      double v = 0.0;
+      if (c < ny) {
+        const int pc = piv_f[c];
+#pragma unroll
+        for (int a = 0; a < NY; ++a)
+          if (a == pc) v = w2[a];
+      }
+      xq[c] = v;
+    }
+#pragma unroll
+    for (int c = 0; c < NY; ++c) {
+      if (c < ny) {
+        double sv = xq[c];
+#pragma unroll
+        for (int a = 0; a < NY; ++a)
+          if (a < c) sv -= q[a] * R[a * ny + c];
+        q[c] = sv * rinv_f[c];
+      } else {
+        q[c] = 0.0;
+      }
+    }
+    double* qo = Qd + (size_t)r * ldq;
+#pragma unroll
+    for (int c = 0; c < NY; ++c)
+      if (c < ny) qo[c] = q[c];
+  }
+  __syncthreads();
+}
+
 // cooperative launch of kOrthT-thread blocks, routed through the shared
 // cooperative stream when one is set (orth.cu, pmp_set_coop_stream)
 cudaError_t coop_launch(const void* fn, int g, void** args, size_t smem, cudaStream_t user);

@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(kOrthT, PMP_MINB) k_solve(SolveArgs A) {
         }
       }
 #ifndef PMP_WG_OPT
-#define PMP_WG_OPT (kOptStamp | kOptCA | kOptFlat | kOptCyc)
+#define PMP_WG_OPT (kOptStamp | kOptCA | kOptFlat | kOptCyc | kOptFuse)
 #endif
 #ifndef PMP_SM_OPT
 #define PMP_SM_OPT kOptFlat
