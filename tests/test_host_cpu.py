@@ -327,3 +327,25 @@ def test_cli_report_writer_round_trip(tmp_path):
     with pytest.raises(ValueError):
         cli.compare_reports(rep, b)
     assert cli.main(["run"]) == cli.EXIT_USAGE
+
+
+def test_solve_layout_and_size_table():
+    """Host-side pieces of the persistent solve / LS planning: workspace
+    offsets are 256-byte aligned, the control-state block is part of the
+    projected-state area (offset 0 stays reserved: pCtl = 0 means "absent"),
+    and the coarsening table equals the closed form."""
+    from paper_1809_06574_b200 import krylov, spai
+    off, proj, wsz = krylov._solve_layout(1000, 8, 68, 18, 49, 70, 2004, ctl=7536)
+    assert all(v % 32 == 0 for v in off.values()) and wsz % 32 == 0
+    assert all(v % 32 == 0 and v > 0 for v in proj.values())
+    names = sorted(proj, key=proj.get)
+    assert names[-1] == "pCtl"
+    assert off["oLog"] - off["oProj"] >= proj["pCtl"] + 7536
+    v = np.random.default_rng(0).integers(1, 5000, size=20000)
+
+    def closed(x):
+        x = np.maximum(np.asarray(x, dtype=np.int64), 8)
+        p = 1 << (np.floor(np.log2(x)).astype(np.int64) - 2)
+        return ((x + p - 1) // p) * p
+    assert np.array_equal(spai._coarse(v), closed(v))          # table path
+    assert np.array_equal(spai._coarse(v[:100]), closed(v[:100]))  # direct path
