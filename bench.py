@@ -407,7 +407,7 @@ def build_rates(pm, model, pts, pol, barrier, torch, reps=3):
     step clock)."""
     from paper_1809_06574_b200.update import update_first_many
     n = model.dim
-    sp_t, up_t, win_t = [], [], []
+    sp_t, up_t, win_t, spw_t, upw_t = [], [], [], [], []
     k = max(1, min(len(pts) - 1, 16))
     for _ in range(reps):
         model.reset_symbolic()
@@ -430,13 +430,30 @@ def build_rates(pm, model, pts, pol, barrier, torch, reps=3):
         e[3].record()
         barrier()
         win_t.append(e[0].elapsed_time(e[3]) / 1e3)
-        del As, A1, A2, P1
+        # the same two calls again with the structure's symbolic state kept
+        # (pattern, LS plans, transpose plan): what every later build of a
+        # sequence on this structure costs
+        barrier()
+        e[0].record()
+        P1w, _ = pm.spai_build(A1, pol.spai)
+        e[1].record()
+        pm.update_first(A1, A2, P1w, pol.update)
+        e[2].record()
+        barrier()
+        spw_t.append(e[0].elapsed_time(e[1]) / 1e3)
+        upw_t.append(e[1].elapsed_time(e[2]) / 1e3)
+        del As, A1, A2, P1, P1w
     ts, tu, tw = float(np.median(sp_t)), float(np.median(up_t)), float(np.median(win_t))
+    tsw, tuw = float(np.median(spw_t)), float(np.median(upw_t))
     return {"spai_columns_per_s": n / ts, "update_columns_per_s": n / tu,
             "update_window_columns_per_s": n * k / tw, "spai_build_s": ts,
             "update_first_s": tu, "update_window_systems": k, "update_window_s": tw,
+            "spai_columns_per_s_warm": n / tsw, "update_columns_per_s_warm": n / tuw,
+            "spai_build_warm_s": tsw, "update_first_warm_s": tuw,
             "reps": reps, "note": "device-resident A in, device-resident factor + stats out; "
-                                  "spai_build on a cold structure"}
+                                  "spai_build / update_first on a cold structure (symbolic "
+                                  "planning included), then with the structure's plans kept "
+                                  "(_warm)"}
 
 
 def roofline(kern, timed, recs, steps):
