@@ -316,18 +316,25 @@ def _team_bytes(lcap, mcap, ncap):
 
 def _pow2(v):
     v = np.maximum(np.asarray(v, dtype=np.int64), 1)
-    return (1 << np.ceil(np.log2(v)).astype(np.int64)).astype(np.int64)
+
+    def up(x):
+        return (1 << np.ceil(np.log2(x)).astype(np.int64)).astype(np.int64)
+    if v.ndim and v.size > 4096:
+        vmax = int(v.max())
+        if vmax <= (1 << 22):   # small integers: one table, one gather
+            return up(np.maximum(np.arange(vmax + 1, dtype=np.int64), 1))[v]
+    return up(v)
 
 
 class _Tier:
     """One launch of pmp_ls_columns.  mode 3 = the semi-normal-equations
     kernel for columns whose dense block exceeds shared memory."""
 
-    def __init__(self, team, glob, lcap, mcap, ncap, cols, mode=0):
+    def __init__(self, team, glob, lcap, mcap, ncap, cols, mode=0, cols_dev=None):
         self.team, self.glob, self.mode = team, glob, mode
         self.lcap, self.mcap, self.ncap = int(lcap), int(mcap), int(ncap)
         self.cols_host = cols
-        self.cols = i32(cols)
+        self.cols = i32(cols) if cols_dev is None else cols_dev
         self.ncols = int(cols.size)
         self.bytes = (_sne_bytes(self.lcap, self.mcap, self.ncap) if mode == 3
                       else _team_bytes(self.lcap, self.mcap, self.ncap))
@@ -340,6 +347,45 @@ def _sne_bytes(lcap, mcap, ncap):
 
 
 def _split_tiers(cols, lcap, m, nI):
+    """_split_tiers_direct, decided on the DISTINCT (list capacity, coarsened
+    |I|, coarsened |J|) triples instead of on every column: the tier logic
+    depends on a column only through that triple (and on the largest true
+    |I| / |J| of a group), so for large column sets the triples are grouped
+    on the device (torch.unique + scatter max: milliseconds at n = 2^21,
+    where the per-column numpy sorts cost 0.25 s per plan), the tiers are
+    formed on the few distinct triples, and every tier's column list is
+    gathered on the device.  Same tiers, same column order."""
+    n = cols.size
+    if n < 65536:
+        return _split_tiers_direct(cols, lcap, m, nI)
+    cm, cn = _coarse(m), _coarse(nI)
+    if max(int(lcap.max()), int(cm.max()), int(cn.max())) >= (1 << 21):
+        return _split_tiers_direct(cols, lcap, m, nI)
+    dev = _dev()
+    key = torch.as_tensor((lcap << 42) | (cn << 21) | cm, device=dev)
+    uk, inv = torch.unique(key, return_inverse=True)
+    U = int(uk.numel())
+    gm = torch.zeros(U, dtype=torch.int64, device=dev).scatter_reduce_(
+        0, inv, torch.as_tensor(m, device=dev), "amax", include_self=False)
+    gn = torch.zeros(U, dtype=torch.int64, device=dev).scatter_reduce_(
+        0, inv, torch.as_tensor(nI, device=dev), "amax", include_self=False)
+    rep = _split_tiers_direct(np.arange(U, dtype=np.int64), uk.cpu().numpy() >> 42,
+                              gm.cpu().numpy(), gn.cpu().numpy())
+    tier_of_key = np.zeros(U, dtype=np.int64)
+    for ti, t in enumerate(rep):
+        tier_of_key[t.cols_host] = ti
+    tcol = torch.as_tensor(tier_of_key, device=dev)[inv]
+    dcols = torch.as_tensor(cols, device=dev)
+    out = []
+    for ti, t in enumerate(rep):
+        c = dcols[torch.nonzero(tcol == ti).flatten()]
+        c = torch.sort(c).values
+        out.append(_Tier(t.team, t.glob, t.lcap, t.mcap, t.ncap, c.cpu().numpy(), mode=t.mode,
+                         cols_dev=c.to(torch.int32)))
+    return out
+
+
+def _split_tiers_direct(cols, lcap, m, nI):
     """Group columns into launch tiers by the team memory they need: dense
     pivoted-QR teams (warp / 128 / 256 threads, shared memory) while the
     dense block fits, the semi-normal-equations kernel (mode 3) beyond."""
@@ -451,7 +497,11 @@ def _plan(pattern, sys_colptr, sys_rowidx, t_colptr, t_rowidx, t_key, sys_key, c
     lcap = _pow2(L)
     # plan pass: |J_j| (mode 1) grouped by list capacity
     msize = torch.zeros(n, dtype=torch.int32, device=_dev())
-    for cap in np.unique(lcap):
+    # (distinct capacities from a histogram of the small integer bounds: no
+    # sort of the per-column array)
+    Lc = np.maximum(L, 1)
+    caps = np.unique(_pow2(np.flatnonzero(np.bincount(Lc)))) if ncols > 4096 else np.unique(lcap)
+    for cap in caps:
         s = np.flatnonzero(lcap == cap)
         nc = int(nI[s].max())
         tb = _team_bytes(int(cap), 0, nc)

@@ -964,3 +964,30 @@ def test_persistent_solve_hands_back_deflating_blocks(pm, n, s):
         assert abs(r.iterations - rh.iterations) <= 2
     assert krylov.FALLBACK_REASONS.get(3, 0) == 3
     krylov.FALLBACK_REASONS.clear()
+
+
+def test_grouped_tier_planning_equals_per_column_planning(pm):
+    """The LS size tiers decided on the distinct (capacity, |I|, |J|) triples
+    (grouped on the device) are the tiers decided column by column: same
+    launches, same dimensions, same column order -- on a stencil-like and on
+    a power-law (c5-like) size distribution."""
+    from paper_1809_06574_b200 import spai
+    rng = np.random.default_rng(11)
+    n = 200000
+    cases = []
+    nI = rng.choice([4, 5, 6, 7], size=n, p=[0.01, 0.04, 0.15, 0.8])
+    m = np.minimum(nI * 4 - rng.integers(0, 4, n), 25)
+    cases.append((nI.astype(np.int64), m.astype(np.int64), spai._pow2(m + nI)))
+    nI = np.clip(np.floor(4.0 * rng.uniform(0, 1, n) ** (-1.0 / 0.98)), 4, 200).astype(np.int64)
+    m = (nI * rng.integers(5, 40, n)).astype(np.int64)
+    cases.append((nI, m, spai._pow2(m + 3 * nI)))
+    cols = np.arange(n, dtype=np.int64)
+    for nI, m, lcap in cases:
+        a = spai._split_tiers(cols, lcap, m, nI)
+        b = spai._split_tiers_direct(cols, lcap, m, nI)
+        assert len(a) == len(b) and len(a) >= 1
+        for x, y in zip(a, b):
+            assert (x.team, x.glob, x.mode, x.lcap, x.mcap, x.ncap) == \
+                   (y.team, y.glob, y.mode, y.lcap, y.mcap, y.ncap)
+            assert np.array_equal(x.cols_host, y.cols_host)
+            assert np.array_equal(x.cols.cpu().numpy(), y.cols.cpu().numpy())
