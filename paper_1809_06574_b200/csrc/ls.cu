@@ -342,11 +342,34 @@ __device__ void ls_residual_store(const LsParams& P, const LsMem& m, const int* 
       res[ent[2 * (tot + q) + 1] & 0xffff] = e < 0 ? 1.0 : P.tvals[e];
     }
     tm.sync();
-    for (int c = 0; c < n; ++c) {
-      const double zc = m.w[c];
-      for (int q = m.off[c] + tid; q < m.off[c + 1]; q += T)
-        res[ent[2 * q + 1] & 0xffff] -= P.avals[ent[2 * q]] * zc;
+    // The column loop below is sequential (columns share rows; its order
+    // fixes the rounding) with only |A(:, c)| <= T entries of work per
+    // column: with the plan entries and values read from global memory
+    // inside it, every column paid two dependent L2 round trips (ncu: 19 %
+    // of the team kernel's stall samples at c3).  Stage them once -- every
+    // load in flight together -- behind `res` in the dead block M when they
+    // fit; same updates in the same order.
+    const size_t mcells = (size_t)P.mcap * (P.ncap + 1);
+    double* sv = res + mm;
+    int* sp = reinterpret_cast<int*>(sv + tot);
+    if (T > 32 && (size_t)mm + tot + (tot + 1) / 2 <= mcells) {
+      for (int q = tid; q < tot; q += T) {
+        sv[q] = P.avals[ent[2 * q]];
+        sp[q] = ent[2 * q + 1] & 0xffff;
+      }
       tm.sync();
+      for (int c = 0; c < n; ++c) {
+        const double zc = m.w[c];
+        for (int q = m.off[c] + tid; q < m.off[c + 1]; q += T) res[sp[q]] -= sv[q] * zc;
+        tm.sync();
+      }
+    } else {
+      for (int c = 0; c < n; ++c) {
+        const double zc = m.w[c];
+        for (int q = m.off[c] + tid; q < m.off[c + 1]; q += T)
+          res[ent[2 * q + 1] & 0xffff] -= P.avals[ent[2 * q]] * zc;
+        tm.sync();
+      }
     }
   } else {
     for (int q = tid; q < tl; q += T) {
