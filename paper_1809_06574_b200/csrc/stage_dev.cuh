@@ -456,15 +456,18 @@ __device__ PMP_STAGED_ATTR void worker_inner_staged(const CycleArgs& P, WBar& wb
       spmm_rows_cyc<NY, false>(P.arp, P.aci, P.ava, src, lds, sb, P.W, P.s, P.n, wb.wi, wb.n);
       wbar(wb);
     } else {
+#ifndef PMP_STAGED_CA
+#define PMP_STAGED_CA 1
+#endif
     for (int f = P.nfac - 1; f >= 0; --f) {
       double* dst = ((P.nfac - 1 - f) & 1) ? P.T1 : P.T0;
-      spmm_rows<NY>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb, dst + (size_t)r0 * P.s, P.s,
-                    r0, nr);
+      spmm_rows<NY, PMP_STAGED_CA != 0>(P.frp[f], P.fci[f], P.fva[f], src, lds, sb,
+                                        dst + (size_t)r0 * P.s, P.s, r0, nr);
       wbar(wb);
       src = dst;
       lds = P.s;
     }
-    spmm_rows<NY>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr);
+    spmm_rows<NY, PMP_STAGED_CA != 0>(P.arp, P.aci, P.ava, src, lds, sb, Wv, ldw, r0, nr);
     }
     cstamp(P, stp, 1);
 
